@@ -1,0 +1,296 @@
+"""Node-centred median-dual meshes for the 3D edge-based FNLH discretization.
+
+The reference meshes are 1D/2D with axis-aligned faces carrying a scalar area
+(``mesh.hpp:24-62``).  The BASELINE configurations are 3D hex / Kuhn-tet sectors,
+so a face here carries an area-weighted normal ``fn`` (a -> b for interior edges,
+outward on inlet/outlet faces).  Slip walls are not faces: their pressure force is
+the node closure source ``-p * closure_i`` (``closure_i`` = sum of the node's
+incident outward normals), which is exactly the reference nozzle's area source
+``-p (A_R - A_L)`` (``disc_euler.cpp:95-100``) on a line mesh.
+
+Node ordering (the ILU(0) order): seeded random permutation -> reverse
+Cuthill-McKee -> stable colour-major sort, so ILU(0) rows of one colour are
+independent and the device factorizes / substitutes colour by colour while staying
+the reference's natural-order algorithm (``sparse.cpp:187-291``) on this ordering.
+"""
+from __future__ import annotations
+
+import dataclasses
+import itertools
+
+import numpy as np
+
+
+@dataclasses.dataclass
+class Mesh3D:
+    n: int
+    nf: int
+    b: int
+    fa: np.ndarray        # int32 [nf]
+    fb: np.ndarray        # int32 [nf], -1 on boundary faces
+    fbc: np.ndarray       # int32 [nf], -1 interior, 0 inlet (west), 1 outlet (east)
+    ford: np.ndarray      # int32 [nf], global boundary ordinal (forcing slot), 0 interior
+    fn: np.ndarray        # float64 [nf*3]
+    farea: np.ndarray     # float64 [nf]
+    fnh: np.ndarray       # float64 [nf*3]
+    fvis: np.ndarray      # float64 [nf]
+    vol: np.ndarray       # float64 [n]
+    closure: np.ndarray   # float64 [n*3]
+    mu: np.ndarray        # float64 [n]
+    nf_ptr: np.ndarray    # int32 [n+1]
+    nf_idx: np.ndarray    # int32
+    bflag: np.ndarray     # int32 [n]
+    gamma: float = 1.4
+    gas_constant: float = 287.05
+    p0: float = 101325.0
+    T0: float = 300.0
+    p_out: float = 98000.0
+    nt_in: float = 0.0
+    forcing_scale: float = 98000.0
+    colour: np.ndarray | None = None       # int32 [n], nondecreasing in colour-major orders
+    partition: np.ndarray | None = None    # int32 [n]
+    coords: np.ndarray | None = None       # float64 [n,3]
+    n_boundary: int = 0
+
+    # --- sparsity pattern of the block LHS (sparse.cpp:61-117): adjacency + diagonal
+    def pattern(self, b: int | None = None):
+        n = self.n
+        interior = self.fbc < 0
+        a = self.fa[interior].astype(np.int64)
+        c = self.fb[interior].astype(np.int64)
+        rows = np.concatenate([np.arange(n), a, c])
+        cols = np.concatenate([np.arange(n), c, a])
+        key = np.unique(rows * n + cols)
+        rows = (key // n).astype(np.int32)
+        cols = (key % n).astype(np.int32)
+        row_ptr = np.zeros(n + 1, np.int32)
+        np.cumsum(np.bincount(rows, minlength=n), out=row_ptr[1:])
+        diag = np.flatnonzero(rows == cols).astype(np.int32)
+        part = self.partition if self.partition is not None else np.zeros(n, np.int32)
+        return dict(b=self.b if b is None else b, row_ptr=row_ptr, col_idx=cols, diag_idx=diag,
+                    partition=np.ascontiguousarray(part, np.int32))
+
+    def forcing_size(self):
+        return 3 * self.n_boundary
+
+
+def from_faces(n, fa, fb, fbc, ford, fn, vol, *, b=5, gamma=1.4, gas_constant=287.05, p0=101325.0, T0=300.0,
+               p_out=98000.0, nt_in=0.0, forcing_scale=None, coords=None, mu=None, colour=None, partition=None):
+    """Assemble the derived arrays (areas, unit normals, node->face CSR in ascending face
+    order as mesh.cpp:44-59, slip-wall closure accumulated in face order)."""
+    fa = np.ascontiguousarray(fa, np.int32)
+    fb = np.ascontiguousarray(fb, np.int32)
+    fbc = np.ascontiguousarray(fbc, np.int32)
+    ford = np.ascontiguousarray(ford, np.int32)
+    fn = np.ascontiguousarray(np.asarray(fn, np.float64).reshape(-1, 3))
+    nf = len(fa)
+    farea = np.sqrt(fn[:, 0] * fn[:, 0] + fn[:, 1] * fn[:, 1] + fn[:, 2] * fn[:, 2])
+    fnh = fn / farea[:, None]
+    interior = fbc < 0
+    # node -> face CSR, ascending face index per node (Mesh::build_adjacency)
+    ev_node = np.stack([fa, np.where(interior, fb, -1)], axis=1).reshape(-1)
+    ev_face = np.repeat(np.arange(nf, dtype=np.int32), 2)
+    ev_sign = np.tile(np.array([1.0, -1.0]), nf)
+    keep = ev_node >= 0
+    ev_node, ev_face, ev_sign = ev_node[keep], ev_face[keep], ev_sign[keep]
+    order = np.argsort(ev_node, kind="stable")  # events are in face order already
+    nf_ptr = np.zeros(n + 1, np.int32)
+    np.cumsum(np.bincount(ev_node, minlength=n), out=nf_ptr[1:])
+    nf_idx = np.ascontiguousarray(ev_face[order], np.int32)
+    # closure: start at 0.0 and add +-fn in face order per node (np.add.at is sequential)
+    closure = np.zeros((n, 3))
+    np.add.at(closure, ev_node, fn[ev_face] * ev_sign[:, None])
+    bflag = np.zeros(n, np.int32)
+    bflag[fa[~interior]] = 1
+    if coords is not None and interior.any():
+        d = coords[fb[interior]] - coords[fa[interior]]
+        fvis = np.zeros(nf)
+        fvis[interior] = farea[interior] / np.sqrt((d * d).sum(1))
+    else:
+        fvis = np.zeros(nf)
+    m = Mesh3D(n=n, nf=nf, b=b, fa=fa, fb=fb, fbc=fbc, ford=ford, fn=fn.reshape(-1).copy(), farea=farea,
+               fnh=np.ascontiguousarray(fnh.reshape(-1)), fvis=fvis, vol=np.ascontiguousarray(vol, np.float64),
+               closure=closure.reshape(-1).copy(),
+               mu=np.zeros(n) if mu is None else np.ascontiguousarray(mu, np.float64),
+               nf_ptr=nf_ptr, nf_idx=nf_idx, bflag=bflag, gamma=gamma, gas_constant=gas_constant, p0=p0, T0=T0,
+               p_out=p_out, nt_in=nt_in, forcing_scale=p_out if forcing_scale is None else forcing_scale,
+               colour=None if colour is None else np.ascontiguousarray(colour, np.int32),
+               partition=None if partition is None else np.ascontiguousarray(partition, np.int32),
+               coords=coords, n_boundary=int((~interior).sum()))
+    return m
+
+
+# ---------------------------------------------------------------------------- generators
+def _cross(a, b):
+    return np.stack([a[:, 1] * b[:, 2] - a[:, 2] * b[:, 1], a[:, 2] * b[:, 0] - a[:, 0] * b[:, 2],
+                     a[:, 0] * b[:, 1] - a[:, 1] * b[:, 0]], axis=1)
+
+
+_HEX_EDGES = [(p, p | (1 << d)) for d in range(3) for p in range(8) if not (p >> d) & 1]
+_KUHN = [(0, 1 << a, (1 << a) | (1 << b), 7) for a, b, _ in itertools.permutations(range(3))]
+
+
+def _hex_edge_faces(p, q):
+    d = (p ^ q).bit_length() - 1
+    faces = []
+    for e in range(3):
+        if e == d:
+            continue
+        bit = (p >> e) & 1
+        faces.append([v for v in range(8) if ((v >> e) & 1) == bit])
+    return faces
+
+
+def structured_sector(ci, cj, ck, *, geometry="annular", length=2.0, pitch_deg=10.0, r_in=0.5, r_out=1.0,
+                      width=1.0, height=0.5, periodic_j=False, tets=False, jitter=0.0, seed=0, b=5, permute=True,
+                      gas=None, nt_in=0.0, mu_range=None):
+    """Hex (or Kuhn 6-tet) sector mesh, node-centred median dual.
+
+    i: axial (inlet i=0, outlet i=ci), j: pitch, k: span/radius.  Walls (hub, casing,
+    non-periodic pitch sides) enter through the closure source.  Returns a Mesh3D in
+    colour-major RCM order (2 colours for hex, 8 for Kuhn tets)."""
+    rng = np.random.default_rng(seed)
+    ni, nj_u, nk = ci + 1, cj + 1, ck + 1
+    nj = cj if periodic_j else cj + 1
+    I, J, K = np.meshgrid(np.arange(ni), np.arange(nj_u), np.arange(nk), indexing="ij")
+    fi, fj, fk = I.astype(float), J.astype(float), K.astype(float)
+    if jitter > 0.0:
+        inner = (I > 0) & (I < ci) & (J > 0) & (J < cj) & (K > 0) & (K < ck)
+        jit = rng.uniform(-jitter, jitter, size=(3,) + I.shape)
+        fi = fi + np.where(inner, jit[0], 0.0)
+        fj = fj + np.where(inner, jit[1], 0.0)
+        fk = fk + np.where(inner, jit[2], 0.0)
+    if geometry == "annular":
+        th = np.deg2rad(pitch_deg) * fj / cj
+        r = r_in + (r_out - r_in) * fk / ck
+        X = np.stack([length * fi / ci, r * np.cos(th), r * np.sin(th)], axis=-1)
+    else:
+        X = np.stack([length * fi / ci, width * fj / cj, height * fk / ck], axis=-1)
+    Xu = X.reshape(-1, 3)                                            # unwrapped coordinates
+    gid = ((I * nj + (J % nj)) * nk + K).reshape(-1)                 # mapped node id
+    n = ni * nj * nk
+    coords = np.ascontiguousarray(X[:, :nj, :].reshape(-1, 3))     # gid order (seam copies dropped)
+    uid = lambda i, j, k: (i * nj_u + j) * nk + k  # noqa: E731
+    # hex cells: corner c = di + 2 dj + 4 dk
+    ic, jc, kc = np.meshgrid(np.arange(ci), np.arange(cj), np.arange(ck), indexing="ij")
+    ic, jc, kc = ic.reshape(-1), jc.reshape(-1), kc.reshape(-1)
+    corners_u = np.stack([uid(ic + (c & 1), jc + ((c >> 1) & 1), kc + ((c >> 2) & 1)) for c in range(8)], axis=1)
+    corners = gid[corners_u]
+    P = Xu[corners_u]                                                # [ncell, 8, 3]
+    e_keys, e_vecs = [], []
+    vol_node = np.zeros(n)
+
+    def tet_vol(a, b_, c, d):
+        return np.abs(np.einsum("ij,ij->i", b_ - a, _cross(c - a, d - a))) / 6.0
+
+    def add_edge(p_id, q_id, S, xp, xq):
+        sgn = np.sign(np.einsum("ij,ij->i", S, xq - xp))
+        S = S * sgn[:, None]
+        lo = np.minimum(p_id, q_id)
+        hi = np.maximum(p_id, q_id)
+        flip = np.where(p_id < q_id, 1.0, -1.0)
+        e_keys.append(lo.astype(np.int64) * n + hi)
+        e_vecs.append(S * flip[:, None])
+
+    if not tets:
+        cen = P.mean(axis=1)
+        for (p, q) in _HEX_EDGES:
+            f1, f2 = _hex_edge_faces(p, q)
+            m = 0.5 * (P[:, p] + P[:, q])
+            c1 = P[:, f1].mean(axis=1)
+            c2 = P[:, f2].mean(axis=1)
+            add_edge(corners[:, p], corners[:, q], 0.5 * _cross(cen - m, c2 - c1), P[:, p], P[:, q])
+        vc = sum(tet_vol(P[:, t[0]], P[:, t[1]], P[:, t[2]], P[:, t[3]]) for t in _KUHN)
+        for c in range(8):
+            vol_node += np.bincount(corners[:, c], weights=vc / 8.0, minlength=n)
+    else:
+        for t in _KUHN:
+            T = P[:, list(t)]
+            tid = corners[:, list(t)]
+            cen = T.mean(axis=1)
+            vt = tet_vol(T[:, 0], T[:, 1], T[:, 2], T[:, 3])
+            for c in range(4):
+                vol_node += np.bincount(tid[:, c], weights=vt / 4.0, minlength=n)
+            for (p, q) in itertools.combinations(range(4), 2):
+                r, s = [v for v in range(4) if v not in (p, q)]
+                m = 0.5 * (T[:, p] + T[:, q])
+                c1 = (T[:, p] + T[:, q] + T[:, r]) / 3.0
+                c2 = (T[:, p] + T[:, q] + T[:, s]) / 3.0
+                add_edge(tid[:, p], tid[:, q], 0.5 * _cross(cen - m, c2 - c1), T[:, p], T[:, q])
+    keys = np.concatenate(e_keys)
+    vecs = np.concatenate(e_vecs)
+    ukeys, inv = np.unique(keys, return_inverse=True)
+    en = np.stack([np.bincount(inv, weights=vecs[:, d], minlength=len(ukeys)) for d in range(3)], axis=1)
+    ea = (ukeys // n).astype(np.int64)
+    eb = (ukeys % n).astype(np.int64)
+
+    # inlet (i=0, outward -x) and outlet (i=ci, outward +x) dual boundary areas
+    jq, kq = np.meshgrid(np.arange(cj), np.arange(ck), indexing="ij")
+    jq, kq = jq.reshape(-1), kq.reshape(-1)
+    b_nodes, b_vecs, b_kind = [], [], []
+    for kind, iplane, out in ((0, 0, -1.0), (1, ci, 1.0)):
+        q_u = np.stack([uid(iplane, jq, kq), uid(iplane, jq + 1, kq), uid(iplane, jq + 1, kq + 1),
+                        uid(iplane, jq, kq + 1)], axis=1)
+        Q = Xu[q_u]
+        polys = [[0, 1, 2], [0, 2, 3]] if tets else [[0, 1, 2, 3]]
+        acc = np.zeros(n)
+        for poly in polys:
+            V = Q[:, poly]
+            cen = V.mean(axis=1)
+            L = len(poly)
+            for t in range(L):
+                p, nx_, pv = V[:, t], V[:, (t + 1) % L], V[:, (t - 1) % L]
+                S = 0.5 * _cross(cen - p, 0.5 * (p + pv) - 0.5 * (p + nx_))
+                acc += np.bincount(gid[q_u[:, poly[t]]], weights=np.abs(S[:, 0]), minlength=n)
+        nodes = np.flatnonzero(acc > 0)
+        b_nodes.append(nodes)
+        b_vecs.append(np.stack([out * acc[nodes], np.zeros(len(nodes)), np.zeros(len(nodes))], axis=1))
+        b_kind.append(np.full(len(nodes), kind))
+    b_nodes = np.concatenate(b_nodes)
+    b_vecs = np.concatenate(b_vecs)
+    b_kind = np.concatenate(b_kind)
+
+    # structural colouring: 2 colours (hex, (i+j+k) mod 2), 8 colours (Kuhn tets)
+    In, Jn, Kn = np.meshgrid(np.arange(ni), np.arange(nj), np.arange(nk), indexing="ij")
+    col = ((In + Jn + Kn) % 2) if not tets else ((In + 2 * Jn + 4 * Kn) % 8)
+    col = col.reshape(-1).astype(np.int32)
+    if periodic_j and not tets:
+        assert cj % 2 == 0, "periodic 2-colouring needs an even pitch count"
+
+    # ordering: seeded permutation -> RCM -> colour-major (stable)
+    perm0 = rng.permutation(n) if permute else np.arange(n)        # perm0[new] = old
+    inv0 = np.empty(n, np.int64)
+    inv0[perm0] = np.arange(n)
+    from scipy.sparse import coo_matrix
+    from scipy.sparse.csgraph import reverse_cuthill_mckee
+    ra, rb = inv0[ea], inv0[eb]
+    G = coo_matrix((np.ones(2 * len(ra)), (np.concatenate([ra, rb]), np.concatenate([rb, ra]))), shape=(n, n)).tocsr()
+    rcm = np.asarray(reverse_cuthill_mckee(G, symmetric_mode=True), np.int64)   # rcm[pos] = permuted id
+    rank = np.empty(n, np.int64)
+    rank[perm0[rcm]] = np.arange(n)                                  # rank[old] = RCM position
+    order = np.lexsort((rank, col))                                  # order[new] = old
+    new = np.empty(n, np.int64)
+    new[order] = np.arange(n)
+
+    a2, b2 = new[ea], new[eb]
+    sw = a2 > b2
+    en = np.where(sw[:, None], -en, en)
+    a2, b2 = np.where(sw, b2, a2), np.where(sw, a2, b2)
+    o = np.lexsort((b2, a2))
+    a2, b2, en = a2[o], b2[o], en[o]
+    bn = new[b_nodes]
+    ob = np.lexsort((bn, b_kind))
+    bn, b_vecs, b_kind = bn[ob], b_vecs[ob], b_kind[ob]
+    ne, nb = len(a2), len(bn)
+    fa = np.concatenate([a2, bn]).astype(np.int32)
+    fb = np.concatenate([b2, -np.ones(nb, np.int64)]).astype(np.int32)
+    fbc = np.concatenate([-np.ones(ne, np.int64), b_kind]).astype(np.int32)
+    ford = np.concatenate([np.zeros(ne, np.int64), np.arange(nb)]).astype(np.int32)
+    fnv = np.concatenate([en, b_vecs])
+    g = gas or {}
+    mu = None
+    if mu_range is not None:
+        lo_, hi_ = np.log(mu_range[0]), np.log(mu_range[1])
+        mu = np.exp(rng.uniform(lo_, hi_, size=n))
+    return from_faces(n, fa, fb, fbc, ford, fnv, vol_node[order], b=b, coords=coords[order], colour=col[order],
+                      mu=mu, nt_in=nt_in, **g)

@@ -1,0 +1,56 @@
+"""Shared test helpers: the reference nozzle embedded as a 3D line mesh (b = 5).
+
+The reference's quasi-1D nozzle (disc_euler.cpp) is the special case of the 3D
+edge-based discretization with face normals (A, 0, 0): these helpers build that line
+mesh from the reference's own mesh arrays and map states between b = 3
+(rho, u, p) and b = 5 (rho, u, v=0, w=0, p)."""
+import numpy as np
+
+from paper_2404_01407_b200.mesh import from_faces
+
+IDX3 = np.array([0, 1, 4])
+
+
+def line_mesh_from_ref(noz):
+    nf = noz.nf
+    fn = np.zeros((nf, 3))
+    sign = np.where(noz.fbc == 0, -1.0, 1.0)      # west boundary faces point to -x
+    fn[:, 0] = sign * noz.area
+    fbc = np.where(noz.fbc < 0, -1, noz.fbc).astype(np.int32)
+    ford = np.zeros(nf, np.int32)
+    bidx = np.flatnonzero(fbc >= 0)
+    ford[bidx] = np.arange(len(bidx))
+    m = from_faces(noz.n, noz.fa, noz.fb, fbc, ford, fn, noz.vol, b=5, gamma=noz.gamma,
+                   gas_constant=noz.gas_constant, p0=noz.p0, T0=noz.T0, p_out=noz.p_out,
+                   forcing_scale=noz.forcing_scale)
+    assert np.array_equal(m.nf_ptr, noz.nf_ptr) and np.array_equal(m.nf_idx, noz.nf_idx)
+    return m
+
+
+def embed(v3, n, dtype=np.float64):
+    v = np.zeros((n, 5), dtype)
+    v[:, IDX3] = np.asarray(v3).reshape(n, 3)
+    return v.reshape(-1)
+
+
+def extract(v5, n):
+    return np.asarray(v5).reshape(n, 5)[:, IDX3].reshape(-1)
+
+
+def forcing_triplets(f3, nbfaces=2):
+    return np.tile(np.asarray(f3), nbfaces)
+
+
+def extract_blocks(J5, nblocks):
+    J = np.asarray(J5).reshape(nblocks, 5, 5)
+    return J[:, IDX3][:, :, IDX3].reshape(-1)
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+NOZZLE_CASE = "kind = nozzle-euler\nnx = {nx}\nharmonics = {nh}\nbase_omega = 500\n"
