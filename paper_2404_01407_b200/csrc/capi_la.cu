@@ -1,0 +1,171 @@
+// capi_la.cu -- extern "C" entry points for the L1 block-sparse LA (include/fnlh_b200.h).
+#include <memory>
+#include <string>
+
+#include "fnlh_b200.h"
+#include "capi_util.hpp"
+#include "la.cuh"
+
+using namespace fnlh;
+
+struct fnlh_pattern {
+    std::unique_ptr<DevicePattern> p;
+};
+
+namespace {
+
+template <class S>
+struct HostSystem {
+    DeviceBuffer<double> real_vals;
+    DeviceBuffer<S> vals;
+    DeviceBuffer<double> shift;
+    SystemView<S> view;
+    HostSystem(const DevicePattern* p, const double* A, int A_complex, const double* shift_im) {
+        const std::size_t n = (std::size_t)p->nnzb * p->b * p->b;
+        view.p = p;
+        if (A_complex) {
+            vals.upload(reinterpret_cast<const S*>(A), n);
+            view.vals = vals.ptr;
+        } else {
+            real_vals.upload(A, n);
+            view.real_vals = real_vals.ptr;
+            if (shift_im) {
+                shift.upload(shift_im, p->rows);
+                view.shift_im = shift.ptr;
+            }
+        }
+    }
+};
+
+template <class S>
+int factorize_impl(const fnlh_pattern* p, const double* A, int A_complex, const double* shift_im, double* vals,
+                   double* diag_lu, int* diag_piv, double* diag_inv) {
+    const DevicePattern* dp = p->p.get();
+    HostSystem<S> sys(dp, A, A_complex, shift_im);
+    Workspace ws(1);
+    DeviceIlu<S> f(dp);
+    ilu_factorize(sys.view, f, ws);
+    const std::size_t bb = (std::size_t)dp->b * dp->b;
+    if (vals) download(reinterpret_cast<S*>(vals), f.vals, (std::size_t)dp->nnzb * bb);
+    if (diag_lu) download(reinterpret_cast<S*>(diag_lu), f.diag_lu, (std::size_t)dp->rows * bb);
+    if (diag_piv) download(diag_piv, f.diag_piv, (std::size_t)dp->rows * dp->b);
+    if (diag_inv) download(reinterpret_cast<S*>(diag_inv), f.diag_inv, (std::size_t)dp->rows * bb);
+    return 0;
+}
+
+template <class S>
+int apply_impl(const fnlh_pattern* p, const double* A, int A_complex, const double* shift_im, const double* rhs,
+               double* x) {
+    const DevicePattern* dp = p->p.get();
+    const std::size_t len = (std::size_t)dp->rows * dp->b;
+    HostSystem<S> sys(dp, A, A_complex, shift_im);
+    Workspace ws(len);
+    DeviceIlu<S> f(dp);
+    ilu_factorize(sys.view, f, ws);
+    DeviceBuffer<S> r, z;
+    r.upload(reinterpret_cast<const S*>(rhs), len);
+    z.alloc(len);
+    ilu_apply(f, r.ptr, z.ptr, ws);
+    FNLH_CUDA(cudaStreamSynchronize(ws.stream));
+    download(reinterpret_cast<S*>(x), z.ptr, len);
+    return 0;
+}
+
+template <class S>
+int matvec_impl(const fnlh_pattern* p, const double* A, int A_complex, const double* shift_im, const double* x,
+                double* y) {
+    const DevicePattern* dp = p->p.get();
+    const std::size_t len = (std::size_t)dp->rows * dp->b;
+    HostSystem<S> sys(dp, A, A_complex, shift_im);
+    Workspace ws(len);
+    DeviceBuffer<S> xv, yv;
+    xv.upload(reinterpret_cast<const S*>(x), len);
+    yv.alloc(len);
+    matvec(sys.view, xv.ptr, yv.ptr, ws);
+    FNLH_CUDA(cudaStreamSynchronize(ws.stream));
+    download(reinterpret_cast<S*>(y), yv.ptr, len);
+    return 0;
+}
+
+template <class S>
+int solve_impl(const fnlh_pattern* p, const double* A, int A_complex, const double* shift_im, const double* rhs,
+               double tol, int max_iter, double* x, fnlh_linear_report* rep) {
+    const DevicePattern* dp = p->p.get();
+    const std::size_t len = (std::size_t)dp->rows * dp->b;
+    HostSystem<S> sys(dp, A, A_complex, shift_im);
+    Workspace ws(len);
+    DeviceIlu<S> f(dp);
+    ilu_factorize(sys.view, f, ws);
+    DeviceBuffer<S> b, xv;
+    b.upload(reinterpret_cast<const S*>(rhs), len);
+    xv.alloc(len);
+    LinearSolveReport r = smoothed_solve(sys.view, b.ptr, f, tol, max_iter, xv.ptr, ws);
+    FNLH_CUDA(cudaStreamSynchronize(ws.stream));
+    download(reinterpret_cast<S*>(x), xv.ptr, len);
+    if (rep) *rep = fnlh_linear_report{r.iterations, r.initial_residual, r.final_residual, r.converged};
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fnlh_pattern_create(int b, int rows, const int* row_ptr, const int* col_idx, const int* partition,
+                        fnlh_pattern** out) {
+    return guarded([&] {
+        auto h = std::make_unique<fnlh_pattern>();
+        h->p = std::make_unique<DevicePattern>(b, rows, row_ptr, col_idx, partition);
+        *out = h.release();
+    });
+}
+
+void fnlh_pattern_destroy(fnlh_pattern* p) { delete p; }
+
+int fnlh_pattern_levels(const fnlh_pattern* p, int* fwd, int* bwd) {
+    *fwd = p->p->fwd_levels();
+    *bwd = p->p->bwd_levels();
+    return 0;
+}
+
+int fnlh_ilu_factorize(const fnlh_pattern* p, int is_complex, const double* A, int A_complex, const double* shift_im,
+                       double* vals, double* diag_lu, int* diag_piv, double* diag_inv) {
+    return guarded([&] {
+        if (is_complex)
+            factorize_impl<cplx>(p, A, A_complex, shift_im, vals, diag_lu, diag_piv, diag_inv);
+        else
+            factorize_impl<double>(p, A, 0, nullptr, vals, diag_lu, diag_piv, diag_inv);
+    });
+}
+
+int fnlh_ilu_apply(const fnlh_pattern* p, int is_complex, const double* A, int A_complex, const double* shift_im,
+                   const double* rhs, double* x) {
+    return guarded([&] {
+        if (is_complex)
+            apply_impl<cplx>(p, A, A_complex, shift_im, rhs, x);
+        else
+            apply_impl<double>(p, A, 0, nullptr, rhs, x);
+    });
+}
+
+int fnlh_matvec(const fnlh_pattern* p, int is_complex, const double* A, int A_complex, const double* shift_im,
+                const double* x, double* y) {
+    return guarded([&] {
+        if (is_complex)
+            matvec_impl<cplx>(p, A, A_complex, shift_im, x, y);
+        else
+            matvec_impl<double>(p, A, 0, nullptr, x, y);
+    });
+}
+
+int fnlh_smoothed_solve(const fnlh_pattern* p, int is_complex, const double* A, int A_complex,
+                        const double* shift_im, const double* rhs, double tol_rel, int max_iter, double* x,
+                        fnlh_linear_report* rep) {
+    return guarded([&] {
+        if (is_complex)
+            solve_impl<cplx>(p, A, A_complex, shift_im, rhs, tol_rel, max_iter, x, rep);
+        else
+            solve_impl<double>(p, A, 0, nullptr, rhs, tol_rel, max_iter, x, rep);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,641 @@
+// la.cu -- device block-sparse LA (sparse.hpp/.cpp restated for sm_100a).
+//
+// Ordering contract: the device runs the reference's natural-order ILU(0) loops
+// (sparse.cpp:187-291) level by level.  Within a row the arithmetic follows the
+// reference operation by operation (compiled with --fmad=false), so factors and
+// substitutions are bitwise identical to the reference except where a complex
+// magnitude (hypot vs cabs) breaks a pivot tie.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "errors.hpp"
+#include "la.cuh"
+
+namespace fnlh {
+
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs
+
+struct PatDev {
+    int b, rows, nnzb;
+    const int* __restrict__ row_ptr;
+    const int* __restrict__ col_idx;
+    const int* __restrict__ diag_idx;
+    const int* __restrict__ part;
+};
+
+PatDev dev(const DevicePattern& p) { return PatDev{p.b, p.rows, p.nnzb, p.row_ptr, p.col_idx, p.diag_idx, p.part}; }
+
+inline int nblocks(long long n, int t = kThreads) { return static_cast<int>((n + t - 1) / t); }
+
+__device__ __forceinline__ int find_entry(const PatDev& p, int i, int j) {  // sparse.cpp:42-48
+    int lo = p.row_ptr[i], hi = p.row_ptr[i + 1];
+    const int end = hi;
+    while (lo < hi) {
+        const int mid = lo + ((hi - lo) >> 1);
+        if (p.col_idx[mid] < j)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return (lo == end || p.col_idx[lo] != j) ? -1 : lo;
+}
+
+// value of system entry e (row i) element k = r*B+c
+template <int B, class S>
+__device__ __forceinline__ S sys_entry(const SystemView<S>& A, int e, int k, bool diag, int i) {
+    if (A.vals) return A.vals[(size_t)e * B * B + k];
+    S v = from_real<S>(A.real_vals[(size_t)e * B * B + k]);
+    if constexpr (sizeof(S) == sizeof(cplx)) {
+        if (diag && A.shift_im && (k / B == k % B)) v = v + mk(0.0, A.shift_im[i]);  // d[m][m] += s_i
+    }
+    return v;
+}
+
+// Ilu::factorize copy phase (sparse.cpp:199-209)
+template <int B, class S>
+__global__ void k_ilu_copy(PatDev p, SystemView<S> A, S* __restrict__ vals) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.rows) return;
+    const int pi = p.part[i];
+    const int di = p.diag_idx[i];
+    for (int e = p.row_ptr[i]; e < p.row_ptr[i + 1]; ++e) {
+        const int j = p.col_idx[e];
+        S* dst = vals + (size_t)e * B * B;
+        if (p.part[j] == pi) {
+#pragma unroll
+            for (int k = 0; k < B * B; ++k) dst[k] = sys_entry<B, S>(A, e, k, e == di, i);
+        } else {
+#pragma unroll
+            for (int k = 0; k < B * B; ++k) dst[k] = zero<S>();
+        }
+    }
+}
+
+// Ilu::factorize elimination + pivot phase for the rows of one level (sparse.cpp:214-255)
+template <int B, class S>
+__global__ void __launch_bounds__(kThreads) k_ilu_factor(PatDev p, const int* __restrict__ rows, int nrows,
+                                                         S* vals, S* __restrict__ diag_lu,
+                                                         int* __restrict__ diag_piv, S* diag_inv,
+                                                         int* __restrict__ status) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nrows) return;
+    const int i = rows[t];
+    const int pi = p.part[i];
+    const int rb = p.row_ptr[i], re = p.row_ptr[i + 1];
+    for (int ek = rb; ek < re; ++ek) {
+        const int k = p.col_idx[ek];
+        if (k >= i) break;
+        if (p.part[k] != pi) continue;
+        // L_ik = A_ik * U_kk^{-1}
+        S lik[B * B], tmp[B * B];
+        load_block<B>(vals + (size_t)ek * B * B, lik);
+        const S* uinv = diag_inv + (size_t)k * B * B;
+#pragma unroll
+        for (int r = 0; r < B; ++r)
+#pragma unroll
+            for (int c = 0; c < B; ++c) {
+                S acc = zero<S>();
+#pragma unroll
+                for (int m = 0; m < B; ++m) acc += lik[r * B + m] * uinv[m * B + c];
+                tmp[r * B + c] = acc;
+            }
+        store_block<B>(vals + (size_t)ek * B * B, tmp);
+        // A_ij -= L_ik U_kj for j > k present in both rows (zero-skip, dense.hpp:47)
+        for (int ej = rb; ej < re; ++ej) {
+            const int j = p.col_idx[ej];
+            if (j <= k) continue;
+            if (p.part[j] != pi) continue;
+            const int ekj = find_entry(p, k, j);
+            if (ekj < 0) continue;
+            if (p.part[k] != p.part[j]) continue;
+            const S* u = vals + (size_t)ekj * B * B;
+            S* cblk = vals + (size_t)ej * B * B;
+            S cc[B * B];
+            load_block<B>(cblk, cc);
+#pragma unroll
+            for (int r = 0; r < B; ++r)
+#pragma unroll
+                for (int kk = 0; kk < B; ++kk) {
+                    const S a = tmp[r * B + kk];
+                    if (is_zero(a)) continue;
+#pragma unroll
+                    for (int c = 0; c < B; ++c) cc[r * B + c] -= a * u[kk * B + c];
+                }
+            store_block<B>(cblk, cc);
+        }
+    }
+    // pivot block: partial-pivot LU, condition check, explicit inverse
+    S lu[B * B];
+    int piv[B];
+    load_block<B>(vals + (size_t)p.diag_idx[i] * B * B, lu);
+    double cond = 0.0;
+    const int sing = lu_factor_reg<B>(lu, piv, cond);
+    if (sing || !(cond < 1e14)) atomicMin(status + 1, i);
+    store_block<B>(diag_lu + (size_t)i * B * B, lu);
+#pragma unroll
+    for (int k = 0; k < B; ++k) diag_piv[(size_t)i * B + k] = piv[k];
+    S* inv = diag_inv + (size_t)i * B * B;
+#pragma unroll
+    for (int c = 0; c < B; ++c) {
+        S col[B];
+#pragma unroll
+        for (int r = 0; r < B; ++r) col[r] = (r == c) ? one<S>() : zero<S>();
+        lu_solve_reg<B>(lu, piv, col);
+#pragma unroll
+        for (int r = 0; r < B; ++r) inv[r * B + c] = col[r];
+    }
+}
+
+// Ilu::apply forward substitution (sparse.cpp:267-278) for one level
+template <int B, class S>
+__global__ void __launch_bounds__(kThreads) k_ilu_fwd(PatDev p, const int* __restrict__ rows, int nrows,
+                                                      const S* __restrict__ vals, const S* __restrict__ rhs,
+                                                      S* x) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nrows) return;
+    const int i = rows[t];
+    const int pi = p.part[i];
+    S xi[B];
+    load_vec<B>(rhs + (size_t)i * B, xi);
+    for (int e = p.row_ptr[i]; e < p.row_ptr[i + 1]; ++e) {
+        const int k = p.col_idx[e];
+        if (k >= i) break;
+        if (p.part[k] != pi) continue;
+        const S* blk = vals + (size_t)e * B * B;
+        const S* xk = x + (size_t)k * B;
+        S xkv[B];
+        load_vec<B>(xk, xkv);
+#pragma unroll
+        for (int r = 0; r < B; ++r) {  // block_matvec_sub (dense.hpp:31-39)
+            S acc = zero<S>();
+#pragma unroll
+            for (int c = 0; c < B; ++c) acc += blk[r * B + c] * xkv[c];
+            xi[r] -= acc;
+        }
+    }
+    store_vec<B>(x + (size_t)i * B, xi);
+}
+
+// Ilu::apply backward substitution + pivot solve (sparse.cpp:279-290) for one level;
+// optionally x_accum += x (the smoothed_solve update x += z, sparse.hpp:317)
+template <int B, class S>
+__global__ void __launch_bounds__(kThreads) k_ilu_bwd(PatDev p, const int* __restrict__ rows, int nrows,
+                                                      const S* __restrict__ vals, const S* __restrict__ diag_lu,
+                                                      const int* __restrict__ diag_piv, S* x, S* x_accum) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nrows) return;
+    const int i = rows[t];
+    const int pi = p.part[i];
+    S xi[B];
+    load_vec<B>(x + (size_t)i * B, xi);
+    for (int e = p.row_ptr[i + 1] - 1; e >= p.row_ptr[i]; --e) {
+        const int j = p.col_idx[e];
+        if (j <= i) break;
+        if (p.part[j] != pi) continue;
+        const S* blk = vals + (size_t)e * B * B;
+        S xjv[B];
+        load_vec<B>(x + (size_t)j * B, xjv);
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+            S acc = zero<S>();
+#pragma unroll
+            for (int c = 0; c < B; ++c) acc += blk[r * B + c] * xjv[c];
+            xi[r] -= acc;
+        }
+    }
+    S lu[B * B];
+    int piv[B];
+    load_block<B>(diag_lu + (size_t)i * B * B, lu);
+#pragma unroll
+    for (int k = 0; k < B; ++k) piv[k] = diag_piv[(size_t)i * B + k];
+    lu_solve_reg<B>(lu, piv, xi);
+    store_vec<B>(x + (size_t)i * B, xi);
+    if (x_accum) {
+        S* xa = x_accum + (size_t)i * B;
+#pragma unroll
+        for (int k = 0; k < B; ++k) xa[k] += xi[k];
+    }
+}
+
+// y_i = sum_e A_e x_col(e) (Bsr::matvec, sparse.hpp:259-270); with rhs: r = rhs - y
+// (sparse.hpp:319) and per-block partial sums of |r|^2
+template <int B, class S>
+__global__ void __launch_bounds__(kThreads) k_matvec(PatDev p, SystemView<S> A, const S* __restrict__ x,
+                                                     const S* __restrict__ rhs, S* __restrict__ out,
+                                                     double* __restrict__ partials) {
+    __shared__ double red[kThreads / 32];
+    double local = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.rows; i += gridDim.x * blockDim.x) {
+        S y[B];
+#pragma unroll
+        for (int r = 0; r < B; ++r) y[r] = zero<S>();
+        const int di = p.diag_idx[i];
+        for (int e = p.row_ptr[i]; e < p.row_ptr[i + 1]; ++e) {
+            S xc[B];
+            load_vec<B>(x + (size_t)p.col_idx[e] * B, xc);
+            const bool diag = e == di;
+            if (A.vals) {
+                const S* blk = A.vals + (size_t)e * B * B;
+#pragma unroll
+                for (int r = 0; r < B; ++r) {
+                    S acc = zero<S>();
+#pragma unroll
+                    for (int c = 0; c < B; ++c) acc += blk[r * B + c] * xc[c];
+                    y[r] += acc;
+                }
+            } else {
+                const double* blk = A.real_vals + (size_t)e * B * B;
+#pragma unroll
+                for (int r = 0; r < B; ++r) {
+                    S acc = zero<S>();
+#pragma unroll
+                    for (int c = 0; c < B; ++c) {
+                        if constexpr (sizeof(S) == sizeof(cplx)) {
+                            if (diag && r == c && A.shift_im)
+                                acc += mk(blk[r * B + c] + 0.0, 0.0 + A.shift_im[i]) * xc[c];
+                            else
+                                acc += rmul(blk[r * B + c], xc[c]);
+                        } else {
+                            acc += rmul(blk[r * B + c], xc[c]);
+                        }
+                    }
+                    y[r] += acc;
+                }
+            }
+        }
+        S* o = out + (size_t)i * B;
+        if (rhs) {
+            const S* b = rhs + (size_t)i * B;
+#pragma unroll
+            for (int r = 0; r < B; ++r) {
+                const S v = b[r] - y[r];
+                o[r] = v;
+                local += sq(v);
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < B; ++r) o[r] = y[r];
+        }
+    }
+    if (partials) {
+        for (int off = 16; off > 0; off >>= 1) local += __shfl_down_sync(0xffffffffu, local, off);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = local;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+            for (int w = 0; w < kThreads / 32; ++w) s += red[w];
+            partials[blockIdx.x] = s;
+        }
+    }
+}
+
+template <class S>
+__global__ void k_sumsq(const S* __restrict__ x, std::size_t len, double* __restrict__ partials) {
+    __shared__ double red[kThreads / 32];
+    double local = 0.0;
+    for (std::size_t k = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; k < len;
+         k += (std::size_t)gridDim.x * blockDim.x)
+        local += sq(x[k]);
+    for (int off = 16; off > 0; off >>= 1) local += __shfl_down_sync(0xffffffffu, local, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = local;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kThreads / 32; ++w) s += red[w];
+        partials[blockIdx.x] = s;
+    }
+}
+
+// fixed-order final reduction of the per-block partials (deterministic run to run)
+__global__ void k_finish(const double* __restrict__ partials, int n, double* __restrict__ out) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) s += partials[k];
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        *out = t;
+    }
+}
+
+template <class S>
+__global__ void k_axpy_copy(S* __restrict__ dst, const S* __restrict__ src, std::size_t len) {
+    for (std::size_t k = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; k < len;
+         k += (std::size_t)gridDim.x * blockDim.x)
+        dst[k] = src[k];
+}
+
+template <int B, class S>
+__global__ void k_block_diag_solve(int n, const S* __restrict__ lu, const int* __restrict__ piv,
+                                   const S* __restrict__ rhs, S* __restrict__ x) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    S L[B * B], v[B];
+    int pv[B];
+    load_block<B>(lu + (size_t)i * B * B, L);
+#pragma unroll
+    for (int k = 0; k < B; ++k) pv[k] = piv[(size_t)i * B + k];
+    load_vec<B>(rhs + (size_t)i * B, v);
+    lu_solve_reg<B>(L, pv, v);
+    store_vec<B>(x + (size_t)i * B, v);
+}
+
+template <int B, class S>
+__global__ void k_block_diag_factor(int n, S* __restrict__ blocks, int* __restrict__ piv, int* __restrict__ status) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    S L[B * B];
+    int pv[B];
+    load_block<B>(blocks + (size_t)i * B * B, L);
+    double cond;
+    if (lu_factor_reg<B>(L, pv, cond)) atomicMin(status + 1, i);
+    store_block<B>(blocks + (size_t)i * B * B, L);
+#pragma unroll
+    for (int k = 0; k < B; ++k) piv[(size_t)i * B + k] = pv[k];
+}
+
+#define FNLH_DISPATCH_B(b, ...)                                              \
+    switch (b) {                                                             \
+        case 1: { constexpr int B = 1; __VA_ARGS__; } break;                 \
+        case 3: { constexpr int B = 3; __VA_ARGS__; } break;                 \
+        case 5: { constexpr int B = 5; __VA_ARGS__; } break;                 \
+        case 6: { constexpr int B = 6; __VA_ARGS__; } break;                 \
+        default: throw ShapeError("unsupported block size " + std::to_string(b)); \
+    }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// DevicePattern
+// ---------------------------------------------------------------------------
+DevicePattern::DevicePattern(int b_, int rows_, const int* row_ptr_, const int* col_idx_, const int* partition)
+    : b(b_), rows(rows_) {
+    nnzb = row_ptr_[rows];
+    h_row_ptr.assign(row_ptr_, row_ptr_ + rows + 1);
+    h_col_idx.assign(col_idx_, col_idx_ + nnzb);
+    h_part.assign(rows, 0);
+    if (partition) h_part.assign(partition, partition + rows);
+    h_diag_idx.assign(rows, -1);
+    for (int i = 0; i < rows; ++i) {
+        max_deg = std::max(max_deg, h_row_ptr[i + 1] - h_row_ptr[i]);
+        for (int e = h_row_ptr[i]; e < h_row_ptr[i + 1]; ++e) {
+            if (e > h_row_ptr[i] && h_col_idx[e] <= h_col_idx[e - 1])
+                throw ShapeError("pattern: columns must ascend in row " + std::to_string(i));
+            if (h_col_idx[e] == i) h_diag_idx[i] = e;
+        }
+        if (h_diag_idx[i] < 0) throw ShapeError("pattern: missing diagonal entry in row " + std::to_string(i));
+        if (h_part[i] != h_part[0]) single_partition = false;
+    }
+    // structural symmetry (BlockSparsityPattern::validate, sparse.cpp:50-59)
+    for (int i = 0; i < rows; ++i)
+        for (int e = h_row_ptr[i]; e < h_row_ptr[i + 1]; ++e) {
+            const int j = h_col_idx[e];
+            if (!std::binary_search(h_col_idx.begin() + h_row_ptr[j], h_col_idx.begin() + h_row_ptr[j + 1], i))
+                throw ShapeError("pattern: structurally unsymmetric at (" + std::to_string(i) + "," +
+                                 std::to_string(j) + ")");
+        }
+    // level schedules
+    std::vector<int> lf(rows, 0), lb(rows, 0);
+    int nf = 0, nb = 0;
+    for (int i = 0; i < rows; ++i) {
+        int l = 0;
+        for (int e = h_row_ptr[i]; e < h_row_ptr[i + 1]; ++e) {
+            const int k = h_col_idx[e];
+            if (k >= i) break;
+            if (h_part[k] == h_part[i]) l = std::max(l, lf[k] + 1);
+        }
+        lf[i] = l;
+        nf = std::max(nf, l + 1);
+    }
+    for (int i = rows - 1; i >= 0; --i) {
+        int l = 0;
+        for (int e = h_row_ptr[i + 1] - 1; e >= h_row_ptr[i]; --e) {
+            const int j = h_col_idx[e];
+            if (j <= i) break;
+            if (h_part[j] == h_part[i]) l = std::max(l, lb[j] + 1);
+        }
+        lb[i] = l;
+        nb = std::max(nb, l + 1);
+    }
+    auto group = [&](const std::vector<int>& lev, int nl, std::vector<int>& ptr) {
+        ptr.assign(nl + 1, 0);
+        for (int i = 0; i < rows; ++i) ptr[lev[i] + 1]++;
+        for (int l = 0; l < nl; ++l) ptr[l + 1] += ptr[l];
+        std::vector<int> fill(ptr.begin(), ptr.end() - 1), out(rows);
+        for (int i = 0; i < rows; ++i) out[fill[lev[i]]++] = i;
+        return out;
+    };
+    std::vector<int> fr = group(lf, nf, fwd_ptr), br = group(lb, nb, bwd_ptr);
+    auto up = [](int** d, const std::vector<int>& h) {
+        FNLH_CUDA(cudaMalloc(d, std::max<std::size_t>(h.size(), 1) * sizeof(int)));
+        if (!h.empty()) FNLH_CUDA(cudaMemcpy(*d, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice));
+    };
+    up(&row_ptr, h_row_ptr);
+    up(&col_idx, h_col_idx);
+    up(&diag_idx, h_diag_idx);
+    up(&part, h_part);
+    up(&fwd_rows, fr);
+    up(&bwd_rows, br);
+}
+
+DevicePattern::~DevicePattern() {
+    cudaFree(row_ptr);
+    cudaFree(col_idx);
+    cudaFree(diag_idx);
+    cudaFree(part);
+    cudaFree(fwd_rows);
+    cudaFree(bwd_rows);
+}
+
+template <class S>
+DeviceIlu<S>::DeviceIlu(const DevicePattern* pat) : p(pat) {
+    const std::size_t bb = (std::size_t)p->b * p->b;
+    FNLH_CUDA(cudaMalloc(&vals, (std::size_t)p->nnzb * bb * sizeof(S)));
+    FNLH_CUDA(cudaMalloc(&diag_lu, (std::size_t)p->rows * bb * sizeof(S)));
+    FNLH_CUDA(cudaMalloc(&diag_piv, (std::size_t)p->rows * p->b * sizeof(int)));
+    FNLH_CUDA(cudaMalloc(&diag_inv, (std::size_t)p->rows * bb * sizeof(S)));
+}
+
+template <class S>
+DeviceIlu<S>::~DeviceIlu() {
+    cudaFree(vals);
+    cudaFree(diag_lu);
+    cudaFree(diag_piv);
+    cudaFree(diag_inv);
+}
+
+template <class S>
+std::size_t DeviceIlu<S>::bytes() const {
+    const std::size_t bb = (std::size_t)p->b * p->b;
+    return ((std::size_t)p->nnzb * bb + 2 * (std::size_t)p->rows * bb) * sizeof(S) +
+           (std::size_t)p->rows * p->b * sizeof(int);
+}
+
+Workspace::Workspace(std::size_t max_len) : vec_len(max_len) {
+    FNLH_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    n_partials = 4096;
+    FNLH_CUDA(cudaMalloc(&partials, n_partials * sizeof(double)));
+    FNLH_CUDA(cudaMalloc(&scalars, 64 * sizeof(double)));
+    FNLH_CUDA(cudaMallocHost(&h_scalars, 64 * sizeof(double)));
+    FNLH_CUDA(cudaMalloc(&status, 8 * sizeof(int)));
+    FNLH_CUDA(cudaMallocHost(&h_status, 8 * sizeof(int)));
+    for (auto& v : vec) FNLH_CUDA(cudaMalloc(&v, std::max<std::size_t>(max_len, 1) * sizeof(cplx)));
+}
+
+Workspace::~Workspace() {
+    for (auto& v : vec) cudaFree(v);
+    cudaFree(partials);
+    cudaFree(scalars);
+    cudaFreeHost(h_scalars);
+    cudaFree(status);
+    cudaFreeHost(h_status);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+// ---------------------------------------------------------------------------
+// operations
+// ---------------------------------------------------------------------------
+template <class S>
+void ilu_factorize(const SystemView<S>& A, DeviceIlu<S>& f, Workspace& ws) {
+    const DevicePattern& p = *f.p;
+    const PatDev pd = dev(p);
+    const int init[2] = {0, 0x7fffffff};
+    FNLH_CUDA(cudaMemcpyAsync(ws.status, init, sizeof init, cudaMemcpyHostToDevice, ws.stream));
+    FNLH_DISPATCH_B(p.b, {
+        k_ilu_copy<B, S><<<nblocks(p.rows), kThreads, 0, ws.stream>>>(pd, A, f.vals);
+        for (int l = 0; l < p.fwd_levels(); ++l) {
+            const int n = p.fwd_ptr[l + 1] - p.fwd_ptr[l];
+            k_ilu_factor<B, S><<<nblocks(n), kThreads, 0, ws.stream>>>(pd, p.fwd_rows + p.fwd_ptr[l], n, f.vals,
+                                                                       f.diag_lu, f.diag_piv, f.diag_inv,
+                                                                       ws.status);
+        }
+    });
+    FNLH_CUDA(cudaGetLastError());
+    FNLH_CUDA(cudaMemcpyAsync(ws.h_status, ws.status, 2 * sizeof(int), cudaMemcpyDeviceToHost, ws.stream));
+    FNLH_CUDA(cudaStreamSynchronize(ws.stream));
+    if (ws.h_status[1] != 0x7fffffff)
+        throw FactorizationError("near-singular ILU pivot block", ws.h_status[1]);
+}
+
+template <class S>
+void ilu_apply(const DeviceIlu<S>& f, const S* rhs, S* x, Workspace& ws, S* x_accum) {
+    const DevicePattern& p = *f.p;
+    const PatDev pd = dev(p);
+    FNLH_DISPATCH_B(p.b, {
+        for (int l = 0; l < p.fwd_levels(); ++l) {
+            const int n = p.fwd_ptr[l + 1] - p.fwd_ptr[l];
+            k_ilu_fwd<B, S><<<nblocks(n), kThreads, 0, ws.stream>>>(pd, p.fwd_rows + p.fwd_ptr[l], n, f.vals, rhs, x);
+        }
+        for (int l = 0; l < p.bwd_levels(); ++l) {
+            const int n = p.bwd_ptr[l + 1] - p.bwd_ptr[l];
+            k_ilu_bwd<B, S><<<nblocks(n), kThreads, 0, ws.stream>>>(pd, p.bwd_rows + p.bwd_ptr[l], n, f.vals,
+                                                                    f.diag_lu, f.diag_piv, x, x_accum);
+        }
+    });
+    FNLH_CUDA(cudaGetLastError());
+}
+
+template <class S>
+void residual_norm(const SystemView<S>& A, const S* rhs, const S* x, S* r, double* d_norm2, Workspace& ws) {
+    const DevicePattern& p = *A.p;
+    const int grid = std::min(nblocks(p.rows), kRedBlocks);
+    FNLH_DISPATCH_B(p.b, {
+        k_matvec<B, S><<<grid, kThreads, 0, ws.stream>>>(dev(p), A, x, rhs, r, ws.partials);
+    });
+    k_finish<<<1, 256, 0, ws.stream>>>(ws.partials, grid, d_norm2);
+    FNLH_CUDA(cudaGetLastError());
+}
+
+template <class S>
+void matvec(const SystemView<S>& A, const S* x, S* y, Workspace& ws) {
+    const DevicePattern& p = *A.p;
+    const int grid = std::min(nblocks(p.rows), kRedBlocks);
+    FNLH_DISPATCH_B(p.b, {
+        k_matvec<B, S><<<grid, kThreads, 0, ws.stream>>>(dev(p), A, x, nullptr, y, nullptr);
+    });
+    FNLH_CUDA(cudaGetLastError());
+}
+
+template <class S>
+void norm2_sq(const S* x, std::size_t len, double* d_out, Workspace& ws) {
+    const int grid = std::min<long long>(nblocks((long long)len), kRedBlocks);
+    k_sumsq<S><<<grid, kThreads, 0, ws.stream>>>(x, len, ws.partials);
+    k_finish<<<1, 256, 0, ws.stream>>>(ws.partials, grid, d_out);
+    FNLH_CUDA(cudaGetLastError());
+}
+
+// smoothed_solve (sparse.hpp:295-331): x0 = 0, z = M^{-1} r, x += z, r = b - A x, ||r||
+template <class S>
+LinearSolveReport smoothed_solve(const SystemView<S>& A, const S* rhs, const DeviceIlu<S>& f, double tol_rel,
+                                 int max_iter, S* x, Workspace& ws) {
+    if (!(tol_rel > 0.0 && tol_rel < 1.0)) throw ConfigError("smoothed_solve: tol_rel must be in (0,1)");
+    if (max_iter < 1) throw ConfigError("smoothed_solve: max_iter must be >= 1");
+    const DevicePattern& p = *A.p;
+    const std::size_t len = (std::size_t)p.rows * p.b;
+    S* r = static_cast<S*>(ws.vec[0]);
+    S* z = static_cast<S*>(ws.vec[1]);
+    FNLH_CUDA(cudaMemsetAsync(x, 0, len * sizeof(S), ws.stream));
+    LinearSolveReport rep;
+    norm2_sq(rhs, len, ws.scalars, ws);
+    FNLH_CUDA(cudaMemcpyAsync(ws.h_scalars, ws.scalars, sizeof(double), cudaMemcpyDeviceToHost, ws.stream));
+    FNLH_CUDA(cudaStreamSynchronize(ws.stream));
+    rep.initial_residual = std::sqrt(ws.h_scalars[0]);
+    rep.final_residual = rep.initial_residual;
+    if (rep.initial_residual == 0.0) {
+        rep.converged = 1;
+        return rep;
+    }
+    const double target = tol_rel * rep.initial_residual;
+    FNLH_CUDA(cudaMemcpyAsync(r, rhs, len * sizeof(S), cudaMemcpyDeviceToDevice, ws.stream));
+    for (int it = 1; it <= max_iter; ++it) {
+        ilu_apply(f, r, z, ws, x);  // z = M^{-1} r; x += z fused into the backward sweep
+        residual_norm(A, rhs, x, r, ws.scalars + 1, ws);
+        FNLH_CUDA(cudaMemcpyAsync(ws.h_scalars + 1, ws.scalars + 1, sizeof(double), cudaMemcpyDeviceToHost,
+                                  ws.stream));
+        FNLH_CUDA(cudaStreamSynchronize(ws.stream));
+        rep.iterations = it;
+        rep.final_residual = std::sqrt(ws.h_scalars[1]);
+        if (!std::isfinite(rep.final_residual)) throw DivergenceError("non-finite iterate in smoothed_solve", it, "linear");
+        if (rep.final_residual <= target) {
+            rep.converged = 1;
+            break;
+        }
+    }
+    return rep;
+}
+
+template <class S>
+void block_diag_solve(int b, int n, const S* lu, const int* piv, const S* rhs, S* x, cudaStream_t st) {
+    FNLH_DISPATCH_B(b, { k_block_diag_solve<B, S><<<nblocks(n), kThreads, 0, st>>>(n, lu, piv, rhs, x); });
+    FNLH_CUDA(cudaGetLastError());
+}
+
+template <class S>
+void block_diag_factor(int b, int n, S* blocks, int* piv, int* status, cudaStream_t st) {
+    FNLH_DISPATCH_B(b, { k_block_diag_factor<B, S><<<nblocks(n), kThreads, 0, st>>>(n, blocks, piv, status); });
+    FNLH_CUDA(cudaGetLastError());
+}
+
+#define FNLH_INST(S)                                                                                       \
+    template struct DeviceIlu<S>;                                                                          \
+    template void ilu_factorize<S>(const SystemView<S>&, DeviceIlu<S>&, Workspace&);                       \
+    template void ilu_apply<S>(const DeviceIlu<S>&, const S*, S*, Workspace&, S*);                         \
+    template void residual_norm<S>(const SystemView<S>&, const S*, const S*, S*, double*, Workspace&);     \
+    template void matvec<S>(const SystemView<S>&, const S*, S*, Workspace&);                               \
+    template void norm2_sq<S>(const S*, std::size_t, double*, Workspace&);                                 \
+    template LinearSolveReport smoothed_solve<S>(const SystemView<S>&, const S*, const DeviceIlu<S>&,      \
+                                                 double, int, S*, Workspace&);                             \
+    template void block_diag_solve<S>(int, int, const S*, const int*, const S*, S*, cudaStream_t);         \
+    template void block_diag_factor<S>(int, int, S*, int*, int*, cudaStream_t);
+
+FNLH_INST(double)
+FNLH_INST(cplx)
+
+}  // namespace fnlh

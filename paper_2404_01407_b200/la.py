@@ -1,0 +1,110 @@
+"""Python mirror of the reference's block-sparse LA operators (sparse.hpp), backed by
+the device kernels through the C ABI.  Argument meaning and error behaviour follow
+the reference: ``FnlhError`` carries ConfigError / FactorizationError(node) /
+DivergenceError(stage) exactly where the reference throws them."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import LinearReport, as_pairs, check, f64, lib, ptr
+
+_i, _d = C.c_int, C.c_double
+
+
+class Pattern:
+    """BlockSparsityPattern (sparse.hpp:106-121) resident on the device."""
+
+    def __init__(self, b, row_ptr, col_idx, partition=None):
+        self.b = int(b)
+        self.row_ptr = np.ascontiguousarray(row_ptr, np.int32)
+        self.col_idx = np.ascontiguousarray(col_idx, np.int32)
+        self.partition = None if partition is None else np.ascontiguousarray(partition, np.int32)
+        self.rows = len(self.row_ptr) - 1
+        self.nnzb = len(self.col_idx)
+        h = C.c_void_p()
+        check(lib().fnlh_pattern_create(_i(self.b), _i(self.rows), ptr(self.row_ptr), ptr(self.col_idx),
+                                        ptr(self.partition), C.byref(h)))
+        self.h = h
+
+    @classmethod
+    def from_dict(cls, pat):
+        return cls(pat["b"], pat["row_ptr"], pat["col_idx"], pat.get("partition"))
+
+    def levels(self):
+        f, b = _i(), _i()
+        lib().fnlh_pattern_levels(self.h, C.byref(f), C.byref(b))
+        return f.value, b.value
+
+    def __del__(self):
+        try:
+            lib().fnlh_pattern_destroy(self.h)
+        except Exception:
+            pass
+
+
+def _system(A, shift_im):
+    """-> (is_complex, A buffer, A_complex flag, shift buffer)"""
+    if np.iscomplexobj(A):
+        return 1, as_pairs(A), 1, None
+    if shift_im is not None:
+        return 1, f64(A), 0, f64(shift_im)
+    return 0, f64(A), 0, None
+
+
+def ilu_factorize(pat: Pattern, A, shift_im=None):
+    """Ilu<S>::factorize (sparse.cpp:187-257); A complex, or real A5 (+ per-node i*shift)."""
+    cplx, Ab, Ac, sh = _system(A, shift_im)
+    dt = np.complex128 if cplx else np.float64
+    b, n = pat.b, pat.rows
+    vals = np.zeros(pat.nnzb * b * b, dt)
+    dlu = np.zeros(n * b * b, dt)
+    piv = np.zeros(n * b, np.int32)
+    dinv = np.zeros(n * b * b, dt)
+    v = (lambda a: a.view(np.float64)) if cplx else (lambda a: a)
+    check(lib().fnlh_ilu_factorize(pat.h, _i(cplx), ptr(Ab), _i(Ac), ptr(sh), ptr(v(vals)), ptr(v(dlu)), ptr(piv),
+                                   ptr(v(dinv))))
+    return dict(vals=vals, diag_lu=dlu, diag_piv=piv, diag_inv=dinv)
+
+
+def ilu_apply(pat: Pattern, A, rhs, shift_im=None):
+    cplx, Ab, Ac, sh = _system(A, shift_im)
+    if cplx:
+        r = as_pairs(rhs)
+        x = np.zeros(pat.rows * pat.b, np.complex128)
+        check(lib().fnlh_ilu_apply(pat.h, _i(1), ptr(Ab), _i(Ac), ptr(sh), ptr(r), ptr(x.view(np.float64))))
+    else:
+        r = f64(rhs)
+        x = np.zeros(pat.rows * pat.b)
+        check(lib().fnlh_ilu_apply(pat.h, _i(0), ptr(Ab), _i(0), None, ptr(r), ptr(x)))
+    return x
+
+
+def matvec(pat: Pattern, A, x, shift_im=None):
+    cplx, Ab, Ac, sh = _system(A, shift_im)
+    if cplx or np.iscomplexobj(x):
+        if not cplx:
+            cplx, Ab, Ac = 1, f64(A), 0
+        xv = as_pairs(x)
+        y = np.zeros(pat.rows * pat.b, np.complex128)
+        check(lib().fnlh_matvec(pat.h, _i(1), ptr(Ab), _i(Ac), ptr(sh), ptr(xv), ptr(y.view(np.float64))))
+    else:
+        y = np.zeros(pat.rows * pat.b)
+        check(lib().fnlh_matvec(pat.h, _i(0), ptr(Ab), _i(0), None, ptr(f64(x)), ptr(y)))
+    return y
+
+
+def smoothed_solve(pat: Pattern, A, rhs, tol_rel, max_iter, shift_im=None):
+    """factorize + smoothed_solve (sparse.hpp:295-331) -> (x, (iterations, r0, r1, converged))"""
+    cplx, Ab, Ac, sh = _system(A, shift_im)
+    rep = LinearReport()
+    if cplx:
+        x = np.zeros(pat.rows * pat.b, np.complex128)
+        check(lib().fnlh_smoothed_solve(pat.h, _i(1), ptr(Ab), _i(Ac), ptr(sh), ptr(as_pairs(rhs)), _d(tol_rel),
+                                        _i(max_iter), ptr(x.view(np.float64)), C.byref(rep)))
+    else:
+        x = np.zeros(pat.rows * pat.b)
+        check(lib().fnlh_smoothed_solve(pat.h, _i(0), ptr(Ab), _i(0), None, ptr(f64(rhs)), _d(tol_rel), _i(max_iter),
+                                        ptr(x), C.byref(rep)))
+    return x, rep.as_tuple()
