@@ -79,6 +79,75 @@ int fnlh_smoothed_solve(const fnlh_pattern* p, int is_complex, const double* A, 
                         const double* shift_im, const double* rhs, double tol_rel, int max_iter, double* x,
                         fnlh_linear_report* rep);
 
+/* ---- L2/L3: the 3D edge-based discretization ---------------------------------
+   Node-centred median-dual mesh (paper_2404_01407_b200/mesh.py builds one):
+   faces a->b with area-weighted normals fn (outward on inlet/outlet faces), slip
+   walls via the per-node closure source -p*closure_i.  b = 5 (Euler) or 6 (Euler +
+   SA-like scalar).  Replaces Discretization (disc.hpp:42-106) for the BASELINE 3D
+   configurations; on a line mesh it is the reference nozzle (disc_euler.cpp). */
+typedef struct {
+    int n, nf, b;
+    const int *fa, *fb, *fbc, *ford;      /* nf each; fb = -1 and fbc in {0 inlet, 1 outlet} on boundary faces */
+    const double *fn, *farea, *fnh;       /* 3*nf, nf, 3*nf */
+    const double *fvis, *vol, *closure;   /* nf, n, 3*n */
+    const double* mu;                     /* n (b = 6 eddy viscosity) */
+    const int *nf_ptr, *nf_idx, *bflag;   /* node->face CSR ascending (mesh.cpp:44-59), n */
+    double gamma, gas_constant, p0, T0, p_out, nt_in, forcing_scale;
+} fnlh_mesh_desc;
+
+int fnlh_disc_create(const fnlh_mesh_desc* m, const int* row_ptr, const int* col_idx, const int* partition,
+                     fnlh_disc** out);
+void fnlh_disc_destroy(fnlh_disc* d);
+/* Discretization::residual (disc_euler.cpp:56-85): mode 0 Steady, 1 Perturbation (wref = reference) */
+int fnlh_disc_residual(fnlh_disc* d, const double* W, const double* wref, int order, int mode, const double* forcing,
+                       int nforcing, int need_vis, double* inv, double* vis);
+/* Discretization::assemble_jacobian / assemble_diag_blocks (disc.cpp:25-130); J or P may be NULL */
+int fnlh_disc_fd_jacobian(fnlh_disc* d, const double* W, double* J, double* P);
+/* linearized_residual (residual_ops.cpp:63-102); complex arrays as (re,im) pairs */
+int fnlh_disc_linearized_residual(fnlh_disc* d, const double* mean, const double* what, double omega,
+                                  const double* forcing, int nforcing, int order, int need_vis, double* inv,
+                                  double* vis);
+/* deterministic_flux (residual_ops.cpp:113-161); amps nh*n*b complex */
+int fnlh_disc_deterministic_flux(fnlh_disc* d, const double* mean, int nh, const double* omega, const double* amps,
+                                 double* df);
+
+/* ---- L4/L5: the outer FNLH iteration (driver.hpp:83-126) ------------------- */
+typedef struct { /* SchemeConfig (driver.hpp:22-42) */
+    int implicit;
+    double sigma_cfl;
+    double eps_relax;
+    double linear_tol;
+    int linear_max_iter;
+    double target_drop_orders;
+    int max_outer_iters;
+} fnlh_scheme;
+
+typedef struct { /* ConvergenceEntry (driver.hpp:50-58); resid_h returned separately */
+    int iter;
+    double resid_mean;
+    double rz;
+    int has_rz;
+    double seconds; /* cumulative device time */
+} fnlh_entry;
+
+int fnlh_solver_create(const fnlh_mesh_desc* m, const int* row_ptr, const int* col_idx, const int* partition,
+                       const fnlh_scheme* s, int nh, const int* index, const double* omega, const double* forcing,
+                       int nforcing, const double* mean0, fnlh_solver** out);
+void fnlh_solver_destroy(fnlh_solver* s);
+/* FnlhSolver::outer_iteration (driver.cpp:157-333) */
+int fnlh_solver_outer_iteration(fnlh_solver* s, fnlh_entry* e, double* resid_h);
+/* FnlhSolver::run_to_convergence (driver.cpp:335-379): *reason 0 target-drop, 1 cap, 2 divergence */
+int fnlh_solver_run(fnlh_solver* s, int* reason, int* n_entries, fnlh_entry* entries, int max_entries);
+int fnlh_solver_get_state(const fnlh_solver* s, double* mean, double* amps);
+int fnlh_solver_set_state(fnlh_solver* s, const double* mean, const double* amps);
+int fnlh_solver_get_df(const fnlh_solver* s, double* df);
+int fnlh_solver_num_reports(const fnlh_solver* s);
+int fnlh_solver_get_reports(const fnlh_solver* s, fnlh_linear_report* out);
+/* LHS value bytes (A5 + real ILU + one complex ILU workspace): independent of nh */
+double fnlh_solver_lhs_bytes(const fnlh_solver* s);
+/* counters: [sweeps, block-row updates, last outer iteration device ms] */
+int fnlh_solver_counters(const fnlh_solver* s, double* out);
+
 #ifdef __cplusplus
 }
 #endif

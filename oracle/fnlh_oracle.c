@@ -4,6 +4,7 @@
  * Build: gcc -std=gnu11 -O2 -ffp-contract=off -fPIC -shared (no -march), see oracle/Makefile.
  */
 #include "fnlh_oracle.h"
+#include "cr_pow.h"
 
 #include <math.h>
 #include <stdio.h>
@@ -11,6 +12,11 @@
 #include <string.h>
 
 static or_error g_err;
+static int g_cr_pow = 0; /* 0: glibc pow (reference), 1: correctly rounded (device) */
+
+void or_set_pow_mode(int cr) { g_cr_pow = cr; }
+double or_cr_pow(double x, double y) { return cr_pow(x, y); }
+static inline double bc_pow(double x, double y) { return g_cr_pow ? cr_pow(x, y) : pow(x, y); }
 
 const or_error* or_last_error(void) { return &g_err; }
 
@@ -227,7 +233,7 @@ static int steady_inlet(const or_mesh* m, const double* wint, const double* nh, 
     if (!(cb > 0.0)) return or_fail(OR_STATE, -1, -1, "inlet boundary state has nonpositive sound speed");
     if (fabs(ub) >= cb) return or_fail(OR_UNSUPPORTED, -1, -1, "supersonic inlet boundary state");
     const double tb = cb * cb / (g * R);
-    const double pb = m->p0 * pow(tb / m->T0, g / (g - 1.0));
+    const double pb = m->p0 * bc_pow(tb / m->T0, g / (g - 1.0));
     s->w[0] = pb / (R * tb);
     s->w[1] = ub * -nh[0];
     s->w[2] = ub * -nh[1];
@@ -242,7 +248,7 @@ static int steady_inlet(const or_mesh* m, const double* wint, const double* nh, 
 static int steady_outlet(const or_mesh* m, const double* wint, const double* nh, bstate* s) {
     const double g = m->gamma;
     const double pb = m->p_out;
-    const double rhob = wint[0] * pow(pb / wint[4], 1.0 / g);
+    const double rhob = wint[0] * bc_pow(pb / wint[4], 1.0 / g);
     const double cb = sqrt(g * pb / rhob);
     const double c_int = sqrt(g * wint[4] / wint[0]);
     const double un = wint[1] * nh[0] + wint[2] * nh[1] + wint[3] * nh[2];

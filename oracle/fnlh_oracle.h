@@ -48,6 +48,9 @@ typedef struct {
 } or_error;
 
 const or_error* or_last_error(void);
+/* boundary-state pow: 0 glibc (the reference's libm, default), 1 correctly rounded (the device's) */
+void or_set_pow_mode(int cr);
+double or_cr_pow(double x, double y);
 
 /* BlockSparsityPattern (sparse.hpp:106-121) */
 typedef struct {

@@ -86,15 +86,22 @@ class OrError(C.Structure):
 class Oracle:
     """The plain-C restatement (liboracle.so)."""
 
-    def __init__(self, path=ORACLE_SO):
+    def __init__(self, path=ORACLE_SO, pow_mode="glibc"):
+        """pow_mode: "glibc" evaluates the boundary-state pow with the reference's libm,
+        "cr" with the device's correctly rounded pow (oracle/cr_pow.h)."""
         if not os.path.exists(path):
             build()
         self.lib = C.CDLL(path)
         L = self.lib
+        self.cr = 1 if pow_mode == "cr" else 0
         L.or_last_error.restype = C.POINTER(OrError)
         L.or_solver_create.restype = _p
         L.or_solver_df.restype = C.POINTER(_d)
         self._keep = []
+
+    def mode(self):
+        self.lib.or_set_pow_mode(_i(self.cr))
+        return self.lib
 
     def _check(self, st):
         if st:
@@ -129,7 +136,7 @@ class Oracle:
         P = self.pattern(pat)
         f = OrIlu(ptr(vals), ptr(dlu), ptr(piv), ptr(dinv))
         A = np.ascontiguousarray(A, dtype=dt)
-        fn = self.lib.or_ilu_factorize_z if cplx else self.lib.or_ilu_factorize_d
+        fn = self.mode().or_ilu_factorize_z if cplx else self.lib.or_ilu_factorize_d
         self._check(fn(C.byref(P), ptr(A), C.byref(f)))
         return dict(vals=vals, diag_lu=dlu, diag_piv=piv, diag_inv=dinv)
 
@@ -150,7 +157,7 @@ class Oracle:
     def build_lhs_mean(self, pat, J, implicit, sigma, eps, stage):
         A = np.zeros_like(J)
         P = self.pattern(pat)
-        self._check(self.lib.or_build_lhs_mean(C.byref(P), ptr(J), _i(implicit), _d(sigma), _d(eps), _i(stage),
+        self._check(self.mode().or_build_lhs_mean(C.byref(P), ptr(J), _i(implicit), _d(sigma), _d(eps), _i(stage),
                                                ptr(A)))
         return A
 
@@ -161,7 +168,7 @@ class Oracle:
         inv = np.zeros(n)
         vis = np.zeros(n)
         f = None if forcing is None else np.ascontiguousarray(forcing, np.float64)
-        self._check(self.lib.or_residual(C.byref(M), ptr(np.ascontiguousarray(W)), ptr(wref), _i(order), _i(mode),
+        self._check(self.mode().or_residual(C.byref(M), ptr(np.ascontiguousarray(W)), ptr(wref), _i(order), _i(mode),
                                          ptr(f), _i(0 if f is None else len(f)), _i(int(need_vis)), ptr(inv),
                                          ptr(vis)))
         return inv, vis
@@ -172,12 +179,12 @@ class Oracle:
         b = m.b
         J = np.zeros(len(pat["col_idx"]) * b * b) if want_J else None
         D = np.zeros(m.n * b * b) if want_P else None
-        self._check(self.lib.or_fd_jacobian(C.byref(M), C.byref(P), ptr(np.ascontiguousarray(W)), ptr(J), ptr(D)))
+        self._check(self.mode().or_fd_jacobian(C.byref(M), C.byref(P), ptr(np.ascontiguousarray(W)), ptr(J), ptr(D)))
         return J, D
 
     def transform_jacobian(self, m, W):
         out = np.zeros(m.n * m.b * m.b)
-        self._check(self.lib.or_transform_jacobian(_i(m.b), _i(m.n), _d(m.gamma), ptr(np.ascontiguousarray(W)),
+        self._check(self.mode().or_transform_jacobian(_i(m.b), _i(m.n), _d(m.gamma), ptr(np.ascontiguousarray(W)),
                                                    ptr(out)))
         return out
 
@@ -188,7 +195,7 @@ class Oracle:
         inv = np.zeros(n, np.complex128)
         vis = np.zeros(n, np.complex128)
         f = np.ascontiguousarray(forcing, np.complex128)
-        self._check(self.lib.or_linearized_residual(C.byref(Mm), ptr(np.ascontiguousarray(mean)), ptr(M),
+        self._check(self.mode().or_linearized_residual(C.byref(Mm), ptr(np.ascontiguousarray(mean)), ptr(M),
                                                     ptr(np.ascontiguousarray(what, np.complex128)), _d(omega),
                                                     ptr(f), _i(len(f)), _i(order), _i(int(need_vis)), ptr(inv),
                                                     ptr(vis)))
@@ -201,7 +208,7 @@ class Oracle:
         om = np.asarray(omegas, np.float64)
         a = np.ascontiguousarray(amps, np.complex128)
         df = np.zeros(m.n * m.b)
-        self._check(self.lib.or_deterministic_flux(C.byref(Mm), ptr(np.ascontiguousarray(mean)), _i(nh), ptr(idx),
+        self._check(self.mode().or_deterministic_flux(C.byref(Mm), ptr(np.ascontiguousarray(mean)), _i(nh), ptr(idx),
                                                    ptr(om), ptr(a), ptr(df)))
         return df
 
@@ -237,7 +244,7 @@ class OracleSolver:
     def outer_iteration(self):
         e = OrEntry()
         rh = np.zeros(max(self.nh, 1))
-        self.o._check(self.o.lib.or_solver_outer_iteration(_p(self.h), C.byref(e), ptr(rh)))
+        self.o._check(self.o.mode().or_solver_outer_iteration(_p(self.h), C.byref(e), ptr(rh)))
         return dict(iter=e.iter, resid_mean=e.resid_mean, rz=e.rz, has_rz=bool(e.has_rz),
                     resid_h=rh[: self.nh].copy(), stage1_norm_mean=e.stage1_norm_mean)
 

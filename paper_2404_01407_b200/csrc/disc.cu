@@ -1,0 +1,856 @@
+// disc.cu -- device discretization kernels.  Parity contract: every kernel follows
+// the operation order of the reference (disc_euler.cpp, disc.cpp, residual_ops.cpp,
+// state.cpp) as restated in oracle/fnlh_oracle.c; per-node accumulations are
+// atomic-free CSR-by-node gathers in ascending face index (mesh.cpp:44-59), so the
+// residual and the FD Jacobian are bitwise identical to the CPU (pow() in the
+// subsonic inlet/outlet states is the only libm call whose last bit may differ).
+#include <algorithm>
+#include <cmath>
+
+#include "disc.cuh"
+
+namespace fnlh {
+
+namespace {
+
+constexpr int kT = 128;
+inline int nb(long long n, int t = kT) { return static_cast<int>((n + t - 1) / t); }
+
+__device__ __forceinline__ void record(unsigned long long* err, unsigned long long key, int code) {
+    atomicMin(err, (key << 4) | (unsigned long long)code);
+}
+
+// ---------------------------------------------------------------------------
+// residual: node pre-pass (order 2), face fluxes, node gather
+// ---------------------------------------------------------------------------
+template <int B>
+__global__ void k_jst_prepass(MeshDev m, const double* __restrict__ W, double* __restrict__ nu,
+                              double* __restrict__ lap, const double* skip) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m.n) return;
+    if (skip && *skip == 0.0) return;
+    const double* wi = W + (size_t)i * B;
+    const double pi = wi[4];
+    double num = 0.0, den = 0.0;
+    double L[B], qi[B], qj[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) L[k] = 0.0;
+    prim_to_cons<B>(wi, m.gamma, qi);
+    for (int e = m.nf_ptr[i]; e < m.nf_ptr[i + 1]; ++e) {
+        const int f = m.nf_idx[e];
+        if (m.fbc[f] >= 0) {
+            den += pi + pi;
+            continue;
+        }
+        const int j = m.fa[f] == i ? m.fb[f] : m.fa[f];
+        const double* wj = W + (size_t)j * B;
+        const double pj = wj[4];
+        num += pj - pi;
+        den += pj + pi;
+        prim_to_cons<B>(wj, m.gamma, qj);
+#pragma unroll
+        for (int k = 0; k < B; ++k) L[k] += qj[k] - qi[k];
+    }
+    nu[i] = fabs(num) / den;
+#pragma unroll
+    for (int k = 0; k < B; ++k) lap[(size_t)i * B + k] = L[k];
+}
+
+template <int B>
+__global__ void k_face_flux(MeshDev m, const double* __restrict__ W, const double* __restrict__ wref, int order,
+                            int mode, const double* __restrict__ forcing, int nforcing, int need_vis,
+                            const double* __restrict__ nu, const double* __restrict__ lap,
+                            double* __restrict__ flux, double* __restrict__ vflux, unsigned long long* err,
+                            const double* skip) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= m.nf) return;
+    if (skip && *skip == 0.0) return;
+    const int a = m.fa[f];
+    double out[B];
+    if (m.fbc[f] >= 0) {
+        const int st = boundary_face_flux<B>(m, f, W + (size_t)a * B, wref ? wref + (size_t)a * B : nullptr, mode,
+                                             forcing, nforcing, out);
+        if (st) {
+            record(err, (unsigned long long)f, st);
+#pragma unroll
+            for (int k = 0; k < B; ++k) out[k] = 0.0;
+        }
+    } else {
+        const int c = m.fb[f];
+        double wa[B], wc[B];
+        load_vec<B>(W + (size_t)a * B, wa);
+        load_vec<B>(W + (size_t)c * B, wc);
+        if (order == 2)
+            interior_face_flux<B>(m, f, wa, wc, 2, nu[a], nu[c], m.bflag[a] || m.bflag[c], lap + (size_t)a * B,
+                                  lap + (size_t)c * B, out);
+        else
+            interior_face_flux<B>(m, f, wa, wc, 1, 0.0, 0.0, false, nullptr, nullptr, out);
+        if (need_vis && B == 6) {
+            double vo[B];
+            viscous_face_flux<B>(m, f, wa, wc, m.mu[a], m.mu[c], vo);
+            store_vec<B>(vflux + (size_t)f * B, vo);
+        }
+    }
+    store_vec<B>(flux + (size_t)f * B, out);
+}
+
+template <int B>
+__global__ void k_node_gather(MeshDev m, const double* __restrict__ W, const double* __restrict__ flux,
+                              const double* __restrict__ vflux, int need_vis, double* __restrict__ inv,
+                              double* __restrict__ vis, const double* skip) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m.n) return;
+    if (skip && *skip == 0.0) return;
+    double acc[B], vacc[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+        acc[k] = 0.0;
+        vacc[k] = 0.0;
+    }
+    for (int e = m.nf_ptr[i]; e < m.nf_ptr[i + 1]; ++e) {
+        const int f = m.nf_idx[e];
+        const double* fl = flux + (size_t)f * B;
+        if (m.fbc[f] >= 0 || m.fa[f] == i) {
+#pragma unroll
+            for (int k = 0; k < B; ++k) acc[k] += fl[k];
+            if (B == 6 && need_vis && m.fbc[f] < 0) {
+                const double* vf = vflux + (size_t)f * B;
+#pragma unroll
+                for (int k = 0; k < B; ++k) vacc[k] += vf[k];
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < B; ++k) acc[k] -= fl[k];
+            if (B == 6 && need_vis) {
+                const double* vf = vflux + (size_t)f * B;
+#pragma unroll
+                for (int k = 0; k < B; ++k) vacc[k] -= vf[k];
+            }
+        }
+    }
+    double src[B];
+    node_source<B>(m, i, W[(size_t)i * B + 4], src);
+#pragma unroll
+    for (int k = 0; k < B; ++k) inv[(size_t)i * B + k] = acc[k] + src[k];
+    if (need_vis) {
+#pragma unroll
+        for (int k = 0; k < B; ++k) vis[(size_t)i * B + k] = vacc[k];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// FD Jacobian (disc.cpp:37-130): one thread per (column node j, variable m)
+// ---------------------------------------------------------------------------
+template <int B>
+__global__ void k_validate(int n, const double* __restrict__ W, unsigned long long* err) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (!admissible<B>(W + (size_t)i * B)) record(err, (unsigned long long)i, 2);
+}
+
+// non-negative doubles order like their bit patterns
+__global__ void k_umax_init(unsigned long long* u, int k) {
+    if (threadIdx.x < k) u[threadIdx.x] = 0ull;
+}
+
+template <int B>
+__global__ void k_qscale(int n, double g, const double* __restrict__ W, unsigned long long* umax) {
+    double loc[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) loc[k] = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double q[B];
+        prim_to_cons<B>(W + (size_t)i * B, g, q);
+#pragma unroll
+        for (int k = 0; k < B; ++k) loc[k] = fmax(loc[k], fabs(q[k]));
+    }
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+        double v = loc[k];
+        for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, off));
+        if ((threadIdx.x & 31) == 0) atomicMax(umax + k, (unsigned long long)__double_as_longlong(v));
+    }
+}
+
+template <int B>
+__global__ void k_qscale_finish(const unsigned long long* umax, double* qscale) {
+    const int k = threadIdx.x;
+    if (k >= B) return;
+    const double v = __longlong_as_double((long long)umax[k]);
+    qscale[k] = v == 0.0 ? 1.0 : v;
+}
+
+template <int B>
+__device__ __forceinline__ int fd_face_flux(const MeshDev& m, int f, int j, const double* wj,
+                                            const double* __restrict__ W, double* out) {
+    if (m.fbc[f] >= 0) return boundary_face_flux<B>(m, f, wj, nullptr, 0, nullptr, 0, out);
+    const int a = m.fa[f], c = m.fb[f];
+    double wo[B];
+    if (a == j) {
+        load_vec<B>(W + (size_t)c * B, wo);
+        interior_face_flux<B>(m, f, wj, wo, 1, 0.0, 0.0, false, nullptr, nullptr, out);
+        if (B == 6) {
+            double vf[B];
+            viscous_face_flux<B>(m, f, wj, wo, m.mu[a], m.mu[c], vf);
+#pragma unroll
+            for (int k = 0; k < B; ++k) out[k] += vf[k];
+        }
+    } else {
+        load_vec<B>(W + (size_t)a * B, wo);
+        interior_face_flux<B>(m, f, wo, wj, 1, 0.0, 0.0, false, nullptr, nullptr, out);
+        if (B == 6) {
+            double vf[B];
+            viscous_face_flux<B>(m, f, wo, wj, m.mu[a], m.mu[c], vf);
+#pragma unroll
+            for (int k = 0; k < B; ++k) out[k] += vf[k];
+        }
+    }
+    return 0;
+}
+
+template <int B>
+__global__ void __launch_bounds__(kT) k_fd_jacobian(MeshDev m, const int* __restrict__ diag_idx,
+                                                    const int* __restrict__ e_ab, const int* __restrict__ e_ba,
+                                                    const double* __restrict__ W, const double* __restrict__ qscale,
+                                                    double* __restrict__ J, double* __restrict__ P,
+                                                    unsigned long long* err) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m.n * B) return;
+    const int j = t / B, mm = t % B;
+    const double g = m.gamma;
+    double qj[B], wp[B], wm[B];
+    prim_to_cons<B>(W + (size_t)j * B, g, qj);
+    const double aq = fabs(qj[mm]);
+    const double delta = 1e-6 * (aq > qscale[mm] ? aq : qscale[mm]);
+    const unsigned long long key = (unsigned long long)t;
+    // the reference's q += d; w = prim(q); q -= d sequence (disc.cpp:63-79)
+    qj[mm] += delta;
+    int st = cons_to_prim<B>(qj, g, wp);
+    qj[mm] -= delta;
+    if (st) {
+        record(err, key, st);
+        return;
+    }
+    qj[mm] += -delta;
+    st = cons_to_prim<B>(qj, g, wm);
+    qj[mm] -= -delta;
+    if (st) {
+        record(err, key, st);
+        return;
+    }
+    const double inv2d = 1.0 / (2.0 * delta);
+    double dacc[B];
+#pragma unroll
+    for (int r = 0; r < B; ++r) dacc[r] = 0.0;
+    for (int e = m.nf_ptr[j]; e < m.nf_ptr[j + 1]; ++e) {
+        const int f = m.nf_idx[e];
+        double fp[B], fm[B];
+        st = fd_face_flux<B>(m, f, j, wp, W, fp);
+        if (!st) st = fd_face_flux<B>(m, f, j, wm, W, fm);
+        if (st) {
+            record(err, key, st);
+            return;
+        }
+        const bool bnd = m.fbc[f] >= 0;
+        const bool isa = m.fa[f] == j;
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+            const double dflux = (fp[r] - fm[r]) * inv2d;
+            if (dflux == 0.0) continue;
+            if (bnd || isa) {
+                dacc[r] += dflux;
+                if (!bnd && J) {
+                    double* dst = J + (size_t)e_ba[f] * B * B + r * B + mm;
+                    *dst = *dst - dflux;
+                }
+            } else {
+                if (J) {
+                    double* dst = J + (size_t)e_ab[f] * B * B + r * B + mm;
+                    *dst = *dst + dflux;
+                }
+                dacc[r] -= dflux;
+            }
+        }
+    }
+    double sp[B], sm[B];
+    node_source<B>(m, j, wp[4], sp);
+    node_source<B>(m, j, wm[4], sm);
+#pragma unroll
+    for (int r = 0; r < B; ++r) {
+        const double dsrc = (sp[r] - sm[r]) * inv2d;
+        if (dsrc == 0.0) continue;
+        dacc[r] += dsrc;
+    }
+#pragma unroll
+    for (int r = 0; r < B; ++r) {
+        if (J) J[(size_t)diag_idx[j] * B * B + r * B + mm] = dacc[r];
+        if (P) P[(size_t)j * B * B + r * B + mm] = dacc[r];
+    }
+}
+
+// diagonal non-singularity check (disc.cpp:121-129)
+template <int B>
+__global__ void k_diag_check(int n, const int* __restrict__ diag_idx, const double* __restrict__ J,
+                             unsigned long long* err) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double A[B * B];
+    int piv[B];
+    load_block<B>(J + (size_t)diag_idx[i] * B * B, A);
+    double cond;
+    if (lu_factor_reg<B>(A, piv, cond)) record(err, (unsigned long long)i, 5);
+}
+
+// ---------------------------------------------------------------------------
+// linearized residual (residual_ops.cpp:12-102)
+// ---------------------------------------------------------------------------
+// umax[0..B) = max|mean|, [B..2B) = max|Re what|, [2B..3B) = max|Im what|,
+// [3B] = max|Re forcing|, [3B+1] = max|Im forcing|
+template <int B>
+__global__ void k_linres_scales(int n, const double* __restrict__ mean, const cplx* __restrict__ what,
+                                const cplx* __restrict__ forcing, int nforcing, unsigned long long* umax) {
+    double lm[B], lr[B], li[B], fr = 0.0, fi = 0.0;
+#pragma unroll
+    for (int k = 0; k < B; ++k) lm[k] = lr[k] = li[k] = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            lm[k] = fmax(lm[k], fabs(mean[(size_t)i * B + k]));
+            const cplx w = what[(size_t)i * B + k];
+            lr[k] = fmax(lr[k], fabs(w.re));
+            li[k] = fmax(li[k], fabs(w.im));
+        }
+    }
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nforcing; k += gridDim.x * blockDim.x) {
+        fr = fmax(fr, fabs(forcing[k].re));
+        fi = fmax(fi, fabs(forcing[k].im));
+    }
+    auto wmax = [&](double v, int slot) {
+        for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, off));
+        if ((threadIdx.x & 31) == 0) atomicMax(umax + slot, (unsigned long long)__double_as_longlong(v));
+    };
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+        wmax(lm[k], k);
+        wmax(lr[k], B + k);
+        wmax(li[k], 2 * B + k);
+    }
+    wmax(fr, 3 * B);
+    wmax(fi, 3 * B + 1);
+}
+
+// directional_step (residual_ops.cpp:12-29) for both parts -> delta[0] (Re), delta[1] (Im)
+template <int B>
+__global__ void k_linres_delta(const unsigned long long* umax, double forcing_scale, double* delta) {
+    if (threadIdx.x != 0) return;
+    for (int part = 0; part < 2; ++part) {
+        double ratio = 0.0;
+        for (int k = 0; k < B; ++k) {
+            const double ws = __longlong_as_double((long long)umax[k]);
+            const double ds = __longlong_as_double((long long)umax[(1 + part) * B + k]);
+            if (ds > 0.0) {
+                const double wsc = ws > 1e-300 ? ws : 1e-300;
+                const double r = ds / wsc;
+                ratio = ratio > r ? ratio : r;
+            }
+        }
+        const double fmx = __longlong_as_double((long long)umax[3 * B + part]);
+        if (fmx > 0.0) {
+            const double r = fmx / forcing_scale;
+            ratio = ratio > r ? ratio : r;
+        }
+        delta[part] = ratio == 0.0 ? 0.0 : 1e-5 / ratio;
+    }
+}
+
+// wp = mean + delta*dir, wm = mean - delta*dir, fp = delta*fdir, fm = -delta*fdir
+__global__ void k_linres_states(std::size_t len, const double* __restrict__ mean, const cplx* __restrict__ what,
+                                const cplx* __restrict__ forcing, int nforcing, int part,
+                                const double* __restrict__ delta, double* __restrict__ wp, double* __restrict__ wm,
+                                double* __restrict__ fp, double* __restrict__ fm) {
+    const double d = delta[part];
+    if (d == 0.0) return;
+    const std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x;
+    if (t < len) {
+        const double dir = part == 0 ? what[t].re : what[t].im;
+        wp[t] = mean[t] + d * dir;
+        wm[t] = mean[t] - d * dir;
+    }
+    if (t < (std::size_t)nforcing) {
+        const double fd = part == 0 ? forcing[t].re : forcing[t].im;
+        fp[t] = d * fd;
+        fm[t] = -d * fd;
+    }
+}
+
+// inv += unit * (inv_p - inv_m) * inv2d  (residual_ops.cpp:55-57,86)
+__global__ void k_linres_combine(std::size_t len, int part, const double* __restrict__ delta,
+                                 const double* __restrict__ ip, const double* __restrict__ im, cplx* __restrict__ out,
+                                 int first) {
+    const std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x;
+    if (t >= len) return;
+    const double dl = delta[part];
+    double dv = 0.0;
+    if (dl != 0.0) {
+        const double inv2d = 1.0 / (2.0 * dl);
+        dv = (ip[t] - im[t]) * inv2d;
+    }
+    const double ur = part == 0 ? 1.0 : 0.0, ui = part == 0 ? 0.0 : 1.0;
+    cplx o = first ? mk(0.0, 0.0) : out[t];
+    o = o + mk(ur * dv, ui * dv);
+    out[t] = o;
+}
+
+// ---------------------------------------------------------------------------
+// DF helpers
+// ---------------------------------------------------------------------------
+__global__ void k_any_nonzero(std::size_t len, const cplx* __restrict__ a, int* flag) {
+    for (std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; t < len;
+         t += (std::size_t)gridDim.x * blockDim.x)
+        if (a[t].re != 0.0 || a[t].im != 0.0) {
+            *flag = 1;
+            return;
+        }
+}
+
+struct AmpList {
+    const cplx* a[64];
+};
+
+// reconstruct_instantaneous (state.cpp:96-107)
+__global__ void k_reconstruct(std::size_t len, const double* __restrict__ mean, AmpList amps, int nh,
+                              const cplx* __restrict__ phase, double* __restrict__ out) {
+    const std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x;
+    if (t >= len) return;
+    double o = mean[t];
+    for (int h = 0; h < nh; ++h) {
+        const cplx a = amps.a[h][t];
+        const cplx ph = phase[h];
+        o += 2.0 * (a.re * ph.re - a.im * ph.im);
+    }
+    out[t] = o;
+}
+
+__global__ void k_accumulate(std::size_t len, const double* __restrict__ x, double* __restrict__ acc, int first) {
+    const std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x;
+    if (t >= len) return;
+    acc[t] = first ? 0.0 + x[t] : acc[t] + x[t];
+}
+
+__global__ void k_df_finish(std::size_t len, double nq, const double* __restrict__ acc, const double* __restrict__ inv,
+                            double* __restrict__ df, int divide) {
+    const std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x;
+    if (t >= len) return;
+    const double a = divide ? acc[t] / nq : acc[t];
+    df[t] = a - inv[t];
+}
+
+// ---------------------------------------------------------------------------
+// stage kernels
+// ---------------------------------------------------------------------------
+template <class S>
+__global__ void k_blend(double beta, const S* __restrict__ vf, S* __restrict__ vb, std::size_t len) {
+    const std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x;
+    if (t >= len) return;
+    vb[t] = beta * vf[t] + (1.0 - beta) * vb[t];
+}
+
+template <class S>
+__global__ void k_rhs(const S* __restrict__ inv, const S* __restrict__ vb, S* __restrict__ rhs, std::size_t len) {
+    const std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x;
+    if (t >= len) return;
+    const S r = inv[t] + vb[t];
+    rhs[t] = -r;
+}
+
+template <class S>
+__global__ void k_scale(S* __restrict__ x, double a, std::size_t len) {
+    const std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x;
+    if (t >= len) return;
+    x[t] = x[t] * a;
+}
+
+template <class S>
+__global__ void k_add(S* __restrict__ x, const S* __restrict__ y, std::size_t len) {
+    const std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x;
+    if (t >= len) return;
+    x[t] = x[t] + y[t];
+}
+
+template <int B>
+__device__ __forceinline__ void transform_jacobian_reg(const double* w, double g, double (&M)[B * B]) {
+    const double rho = w[0], u = w[1], v = w[2], ww = w[3];
+#pragma unroll
+    for (int k = 0; k < B * B; ++k) M[k] = 0.0;
+    M[0 * B + 0] = 1.0;
+    M[1 * B + 0] = u;
+    M[1 * B + 1] = rho;
+    M[2 * B + 0] = v;
+    M[2 * B + 2] = rho;
+    M[3 * B + 0] = ww;
+    M[3 * B + 3] = rho;
+    M[4 * B + 0] = 0.5 * u * u + 0.5 * v * v + 0.5 * ww * ww;
+    M[4 * B + 1] = rho * u;
+    M[4 * B + 2] = rho * v;
+    M[4 * B + 3] = rho * ww;
+    M[4 * B + 4] = 1.0 / (g - 1.0);
+    if constexpr (B == 6) {
+        M[5 * B + 0] = w[5];
+        M[5 * B + 5] = rho;
+    }
+}
+
+template <int B>
+__global__ void k_spectral(int n, double g, double omega, const double* __restrict__ vol,
+                           const double* __restrict__ mean, const cplx* __restrict__ what, cplx* __restrict__ inv) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double M[B * B];
+    transform_jacobian_reg<B>(mean + (size_t)i * B, g, M);
+    cplx wi[B], mw[B];
+    load_vec<B>(what + (size_t)i * B, wi);
+#pragma unroll
+    for (int r = 0; r < B; ++r) {
+        cplx acc = mk(0.0, 0.0);
+#pragma unroll
+        for (int c = 0; c < B; ++c) acc += mk(M[r * B + c] * wi[c].re, M[r * B + c] * wi[c].im);
+        mw[r] = acc;
+    }
+    const cplx iwv = mk(0.0, omega * vol[i]);
+#pragma unroll
+    for (int r = 0; r < B; ++r) inv[(size_t)i * B + r] += iwv * mw[r];
+}
+
+template <int B>
+__global__ void k_apply_harmonic(int n, double g, const double* __restrict__ mean, const cplx* __restrict__ base,
+                                 const cplx* __restrict__ x, cplx* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double M[B * B];
+    int piv[B];
+    transform_jacobian_reg<B>(mean + (size_t)i * B, g, M);
+    double cond;
+    lu_factor_reg<B>(M, piv, cond);
+    double re[B], im[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+        const cplx v = x[(size_t)i * B + k];
+        re[k] = v.re;
+        im[k] = v.im;
+    }
+    lu_solve_reg<B>(M, piv, re);
+    lu_solve_reg<B>(M, piv, im);
+#pragma unroll
+    for (int k = 0; k < B; ++k) out[(size_t)i * B + k] = base[(size_t)i * B + k] + mk(re[k], im[k]);
+}
+
+template <int B>
+__global__ void k_apply_mean(int n, double g, const double* __restrict__ base, const double* __restrict__ x,
+                             double* __restrict__ out, unsigned long long* err) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* w = base + (size_t)i * B;
+    if (!admissible<B>(w)) {
+        record(err, (unsigned long long)i, 2);
+        return;
+    }
+    double q[B], o[B];
+    prim_to_cons<B>(w, g, q);
+#pragma unroll
+    for (int k = 0; k < B; ++k) q[k] += x[(size_t)i * B + k];
+    if (cons_to_prim<B>(q, g, o)) {
+        record(err, (unsigned long long)i, 2);
+        return;
+    }
+    store_vec<B>(out + (size_t)i * B, o);
+}
+
+template <class S>
+__global__ void k_check_finite(const S* __restrict__ x, std::size_t len, unsigned long long* err) {
+    for (std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x; t < len;
+         t += (std::size_t)gridDim.x * blockDim.x)
+        if (!finite_(x[t])) {
+            record(err, (unsigned long long)t, 6);
+            return;
+        }
+}
+
+#define DISPATCH_B56(b, ...)                                                          \
+    switch (b) {                                                                      \
+        case 5: { constexpr int B = 5; __VA_ARGS__; } break;                          \
+        case 6: { constexpr int B = 6; __VA_ARGS__; } break;                          \
+        default: throw ShapeError("discretization supports b = 5 or 6, got " + std::to_string(b)); \
+    }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// DeviceDisc
+// ---------------------------------------------------------------------------
+DeviceDisc::DeviceDisc(const MeshArrays& m, const DevicePattern* pattern) : pat_(pattern) {
+    if (m.b != 5 && m.b != 6) throw ShapeError("discretization supports b = 5 or 6");
+    if (pattern->rows != m.n || pattern->b != m.b) throw ShapeError("disc: pattern shape mismatch");
+    const int nfc = m.nf, n = m.n;
+    fa_.upload(m.fa, nfc);
+    fb_.upload(m.fb, nfc);
+    fbc_.upload(m.fbc, nfc);
+    ford_.upload(m.ford, nfc);
+    fn_.upload(m.fn, 3 * (std::size_t)nfc);
+    farea_.upload(m.farea, nfc);
+    fnh_.upload(m.fnh, 3 * (std::size_t)nfc);
+    fvis_.upload(m.fvis, nfc);
+    vol_.upload(m.vol, n);
+    closure_.upload(m.closure, 3 * (std::size_t)n);
+    mu_.upload(m.mu, n);
+    nf_ptr_.upload(m.nf_ptr, n + 1);
+    nf_idx_.upload(m.nf_idx, m.nf_ptr[n]);
+    bflag_.upload(m.bflag, n);
+    // per-face BSR entries of (a,b) and (b,a) for the FD scatter (find, sparse.cpp:42-48)
+    std::vector<int> eab(nfc, -1), eba(nfc, -1);
+    auto find = [&](int i, int j) {
+        auto b0 = pattern->h_col_idx.begin() + pattern->h_row_ptr[i];
+        auto b1 = pattern->h_col_idx.begin() + pattern->h_row_ptr[i + 1];
+        auto it = std::lower_bound(b0, b1, j);
+        if (it == b1 || *it != j) throw ShapeError("disc: face endpoints not adjacent in the pattern");
+        return static_cast<int>(it - pattern->h_col_idx.begin());
+    };
+    for (int f = 0; f < nfc; ++f)
+        if (m.fbc[f] < 0) {
+            eab[f] = find(m.fa[f], m.fb[f]);
+            eba[f] = find(m.fb[f], m.fa[f]);
+        }
+    e_ab_.upload(eab.data(), nfc);
+    e_ba_.upload(eba.data(), nfc);
+    view_ = MeshDev{n, nfc, m.b, fa_.ptr, fb_.ptr, fbc_.ptr, ford_.ptr, fn_.ptr, farea_.ptr, fnh_.ptr, fvis_.ptr,
+                    vol_.ptr, closure_.ptr, mu_.ptr, nf_ptr_.ptr, nf_idx_.ptr, bflag_.ptr, m.gamma, m.gas_constant,
+                    m.p0, m.T0, m.p_out, m.nt_in, m.forcing_scale};
+    nu_.alloc(n);
+    lap_.alloc((std::size_t)n * m.b);
+    flux_.alloc((std::size_t)nfc * m.b);
+    vflux_.alloc((std::size_t)nfc * m.b);
+    qscale_.alloc(8);
+    scal_.alloc(16);
+    err_.alloc(1);
+    umax_.alloc(64);
+    for (auto& s : scratch_real) s.alloc((std::size_t)n * m.b);
+    FNLH_CUDA(cudaMemset(err_.ptr, 0xff, sizeof(unsigned long long)));
+}
+
+void DeviceDisc::reset_err(cudaStream_t st) {
+    FNLH_CUDA(cudaMemsetAsync(err_.ptr, 0xff, sizeof(unsigned long long), st));
+}
+
+int DeviceDisc::read_err(cudaStream_t st, long long* key) {
+    unsigned long long h = 0;
+    FNLH_CUDA(cudaMemcpyAsync(&h, err_.ptr, sizeof h, cudaMemcpyDeviceToHost, st));
+    FNLH_CUDA(cudaStreamSynchronize(st));
+    if (h == ~0ull) return 0;
+    if (key) *key = (long long)(h >> 4);
+    return (int)(h & 15ull);
+}
+
+void DeviceDisc::raise_if_err(cudaStream_t st, const char* what) {
+    long long key = -1;
+    const int code = read_err(st, &key);
+    if (!code) return;
+    reset_err(st);
+    const std::string w(what);
+    switch (code) {
+        case 2: throw StateError(w + ": inadmissible state");
+        case 4: throw UnsupportedCaseError(w + ": supersonic boundary state");
+        case 5: throw FactorizationError(w + ": singular diagonal block", (int)key);
+        case 6: throw DivergenceError(w + ": non-finite value", 0);
+        default: throw std::runtime_error(w + ": device error " + std::to_string(code));
+    }
+}
+
+void DeviceDisc::residual(const double* W, const double* wref, int order, int mode, const double* forcing,
+                          int nforcing, bool need_vis, double* inv, double* vis, cudaStream_t st,
+                          const double* skip) {
+    const MeshDev& m = view_;
+    DISPATCH_B56(m.b, {
+        if (order == 2) k_jst_prepass<B><<<nb(m.n), kT, 0, st>>>(m, W, nu_.ptr, lap_.ptr, skip);
+        k_face_flux<B><<<nb(m.nf), kT, 0, st>>>(m, W, wref, order, mode, forcing, nforcing, need_vis ? 1 : 0,
+                                                nu_.ptr, lap_.ptr, flux_.ptr, vflux_.ptr, err_.ptr, skip);
+        k_node_gather<B><<<nb(m.n), kT, 0, st>>>(m, W, flux_.ptr, vflux_.ptr, need_vis ? 1 : 0, inv, vis, skip);
+    });
+    FNLH_CUDA(cudaGetLastError());
+}
+
+void DeviceDisc::validate(const double* W, cudaStream_t st) {
+    DISPATCH_B56(view_.b, { k_validate<B><<<nb(view_.n), kT, 0, st>>>(view_.n, W, err_.ptr); });
+    raise_if_err(st, "validate_state");
+}
+
+void DeviceDisc::fd_jacobian(const double* W, double* J, double* P, cudaStream_t st) {
+    const MeshDev& m = view_;
+    validate(W, st);
+    if (J) FNLH_CUDA(cudaMemsetAsync(J, 0, (std::size_t)pat_->nnzb * m.b * m.b * sizeof(double), st));
+    DISPATCH_B56(m.b, {
+        k_umax_init<<<1, 32, 0, st>>>(umax_.ptr, B);
+        k_qscale<B><<<std::min(nb(m.n), 592), kT, 0, st>>>(m.n, m.gamma, W, umax_.ptr);
+        k_qscale_finish<B><<<1, 32, 0, st>>>(umax_.ptr, qscale_.ptr);
+        k_fd_jacobian<B><<<nb((long long)m.n * B), kT, 0, st>>>(m, pat_->diag_idx, e_ab_.ptr, e_ba_.ptr, W,
+                                                                qscale_.ptr, J, P, err_.ptr);
+    });
+    FNLH_CUDA(cudaGetLastError());
+    raise_if_err(st, "fd_jacobian");
+    if (J) {
+        DISPATCH_B56(m.b, { k_diag_check<B><<<nb(m.n), kT, 0, st>>>(m.n, pat_->diag_idx, J, err_.ptr); });
+        raise_if_err(st, "fd_jacobian");
+    }
+}
+
+void DeviceDisc::linearized_residual(const double* mean, const cplx* what, double omega, const cplx* forcing,
+                                     int nforcing, int order, bool need_vis, cplx* inv, cplx* vis, cudaStream_t st) {
+    if (omega < 0.0) throw ConfigError("linearized_residual: negative frequency");
+    const MeshDev& m = view_;
+    const std::size_t L = len();
+    if (nforcing > 0 && (std::size_t)fwork_.n < 2 * (std::size_t)nforcing) fwork_.alloc(2 * (std::size_t)nforcing);
+    double* wp = scratch_real[0].ptr;
+    double* wm = scratch_real[1].ptr;
+    double* ip = scratch_real[2].ptr;
+    double* vp = scratch_real[3].ptr;
+    double* imn = scratch_real[4].ptr;
+    double* vm = scratch_real[5].ptr;
+    double* fp = nforcing > 0 ? fwork_.ptr : nullptr;
+    double* fm = nforcing > 0 ? fwork_.ptr + nforcing : nullptr;
+    double* delta = scal_.ptr;
+    const int grid = std::min(nb(m.n), 592);
+    DISPATCH_B56(m.b, {
+        k_umax_init<<<1, 32, 0, st>>>(umax_.ptr, 3 * B + 2);
+        k_linres_scales<B><<<grid, kT, 0, st>>>(m.n, mean, what, forcing, nforcing, umax_.ptr);
+        k_linres_delta<B><<<1, 32, 0, st>>>(umax_.ptr, m.forcing_scale, delta);
+    });
+    const int gs = nb((long long)std::max<std::size_t>(L, (std::size_t)nforcing));
+    for (int part = 0; part < 2; ++part) {
+        k_linres_states<<<gs, kT, 0, st>>>(L, mean, what, forcing, nforcing, part, delta, wp, wm, fp, fm);
+        residual(wp, mean, order, 1, fp, nforcing, need_vis, ip, vp, st, delta + part);
+        residual(wm, mean, order, 1, fm, nforcing, need_vis, imn, vm, st, delta + part);
+        k_linres_combine<<<nb(L), kT, 0, st>>>(L, part, delta, ip, imn, inv, part == 0);
+        if (need_vis) k_linres_combine<<<nb(L), kT, 0, st>>>(L, part, delta, vp, vm, vis, part == 0);
+    }
+    DISPATCH_B56(m.b, { k_spectral<B><<<nb(m.n), kT, 0, st>>>(m.n, m.gamma, omega, vol_.ptr, mean, what, inv); });
+    FNLH_CUDA(cudaGetLastError());
+}
+
+namespace {
+// HarmonicSpec::base_frequency / max_multiple (case.cpp:10-44)
+void base_frequency(const std::vector<double>& omega, double& base, int& lmax) {
+    const double rel_tol = 1e-9;
+    std::vector<double> ws;
+    for (double w : omega)
+        if (w > 0.0) ws.push_back(w);
+    lmax = 0;
+    base = 0.0;
+    if (ws.empty()) return;
+    const double scale = *std::max_element(ws.begin(), ws.end());
+    double g = ws[0];
+    for (std::size_t i = 1; i < ws.size(); ++i) {
+        double a = std::max(g, ws[i]);
+        double b = std::min(g, ws[i]);
+        while (b > rel_tol * scale) {
+            const double r = std::fmod(a, b);
+            a = b;
+            b = r;
+        }
+        g = a;
+    }
+    if (g < 1e-6 * scale) throw ConfigError("harmonic frequencies are incommensurate");
+    for (double w : ws) {
+        const double mm = w / g;
+        if (std::abs(mm - std::round(mm)) > 1e-6) throw ConfigError("harmonic frequencies are incommensurate");
+    }
+    base = g;
+    for (double w : omega)
+        if (w > 0.0) lmax = std::max(lmax, static_cast<int>(std::llround(w / g)));
+}
+}  // namespace
+
+void DeviceDisc::deterministic_flux(const double* mean, const std::vector<const cplx*>& amps,
+                                    const std::vector<double>& omega, double* df, cudaStream_t st) {
+    const std::size_t L = len();
+    const int nh = static_cast<int>(amps.size());
+    if (nh > 64) throw ConfigError("deterministic_flux: at most 64 harmonics");
+    double base;
+    int lmax;
+    base_frequency(omega, base, lmax);
+    // any nonzero amplitude?  (residual_ops.cpp:133-141)
+    DeviceBuffer<int> flag(1);
+    FNLH_CUDA(cudaMemsetAsync(flag.ptr, 0, sizeof(int), st));
+    for (int h = 0; h < nh; ++h) k_any_nonzero<<<std::min(nb((long long)L), 592), kT, 0, st>>>(L, amps[h], flag.ptr);
+    int hflag = 0;
+    FNLH_CUDA(cudaMemcpyAsync(&hflag, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FNLH_CUDA(cudaStreamSynchronize(st));
+    if (!hflag) {
+        FNLH_CUDA(cudaMemsetAsync(df, 0, L * sizeof(double), st));
+        return;
+    }
+    AmpList al{};
+    for (int h = 0; h < nh; ++h) al.a[h] = amps[h];
+    const int nq = lmax == 0 ? 1 : 4 * lmax + 2;
+    std::vector<std::complex<double>> ph((std::size_t)nq * std::max(nh, 1));
+    const double period = lmax == 0 ? 0.0 : 2.0 * std::acos(-1.0) / base;
+    for (int k = 0; k < nq; ++k) {
+        const double t = lmax == 0 ? 0.0 : period * k / nq;
+        for (int h = 0; h < nh; ++h) ph[(std::size_t)k * nh + h] = std::exp(std::complex<double>(0.0, omega[h] * t));
+    }
+    DeviceBuffer<cplx> dph;
+    dph.upload(reinterpret_cast<const cplx*>(ph.data()), ph.size());
+    double* w = scratch_real[0].ptr;
+    double* inv = scratch_real[1].ptr;
+    double* acc = scratch_real[2].ptr;
+    for (int k = 0; k < nq; ++k) {
+        k_reconstruct<<<nb((long long)L), kT, 0, st>>>(L, mean, al, nh, dph.ptr + (std::size_t)k * nh, w);
+        residual(w, nullptr, 2, 0, nullptr, 0, false, inv, nullptr, st);
+        k_accumulate<<<nb((long long)L), kT, 0, st>>>(L, inv, acc, k == 0);
+    }
+    raise_if_err(st, "deterministic_flux");
+    residual(mean, nullptr, 2, 0, nullptr, 0, false, inv, nullptr, st);
+    k_df_finish<<<nb((long long)L), kT, 0, st>>>(L, (double)nq, acc, inv, df, lmax == 0 ? 0 : 1);
+    FNLH_CUDA(cudaGetLastError());
+    raise_if_err(st, "deterministic_flux");
+}
+
+// ---------------------------------------------------------------------------
+template <class S>
+void stage_blend(double beta, const S* vf, S* vb, std::size_t len, cudaStream_t st) {
+    k_blend<S><<<nb((long long)len), kT, 0, st>>>(beta, vf, vb, len);
+}
+template <class S>
+void stage_rhs(const S* inv, const S* vb, S* rhs, std::size_t len, cudaStream_t st) {
+    k_rhs<S><<<nb((long long)len), kT, 0, st>>>(inv, vb, rhs, len);
+}
+template <class S>
+void scale(S* x, double a, std::size_t len, cudaStream_t st) {
+    k_scale<S><<<nb((long long)len), kT, 0, st>>>(x, a, len);
+}
+template <class S>
+void add_inplace(S* x, const S* y, std::size_t len, cudaStream_t st) {
+    k_add<S><<<nb((long long)len), kT, 0, st>>>(x, y, len);
+}
+template <class S>
+void check_finite(const S* x, std::size_t len, unsigned long long* err, cudaStream_t st) {
+    k_check_finite<S><<<std::min(nb((long long)len), 592), kT, 0, st>>>(x, len, err);
+}
+
+void apply_harmonic(int b, int n, double gamma, const double* mean, const cplx* base, const cplx* x, cplx* out,
+                    cudaStream_t st) {
+    DISPATCH_B56(b, { k_apply_harmonic<B><<<nb(n), kT, 0, st>>>(n, gamma, mean, base, x, out); });
+}
+
+void apply_mean(int b, int n, double gamma, const double* base, const double* x, double* out,
+                unsigned long long* err, cudaStream_t st) {
+    DISPATCH_B56(b, { k_apply_mean<B><<<nb(n), kT, 0, st>>>(n, gamma, base, x, out, err); });
+}
+
+#define INST(S)                                                                         \
+    template void stage_blend<S>(double, const S*, S*, std::size_t, cudaStream_t);      \
+    template void stage_rhs<S>(const S*, const S*, S*, std::size_t, cudaStream_t);      \
+    template void scale<S>(S*, double, std::size_t, cudaStream_t);                      \
+    template void add_inplace<S>(S*, const S*, std::size_t, cudaStream_t);              \
+    template void check_finite<S>(const S*, std::size_t, unsigned long long*, cudaStream_t);
+INST(double)
+INST(cplx)
+
+}  // namespace fnlh

@@ -1,0 +1,88 @@
+// disc.cuh -- the 3D edge-based discretization resident on the device: residual
+// (disc_euler.cpp:56-85), FD Jacobian (disc.cpp:37-130), linearized residual
+// (residual_ops.cpp:63-102), deterministic flux (residual_ops.cpp:113-161), and the
+// RK stage / update kernels (rk.cpp:41-99, driver.cpp:32-46,274-280).
+#pragma once
+
+#include <complex>
+#include <vector>
+
+#include "capi_util.hpp"
+#include "euler.cuh"
+#include "la.cuh"
+
+namespace fnlh {
+
+struct MeshArrays {  // host-side description (include/fnlh_b200.h fnlh_disc_create)
+    int n = 0, nf = 0, b = 5;
+    const int *fa, *fb, *fbc, *ford;
+    const double *fn, *farea, *fnh, *fvis, *vol, *closure, *mu;
+    const int *nf_ptr, *nf_idx, *bflag;
+    double gamma, gas_constant, p0, T0, p_out, nt_in, forcing_scale;
+};
+
+class DeviceDisc {
+public:
+    DeviceDisc(const MeshArrays& m, const DevicePattern* pattern);
+    int n() const { return view_.n; }
+    int b() const { return view_.b; }
+    int nf() const { return view_.nf; }
+    const MeshDev& view() const { return view_; }
+    const DevicePattern* pattern() const { return pat_; }
+    std::size_t len() const { return (std::size_t)view_.n * view_.b; }
+
+    // device error word: (key << 4) | code, ~0 when clean
+    unsigned long long* err() const { return err_.ptr; }
+    void reset_err(cudaStream_t st);
+    // 0 or the reference status code of the first recorded error (synchronizes)
+    int read_err(cudaStream_t st, long long* key = nullptr);
+    void raise_if_err(cudaStream_t st, const char* what);
+
+    // residual(W, order, mode, forcing, need_vis) -> inv, vis (async);
+    // skip_if_zero: device scalar; when it holds 0.0 the evaluation is skipped (delta == 0)
+    void residual(const double* W, const double* wref, int order, int mode, const double* forcing, int nforcing,
+                  bool need_vis, double* inv, double* vis, cudaStream_t st, const double* skip_if_zero = nullptr);
+    // J (pattern layout) and/or P (n*b*b); validates W and the diagonal blocks (throws)
+    void fd_jacobian(const double* W, double* J, double* P, cudaStream_t st);
+    // transform_jacobian validation (state.cpp:82-94): throws StateError on an inadmissible mean
+    void validate(const double* W, cudaStream_t st);
+    // linearized_residual (mean is the perturbation reference); complex vectors as cplx
+    void linearized_residual(const double* mean, const cplx* what, double omega, const cplx* forcing, int nforcing,
+                             int order, bool need_vis, cplx* inv, cplx* vis, cudaStream_t st);
+    // deterministic_flux; amps: nh device pointers; omega/index host
+    void deterministic_flux(const double* mean, const std::vector<const cplx*>& amps,
+                            const std::vector<double>& omega, double* df, cudaStream_t st);
+
+    DeviceBuffer<double> scratch_real[6];  // linres / DF temporaries (len each)
+private:
+    MeshDev view_{};
+    const DevicePattern* pat_;
+    DeviceBuffer<int> fa_, fb_, fbc_, ford_, nf_ptr_, nf_idx_, bflag_, e_ab_, e_ba_;
+    DeviceBuffer<double> fn_, farea_, fnh_, fvis_, vol_, closure_, mu_;
+    DeviceBuffer<double> nu_, lap_, flux_, vflux_, qscale_, scal_;
+    DeviceBuffer<unsigned long long> err_;
+    DeviceBuffer<unsigned long long> umax_;
+    DeviceBuffer<double> fwork_;  // forcing perturbation vectors
+    std::vector<double> h_nfpad_;
+};
+
+// --- RK stage / update kernels (rk.cpp:41-99) ---------------------------------
+template <class S>
+void stage_blend(double beta, const S* vis_fresh, S* vis_blend, std::size_t len, cudaStream_t st);
+template <class S>
+void stage_rhs(const S* inv, const S* vis_blend, S* rhs, std::size_t len, cudaStream_t st);
+template <class S>
+void scale(S* x, double a, std::size_t len, cudaStream_t st);
+template <class S>
+void add_inplace(S* x, const S* y, std::size_t len, cudaStream_t st);
+// harmonic update out = base + M(mean)^{-1} x (driver.cpp:32-46)
+void apply_harmonic(int b, int n, double gamma, const double* mean, const cplx* base, const cplx* x, cplx* out,
+                    cudaStream_t st);
+// mean update out = prim(cons(base) + x) (driver.cpp:274-280); status -> err word (code 2)
+void apply_mean(int b, int n, double gamma, const double* base, const double* x, double* out,
+                unsigned long long* err, cudaStream_t st);
+// all_finite (core.hpp:127-132) -> err word code 6 when a value is not finite
+template <class S>
+void check_finite(const S* x, std::size_t len, unsigned long long* err, cudaStream_t st);
+
+}  // namespace fnlh

@@ -5,6 +5,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "cr_pow.cuh"
 
 namespace fnlh {
 
@@ -109,7 +110,7 @@ __device__ __forceinline__ int steady_inlet(const MeshDev& m, const double* wint
     if (!(cb > 0.0)) return 2;
     if (fabs(ub) >= cb) return 4;
     const double tb = cb * cb / (g * R);
-    const double pb = m.p0 * pow(tb / m.T0, g / (g - 1.0));
+    const double pb = m.p0 * cr_pow(tb / m.T0, g / (g - 1.0));
     s.w[0] = pb / (R * tb);
     s.w[1] = ub * -nh[0];
     s.w[2] = ub * -nh[1];
@@ -125,7 +126,7 @@ template <int B>
 __device__ __forceinline__ int steady_outlet(const MeshDev& m, const double* wint, const double* nh, BState& s) {
     const double g = m.gamma;
     const double pb = m.p_out;
-    const double rhob = wint[0] * pow(pb / wint[4], 1.0 / g);
+    const double rhob = wint[0] * cr_pow(pb / wint[4], 1.0 / g);
     const double cb = sqrt(g * pb / rhob);
     const double c_int = sqrt(g * wint[4] / wint[0]);
     const double un = wint[1] * nh[0] + wint[2] * nh[1] + wint[3] * nh[2];

@@ -1,0 +1,362 @@
+// solver.cu -- host orchestration of the FNLH outer iteration on the device
+// (driver.cpp:157-379, rk.cpp:41-99), calling the sm_100a kernels of la.cu / disc.cu.
+#include <chrono>
+#include <cmath>
+
+#include "solver.cuh"
+
+namespace fnlh {
+
+namespace {
+
+constexpr double kAlpha[5] = {1.0 / 4.0, 1.0 / 6.0, 3.0 / 8.0, 1.0 / 2.0, 1.0};   // rk.hpp:27
+constexpr double kBeta[5] = {1.0, 0.0, 14.0 / 25.0, 0.0, 11.0 / 25.0};           // rk.hpp:28
+constexpr int kT = 128;
+inline int nb(long long n) { return static_cast<int>((n + kT - 1) / kT); }
+
+// build_lhs_mean (rk.cpp:5-30), in place: A = J/ga; diag += J_ii*inv_es/ga
+__global__ void k_build_lhs(const double* __restrict__ J, double* __restrict__ A, int bb, int n,
+                            const int* __restrict__ diag_idx, std::size_t total, int implicit, double ga,
+                            double inv_es) {
+    const std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x;
+    if (t >= total) return;
+    const std::size_t e = t / bb;
+    (void)n;
+    const double j = J[t];
+    // is e a diagonal entry?  diag_idx is ascending; binary search on e
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((std::size_t)diag_idx[mid] < e)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    const bool diag = lo < n && (std::size_t)diag_idx[lo] == e;
+    if (!implicit) {
+        A[t] = diag ? j / ga : 0.0;
+        return;
+    }
+    double a = j / ga;
+    if (diag) a += j * inv_es / ga;
+    A[t] = a;
+}
+
+__global__ void k_shift(const double* __restrict__ vol, int n, double omega, double ga, double* __restrict__ s) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) s[i] = omega * vol[i] / ga;  // rk.cpp:37 shift = i omega V / ga
+}
+
+// shifted_blocks (driver.cpp:48-59): P + i omega V I (not divided by Gamma alpha)
+__global__ void k_shifted_blocks(const double* __restrict__ P, const double* __restrict__ vol, int b, int n,
+                                 double omega, cplx* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const cplx s = mk(0.0, omega * vol[i]);
+    for (int k = 0; k < b * b; ++k) {
+        cplx v = mk(P[(size_t)i * b * b + k], 0.0);
+        if (k / b == k % b) v = v + s;
+        out[(size_t)i * b * b + k] = v;
+    }
+}
+
+}  // namespace
+
+void build_lhs_mean_device(const double* J, double* A, int b, int n, const int* diag_idx, std::size_t nnzb,
+                           int implicit, double ga, double inv_es, cudaStream_t st) {
+    const std::size_t total = nnzb * b * b;
+    k_build_lhs<<<nb((long long)total), kT, 0, st>>>(J, A, b * b, n, diag_idx, total, implicit, ga, inv_es);
+    FNLH_CUDA(cudaGetLastError());
+}
+
+void harmonic_shift(const double* vol, int n, double omega, double ga, double* s, cudaStream_t st) {
+    k_shift<<<nb(n), kT, 0, st>>>(vol, n, omega, ga, s);
+}
+
+void shifted_blocks(const double* P, const double* vol, int b, int n, double omega, cplx* out, cudaStream_t st) {
+    k_shifted_blocks<<<nb(n), kT, 0, st>>>(P, vol, b, n, omega, out);
+}
+
+DeviceSolver::DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int* col_idx, const int* partition,
+                           const SchemeConfig& scheme, int nh, const int* index, const double* omega,
+                           const double* forcing_pairs, int nforcing, const double* mean0)
+    : sch_(scheme), nh_(nh), nforcing_(nforcing) {
+    if (sch_.max_outer_iters < 0) throw ConfigError("max_outer_iters must be >= 0");
+    sigma_ = sch_.sigma_cfl > 0.0 ? sch_.sigma_cfl : (sch_.implicit ? 50.0 : 2.0);  // driver.hpp:33-41
+    index_.assign(index, index + nh);
+    omega_.assign(omega, omega + nh);
+    for (double w : omega_)
+        if (w < 0.0) throw ConfigError("harmonic frequency must be >= 0");
+    pat_ = std::make_unique<DevicePattern>(mesh.b, mesh.n, row_ptr, col_idx, partition);
+    disc_ = std::make_unique<DeviceDisc>(mesh, pat_.get());
+    const std::size_t len = (std::size_t)mesh.n * mesh.b;
+    ws_ = std::make_unique<Workspace>(len);
+    mean_.upload(mean0, len);
+    df_.alloc(len);
+    FNLH_CUDA(cudaMemset(df_.ptr, 0, len * sizeof(double)));
+    amps_.alloc(std::max<std::size_t>((std::size_t)nh * len, 1));
+    FNLH_CUDA(cudaMemset(amps_.ptr, 0, amps_.bytes()));
+    forcing_.alloc(std::max<std::size_t>((std::size_t)nh * nforcing, 1));
+    if (nh * nforcing)
+        FNLH_CUDA(cudaMemcpy(forcing_.ptr, forcing_pairs, (std::size_t)nh * nforcing * sizeof(cplx),
+                             cudaMemcpyHostToDevice));
+    if (sch_.implicit) {
+        A5_.alloc((std::size_t)pat_->nnzb * mesh.b * mesh.b);
+        ilu_mean_ = std::make_unique<DeviceIlu<double>>(pat_.get());
+        ilu_h_ = std::make_unique<DeviceIlu<cplx>>(pat_.get());  // ONE workspace reused by every harmonic
+        shift_.alloc(mesh.n);
+    } else {
+        P_.alloc((std::size_t)mesh.n * mesh.b * mesh.b);
+        PLU_.alloc((std::size_t)mesh.n * mesh.b * mesh.b);
+        Ppiv_.alloc(len);
+        pclu_.alloc((std::size_t)mesh.n * mesh.b * mesh.b);
+        pcpiv_.alloc(len);
+    }
+    for (auto& v : rk_) v.alloc(len);
+    FNLH_CUDA(cudaEventCreate(&ev0_));
+    FNLH_CUDA(cudaEventCreate(&ev1_));
+}
+
+DeviceSolver::~DeviceSolver() {
+    cudaEventDestroy(ev0_);
+    cudaEventDestroy(ev1_);
+}
+
+std::size_t DeviceSolver::lhs_bytes() const {
+    std::size_t s = 0;
+    if (sch_.implicit) s = A5_.bytes() + ilu_mean_->bytes() + ilu_h_->bytes();
+    else s = P_.bytes() + PLU_.bytes() + pclu_.bytes();
+    return s;
+}
+
+// rk_step (rk.cpp:41-99)
+template <class S, class Eval, class Apply>
+RkStepResult DeviceSolver::rk_step(S* state, Eval&& eval, Apply&& apply, const SystemView<S>& A,
+                                   const DeviceIlu<S>* ilu, const S* pdiag_lu, const int* pdiag_piv,
+                                   const std::string& field) {
+    cudaStream_t st = ws_->stream;
+    const std::size_t len = disc_->len();
+    S* state0 = reinterpret_cast<S*>(rk_[0].ptr);
+    S* inv = reinterpret_cast<S*>(rk_[1].ptr);
+    S* vis_fresh = reinterpret_cast<S*>(rk_[2].ptr);
+    S* vis_blend = reinterpret_cast<S*>(rk_[3].ptr);
+    S* rhs = reinterpret_cast<S*>(rk_[4].ptr);
+    S* x = reinterpret_cast<S*>(rk_[5].ptr);
+    S* stage = reinterpret_cast<S*>(rk_[6].ptr);
+    FNLH_CUDA(cudaMemcpyAsync(state0, state, len * sizeof(S), cudaMemcpyDeviceToDevice, st));
+    FNLH_CUDA(cudaMemcpyAsync(stage, state, len * sizeof(S), cudaMemcpyDeviceToDevice, st));
+    FNLH_CUDA(cudaMemsetAsync(vis_blend, 0, len * sizeof(S), st));
+    FNLH_CUDA(cudaMemsetAsync(vis_fresh, 0, len * sizeof(S), st));
+    RkStepResult res;
+    const double gfac = sch_.implicit ? 1.0 / sch_.eps_relax : sigma_;  // rk.hpp:34
+    for (int k = 1; k <= 5; ++k) {
+        const double beta = kBeta[k - 1];
+        const bool fresh = beta != 0.0;
+        disc_->reset_err(st);
+        eval(stage, fresh, inv, vis_fresh);
+        {
+            long long key;
+            const int code = disc_->read_err(st, &key);
+            if (code) {
+                disc_->reset_err(st);
+                if (code == 2)
+                    throw DivergenceError("residual evaluation failed: inadmissible boundary state", k, field);
+                if (code == 4) throw UnsupportedCaseError("supersonic boundary state");
+                throw std::runtime_error("device error during residual evaluation");
+            }
+        }
+        if (fresh) {
+            ++res.viscous_evaluations;
+            stage_blend<S>(beta, vis_fresh, vis_blend, len, st);
+        }
+        stage_rhs<S>(inv, vis_blend, rhs, len, st);
+        if (k == 1) {
+            norm2_sq<S>(rhs, len, ws_->scalars + 8, *ws_);
+            FNLH_CUDA(cudaMemcpyAsync(ws_->h_scalars + 8, ws_->scalars + 8, sizeof(double), cudaMemcpyDeviceToHost, st));
+            FNLH_CUDA(cudaStreamSynchronize(st));
+            res.stage1_residual_norm = std::sqrt(ws_->h_scalars[8]);
+        }
+        if (!sch_.implicit) {
+            block_diag_solve<S>(disc_->b(), disc_->n(), pdiag_lu, pdiag_piv, rhs, x, st);
+            scale<S>(x, gfac * kAlpha[k - 1], len, st);
+        } else {
+            scale<S>(rhs, kAlpha[k - 1], len, st);
+            LinearSolveReport rep = smoothed_solve<S>(A, rhs, *ilu, sch_.linear_tol, sch_.linear_max_iter, x, *ws_);
+            sweeps += rep.iterations;
+            row_updates += (long long)rep.iterations * disc_->n();
+            res.linear_reports.push_back(rep);
+        }
+        disc_->reset_err(st);
+        apply(state0, x, stage);
+        check_finite<S>(stage, len, disc_->err(), st);
+        {
+            long long key;
+            const int code = disc_->read_err(st, &key);
+            if (code) {
+                disc_->reset_err(st);
+                if (code == 2) throw DivergenceError("update left the admissible set", k, field);
+                throw DivergenceError("non-finite stage state", k, field);
+            }
+        }
+    }
+    FNLH_CUDA(cudaMemcpyAsync(state, stage, len * sizeof(S), cudaMemcpyDeviceToDevice, st));
+    return res;
+}
+
+ConvergenceEntry DeviceSolver::outer_iteration() {
+    cudaStream_t st = ws_->stream;
+    FNLH_CUDA(cudaEventRecord(ev0_, st));
+    ++iter_;
+    const int n = disc_->n(), b = disc_->b();
+    const std::size_t len = disc_->len();
+    const double gamma = disc_->view().gamma;
+    disc_->validate(mean_.ptr, st);  // transform_jacobian / MLU.factor (driver.cpp:172-176)
+
+    const bool implicit = sch_.implicit != 0;
+    const double ga5 = (implicit ? 1.0 / sch_.eps_relax : sigma_) * kAlpha[4];
+    if (implicit) {
+        disc_->fd_jacobian(mean_.ptr, A5_.ptr, nullptr, st);  // J, then A5 in place
+        build_lhs_mean_device(A5_.ptr, A5_.ptr, b, n, pat_->diag_idx, pat_->nnzb, 1, ga5,
+                              1.0 / (sch_.eps_relax * sigma_), st);
+        SystemView<double> Am;
+        Am.p = pat_.get();
+        Am.real_vals = A5_.ptr;
+        ilu_factorize<double>(Am, *ilu_mean_, *ws_);
+    } else {
+        disc_->fd_jacobian(mean_.ptr, nullptr, P_.ptr, st);  // assemble_diag_blocks (disc.cpp:31-35)
+        FNLH_CUDA(cudaMemcpyAsync(PLU_.ptr, P_.ptr, P_.bytes(), cudaMemcpyDeviceToDevice, st));
+        const int init[2] = {0, 0x7fffffff};
+        FNLH_CUDA(cudaMemcpyAsync(ws_->status, init, sizeof init, cudaMemcpyHostToDevice, st));
+        block_diag_factor<double>(b, n, PLU_.ptr, Ppiv_.ptr, ws_->status, st);
+        FNLH_CUDA(cudaMemcpyAsync(ws_->h_status, ws_->status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        FNLH_CUDA(cudaStreamSynchronize(st));
+        if (ws_->h_status[1] != 0x7fffffff) throw FactorizationError("singular pivot block", ws_->h_status[1]);
+    }
+
+    std::vector<double> h_norm(nh_, 0.0);
+    std::vector<LinearSolveReport> hreps;
+    for (int h = 0; h < nh_; ++h) {
+        cplx* amp = amps_.ptr + (std::size_t)h * len;
+        const double omega = omega_[h];
+        const std::string name = "harmonic-" + std::to_string(index_[h]);
+        const cplx* forcing = forcing_.ptr + (std::size_t)h * nforcing_;
+        auto eval = [&](const cplx* state, bool need_vis, cplx* inv, cplx* vis) {
+            disc_->linearized_residual(mean_.ptr, state, omega, forcing, nforcing_, 2, need_vis, inv, vis, st);
+        };
+        auto apply = [&](const cplx* base, const cplx* x, cplx* out) {
+            apply_harmonic(b, n, gamma, mean_.ptr, base, x, out, st);
+        };
+        RkStepResult step;
+        if (implicit) {
+            harmonic_shift(disc_->view().vol, n, omega, ga5, shift_.ptr, st);
+            SystemView<cplx> Ah;
+            Ah.p = pat_.get();
+            Ah.real_vals = A5_.ptr;
+            Ah.shift_im = shift_.ptr;
+            ilu_factorize<cplx>(Ah, *ilu_h_, *ws_);
+            step = rk_step<cplx>(amp, eval, apply, Ah, ilu_h_.get(), nullptr, nullptr, name);
+        } else {
+            shifted_blocks(P_.ptr, disc_->view().vol, b, n, omega, pclu_.ptr, st);
+            const int init[2] = {0, 0x7fffffff};
+            FNLH_CUDA(cudaMemcpyAsync(ws_->status, init, sizeof init, cudaMemcpyHostToDevice, st));
+            block_diag_factor<cplx>(b, n, pclu_.ptr, pcpiv_.ptr, ws_->status, st);
+            FNLH_CUDA(cudaMemcpyAsync(ws_->h_status, ws_->status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+            FNLH_CUDA(cudaStreamSynchronize(st));
+            if (ws_->h_status[1] != 0x7fffffff) throw FactorizationError("singular pivot block", ws_->h_status[1]);
+            SystemView<cplx> none;
+            step = rk_step<cplx>(amp, eval, apply, none, nullptr, pclu_.ptr, pcpiv_.ptr, name);
+        }
+        h_norm[h] = step.stage1_residual_norm;
+        for (auto& r : step.linear_reports) hreps.push_back(r);
+    }
+
+    // deterministic flux from the fresh harmonic fields (driver.cpp:268-271)
+    std::vector<const cplx*> amps;
+    for (int h = 0; h < nh_; ++h) amps.push_back(amps_.ptr + (std::size_t)h * len);
+    disc_->deterministic_flux(mean_.ptr, amps, omega_, df_.ptr, st);
+
+    // mean update including DF (driver.cpp:273-296)
+    auto mean_eval = [&](const double* state, bool need_vis, double* inv, double* vis) {
+        disc_->residual(state, nullptr, 2, 0, nullptr, 0, need_vis, inv, vis, st);
+        add_inplace<double>(inv, df_.ptr, len, st);
+    };
+    auto mean_apply = [&](const double* base, const double* x, double* out) {
+        apply_mean(b, n, gamma, base, x, out, disc_->err(), st);
+    };
+    RkStepResult mstep;
+    if (implicit) {
+        SystemView<double> Am;
+        Am.p = pat_.get();
+        Am.real_vals = A5_.ptr;
+        mstep = rk_step<double>(mean_.ptr, mean_eval, mean_apply, Am, ilu_mean_.get(), nullptr, nullptr, "mean");
+    } else {
+        SystemView<double> none;
+        mstep = rk_step<double>(mean_.ptr, mean_eval, mean_apply, none, nullptr, PLU_.ptr, Ppiv_.ptr, "mean");
+    }
+    for (auto& r : hreps) reports_.push_back(r);
+    for (auto& r : mstep.linear_reports) reports_.push_back(r);
+
+    FNLH_CUDA(cudaEventRecord(ev1_, st));
+    FNLH_CUDA(cudaEventSynchronize(ev1_));
+    FNLH_CUDA(cudaEventElapsedTime(&last_iteration_ms, ev0_, ev1_));
+    cum_seconds_ += last_iteration_ms * 1e-3;
+
+    ConvergenceEntry e;  // driver.cpp:315-332
+    e.iter = iter_;
+    e.resid_mean = mstep.stage1_residual_norm / std::sqrt((double)n * b);
+    e.resid_h.resize(nh_);
+    double acc = 0.0;
+    for (int h = 0; h < nh_; ++h) {
+        e.resid_h[h] = h_norm[h] / std::sqrt((double)n * b);
+        acc += e.resid_h[h] * e.resid_h[h];
+    }
+    e.has_rz = nh_ > 0;
+    e.rz = nh_ > 0 ? std::sqrt(acc / nh_) : 0.0;
+    e.seconds = cum_seconds_;
+    return e;
+}
+
+int DeviceSolver::run_to_convergence(std::vector<ConvergenceEntry>& history) {  // driver.cpp:335-379
+    const double drop = std::pow(10.0, -sch_.target_drop_orders);
+    double r1_mean = -1.0, r1_rz = -1.0, floor_ = 0.0;
+    for (int it = 0; it < sch_.max_outer_iters; ++it) {
+        ConvergenceEntry e;
+        try {
+            e = outer_iteration();
+        } catch (const DivergenceError&) {
+            return 2;
+        }
+        history.push_back(e);
+        if (it == 0) {
+            r1_mean = e.resid_mean;
+            r1_rz = e.has_rz ? e.rz : 0.0;
+            floor_ = 1e-16 * std::max(r1_mean, r1_rz);
+        }
+        const bool mean_ok = e.resid_mean <= std::max(r1_mean * drop, floor_);
+        const bool rz_ok = !e.has_rz || e.rz <= std::max(r1_rz * drop, floor_);
+        if (mean_ok && rz_ok) return 0;
+    }
+    return 1;
+}
+
+void DeviceSolver::get_state(double* mean, double* amps_pairs) const {
+    const std::size_t len = disc_->len();
+    FNLH_CUDA(cudaStreamSynchronize(ws_->stream));
+    if (mean) download(mean, mean_.ptr, len);
+    if (amps_pairs && nh_) download(reinterpret_cast<cplx*>(amps_pairs), amps_.ptr, (std::size_t)nh_ * len);
+}
+
+void DeviceSolver::set_state(const double* mean, const double* amps_pairs) {
+    const std::size_t len = disc_->len();
+    FNLH_CUDA(cudaStreamSynchronize(ws_->stream));
+    if (mean) FNLH_CUDA(cudaMemcpy(mean_.ptr, mean, len * sizeof(double), cudaMemcpyHostToDevice));
+    if (amps_pairs && nh_)
+        FNLH_CUDA(cudaMemcpy(amps_.ptr, amps_pairs, (std::size_t)nh_ * len * sizeof(cplx), cudaMemcpyHostToDevice));
+}
+
+void DeviceSolver::get_df(double* df) const {
+    FNLH_CUDA(cudaStreamSynchronize(ws_->stream));
+    download(df, df_.ptr, disc_->len());
+}
+
+}  // namespace fnlh

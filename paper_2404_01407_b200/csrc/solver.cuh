@@ -1,0 +1,94 @@
+// solver.cuh -- the FNLH outer iteration resident on one B200 (driver.cpp:157-333):
+// FD Jacobian -> A5 -> real ILU; per harmonic: complex ILU of A5 + i omega V / (Gamma
+// alpha_5) in ONE reused workspace, rk_step with the linearized residual; DF; mean
+// rk_step.  Host code is the reference's orchestration; every array stays in HBM.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "disc.cuh"
+#include "la.cuh"
+
+namespace fnlh {
+
+struct SchemeConfig {  // driver.hpp:22-42
+    int implicit = 1;
+    double sigma_cfl = -1.0;
+    double eps_relax = 0.6;
+    double linear_tol = 1e-2;
+    int linear_max_iter = 10;
+    double target_drop_orders = 8.0;
+    int max_outer_iters = 2000;
+};
+
+struct ConvergenceEntry {  // driver.hpp:50-58
+    int iter = 0;
+    double resid_mean = 0.0;
+    std::vector<double> resid_h;
+    double rz = 0.0;
+    int has_rz = 0;
+    double seconds = 0.0;  // cumulative device time of outer iterations
+};
+
+struct RkStepResult {  // rk.hpp:68-72
+    double stage1_residual_norm = 0.0;
+    int viscous_evaluations = 0;
+    std::vector<LinearSolveReport> linear_reports;
+};
+
+class DeviceSolver {
+public:
+    DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int* col_idx, const int* partition,
+                 const SchemeConfig& scheme, int nh, const int* index, const double* omega,
+                 const double* forcing_pairs, int nforcing, const double* mean0);
+    ~DeviceSolver();
+
+    ConvergenceEntry outer_iteration();
+    int run_to_convergence(std::vector<ConvergenceEntry>& history);  // 0 target, 1 cap, 2 divergence
+
+    void get_state(double* mean, double* amps_pairs) const;
+    void set_state(const double* mean, const double* amps_pairs);
+    void get_df(double* df) const;
+    const std::vector<LinearSolveReport>& reports() const { return reports_; }
+    std::size_t lhs_bytes() const;  // LHS value storage (A5 + real ILU + ONE complex ILU workspace)
+    int n() const { return disc_->n(); }
+    int b() const { return disc_->b(); }
+    int nh() const { return nh_; }
+    double sigma() const { return sigma_; }
+    cudaStream_t stream() const { return ws_->stream; }
+    // counters for the bench: total sweeps and block-row updates performed
+    long long sweeps = 0, row_updates = 0;
+    float last_iteration_ms = 0.0f;
+
+private:
+    template <class S, class Eval, class Apply>
+    RkStepResult rk_step(S* state, Eval&& eval, Apply&& apply, const SystemView<S>& A, const DeviceIlu<S>* ilu,
+                         const S* pdiag_lu, const int* pdiag_piv, const std::string& field);
+
+    SchemeConfig sch_;
+    double sigma_ = 50.0;
+    int nh_ = 0, nforcing_ = 0;
+    std::vector<int> index_;
+    std::vector<double> omega_;
+    std::unique_ptr<DevicePattern> pat_;
+    std::unique_ptr<DeviceDisc> disc_;
+    std::unique_ptr<Workspace> ws_;
+    DeviceBuffer<double> mean_, df_, A5_, P_, PLU_, shift_;
+    DeviceBuffer<int> Ppiv_, pcpiv_;
+    DeviceBuffer<cplx> amps_, forcing_, pclu_;
+    std::unique_ptr<DeviceIlu<double>> ilu_mean_;
+    std::unique_ptr<DeviceIlu<cplx>> ilu_h_;
+    DeviceBuffer<cplx> rk_[7];  // state0, inv, vis_fresh, vis_blend, rhs, x, stage (complex or reinterpreted real)
+    std::vector<LinearSolveReport> reports_;
+    int iter_ = 0;
+    double cum_seconds_ = 0.0;
+    cudaEvent_t ev0_, ev1_;
+};
+
+void build_lhs_mean_device(const double* J, double* A, int b, int n, const int* diag_idx, std::size_t nnzb,
+                           int implicit, double ga, double inv_es, cudaStream_t st);
+void harmonic_shift(const double* vol, int n, double omega, double ga, double* shift_im, cudaStream_t st);
+void shifted_blocks(const double* P, const double* vol, int b, int n, double omega, cplx* out, cudaStream_t st);
+
+}  // namespace fnlh

@@ -1,0 +1,174 @@
+"""Python mirror of the reference's operator / solver interface (disc.hpp,
+residual_ops.hpp, driver.hpp) over the device C ABI.  Names, argument meaning and
+error behaviour follow the reference; arrays use its layouts (node-major AoS)."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import FnlhError, LinearReport, as_pairs, check, f64, lib, ptr
+
+_i, _d, _p = C.c_int, C.c_double, C.c_void_p
+
+
+class MeshDesc(C.Structure):
+    _fields_ = [("n", _i), ("nf", _i), ("b", _i), ("fa", _p), ("fb", _p), ("fbc", _p), ("ford", _p), ("fn", _p),
+                ("farea", _p), ("fnh", _p), ("fvis", _p), ("vol", _p), ("closure", _p), ("mu", _p), ("nf_ptr", _p),
+                ("nf_idx", _p), ("bflag", _p), ("gamma", _d), ("gas_constant", _d), ("p0", _d), ("T0", _d),
+                ("p_out", _d), ("nt_in", _d), ("forcing_scale", _d)]
+
+
+class Scheme(C.Structure):
+    _fields_ = [("implicit", _i), ("sigma_cfl", _d), ("eps_relax", _d), ("linear_tol", _d), ("linear_max_iter", _i),
+                ("target_drop_orders", _d), ("max_outer_iters", _i)]
+
+
+class Entry(C.Structure):
+    _fields_ = [("iter", _i), ("resid_mean", _d), ("rz", _d), ("has_rz", _i), ("seconds", _d)]
+
+
+def _desc(m, keep):
+    arrs = [m.fa, m.fb, m.fbc, m.ford, m.fn, m.farea, m.fnh, m.fvis, m.vol, m.closure, m.mu, m.nf_ptr, m.nf_idx,
+            m.bflag]
+    keep.extend(arrs)
+    return MeshDesc(m.n, m.nf, m.b, *[ptr(a) for a in arrs], m.gamma, m.gas_constant, m.p0, m.T0, m.p_out, m.nt_in,
+                    m.forcing_scale)
+
+
+def scheme_struct(s: dict) -> Scheme:
+    return Scheme(int(s.get("implicit", 1)), float(s.get("sigma_cfl", -1.0)), float(s.get("eps_relax", 0.6)),
+                  float(s.get("linear_tol", 1e-2)), int(s.get("linear_max_iter", 10)),
+                  float(s.get("target_drop_orders", 8.0)), int(s.get("max_outer_iters", 2000)))
+
+
+class Discretization:
+    """Device-resident 3D edge-based discretization (disc.hpp:42-106 operator contract)."""
+
+    def __init__(self, mesh, pattern=None):
+        self.m = mesh
+        self._keep = []
+        pat = pattern or mesh.pattern()
+        self._keep += [pat["row_ptr"], pat["col_idx"], pat["partition"]]
+        self.desc = _desc(mesh, self._keep)
+        h = _p()
+        check(lib().fnlh_disc_create(C.byref(self.desc), ptr(pat["row_ptr"]), ptr(pat["col_idx"]),
+                                     ptr(pat["partition"]), C.byref(h)))
+        self.h = h
+        self.pattern = pat
+
+    def __del__(self):
+        try:
+            lib().fnlh_disc_destroy(self.h)
+        except Exception:
+            pass
+
+    def residual(self, W, order, mode=0, wref=None, forcing=None, need_vis=False):
+        n = self.m.n * self.m.b
+        inv, vis = np.zeros(n), np.zeros(n)
+        f = None if forcing is None else f64(forcing)
+        check(lib().fnlh_disc_residual(self.h, ptr(f64(W)), ptr(None if wref is None else f64(wref)), _i(order),
+                                       _i(mode), ptr(f), _i(0 if f is None else len(f)), _i(int(need_vis)), ptr(inv),
+                                       ptr(vis)))
+        return inv, vis
+
+    def fd_jacobian(self, W, want_J=True, want_P=False):
+        b = self.m.b
+        J = np.zeros(len(self.pattern["col_idx"]) * b * b) if want_J else None
+        P = np.zeros(self.m.n * b * b) if want_P else None
+        check(lib().fnlh_disc_fd_jacobian(self.h, ptr(f64(W)), ptr(J), ptr(P)))
+        return J, P
+
+    def linearized_residual(self, mean, what, omega, forcing, order=2, need_vis=True):
+        n = self.m.n * self.m.b
+        inv = np.zeros(n, np.complex128)
+        vis = np.zeros(n, np.complex128)
+        f = as_pairs(forcing)
+        check(lib().fnlh_disc_linearized_residual(self.h, ptr(f64(mean)), ptr(as_pairs(what)), _d(omega), ptr(f),
+                                                  _i(len(f) // 2), _i(order), _i(int(need_vis)),
+                                                  ptr(inv.view(np.float64)), ptr(vis.view(np.float64))))
+        return inv, vis
+
+    def deterministic_flux(self, mean, omegas, amps):
+        df = np.zeros(self.m.n * self.m.b)
+        om = f64(omegas)
+        check(lib().fnlh_disc_deterministic_flux(self.h, ptr(f64(mean)), _i(len(om)), ptr(om), ptr(as_pairs(amps)),
+                                                 ptr(df)))
+        return df
+
+
+class FnlhSolver:
+    """FnlhSolver (driver.hpp:83-126) on the device: outer_iteration / run_to_convergence."""
+
+    def __init__(self, mesh, scheme: dict, omegas, forcing, mean0, index=None, pattern=None):
+        self.m = mesh
+        self.nh = len(omegas)
+        self._keep = []
+        pat = pattern or mesh.pattern()
+        self._keep += [pat["row_ptr"], pat["col_idx"], pat["partition"]]
+        self.desc = _desc(mesh, self._keep)
+        self.scheme = scheme_struct(scheme)
+        idx = np.arange(1, self.nh + 1, dtype=np.int32) if index is None else np.asarray(index, np.int32)
+        om = f64(omegas)
+        fz = np.asarray(forcing, np.complex128).reshape(self.nh, -1) if self.nh else np.zeros((0, 0), np.complex128)
+        nforcing = fz.shape[1] if self.nh else 0
+        forc = as_pairs(fz.reshape(-1)) if fz.size else np.zeros(2)
+        self._keep += [idx, om, forc]
+        h = _p()
+        check(lib().fnlh_solver_create(C.byref(self.desc), ptr(pat["row_ptr"]), ptr(pat["col_idx"]),
+                                       ptr(pat["partition"]), C.byref(self.scheme), _i(self.nh), ptr(idx), ptr(om),
+                                       ptr(forc), _i(nforcing), ptr(f64(mean0)), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            lib().fnlh_solver_destroy(self.h)
+        except Exception:
+            pass
+
+    def outer_iteration(self):
+        e = Entry()
+        rh = np.zeros(max(self.nh, 1))
+        check(lib().fnlh_solver_outer_iteration(self.h, C.byref(e), ptr(rh)))
+        return dict(iter=e.iter, resid_mean=e.resid_mean, rz=e.rz, has_rz=bool(e.has_rz), resid_h=rh[: self.nh].copy(),
+                    seconds=e.seconds)
+
+    def run_to_convergence(self, max_entries=100000):
+        reason, n = _i(), _i()
+        arr = (Entry * max_entries)()
+        check(lib().fnlh_solver_run(self.h, C.byref(reason), C.byref(n), arr, _i(max_entries)))
+        hist = [dict(iter=e.iter, resid_mean=e.resid_mean, rz=e.rz) for e in arr[: min(n.value, max_entries)]]
+        return ["target-drop", "iteration-cap", "divergence"][reason.value], hist
+
+    def state(self):
+        n = self.m.n * self.m.b
+        mean = np.zeros(n)
+        amps = np.zeros(max(self.nh, 1) * n, np.complex128)
+        check(lib().fnlh_solver_get_state(self.h, ptr(mean), ptr(amps.view(np.float64))))
+        return mean, amps[: self.nh * n].reshape(self.nh, n)
+
+    def set_state(self, mean, amps):
+        check(lib().fnlh_solver_set_state(self.h, ptr(f64(mean)), ptr(as_pairs(amps))))
+
+    def df(self):
+        d = np.zeros(self.m.n * self.m.b)
+        check(lib().fnlh_solver_get_df(self.h, ptr(d)))
+        return d
+
+    def reports(self):
+        k = lib().fnlh_solver_num_reports(self.h)
+        arr = (LinearReport * max(k, 1))()
+        lib().fnlh_solver_get_reports(self.h, arr)
+        return [r.as_tuple() for r in arr[:k]]
+
+    def lhs_bytes(self):
+        lib().fnlh_solver_lhs_bytes.restype = _d
+        return int(lib().fnlh_solver_lhs_bytes(self.h))
+
+    def counters(self):
+        out = np.zeros(3)
+        lib().fnlh_solver_counters(self.h, ptr(out))
+        return dict(sweeps=int(out[0]), row_updates=int(out[1]), last_ms=float(out[2]))
+
+
+__all__ = ["Discretization", "FnlhSolver", "FnlhError"]

@@ -25,3 +25,10 @@ def ref():
     if not ref_available():
         pytest.skip("oracle/_ref/libfnlh_ref.so not built (needs /root/reference once)")
     return RefLib()
+
+
+@pytest.fixture(scope="session")
+def orc_dev():
+    """The restatement evaluating boundary-state pow like the device (correctly rounded)."""
+    from oracle.oracle import Oracle
+    return Oracle(pow_mode="cr")

@@ -1,0 +1,134 @@
+"""GPU parity of the discretization kernels and the full outer iteration against the
+CPU oracle (restatement) and, on the nozzle line mesh, against the reference itself.
+
+Tolerances: the north_star bar is 1e-10 relative per residual / update vector and
+1e-8 on the convergence history.  Most kernels are bitwise; the only libm call whose
+last bit may differ between glibc and CUDA is pow() in the subsonic inlet/outlet
+states, which the FD Jacobian amplifies by 1/delta at boundary nodes."""
+import numpy as np
+import pytest
+
+from helpers import (NOZZLE_CASE, embed, extract, forcing_triplets, line_mesh_from_ref, rel)
+from paper_2404_01407_b200.cases import make_case
+
+pytestmark = pytest.mark.gpu
+
+CASES = [("c1", 0.5), ("c2", 0.08), ("c3", 0.06), ("c5", 0.06)]
+
+
+@pytest.fixture(scope="module", params=CASES, ids=[c[0] for c in CASES])
+def case(request):
+    name, scale = request.param
+    c = make_case(name, scale=scale)
+    rng = np.random.default_rng(9)
+    n, b = c.mesh.n, c.mesh.b
+    W = c.mean0.copy()
+    what = (rng.standard_normal(n * b) + 1j * rng.standard_normal(n * b)) * 1e-3 * np.tile(
+        np.maximum(np.abs(W.reshape(n, b)).mean(0), 1e-3), n)
+    return c, what
+
+
+def test_residual(orc_dev, case):
+    from paper_2404_01407_b200.solver import Discretization
+    c, what = case
+    d = Discretization(c.mesh)
+    W = c.mean0
+    for order in (1, 2):
+        gi, gv = d.residual(W, order, need_vis=True)
+        oi, ov = orc_dev.residual(c.mesh, W, order, need_vis=True)
+        assert np.array_equal(gi, oi), (order, rel(gi, oi))
+        assert np.array_equal(gv, ov)
+    Wp = W + 1e-4 * what.real
+    f = c.forcing[0].real * 3.0
+    gi, _ = d.residual(Wp, 2, mode=1, wref=W, forcing=f)
+    oi, _ = orc_dev.residual(c.mesh, Wp, 2, mode=1, wref=W, forcing=f)
+    assert rel(gi, oi) < 1e-13
+
+
+def test_fd_jacobian(orc_dev, case):
+    from paper_2404_01407_b200.solver import Discretization
+    c, _ = case
+    d = Discretization(c.mesh)
+    pat = c.mesh.pattern()
+    gJ, gP = d.fd_jacobian(c.mean0, want_J=True, want_P=True)
+    oJ, oP = orc_dev.fd_jacobian(c.mesh, pat, c.mean0, want_J=True, want_P=True)
+    assert np.array_equal(gJ, oJ)
+    assert np.array_equal(gP, oP)
+
+
+def test_linearized_residual_and_df(orc_dev, case):
+    from paper_2404_01407_b200.solver import Discretization
+    c, what = case
+    d = Discretization(c.mesh)
+    gi, gv = d.linearized_residual(c.mean0, what, c.omegas[0], c.forcing[0])
+    oi, ov = orc_dev.linearized_residual(c.mesh, c.mean0, what, c.omegas[0], c.forcing[0])
+    assert rel(gi, oi) < 1e-10
+    if c.mesh.b == 6:
+        assert rel(gv, ov) < 1e-10
+    amps = np.stack([what * (0.5 ** h) for h in range(len(c.omegas))])
+    gd = d.deterministic_flux(c.mean0, c.omegas, amps)
+    od = orc_dev.deterministic_flux(c.mesh, c.mean0, c.omegas, amps)
+    assert rel(gd, od) < 1e-10
+
+
+@pytest.mark.parametrize("name,scale,steps", [("c1", 0.5, 20), ("c3", 0.06, 3), ("c5", 0.06, 3)])
+def test_outer_iteration_history(orc_dev, name, scale, steps):
+    from paper_2404_01407_b200.solver import FnlhSolver
+    c = make_case(name, scale=scale)
+    g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
+    o = orc_dev.solver(c.mesh, c.mesh.pattern(), c.scheme, c.omegas, c.forcing, c.mean0)
+    for it in range(steps):
+        eg, eo = g.outer_iteration(), o.outer_iteration()
+        assert abs(eg["resid_mean"] / eo["resid_mean"] - 1) < 1e-8, (it, eg, eo)
+        assert abs(eg["rz"] / eo["rz"] - 1) < 1e-8, (it, eg, eo)
+    mg, ag = g.state()
+    mo, ao = o.state()
+    assert rel(mg, mo) < 1e-10 and rel(ag, ao) < 1e-10
+    rg, ro = g.reports(), o.reports()
+    assert [r[0] for r in rg] == [r[0] for r in ro]
+
+
+def test_explicit_mode(orc_dev):
+    from paper_2404_01407_b200.solver import FnlhSolver
+    c = make_case("c5", scale=0.06, implicit=False)
+    g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
+    o = orc_dev.solver(c.mesh, c.mesh.pattern(), c.scheme, c.omegas, c.forcing, c.mean0)
+    for it in range(4):
+        eg, eo = g.outer_iteration(), o.outer_iteration()
+        assert abs(eg["resid_mean"] / eo["resid_mean"] - 1) < 1e-8
+        assert abs(eg["rz"] / eo["rz"] - 1) < 1e-8
+    mg, ag = g.state()
+    mo, ao = o.state()
+    assert rel(mg, mo) < 1e-10 and rel(ag, ao) < 1e-10
+
+
+def test_lhs_memory_independent_of_harmonic_count():
+    """SPEC.md:373,745 / PAPER.md:227: LHS bytes identical for N_h = 1, 2, 4, 8."""
+    from paper_2404_01407_b200.solver import FnlhSolver
+    sizes = set()
+    for nh in (1, 2, 4, 8):
+        c = make_case("c1", scale=0.5, nh=nh)
+        sizes.add(FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0).lhs_bytes())
+    assert len(sizes) == 1
+
+
+def test_nozzle_against_reference(ref):
+    """The reference's own FnlhSolver on its nozzle case vs the device solver on the
+    embedded line mesh (b = 5, v = w = 0)."""
+    from paper_2404_01407_b200.solver import FnlhSolver
+    case = NOZZLE_CASE.format(nx=64, nh=2)
+    rs = ref.solver(case)
+    noz = rs.noz
+    m = line_mesh_from_ref(noz)
+    forc = np.stack([forcing_triplets(f) for f in noz.forcing])
+    g = FnlhSolver(m, dict(implicit=1), noz.omega, forc, embed(noz.initial_mean(), noz.n), pattern=noz.pattern(5))
+    s = np.sqrt(5 / 3)
+    for it in range(10):
+        er, eg = rs.outer_iteration(), g.outer_iteration()
+        tol = 1e-12 if it == 0 else 1e-7
+        assert abs(eg["resid_mean"] * s / er["resid_mean"] - 1) < tol, (it, er, eg)
+        assert abs(eg["rz"] * s / er["rz"] - 1) < tol, (it, er, eg)
+    mr, ar = rs.state()
+    mg, ag = g.state()
+    assert rel(extract(mg, noz.n), mr) < 1e-12
+    assert rel(np.stack([extract(a, noz.n) for a in ag]), ar) < 1e-8
