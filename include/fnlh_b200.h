@@ -145,6 +145,9 @@ int fnlh_solver_num_reports(const fnlh_solver* s);
 int fnlh_solver_get_reports(const fnlh_solver* s, fnlh_linear_report* out);
 /* LHS value bytes (A5 + real ILU + one complex ILU workspace): independent of nh */
 double fnlh_solver_lhs_bytes(const fnlh_solver* s);
+/* time `sweeps` Richardson sweeps (smoothed_solve, sparse.hpp:315-329) of harmonic h's system at
+   the current mean; *ms = device time of the loop */
+int fnlh_solver_time_sweeps(fnlh_solver* s, int h, int sweeps, double* ms);
 /* counters: [sweeps, block-row updates, last outer iteration device ms] */
 int fnlh_solver_counters(const fnlh_solver* s, double* out);
 

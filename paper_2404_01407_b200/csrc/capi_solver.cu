@@ -198,6 +198,10 @@ int fnlh_solver_get_reports(const fnlh_solver* s, fnlh_linear_report* out) {
     return 0;
 }
 
+int fnlh_solver_time_sweeps(fnlh_solver* s, int h, int sweeps, double* ms) {
+    return guarded([&] { *ms = s->s->time_harmonic_sweeps(h, sweeps); });
+}
+
 double fnlh_solver_lhs_bytes(const fnlh_solver* s) { return static_cast<double>(s->s->lhs_bytes()); }
 
 int fnlh_solver_counters(const fnlh_solver* s, double* out) {

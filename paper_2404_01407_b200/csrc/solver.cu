@@ -316,6 +316,36 @@ ConvergenceEntry DeviceSolver::outer_iteration() {
     return e;
 }
 
+double DeviceSolver::time_harmonic_sweeps(int h, int nsweeps) {
+    if (!sch_.implicit) throw ConfigError("time_harmonic_sweeps: implicit scheme only");
+    cudaStream_t st = ws_->stream;
+    const int n = disc_->n(), b = disc_->b();
+    const std::size_t len = disc_->len();
+    const double ga5 = (1.0 / sch_.eps_relax) * kAlpha[4];
+    disc_->fd_jacobian(mean_.ptr, A5_.ptr, nullptr, st);
+    build_lhs_mean_device(A5_.ptr, A5_.ptr, b, n, pat_->diag_idx, pat_->nnzb, 1, ga5, 1.0 / (sch_.eps_relax * sigma_),
+                          st);
+    harmonic_shift(disc_->view().vol, n, omega_[h], ga5, shift_.ptr, st);
+    SystemView<cplx> Ah;
+    Ah.p = pat_.get();
+    Ah.real_vals = A5_.ptr;
+    Ah.shift_im = shift_.ptr;
+    ilu_factorize<cplx>(Ah, *ilu_h_, *ws_);
+    // rhs: the harmonic's current linearized residual direction (any nonzero vector works)
+    cplx* rhs = rk_[4].ptr;
+    cplx* x = rk_[5].ptr;
+    disc_->linearized_residual(mean_.ptr, amps_.ptr + (std::size_t)h * len, omega_[h],
+                               forcing_.ptr + (std::size_t)h * nforcing_, nforcing_, 2, false, rhs, nullptr, st);
+    FNLH_CUDA(cudaStreamSynchronize(st));
+    FNLH_CUDA(cudaEventRecord(ev0_, st));
+    smoothed_solve<cplx>(Ah, rhs, *ilu_h_, 1e-300, nsweeps, x, *ws_);
+    FNLH_CUDA(cudaEventRecord(ev1_, st));
+    FNLH_CUDA(cudaEventSynchronize(ev1_));
+    float ms = 0.0f;
+    FNLH_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    return ms;
+}
+
 int DeviceSolver::run_to_convergence(std::vector<ConvergenceEntry>& history) {  // driver.cpp:335-379
     const double drop = std::pow(10.0, -sch_.target_drop_orders);
     double r1_mean = -1.0, r1_rz = -1.0, floor_ = 0.0;

@@ -57,6 +57,9 @@ public:
     int nh() const { return nh_; }
     double sigma() const { return sigma_; }
     cudaStream_t stream() const { return ws_->stream; }
+    // time `sweeps` Richardson sweeps of harmonic h's system at the current mean (factorizes
+    // it first); returns device ms for the whole loop (bench.py roofline leg)
+    double time_harmonic_sweeps(int h, int sweeps);
     // counters for the bench: total sweeps and block-row updates performed
     long long sweeps = 0, row_updates = 0;
     float last_iteration_ms = 0.0f;

@@ -165,6 +165,11 @@ class FnlhSolver:
         lib().fnlh_solver_lhs_bytes.restype = _d
         return int(lib().fnlh_solver_lhs_bytes(self.h))
 
+    def time_sweeps(self, h, sweeps):
+        ms = _d()
+        check(lib().fnlh_solver_time_sweeps(self.h, _i(h), _i(sweeps), C.byref(ms)))
+        return ms.value
+
     def counters(self):
         out = np.zeros(3)
         lib().fnlh_solver_counters(self.h, ptr(out))
