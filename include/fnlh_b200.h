@@ -79,6 +79,15 @@ int fnlh_smoothed_solve(const fnlh_pattern* p, int is_complex, const double* A, 
                         const double* shift_im, const double* rhs, double tol_rel, int max_iter, double* x,
                         fnlh_linear_report* rep);
 
+/* 2-colour fast path (rb.cuh): *n0 = size of colour 0 when the pattern is a colour-major
+   2-colour ordering with one partition, else -1.  fnlh_set_red_black(0) forces the general
+   level-scheduled kernels everywhere (both paths are bitwise the reference's iterates). */
+int fnlh_pattern_is_red_black(fnlh_pattern* p, int* n0);
+/* compact factors of the 2-colour ILU(0): pivot LU + piv for every row, inv(U_kk) for colour 0 */
+int fnlh_rb_factorize(fnlh_pattern* p, int is_complex, const double* A, const double* shift_im, double* diag_lu,
+                      int* diag_piv, double* inv0);
+void fnlh_set_red_black(int enable);
+
 /* ---- L2/L3: the 3D edge-based discretization ---------------------------------
    Node-centred median-dual mesh (paper_2404_01407_b200/mesh.py builds one):
    faces a->b with area-weighted normals fn (outward on inlet/outlet faces), slip
@@ -148,6 +157,8 @@ double fnlh_solver_lhs_bytes(const fnlh_solver* s);
 /* time `sweeps` Richardson sweeps (smoothed_solve, sparse.hpp:315-329) of harmonic h's system at
    the current mean; *ms = device time of the loop */
 int fnlh_solver_time_sweeps(fnlh_solver* s, int h, int sweeps, double* ms);
+/* [red_black (0/1), n0 (colour 0 rows), SELL doubles incl. padding, nnzb] */
+int fnlh_solver_info(const fnlh_solver* s, double* out);
 /* counters: [sweeps, block-row updates, last outer iteration device ms] */
 int fnlh_solver_counters(const fnlh_solver* s, double* out);
 

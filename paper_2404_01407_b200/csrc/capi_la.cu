@@ -5,11 +5,18 @@
 #include "fnlh_b200.h"
 #include "capi_util.hpp"
 #include "la.cuh"
+#include "rb.cuh"
 
 using namespace fnlh;
 
 struct fnlh_pattern {
     std::unique_ptr<DevicePattern> p;
+    int rb = -1;  // -1 unknown, 0 no, 1 yes (2-colour colour-major, single partition)
+    int n0 = 0;
+    bool use_rb() {
+        if (rb < 0) rb = rb_eligible(*p, &n0) ? 1 : 0;
+        return rb == 1 && fnlh::rb_enabled();
+    }
 };
 
 namespace {
@@ -88,6 +95,54 @@ int matvec_impl(const fnlh_pattern* p, const double* A, int A_complex, const dou
 }
 
 template <class S>
+int solve_rb(fnlh_pattern* p, const double* A, const double* shift_im, const double* rhs, double tol, int max_iter,
+             double* x, fnlh_linear_report* rep) {
+    const DevicePattern* dp = p->p.get();
+    const std::size_t len = (std::size_t)dp->rows * dp->b;
+    Workspace ws(len);
+    DeviceBuffer<double> a, sh;
+    a.upload(A, (std::size_t)dp->nnzb * dp->b * dp->b);
+    if (shift_im) sh.upload(shift_im, dp->rows);
+    RbSystem sys(dp, p->n0);
+    sys.load(a.ptr, ws.stream);
+    RbIlu<S> f(dp, p->n0);
+    rb_factorize<S>(sys, shift_im ? sh.ptr : nullptr, f, ws);
+    DeviceBuffer<S> b, xv, z, r;
+    DeviceBuffer<RbControl> ctl(1);
+    b.upload(reinterpret_cast<const S*>(rhs), len);
+    xv.alloc(len);
+    z.alloc(len);
+    r.alloc(len);
+    rb_smoothed_solve<S>(sys, shift_im ? sh.ptr : nullptr, f, b.ptr, tol, max_iter, xv.ptr, z.ptr, r.ptr, ctl.ptr, ws);
+    FNLH_CUDA(cudaStreamSynchronize(ws.stream));
+    RbControl h;
+    download(&h, ctl.ptr, 1);
+    download(reinterpret_cast<S*>(x), xv.ptr, len);
+    if (h.status == 6) throw DivergenceError("non-finite iterate in smoothed_solve", h.iterations, "linear");
+    if (rep) *rep = fnlh_linear_report{h.iterations, h.initial_residual, h.final_residual, h.converged};
+    return 0;
+}
+
+template <class S>
+int rb_factor_impl(fnlh_pattern* p, const double* A, const double* shift_im, double* diag_lu, int* diag_piv,
+                   double* inv0) {
+    const DevicePattern* dp = p->p.get();
+    Workspace ws(1);
+    DeviceBuffer<double> a, sh;
+    a.upload(A, (std::size_t)dp->nnzb * dp->b * dp->b);
+    if (shift_im) sh.upload(shift_im, dp->rows);
+    RbSystem sys(dp, p->n0);
+    sys.load(a.ptr, ws.stream);
+    RbIlu<S> f(dp, p->n0);
+    rb_factorize<S>(sys, shift_im ? sh.ptr : nullptr, f, ws);
+    const std::size_t bb = (std::size_t)dp->b * dp->b;
+    if (diag_lu) download(reinterpret_cast<S*>(diag_lu), f.diag_lu, (std::size_t)dp->rows * bb);
+    if (diag_piv) download(diag_piv, f.diag_piv, (std::size_t)dp->rows * dp->b);
+    if (inv0) download(reinterpret_cast<S*>(inv0), f.inv0, (std::size_t)p->n0 * bb);
+    return 0;
+}
+
+template <class S>
 int solve_impl(const fnlh_pattern* p, const double* A, int A_complex, const double* shift_im, const double* rhs,
                double tol, int max_iter, double* x, fnlh_linear_report* rep) {
     const DevicePattern* dp = p->p.get();
@@ -161,11 +216,41 @@ int fnlh_smoothed_solve(const fnlh_pattern* p, int is_complex, const double* A, 
                         const double* shift_im, const double* rhs, double tol_rel, int max_iter, double* x,
                         fnlh_linear_report* rep) {
     return guarded([&] {
+        fnlh_pattern* pm = const_cast<fnlh_pattern*>(p);
+        if (!A_complex && pm->use_rb()) {  // the 2-colour fused path (rb.cuh)
+            if (is_complex)
+                solve_rb<cplx>(pm, A, shift_im, rhs, tol_rel, max_iter, x, rep);
+            else
+                solve_rb<double>(pm, A, nullptr, rhs, tol_rel, max_iter, x, rep);
+            return;
+        }
         if (is_complex)
             solve_impl<cplx>(p, A, A_complex, shift_im, rhs, tol_rel, max_iter, x, rep);
         else
             solve_impl<double>(p, A, 0, nullptr, rhs, tol_rel, max_iter, x, rep);
     });
 }
+
+int fnlh_pattern_is_red_black(fnlh_pattern* p, int* n0) {
+    return guarded([&] {
+        *n0 = -1;
+        if (p->rb < 0) p->rb = rb_eligible(*p->p, &p->n0) ? 1 : 0;
+        if (p->rb == 1) *n0 = p->n0;
+    });
+}
+
+int fnlh_rb_factorize(fnlh_pattern* p, int is_complex, const double* A, const double* shift_im, double* diag_lu,
+                      int* diag_piv, double* inv0) {
+    return guarded([&] {
+        if (p->rb < 0) p->rb = rb_eligible(*p->p, &p->n0) ? 1 : 0;
+        if (p->rb != 1) throw ShapeError("pattern is not a 2-colour colour-major ordering with one partition");
+        if (is_complex)
+            rb_factor_impl<cplx>(p, A, shift_im, diag_lu, diag_piv, inv0);
+        else
+            rb_factor_impl<double>(p, A, nullptr, diag_lu, diag_piv, inv0);
+    });
+}
+
+void fnlh_set_red_black(int enable) { fnlh::rb_enabled() = enable != 0; }
 
 }  // extern "C"

@@ -204,6 +204,10 @@ int fnlh_solver_time_sweeps(fnlh_solver* s, int h, int sweeps, double* ms) {
 
 double fnlh_solver_lhs_bytes(const fnlh_solver* s) { return static_cast<double>(s->s->lhs_bytes()); }
 
+int fnlh_solver_info(const fnlh_solver* s, double* out) {
+    return guarded([&] { s->s->info(out); });
+}
+
 int fnlh_solver_counters(const fnlh_solver* s, double* out) {
     out[0] = static_cast<double>(s->s->sweeps);
     out[1] = static_cast<double>(s->s->row_updates);

@@ -1,0 +1,584 @@
+// rb.cu -- 2-colour fused ILU(0)-Richardson sweep (see rb.cuh for the derivation).
+#include <algorithm>
+#include <vector>
+
+#include "rb.cuh"
+
+namespace fnlh {
+
+namespace {
+
+constexpr int kT = 128;  // 4 slices of 32 rows per CTA
+inline int nb(long long n) { return static_cast<int>((n + kT - 1) / kT); }
+
+struct SellDev {
+    const long long* __restrict__ slice_val;
+    const int* __restrict__ slice_col;
+    const int* __restrict__ deg;
+    const int* __restrict__ cols;
+    const double* __restrict__ vals;
+    int n, n0, nslices0;
+};
+
+struct RowRef {
+    long long vbase;  // vals offset of (slot 0, element 0) for this row
+    int cbase;        // cols offset of slot 0 for this row
+    int deg;
+};
+
+__device__ __forceinline__ RowRef row_ref(const SellDev& L, int i) {
+    const int li = i < L.n0 ? i : i - L.n0;
+    const int s = (i < L.n0 ? 0 : L.nslices0) + (li >> 5);
+    const int lane = li & 31;
+    return RowRef{L.slice_val[s] + lane, L.slice_col[s] + lane, L.deg[i]};
+}
+
+template <int B>
+__device__ __forceinline__ double aval(const SellDev& L, const RowRef& r, int e, int k) {
+    return __ldg(L.vals + r.vbase + (long long)(e * B * B + k) * 32);
+}
+
+__device__ __forceinline__ int acol(const SellDev& L, const RowRef& r, int e) { return __ldg(L.cols + r.cbase + e * 32); }
+
+// y[r] += sum_c A_e[r][c] x[c] (block_matvec_add, dense.hpp:20-28); the diagonal block of
+// a shifted system carries complex(a + 0, 0 + s) on its diagonal (shift_diagonal)
+template <int B, class S>
+__device__ __forceinline__ void blk_matvec_add(const SellDev& L, const RowRef& rr, int e, const S (&x)[B],
+                                               bool diag, double s, S (&y)[B]) {
+#pragma unroll
+    for (int r = 0; r < B; ++r) {
+        S acc = zero<S>();
+#pragma unroll
+        for (int c = 0; c < B; ++c) {
+            const double a = aval<B>(L, rr, e, r * B + c);
+            if constexpr (sizeof(S) == sizeof(cplx)) {
+                if (diag && r == c)
+                    acc += mk(a + 0.0, 0.0 + s) * x[c];
+                else
+                    acc += rmul(a, x[c]);
+            } else {
+                acc += rmul(a, x[c]);
+            }
+        }
+        y[r] += acc;
+    }
+}
+
+// y[r] -= sum_c A_e[r][c] x[c] (block_matvec_sub with U_ij = complex(A_ij))
+template <int B, class S>
+__device__ __forceinline__ void blk_matvec_sub(const SellDev& L, const RowRef& rr, int e, const S (&x)[B],
+                                               S (&y)[B]) {
+#pragma unroll
+    for (int r = 0; r < B; ++r) {
+        S acc = zero<S>();
+#pragma unroll
+        for (int c = 0; c < B; ++c) acc += rmul(aval<B>(L, rr, e, r * B + c), x[c]);
+        y[r] -= acc;
+    }
+}
+
+template <int B, class S>
+__device__ __forceinline__ void ld(const S* __restrict__ p, S (&v)[B]) {
+#pragma unroll
+    for (int k = 0; k < B; ++k) v[k] = p[k];
+}
+template <int B, class S>
+__device__ __forceinline__ void st(S* __restrict__ p, const S (&v)[B]) {
+#pragma unroll
+    for (int k = 0; k < B; ++k) p[k] = v[k];
+}
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < kT / 32; ++w) s += red[w];
+    return s;
+}
+
+// fixed-order sum of partials by one CTA (deterministic run to run)
+__device__ double ordered_sum(const double* __restrict__ p, int n, double* red) {
+    double s = 0.0;
+    const int chunk = (n + kT - 1) / kT;
+    const int b0 = threadIdx.x * chunk, b1 = min(n, b0 + chunk);
+    for (int k = b0; k < b1; ++k) s += p[k];
+    __syncthreads();
+    return block_sum(s, red);
+}
+
+// ---- pre-kernel: ||b||, target, x = 0 --------------------------------------
+template <class S>
+__global__ void k_rb_init(std::size_t len, const S* __restrict__ rhs, double* __restrict__ partials, int nparts,
+                          RbControl* ctl, double tol, unsigned int* counter) {
+    __shared__ double red[kT / 32];
+    __shared__ bool last;
+    double loc = 0.0;
+    for (std::size_t t = blockIdx.x * (std::size_t)kT + threadIdx.x; t < len; t += (std::size_t)gridDim.x * kT)
+        loc += sq(rhs[t]);
+    const double bs = block_sum(loc, red);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = bs;
+        __threadfence();
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    const double tot = ordered_sum(partials, gridDim.x, red);
+    if (threadIdx.x == 0) {
+        const double r0 = sqrt(tot);
+        ctl->initial_residual = r0;
+        ctl->final_residual = r0;
+        ctl->target = tol * r0;
+        ctl->iterations = 0;
+        ctl->converged = r0 == 0.0 ? 1 : 0;
+        ctl->done = r0 == 0.0 ? 1 : 0;
+        ctl->status = 0;
+        *counter = 0u;
+    }
+    (void)nparts;
+}
+
+// ---- K_B: colour 0 rows -----------------------------------------------------
+template <int B, class S>
+__global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const double* __restrict__ shift,
+                                                   const S* __restrict__ diag_lu, const int* __restrict__ piv,
+                                                   const S* __restrict__ rhs, S* __restrict__ x,
+                                                   const S* __restrict__ z, S* __restrict__ r,
+                                                   double* __restrict__ partials0, const RbControl* ctl, int sweep) {
+    __shared__ double red[kT / 32];
+    if (ctl->done) return;
+    const int i = blockIdx.x * kT + threadIdx.x;
+    double loc = 0.0;
+    if (i < L.n0) {
+        const RowRef rr = row_ref(L, i);
+        S t[B];
+        ld<B>((sweep == 1 ? rhs : r) + (size_t)i * B, t);  // forward: colour 0 rows copy r
+        // backward substitution, descending columns (sparse.cpp:280-290)
+        for (int e = rr.deg - 1; e >= 1; --e) {
+            S zj[B];
+            ld<B>(z + (size_t)acol(L, rr, e) * B, zj);
+            blk_matvec_sub<B, S>(L, rr, e, zj, t);
+        }
+        S lu[B * B];
+        int pv[B];
+#pragma unroll
+        for (int k = 0; k < B * B; ++k) lu[k] = diag_lu[(size_t)i * B * B + k];
+#pragma unroll
+        for (int k = 0; k < B; ++k) pv[k] = piv[(size_t)i * B + k];
+        lu_solve_reg<B>(lu, pv, t);
+        S xi[B];
+        ld<B>(x + (size_t)i * B, xi);
+#pragma unroll
+        for (int k = 0; k < B; ++k) xi[k] += t[k];  // x += z (sparse.hpp:317)
+        st<B>(x + (size_t)i * B, xi);
+        // residual row (sparse.hpp:318-319), ascending columns: diagonal first
+        S y[B];
+#pragma unroll
+        for (int k = 0; k < B; ++k) y[k] = zero<S>();
+        const double s = shift ? shift[i] : 0.0;
+        blk_matvec_add<B, S>(L, rr, 0, xi, shift != nullptr, s, y);
+        for (int e = 1; e < rr.deg; ++e) {
+            const int j = acol(L, rr, e);
+            S xj[B], zj[B];
+            ld<B>(x + (size_t)j * B, xj);
+            ld<B>(z + (size_t)j * B, zj);
+#pragma unroll
+            for (int k = 0; k < B; ++k) xj[k] += zj[k];  // colour-1 x += z, applied lazily
+            blk_matvec_add<B, S>(L, rr, e, xj, false, 0.0, y);
+        }
+        S bi[B];
+        ld<B>(rhs + (size_t)i * B, bi);
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            const S v = bi[k] - y[k];
+            r[(size_t)i * B + k] = v;
+            loc += sq(v);
+        }
+    }
+    const double bs = block_sum(loc, red);
+    if (threadIdx.x == 0) partials0[blockIdx.x] = bs;
+}
+
+// ---- K_A: colour 1 rows -----------------------------------------------------
+template <int B, class S>
+__global__ void __launch_bounds__(kT) k_rb_colour1(SellDev L, const double* __restrict__ shift,
+                                                   const S* __restrict__ diag_lu, const int* __restrict__ piv,
+                                                   const S* __restrict__ inv0, const S* __restrict__ rhs,
+                                                   S* __restrict__ x, S* __restrict__ z, const S* __restrict__ r,
+                                                   double* __restrict__ partials, int grid0, RbControl* ctl,
+                                                   int sweep, int forward, int max_iter, unsigned int* counter) {
+    __shared__ double red[kT / 32];
+    __shared__ bool last;
+    if (ctl->done) return;
+    const int i = L.n0 + blockIdx.x * kT + threadIdx.x;
+    double loc = 0.0;
+    if (i < L.n) {
+        const RowRef rr = row_ref(L, i);
+        const int dg = rr.deg - 1;  // diagonal is the last slot
+        S ri[B];
+        const double s = shift ? shift[i] : 0.0;
+        ld<B>(rhs + (size_t)i * B, ri);
+        if (sweep > 1) {
+            S xi[B], zi[B];
+            ld<B>(x + (size_t)i * B, xi);
+            ld<B>(z + (size_t)i * B, zi);
+#pragma unroll
+            for (int k = 0; k < B; ++k) xi[k] += zi[k];
+            st<B>(x + (size_t)i * B, xi);
+            S y[B];
+#pragma unroll
+            for (int k = 0; k < B; ++k) y[k] = zero<S>();
+            for (int e = 0; e < dg; ++e) {
+                S xk[B];
+                ld<B>(x + (size_t)acol(L, rr, e) * B, xk);
+                blk_matvec_add<B, S>(L, rr, e, xk, false, 0.0, y);
+            }
+            blk_matvec_add<B, S>(L, rr, dg, xi, shift != nullptr, s, y);
+#pragma unroll
+            for (int k = 0; k < B; ++k) {
+                ri[k] = ri[k] - y[k];
+                loc += sq(ri[k]);
+            }
+        }
+        if (forward) {
+            // forward substitution with L_ik = A_ik inv(U_kk), rebuilt in the reference's
+            // order (sparse.cpp:221-232 then dense.hpp:31-39)
+            S zf[B];
+#pragma unroll
+            for (int k = 0; k < B; ++k) zf[k] = ri[k];
+            for (int e = 0; e < dg; ++e) {
+                const int kk = acol(L, rr, e);
+                S zk[B];
+                ld<B>((sweep == 1 ? rhs : r) + (size_t)kk * B, zk);
+                S U[B * B];
+#pragma unroll
+                for (int q = 0; q < B * B; ++q) U[q] = inv0[(size_t)kk * B * B + q];
+#pragma unroll
+                for (int rw = 0; rw < B; ++rw) {
+                    double arow[B];
+#pragma unroll
+                    for (int m = 0; m < B; ++m) arow[m] = aval<B>(L, rr, e, rw * B + m);
+                    S acc = zero<S>();
+#pragma unroll
+                    for (int c = 0; c < B; ++c) {
+                        S lrc = zero<S>();
+#pragma unroll
+                        for (int m = 0; m < B; ++m) lrc += rmul(arow[m], U[m * B + c]);
+                        acc += lrc * zk[c];
+                    }
+                    zf[rw] -= acc;
+                }
+            }
+            S lu[B * B];
+            int pv[B];
+#pragma unroll
+            for (int k = 0; k < B * B; ++k) lu[k] = diag_lu[(size_t)i * B * B + k];
+#pragma unroll
+            for (int k = 0; k < B; ++k) pv[k] = piv[(size_t)i * B + k];
+            lu_solve_reg<B>(lu, pv, zf);  // colour 1 rows have no upper entries
+            st<B>(z + (size_t)i * B, zf);
+        }
+    }
+    if (sweep == 1) return;
+    const double bs = block_sum(loc, red);
+    if (threadIdx.x == 0) {
+        partials[grid0 + blockIdx.x] = bs;
+        __threadfence();
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    // stopping rule of sweep - 1 (sparse.hpp:320-328), decided on the device
+    const double tot = ordered_sum(partials, grid0 + gridDim.x, red);
+    if (threadIdx.x == 0) {
+        const double nrm = sqrt(tot);
+        ctl->iterations = sweep - 1;
+        ctl->final_residual = nrm;
+        if (!isfinite(nrm)) {
+            ctl->status = 6;
+            ctl->done = 1;
+        } else if (nrm <= ctl->target) {
+            ctl->converged = 1;
+            ctl->done = 1;
+        } else if (sweep - 1 >= max_iter) {
+            ctl->done = 1;
+        }
+        *counter = 0u;
+    }
+}
+
+// ---- factorization ---------------------------------------------------------
+template <int B, class S>
+__global__ void k_rb_factor0(SellDev L, const double* __restrict__ shift, S* __restrict__ diag_lu,
+                             int* __restrict__ piv, S* __restrict__ inv0, int* __restrict__ status) {
+    const int i = blockIdx.x * kT + threadIdx.x;
+    if (i >= L.n0) return;
+    const RowRef rr = row_ref(L, i);
+    S A[B * B];
+#pragma unroll
+    for (int k = 0; k < B * B; ++k) {
+        A[k] = from_real<S>(aval<B>(L, rr, 0, k));
+        if constexpr (sizeof(S) == sizeof(cplx))
+            if (shift && (k / B == k % B)) A[k] = A[k] + mk(0.0, shift[i]);
+    }
+    int pv[B];
+    double cond;
+    if (lu_factor_reg<B>(A, pv, cond) || !(cond < 1e14)) atomicMin(status + 1, i);
+#pragma unroll
+    for (int k = 0; k < B * B; ++k) diag_lu[(size_t)i * B * B + k] = A[k];
+#pragma unroll
+    for (int k = 0; k < B; ++k) piv[(size_t)i * B + k] = pv[k];
+#pragma unroll
+    for (int c = 0; c < B; ++c) {
+        S col[B];
+#pragma unroll
+        for (int r = 0; r < B; ++r) col[r] = (r == c) ? one<S>() : zero<S>();
+        lu_solve_reg<B>(A, pv, col);
+#pragma unroll
+        for (int r = 0; r < B; ++r) inv0[(size_t)i * B * B + r * B + c] = col[r];
+    }
+}
+
+template <int B, class S>
+__global__ void k_rb_factor1(SellDev L, const int* __restrict__ row_ptr, const long long* __restrict__ trans,
+                             const double* __restrict__ shift, S* __restrict__ diag_lu, int* __restrict__ piv,
+                             const S* __restrict__ inv0, int* __restrict__ status) {
+    const int i = L.n0 + blockIdx.x * kT + threadIdx.x;
+    if (i >= L.n) return;
+    const RowRef rr = row_ref(L, i);
+    const int dg = rr.deg - 1;
+    S Uii[B * B];
+#pragma unroll
+    for (int k = 0; k < B * B; ++k) {
+        Uii[k] = from_real<S>(aval<B>(L, rr, dg, k));
+        if constexpr (sizeof(S) == sizeof(cplx))
+            if (shift && (k / B == k % B)) Uii[k] = Uii[k] + mk(0.0, shift[i]);
+    }
+    const int e0 = row_ptr[i];
+    for (int e = 0; e < dg; ++e) {
+        const int kk = acol(L, rr, e);
+        const S* U = inv0 + (size_t)kk * B * B;
+        S Lb[B * B];
+#pragma unroll
+        for (int r = 0; r < B; ++r)
+#pragma unroll
+            for (int c = 0; c < B; ++c) {
+                S acc = zero<S>();
+#pragma unroll
+                for (int m = 0; m < B; ++m) acc += from_real<S>(aval<B>(L, rr, e, r * B + m)) * U[m * B + c];
+                Lb[r * B + c] = acc;
+            }
+        // U_ii -= L_ik U_ki, U_ki = complex(A_ki) (block_matmul_sub, dense.hpp:42-52)
+        const double* Aki = L.vals + trans[e0 + e];
+#pragma unroll
+        for (int r = 0; r < B; ++r)
+#pragma unroll
+            for (int k2 = 0; k2 < B; ++k2) {
+                const S a = Lb[r * B + k2];
+                if (is_zero(a)) continue;
+#pragma unroll
+                for (int c = 0; c < B; ++c) Uii[r * B + c] -= a * from_real<S>(Aki[(long long)(k2 * B + c) * 32]);
+            }
+    }
+    int pv[B];
+    double cond;
+    if (lu_factor_reg<B>(Uii, pv, cond) || !(cond < 1e14)) atomicMin(status + 1, i);
+#pragma unroll
+    for (int k = 0; k < B * B; ++k) diag_lu[(size_t)i * B * B + k] = Uii[k];
+#pragma unroll
+    for (int k = 0; k < B; ++k) piv[(size_t)i * B + k] = pv[k];
+}
+
+__global__ void k_to_sell(const double* __restrict__ A, const long long* __restrict__ map, int bb, long long nnzb,
+                          double* __restrict__ out) {
+    const long long t = blockIdx.x * (long long)kT + threadIdx.x;
+    if (t >= nnzb * bb) return;
+    const long long e = t / bb;
+    const int k = (int)(t % bb);
+    out[map[e] + (long long)k * 32] = A[t];
+}
+
+#define RB_DISPATCH(b, ...)                                               \
+    switch (b) {                                                          \
+        case 1: { constexpr int B = 1; __VA_ARGS__; } break;              \
+        case 3: { constexpr int B = 3; __VA_ARGS__; } break;              \
+        case 5: { constexpr int B = 5; __VA_ARGS__; } break;              \
+        case 6: { constexpr int B = 6; __VA_ARGS__; } break;              \
+        default: throw ShapeError("rb: unsupported block size");          \
+    }
+
+SellDev sell_dev(const SellLayout& L, const double* vals) {
+    return SellDev{L.slice_val.ptr, L.slice_col.ptr, L.deg.ptr, L.cols.ptr, vals, L.n, L.n0,
+                   (L.n0 + 31) / 32};
+}
+
+}  // namespace
+
+bool rb_eligible(const DevicePattern& p, int* n0) {
+    if (!p.single_partition || p.fwd_levels() != 2 || p.bwd_levels() != 2) return false;
+    const int c0 = p.fwd_ptr[1];
+    // level 0 must be exactly rows [0, c0) (colour-major); level 1 rows [c0, n)
+    std::vector<int> rows(p.rows);
+    FNLH_CUDA(cudaMemcpy(rows.data(), p.fwd_rows, p.rows * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < p.rows; ++k)
+        if (rows[k] != k) return false;
+    // no edges inside a colour
+    for (int i = 0; i < p.rows; ++i)
+        for (int e = p.h_row_ptr[i]; e < p.h_row_ptr[i + 1]; ++e) {
+            const int j = p.h_col_idx[e];
+            if (j != i && ((i < c0) == (j < c0))) return false;
+        }
+    *n0 = c0;
+    return true;
+}
+
+template <class S>
+RbIlu<S>::RbIlu(const DevicePattern* pat, int n0_) : p(pat), n0(n0_) {
+    const std::size_t bb = (std::size_t)p->b * p->b;
+    FNLH_CUDA(cudaMalloc(&diag_lu, (std::size_t)p->rows * bb * sizeof(S)));
+    FNLH_CUDA(cudaMalloc(&diag_piv, (std::size_t)p->rows * p->b * sizeof(int)));
+    FNLH_CUDA(cudaMalloc(&inv0, std::max<std::size_t>((std::size_t)n0 * bb, 1) * sizeof(S)));
+}
+template <class S>
+RbIlu<S>::~RbIlu() {
+    cudaFree(diag_lu);
+    cudaFree(diag_piv);
+    cudaFree(inv0);
+}
+template <class S>
+std::size_t RbIlu<S>::bytes() const {
+    const std::size_t bb = (std::size_t)p->b * p->b;
+    return ((std::size_t)p->rows * bb + (std::size_t)n0 * bb) * sizeof(S) + (std::size_t)p->rows * p->b * sizeof(int);
+}
+
+RbSystem::RbSystem(const DevicePattern* p, int n0) : p_(p) {
+    const int n = p->rows, b = p->b;
+    L_.n = n;
+    L_.n0 = n0;
+    L_.b = b;
+    const int ns0 = (n0 + 31) / 32, ns1 = (n - n0 + 31) / 32;
+    L_.nslices = ns0 + ns1;
+    L_.slice_of_row0 = ns0;
+    std::vector<long long> sval(L_.nslices + 1, 0);
+    std::vector<int> scol(L_.nslices + 1, 0);
+    std::vector<int> deg(n), dslot(n);
+    auto slice_rows = [&](int s, int& r0, int& r1) {
+        if (s < ns0) {
+            r0 = s * 32;
+            r1 = std::min(n0, r0 + 32);
+        } else {
+            r0 = n0 + (s - ns0) * 32;
+            r1 = std::min(n, r0 + 32);
+        }
+    };
+    for (int i = 0; i < n; ++i) {
+        deg[i] = p->h_row_ptr[i + 1] - p->h_row_ptr[i];
+        dslot[i] = p->h_diag_idx[i] - p->h_row_ptr[i];
+    }
+    for (int s = 0; s < L_.nslices; ++s) {
+        int r0, r1, md = 0;
+        slice_rows(s, r0, r1);
+        for (int i = r0; i < r1; ++i) md = std::max(md, deg[i]);
+        sval[s + 1] = sval[s] + (long long)md * b * b * 32;
+        scol[s + 1] = scol[s] + md * 32;
+    }
+    L_.total_vals = sval[L_.nslices];
+    std::vector<int> cols(scol[L_.nslices], 0);
+    std::vector<long long> map(p->nnzb), trans(p->nnzb);
+    for (int s = 0; s < L_.nslices; ++s) {
+        int r0, r1;
+        slice_rows(s, r0, r1);
+        const int md = (scol[s + 1] - scol[s]) / 32;
+        for (int i = r0; i < r1; ++i) {
+            const int lane = i - r0;
+            for (int e = 0; e < md; ++e) {
+                const int ce = e < deg[i] ? p->h_col_idx[p->h_row_ptr[i] + e] : i;  // padding: self, zero block
+                cols[scol[s] + e * 32 + lane] = ce;
+                if (e < deg[i]) map[p->h_row_ptr[i] + e] = sval[s] + (long long)e * b * b * 32 + lane;
+            }
+        }
+    }
+    for (int i = 0; i < n; ++i)
+        for (int e = p->h_row_ptr[i]; e < p->h_row_ptr[i + 1]; ++e) {
+            const int j = p->h_col_idx[e];
+            const auto b0 = p->h_col_idx.begin() + p->h_row_ptr[j];
+            const auto b1 = p->h_col_idx.begin() + p->h_row_ptr[j + 1];
+            trans[e] = map[std::lower_bound(b0, b1, i) - p->h_col_idx.begin()];
+        }
+    L_.slice_val.upload(sval.data(), sval.size());
+    L_.slice_col.upload(scol.data(), scol.size());
+    L_.deg.upload(deg.data(), n);
+    L_.dslot.upload(dslot.data(), n);
+    L_.cols.upload(cols.data(), cols.size());
+    L_.csr_to_sell.upload(map.data(), map.size());
+    trans_.upload(trans.data(), trans.size());
+    vals_.alloc(std::max<long long>(L_.total_vals, 1));
+    FNLH_CUDA(cudaMemset(vals_.ptr, 0, vals_.bytes()));
+    grid0 = nb(n0);
+    grid1 = nb(n - n0);
+    partials.alloc(std::max(grid0 + grid1, nb((long long)n * b)) + 8);
+}
+
+void RbSystem::load(const double* A_csr, cudaStream_t stm) {
+    const int bb = L_.b * L_.b;
+    k_to_sell<<<nb((long long)p_->nnzb * bb), kT, 0, stm>>>(A_csr, L_.csr_to_sell.ptr, bb, p_->nnzb, vals_.ptr);
+    FNLH_CUDA(cudaGetLastError());
+}
+
+template <class S>
+void rb_factorize(const RbSystem& A, const double* shift_im, RbIlu<S>& f, Workspace& ws) {
+    const SellLayout& L = A.layout();
+    const SellDev sd = sell_dev(L, A.vals());
+    const int init[2] = {0, 0x7fffffff};
+    FNLH_CUDA(cudaMemcpyAsync(ws.status, init, sizeof init, cudaMemcpyHostToDevice, ws.stream));
+    RB_DISPATCH(L.b, {
+        k_rb_factor0<B, S><<<A.grid0, kT, 0, ws.stream>>>(sd, shift_im, f.diag_lu, f.diag_piv, f.inv0, ws.status);
+        k_rb_factor1<B, S><<<A.grid1, kT, 0, ws.stream>>>(sd, A.pattern()->row_ptr, A.trans(), shift_im, f.diag_lu,
+                                                           f.diag_piv, f.inv0, ws.status);
+    });
+    FNLH_CUDA(cudaGetLastError());
+    FNLH_CUDA(cudaMemcpyAsync(ws.h_status, ws.status, 2 * sizeof(int), cudaMemcpyDeviceToHost, ws.stream));
+    FNLH_CUDA(cudaStreamSynchronize(ws.stream));
+    if (ws.h_status[1] != 0x7fffffff) throw FactorizationError("near-singular ILU pivot block", ws.h_status[1]);
+}
+
+template <class S>
+void rb_smoothed_solve(const RbSystem& A, const double* shift_im, const RbIlu<S>& f, const S* rhs, double tol_rel,
+                       int max_iter, S* x, S* z, S* r, RbControl* ctl, Workspace& ws) {
+    if (!(tol_rel > 0.0 && tol_rel < 1.0)) throw ConfigError("smoothed_solve: tol_rel must be in (0,1)");
+    if (max_iter < 1) throw ConfigError("smoothed_solve: max_iter must be >= 1");
+    const SellLayout& L = A.layout();
+    const SellDev sd = sell_dev(L, A.vals());
+    const std::size_t len = (std::size_t)L.n * L.b;
+    cudaStream_t stm = ws.stream;
+    unsigned int* counter = reinterpret_cast<unsigned int*>(&ctl->counter);
+    FNLH_CUDA(cudaMemsetAsync(x, 0, len * sizeof(S), stm));
+    FNLH_CUDA(cudaMemsetAsync(ctl, 0, sizeof(RbControl), stm));
+    double* parts = const_cast<double*>(A.partials.ptr);
+    const int gi = std::min(nb((long long)len), 1184);
+    k_rb_init<S><<<gi, kT, 0, stm>>>(len, rhs, parts, gi, ctl, tol_rel, counter);
+    RB_DISPATCH(L.b, {
+        for (int s = 1; s <= max_iter; ++s) {
+            k_rb_colour1<B, S><<<A.grid1, kT, 0, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, f.inv0, rhs, x, z, r,
+                                                         parts, A.grid0, ctl, s, 1, max_iter, counter);
+            k_rb_colour0<B, S><<<A.grid0, kT, 0, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, rhs, x, z, r, parts,
+                                                         ctl, s);
+        }
+        k_rb_colour1<B, S><<<A.grid1, kT, 0, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, f.inv0, rhs, x, z, r, parts,
+                                                     A.grid0, ctl, max_iter + 1, 0, max_iter, counter);
+    });
+    FNLH_CUDA(cudaGetLastError());
+}
+
+template struct RbIlu<double>;
+template struct RbIlu<cplx>;
+template void rb_factorize<double>(const RbSystem&, const double*, RbIlu<double>&, Workspace&);
+template void rb_factorize<cplx>(const RbSystem&, const double*, RbIlu<cplx>&, Workspace&);
+template void rb_smoothed_solve<double>(const RbSystem&, const double*, const RbIlu<double>&, const double*, double,
+                                        int, double*, double*, double*, RbControl*, Workspace&);
+template void rb_smoothed_solve<cplx>(const RbSystem&, const double*, const RbIlu<cplx>&, const cplx*, double, int,
+                                      cplx*, cplx*, cplx*, RbControl*, Workspace&);
+
+}  // namespace fnlh

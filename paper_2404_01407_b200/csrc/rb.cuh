@@ -1,0 +1,107 @@
+// rb.cuh -- the 2-colour ("red-black") fast path of ILU(0)-Richardson.
+//
+// With a colour-major ordering of a 2-colourable graph (every hex mesh) and a single
+// partition, the reference ILU(0) (sparse.cpp:187-291) has a closed form:
+//   colour 0 rows (first N0):  no lower entries; U_ij = A_ij; pivot = A_ii + s_i
+//   colour 1 rows:             L_ik = A_ik * inv(U_kk) (k colour 0); U_ii = A_ii + s_i
+//                              - sum_k L_ik A_ki; no upper entries
+// so the factorization stores only the pivot LUs (and inv(U_kk) for colour 0) and
+// the sweep recomputes L_ik = A_ik * inv(U_kk) from the shared real LHS A5 with the
+// reference's own operation order: the iterates are bitwise those of
+// smoothed_solve (sparse.hpp:295-331), only the residual-norm summation order
+// differs.  One sweep = two fused kernels:
+//   K_B(s)  colour 0: backward substitution + x += z + residual rows (matvec)
+//   K_A(s)  colour 1: x += z of sweep s-1, residual rows of sweep s-1 (matvec),
+//                     norm / stopping decision (last CTA), forward + pivot solve of s
+// so every block of A5 is read from HBM once per sweep.  A5 is stored SELL-32
+// (slice of 32 rows, slot-major, lane-minor) so each warp load is 256 contiguous
+// bytes.  The stopping rule is evaluated on the device: no host round trip per sweep.
+#pragma once
+
+#include "capi_util.hpp"
+#include "la.cuh"
+
+namespace fnlh {
+
+// SELL-32 copy of a BSR on a colour-major 2-colour pattern
+struct SellLayout {
+    int n = 0, n0 = 0, b = 0;
+    int nslices = 0;
+    DeviceBuffer<long long> slice_val;   // element offset of slice s in vals
+    DeviceBuffer<int> slice_col;         // entry offset of slice s in cols
+    DeviceBuffer<int> deg;               // per row: number of entries
+    DeviceBuffer<int> dslot;             // per row: slot of the diagonal
+    DeviceBuffer<int> cols;              // [slice][slot][lane]
+    DeviceBuffer<long long> csr_to_sell; // per CSR entry: element offset of its block's k = 0 entry
+    long long total_vals = 0;               // doubles per scalar component (incl. padding)
+    int slice_of_row0 = 0;                  // first slice of colour 1
+};
+
+struct RbControl {  // device-side Richardson control block
+    double target;
+    double initial_residual;
+    double final_residual;
+    int iterations;
+    int converged;
+    int done;
+    int status;  // 0 ok, 6 divergence (non-finite)
+    unsigned int counter;
+    int pad;
+};
+
+// global switch (fnlh_set_red_black) so tests can force the general level-scheduled path
+inline bool& rb_enabled() {
+    static bool on = true;
+    return on;
+}
+
+// is the pattern a 2-colour colour-major ordering with one partition?
+bool rb_eligible(const DevicePattern& p, int* n0);
+
+template <class S>
+struct RbIlu {
+    const DevicePattern* p = nullptr;
+    int n0 = 0;
+    S* diag_lu = nullptr;   // rows*b*b
+    int* diag_piv = nullptr;
+    S* inv0 = nullptr;      // n0*b*b, inv(U_kk) of colour 0 rows
+    RbIlu(const DevicePattern* pat, int n0_);
+    ~RbIlu();
+    RbIlu(const RbIlu&) = delete;
+    RbIlu& operator=(const RbIlu&) = delete;
+    std::size_t bytes() const;
+};
+
+class RbSystem {
+public:
+    RbSystem(const DevicePattern* p, int n0);
+    // A5 (CSR layout, p's pattern) -> SELL copy
+    void load(const double* A_csr, cudaStream_t st);
+    const SellLayout& layout() const { return L_; }
+    const double* vals() const { return vals_.ptr; }
+    std::size_t bytes() const { return vals_.bytes(); }
+    int n0() const { return L_.n0; }
+    const DevicePattern* pattern() const { return p_; }
+
+private:
+    const DevicePattern* p_;
+    SellLayout L_;
+    DeviceBuffer<double> vals_;
+    DeviceBuffer<long long> trans_;  // per CSR entry (i,k): SELL offset of the (k,i) block
+public:
+    DeviceBuffer<double> partials;   // per-CTA norm partials (colour 0 then colour 1)
+    int grid0 = 0, grid1 = 0;
+    const long long* trans() const { return trans_.ptr; }
+};
+
+// factorize the (shifted) system into the compact RB factors; throws FactorizationError
+template <class S>
+void rb_factorize(const RbSystem& A, const double* shift_im, RbIlu<S>& f, Workspace& ws);
+
+// enqueue a complete smoothed_solve (no host synchronization); the report lands in *ctl
+// (device); x is overwritten.
+template <class S>
+void rb_smoothed_solve(const RbSystem& A, const double* shift_im, const RbIlu<S>& f, const S* rhs, double tol_rel,
+                       int max_iter, S* x, S* z, S* r, RbControl* ctl, Workspace& ws);
+
+}  // namespace fnlh

@@ -102,8 +102,18 @@ DeviceSolver::DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int
                              cudaMemcpyHostToDevice));
     if (sch_.implicit) {
         A5_.alloc((std::size_t)pat_->nnzb * mesh.b * mesh.b);
-        ilu_mean_ = std::make_unique<DeviceIlu<double>>(pat_.get());
-        ilu_h_ = std::make_unique<DeviceIlu<cplx>>(pat_.get());  // ONE workspace reused by every harmonic
+        int n0 = 0;
+        if (rb_enabled() && rb_eligible(*pat_, &n0)) {
+            rbA_ = std::make_unique<RbSystem>(pat_.get(), n0);
+            rb_mean_ = std::make_unique<RbIlu<double>>(pat_.get(), n0);
+            rb_h_ = std::make_unique<RbIlu<cplx>>(pat_.get(), n0);  // ONE workspace reused by every harmonic
+            ctl_.alloc(1);
+            rb_z_.alloc(len);
+            rb_r_.alloc(len);
+        } else {
+            ilu_mean_ = std::make_unique<DeviceIlu<double>>(pat_.get());
+            ilu_h_ = std::make_unique<DeviceIlu<cplx>>(pat_.get());  // ONE workspace reused by every harmonic
+        }
         shift_.alloc(mesh.n);
     } else {
         P_.alloc((std::size_t)mesh.n * mesh.b * mesh.b);
@@ -124,16 +134,32 @@ DeviceSolver::~DeviceSolver() {
 
 std::size_t DeviceSolver::lhs_bytes() const {
     std::size_t s = 0;
-    if (sch_.implicit) s = A5_.bytes() + ilu_mean_->bytes() + ilu_h_->bytes();
+    if (sch_.implicit && rbA_) s = A5_.bytes() + rbA_->bytes() + rb_mean_->bytes() + rb_h_->bytes();
+    else if (sch_.implicit) s = A5_.bytes() + ilu_mean_->bytes() + ilu_h_->bytes();
     else s = P_.bytes() + PLU_.bytes() + pclu_.bytes();
     return s;
 }
 
 // rk_step (rk.cpp:41-99)
-template <class S, class Eval, class Apply>
-RkStepResult DeviceSolver::rk_step(S* state, Eval&& eval, Apply&& apply, const SystemView<S>& A,
-                                   const DeviceIlu<S>* ilu, const S* pdiag_lu, const int* pdiag_piv,
-                                   const std::string& field) {
+template <class S>
+LinearSolveReport DeviceSolver::rb_solve(const double* shift, const RbIlu<S>& f, const S* rhs, S* x) {
+    rb_smoothed_solve<S>(*rbA_, shift, f, rhs, sch_.linear_tol, sch_.linear_max_iter, x,
+                         reinterpret_cast<S*>(rb_z_.ptr), reinterpret_cast<S*>(rb_r_.ptr), ctl_.ptr, *ws_);
+    RbControl h;
+    FNLH_CUDA(cudaMemcpyAsync(&h, ctl_.ptr, sizeof h, cudaMemcpyDeviceToHost, ws_->stream));
+    FNLH_CUDA(cudaStreamSynchronize(ws_->stream));
+    if (h.status == 6) throw DivergenceError("non-finite iterate in smoothed_solve", h.iterations, "linear");
+    LinearSolveReport rep;
+    rep.iterations = h.iterations;
+    rep.initial_residual = h.initial_residual;
+    rep.final_residual = h.final_residual;
+    rep.converged = h.converged;
+    return rep;
+}
+
+template <class S, class Eval, class Apply, class Solve>
+RkStepResult DeviceSolver::rk_step(S* state, Eval&& eval, Apply&& apply, Solve&& solve, const S* pdiag_lu,
+                                   const int* pdiag_piv, const std::string& field) {
     cudaStream_t st = ws_->stream;
     const std::size_t len = disc_->len();
     S* state0 = reinterpret_cast<S*>(rk_[0].ptr);
@@ -181,7 +207,7 @@ RkStepResult DeviceSolver::rk_step(S* state, Eval&& eval, Apply&& apply, const S
             scale<S>(x, gfac * kAlpha[k - 1], len, st);
         } else {
             scale<S>(rhs, kAlpha[k - 1], len, st);
-            LinearSolveReport rep = smoothed_solve<S>(A, rhs, *ilu, sch_.linear_tol, sch_.linear_max_iter, x, *ws_);
+            LinearSolveReport rep = solve(rhs, x);
             sweeps += rep.iterations;
             row_updates += (long long)rep.iterations * disc_->n();
             res.linear_reports.push_back(rep);
@@ -218,10 +244,15 @@ ConvergenceEntry DeviceSolver::outer_iteration() {
         disc_->fd_jacobian(mean_.ptr, A5_.ptr, nullptr, st);  // J, then A5 in place
         build_lhs_mean_device(A5_.ptr, A5_.ptr, b, n, pat_->diag_idx, pat_->nnzb, 1, ga5,
                               1.0 / (sch_.eps_relax * sigma_), st);
-        SystemView<double> Am;
-        Am.p = pat_.get();
-        Am.real_vals = A5_.ptr;
-        ilu_factorize<double>(Am, *ilu_mean_, *ws_);
+        if (rbA_) {
+            rbA_->load(A5_.ptr, st);
+            rb_factorize<double>(*rbA_, nullptr, *rb_mean_, *ws_);
+        } else {
+            SystemView<double> Am;
+            Am.p = pat_.get();
+            Am.real_vals = A5_.ptr;
+            ilu_factorize<double>(Am, *ilu_mean_, *ws_);
+        }
     } else {
         disc_->fd_jacobian(mean_.ptr, nullptr, P_.ptr, st);  // assemble_diag_blocks (disc.cpp:31-35)
         FNLH_CUDA(cudaMemcpyAsync(PLU_.ptr, P_.ptr, P_.bytes(), cudaMemcpyDeviceToDevice, st));
@@ -253,8 +284,17 @@ ConvergenceEntry DeviceSolver::outer_iteration() {
             Ah.p = pat_.get();
             Ah.real_vals = A5_.ptr;
             Ah.shift_im = shift_.ptr;
-            ilu_factorize<cplx>(Ah, *ilu_h_, *ws_);
-            step = rk_step<cplx>(amp, eval, apply, Ah, ilu_h_.get(), nullptr, nullptr, name);
+            if (rbA_) {
+                rb_factorize<cplx>(*rbA_, shift_.ptr, *rb_h_, *ws_);
+                auto solve = [&](const cplx* rhs, cplx* x) { return rb_solve<cplx>(shift_.ptr, *rb_h_, rhs, x); };
+                step = rk_step<cplx>(amp, eval, apply, solve, nullptr, nullptr, name);
+            } else {
+                ilu_factorize<cplx>(Ah, *ilu_h_, *ws_);
+                auto solve = [&](const cplx* rhs, cplx* x) {
+                    return smoothed_solve<cplx>(Ah, rhs, *ilu_h_, sch_.linear_tol, sch_.linear_max_iter, x, *ws_);
+                };
+                step = rk_step<cplx>(amp, eval, apply, solve, nullptr, nullptr, name);
+            }
         } else {
             shifted_blocks(P_.ptr, disc_->view().vol, b, n, omega, pclu_.ptr, st);
             const int init[2] = {0, 0x7fffffff};
@@ -263,8 +303,8 @@ ConvergenceEntry DeviceSolver::outer_iteration() {
             FNLH_CUDA(cudaMemcpyAsync(ws_->h_status, ws_->status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
             FNLH_CUDA(cudaStreamSynchronize(st));
             if (ws_->h_status[1] != 0x7fffffff) throw FactorizationError("singular pivot block", ws_->h_status[1]);
-            SystemView<cplx> none;
-            step = rk_step<cplx>(amp, eval, apply, none, nullptr, pclu_.ptr, pcpiv_.ptr, name);
+            auto none = [&](const cplx*, cplx*) { return LinearSolveReport{}; };
+            step = rk_step<cplx>(amp, eval, apply, none, pclu_.ptr, pcpiv_.ptr, name);
         }
         h_norm[h] = step.stage1_residual_norm;
         for (auto& r : step.linear_reports) hreps.push_back(r);
@@ -284,14 +324,20 @@ ConvergenceEntry DeviceSolver::outer_iteration() {
         apply_mean(b, n, gamma, base, x, out, disc_->err(), st);
     };
     RkStepResult mstep;
-    if (implicit) {
+    if (implicit && rbA_) {
+        auto solve = [&](const double* rhs, double* x) { return rb_solve<double>(nullptr, *rb_mean_, rhs, x); };
+        mstep = rk_step<double>(mean_.ptr, mean_eval, mean_apply, solve, nullptr, nullptr, "mean");
+    } else if (implicit) {
         SystemView<double> Am;
         Am.p = pat_.get();
         Am.real_vals = A5_.ptr;
-        mstep = rk_step<double>(mean_.ptr, mean_eval, mean_apply, Am, ilu_mean_.get(), nullptr, nullptr, "mean");
+        auto solve = [&](const double* rhs, double* x) {
+            return smoothed_solve<double>(Am, rhs, *ilu_mean_, sch_.linear_tol, sch_.linear_max_iter, x, *ws_);
+        };
+        mstep = rk_step<double>(mean_.ptr, mean_eval, mean_apply, solve, nullptr, nullptr, "mean");
     } else {
-        SystemView<double> none;
-        mstep = rk_step<double>(mean_.ptr, mean_eval, mean_apply, none, nullptr, PLU_.ptr, Ppiv_.ptr, "mean");
+        auto none = [&](const double*, double*) { return LinearSolveReport{}; };
+        mstep = rk_step<double>(mean_.ptr, mean_eval, mean_apply, none, PLU_.ptr, Ppiv_.ptr, "mean");
     }
     for (auto& r : hreps) reports_.push_back(r);
     for (auto& r : mstep.linear_reports) reports_.push_back(r);
@@ -330,7 +376,12 @@ double DeviceSolver::time_harmonic_sweeps(int h, int nsweeps) {
     Ah.p = pat_.get();
     Ah.real_vals = A5_.ptr;
     Ah.shift_im = shift_.ptr;
-    ilu_factorize<cplx>(Ah, *ilu_h_, *ws_);
+    if (rbA_) {
+        rbA_->load(A5_.ptr, st);
+        rb_factorize<cplx>(*rbA_, shift_.ptr, *rb_h_, *ws_);
+    } else {
+        ilu_factorize<cplx>(Ah, *ilu_h_, *ws_);
+    }
     // rhs: the harmonic's current linearized residual direction (any nonzero vector works)
     cplx* rhs = rk_[4].ptr;
     cplx* x = rk_[5].ptr;
@@ -338,7 +389,11 @@ double DeviceSolver::time_harmonic_sweeps(int h, int nsweeps) {
                                forcing_.ptr + (std::size_t)h * nforcing_, nforcing_, 2, false, rhs, nullptr, st);
     FNLH_CUDA(cudaStreamSynchronize(st));
     FNLH_CUDA(cudaEventRecord(ev0_, st));
-    smoothed_solve<cplx>(Ah, rhs, *ilu_h_, 1e-300, nsweeps, x, *ws_);
+    if (rbA_)
+        rb_smoothed_solve<cplx>(*rbA_, shift_.ptr, *rb_h_, rhs, 1e-300, nsweeps, x, rb_z_.ptr, rb_r_.ptr, ctl_.ptr,
+                                *ws_);
+    else
+        smoothed_solve<cplx>(Ah, rhs, *ilu_h_, 1e-300, nsweeps, x, *ws_);
     FNLH_CUDA(cudaEventRecord(ev1_, st));
     FNLH_CUDA(cudaEventSynchronize(ev1_));
     float ms = 0.0f;

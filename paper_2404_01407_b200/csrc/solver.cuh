@@ -9,6 +9,7 @@
 
 #include "disc.cuh"
 #include "la.cuh"
+#include "rb.cuh"
 
 namespace fnlh {
 
@@ -63,11 +64,20 @@ public:
     // counters for the bench: total sweeps and block-row updates performed
     long long sweeps = 0, row_updates = 0;
     float last_iteration_ms = 0.0f;
+    bool red_black() const { return rbA_ != nullptr; }
+    void info(double* out) const {
+        out[0] = rbA_ ? 1.0 : 0.0;
+        out[1] = rbA_ ? rbA_->n0() : -1.0;
+        out[2] = rbA_ ? (double)rbA_->layout().total_vals : 0.0;
+        out[3] = pat_->nnzb;
+    }
 
 private:
-    template <class S, class Eval, class Apply>
-    RkStepResult rk_step(S* state, Eval&& eval, Apply&& apply, const SystemView<S>& A, const DeviceIlu<S>* ilu,
-                         const S* pdiag_lu, const int* pdiag_piv, const std::string& field);
+    template <class S, class Eval, class Apply, class Solve>
+    RkStepResult rk_step(S* state, Eval&& eval, Apply&& apply, Solve&& solve, const S* pdiag_lu, const int* pdiag_piv,
+                         const std::string& field);
+    template <class S>
+    LinearSolveReport rb_solve(const double* shift, const RbIlu<S>& f, const S* rhs, S* x);
 
     SchemeConfig sch_;
     double sigma_ = 50.0;
@@ -82,6 +92,11 @@ private:
     DeviceBuffer<cplx> amps_, forcing_, pclu_;
     std::unique_ptr<DeviceIlu<double>> ilu_mean_;
     std::unique_ptr<DeviceIlu<cplx>> ilu_h_;
+    std::unique_ptr<RbSystem> rbA_;  // 2-colour fast path (rb.cuh), null when not eligible
+    std::unique_ptr<RbIlu<double>> rb_mean_;
+    std::unique_ptr<RbIlu<cplx>> rb_h_;
+    DeviceBuffer<RbControl> ctl_;
+    DeviceBuffer<cplx> rb_z_, rb_r_;
     DeviceBuffer<cplx> rk_[7];  // state0, inv, vis_fresh, vis_blend, rhs, x, stage (complex or reinterpreted real)
     std::vector<LinearSolveReport> reports_;
     int iter_ = 0;

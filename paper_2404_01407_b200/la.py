@@ -108,3 +108,30 @@ def smoothed_solve(pat: Pattern, A, rhs, tol_rel, max_iter, shift_im=None):
         check(lib().fnlh_smoothed_solve(pat.h, _i(0), ptr(Ab), _i(0), None, ptr(f64(rhs)), _d(tol_rel), _i(max_iter),
                                         ptr(x), C.byref(rep)))
     return x, rep.as_tuple()
+
+
+def set_red_black(enable: bool):
+    """Enable / disable the 2-colour fused sweep (rb.cuh); both paths give the reference's iterates."""
+    lib().fnlh_set_red_black(_i(1 if enable else 0))
+
+
+def red_black_n0(pat: Pattern) -> int:
+    """Size of colour 0 if the pattern is a colour-major 2-colour ordering with one partition, else -1."""
+    n0 = _i()
+    check(lib().fnlh_pattern_is_red_black(pat.h, C.byref(n0)))
+    return n0.value
+
+
+def rb_factorize(pat: Pattern, A, shift_im=None):
+    """Compact 2-colour ILU(0) factors: pivot LU + piv for all rows, inv(U_kk) for colour 0."""
+    n0 = red_black_n0(pat)
+    cplx = shift_im is not None
+    dt = np.complex128 if cplx else np.float64
+    b, n = pat.b, pat.rows
+    dlu = np.zeros(n * b * b, dt)
+    piv = np.zeros(n * b, np.int32)
+    inv0 = np.zeros(max(n0, 1) * b * b, dt)
+    v = (lambda a: a.view(np.float64)) if cplx else (lambda a: a)
+    check(lib().fnlh_rb_factorize(pat.h, _i(1 if cplx else 0), ptr(f64(A)), ptr(None if shift_im is None else f64(shift_im)),
+                                  ptr(v(dlu)), ptr(piv), ptr(v(inv0))))
+    return dict(diag_lu=dlu, diag_piv=piv, inv0=inv0[: n0 * b * b], n0=n0)

@@ -170,6 +170,11 @@ class FnlhSolver:
         check(lib().fnlh_solver_time_sweeps(self.h, _i(h), _i(sweeps), C.byref(ms)))
         return ms.value
 
+    def info(self):
+        out = np.zeros(4)
+        check(lib().fnlh_solver_info(self.h, ptr(out)))
+        return dict(red_black=bool(out[0]), n0=int(out[1]), sell_vals=int(out[2]), nnzb=int(out[3]))
+
     def counters(self):
         out = np.zeros(3)
         lib().fnlh_solver_counters(self.h, ptr(out))

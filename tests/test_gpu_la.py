@@ -52,12 +52,21 @@ def test_ilu_factor_apply_solve(ref, meshes, b, cplx, kind):
     yr = ref.matvec(pat, Aref, rhs)
     yd = la.matvec(P, A, rhs, shift) if cplx else la.matvec(P, A, rhs)
     assert np.array_equal(yd, yr)
-    for tol, it in ((1e-2, 10), (1e-12, 6)):
-        xr, rr = ref.smoothed_solve(pat, Aref, rhs, tol, it)
-        xd, rd = la.smoothed_solve(P, A, rhs, tol, it, shift) if cplx else la.smoothed_solve(P, A, rhs, tol, it)
-        assert np.array_equal(xd, xr)
-        assert rd[0] == rr[0] and rd[3] == rr[3]
-        assert abs(rd[1] / rr[1] - 1) < 1e-14 and abs(rd[2] / rr[2] - 1) < 1e-12
+    assert (la.red_black_n0(P) > 0) == (kind == "hex")
+    for rb in (True, False):  # the 2-colour fused sweep and the general level-scheduled path
+        la.set_red_black(rb)
+        for tol, it in ((1e-2, 10), (1e-12, 6)):
+            xr, rr = ref.smoothed_solve(pat, Aref, rhs, tol, it)
+            xd, rd = la.smoothed_solve(P, A, rhs, tol, it, shift) if cplx else la.smoothed_solve(P, A, rhs, tol, it)
+            assert np.array_equal(xd, xr), (rb, tol)
+            assert rd[0] == rr[0] and rd[3] == rr[3]
+            assert abs(rd[1] / rr[1] - 1) < 1e-14 and abs(rd[2] / rr[2] - 1) < 1e-12
+    la.set_red_black(True)
+    if kind == "hex":
+        fb = la.rb_factorize(P, A, shift)
+        n0 = fb["n0"]
+        assert np.array_equal(fb["diag_lu"], fr["diag_lu"]) and np.array_equal(fb["diag_piv"], fr["diag_piv"])
+        assert np.array_equal(fb["inv0"], fr["diag_inv"][: n0 * b * b])
 
 
 def test_natural_order_and_partitions(ref, meshes):
