@@ -30,7 +30,7 @@ struct CudaError : std::runtime_error {
 };
 
 // std::complex<double> layout (re, im), reference arithmetic order.
-struct cplx {
+struct alignas(16) cplx {
     double re, im;
 };
 

@@ -30,12 +30,27 @@ __device__ __forceinline__ RowRef row_ref(const SellDev& L, int i) {
     const int li = i < L.n0 ? i : i - L.n0;
     const int s = (i < L.n0 ? 0 : L.nslices0) + (li >> 5);
     const int lane = li & 31;
-    return RowRef{L.slice_val[s] + lane, L.slice_col[s] + lane, L.deg[i]};
+    return RowRef{L.slice_val[s] + 2 * lane, L.slice_col[s] + lane, L.deg[i]};
 }
 
 template <int B>
+__host__ __device__ constexpr int pairs() { return (B * B + 1) / 2; }
+
+template <int B>
 __device__ __forceinline__ double aval(const SellDev& L, const RowRef& r, int e, int k) {
-    return __ldg(L.vals + r.vbase + (long long)(e * B * B + k) * 32);
+    return __ldg(L.vals + r.vbase + ((long long)(e * pairs<B>() + (k >> 1)) * 32) * 2 + (k & 1));
+}
+
+// the whole b x b block, 16-byte loads (pairs of elements, lane-contiguous)
+template <int B>
+__device__ __forceinline__ void ablock(const SellDev& L, const RowRef& r, int e, double (&A)[2 * pairs<B>()]) {
+    const double2* base = reinterpret_cast<const double2*>(L.vals + r.vbase) + (long long)e * pairs<B>() * 32;
+#pragma unroll
+    for (int p = 0; p < pairs<B>(); ++p) {
+        const double2 v = __ldg(base + (long long)p * 32);
+        A[2 * p] = v.x;
+        A[2 * p + 1] = v.y;
+    }
 }
 
 __device__ __forceinline__ int acol(const SellDev& L, const RowRef& r, int e) { return __ldg(L.cols + r.cbase + e * 32); }
@@ -46,11 +61,14 @@ template <int B, class S>
 __device__ __forceinline__ void blk_matvec_add(const SellDev& L, const RowRef& rr, int e, const S (&x)[B],
                                                bool diag, double s, S (&y)[B]) {
 #pragma unroll
+    double A[2 * pairs<B>()];
+    ablock<B>(L, rr, e, A);
+#pragma unroll
     for (int r = 0; r < B; ++r) {
         S acc = zero<S>();
 #pragma unroll
         for (int c = 0; c < B; ++c) {
-            const double a = aval<B>(L, rr, e, r * B + c);
+            const double a = A[r * B + c];
             if constexpr (sizeof(S) == sizeof(cplx)) {
                 if (diag && r == c)
                     acc += mk(a + 0.0, 0.0 + s) * x[c];
@@ -69,10 +87,13 @@ template <int B, class S>
 __device__ __forceinline__ void blk_matvec_sub(const SellDev& L, const RowRef& rr, int e, const S (&x)[B],
                                                S (&y)[B]) {
 #pragma unroll
+    double A[2 * pairs<B>()];
+    ablock<B>(L, rr, e, A);
+#pragma unroll
     for (int r = 0; r < B; ++r) {
         S acc = zero<S>();
 #pragma unroll
-        for (int c = 0; c < B; ++c) acc += rmul(aval<B>(L, rr, e, r * B + c), x[c]);
+        for (int c = 0; c < B; ++c) acc += rmul(A[r * B + c], x[c]);
         y[r] -= acc;
     }
 }
@@ -140,7 +161,66 @@ __global__ void k_rb_init(std::size_t len, const S* __restrict__ rhs, double* __
     (void)nparts;
 }
 
+// ---- K_F: colour 1 forward substitution -------------------------------------
+// zf = r_i - sum_k L_ik r_k (ascending k, sparse.cpp:267-278) with L_ik = A_ik inv(U_kk)
+// rebuilt in the reference's order (sparse.cpp:221-232); colour 1 rows have no upper
+// entries, so the backward step is the pivot solve alone.
+template <int B, class S>
+__global__ void __launch_bounds__(kT) k_rb_forward1(SellDev L, const S* __restrict__ diag_lu,
+                                                    const int* __restrict__ piv, const S* __restrict__ inv0,
+                                                    const S* __restrict__ rhs, const S* __restrict__ r,
+                                                    S* __restrict__ z, const RbControl* ctl, int sweep) {
+    if (ctl->done) return;
+    const int i = L.n0 + blockIdx.x * kT + threadIdx.x;
+    if (i >= L.n) return;
+    const RowRef rr = row_ref(L, i);
+    const int dg = rr.deg - 1;
+    const S* rv = sweep == 1 ? rhs : r;
+    S zf[B];
+    ld<B>(rv + (size_t)i * B, zf);
+    for (int e = 0; e < dg; ++e) {
+        const int kk = acol(L, rr, e);
+        S zk[B];
+        ld<B>(rv + (size_t)kk * B, zk);
+        const S* __restrict__ U = inv0 + (size_t)kk * B * B;
+        double A[2 * pairs<B>()];
+        ablock<B>(L, rr, e, A);
+        S acc[B];
+#pragma unroll
+        for (int rw = 0; rw < B; ++rw) acc[rw] = zero<S>();
+        // column c of inv(U_kk) at a time: L[rw][c] = sum_m A[rw][m] U[m][c] (rounded as
+        // the reference's L_ik), then acc[rw] += L[rw][c] z[c] in ascending c
+#pragma unroll
+        for (int c = 0; c < B; ++c) {
+            S uc[B];
+#pragma unroll
+            for (int m = 0; m < B; ++m) uc[m] = U[m * B + c];
+#pragma unroll
+            for (int rw = 0; rw < B; ++rw) {
+                S lrc = zero<S>();
+#pragma unroll
+                for (int m = 0; m < B; ++m) lrc += rmul(A[rw * B + m], uc[m]);
+                acc[rw] += lrc * zk[c];
+            }
+        }
+#pragma unroll
+        for (int rw = 0; rw < B; ++rw) zf[rw] -= acc[rw];
+    }
+    S lu[B * B];
+    int pv[B];
+#pragma unroll
+    for (int k = 0; k < B * B; ++k) lu[k] = diag_lu[(size_t)i * B * B + k];
+#pragma unroll
+    for (int k = 0; k < B; ++k) pv[k] = piv[(size_t)i * B + k];
+    lu_solve_reg<B>(lu, pv, zf);
+    st<B>(z + (size_t)i * B, zf);
+}
+
 // ---- K_B: colour 0 rows -----------------------------------------------------
+// One descending pass over the row's blocks: A_e z_j feeds the backward sum
+// (sparse.cpp:280-290) and A_e (x_j + z_j) is parked in shared memory; after the
+// pivot solve and x += z the residual row is summed in ascending order
+// (sparse.hpp:317-319).  Every block is read from HBM once.
 template <int B, class S>
 __global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const double* __restrict__ shift,
                                                    const S* __restrict__ diag_lu, const int* __restrict__ piv,
@@ -148,18 +228,37 @@ __global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const double* __re
                                                    const S* __restrict__ z, S* __restrict__ r,
                                                    double* __restrict__ partials0, const RbControl* ctl, int sweep) {
     __shared__ double red[kT / 32];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    S* park = reinterpret_cast<S*>(smem_raw);  // [slot][row][tid]
     if (ctl->done) return;
-    const int i = blockIdx.x * kT + threadIdx.x;
+    const int tid = threadIdx.x;
+    const int i = blockIdx.x * kT + tid;
     double loc = 0.0;
     if (i < L.n0) {
         const RowRef rr = row_ref(L, i);
         S t[B];
         ld<B>((sweep == 1 ? rhs : r) + (size_t)i * B, t);  // forward: colour 0 rows copy r
-        // backward substitution, descending columns (sparse.cpp:280-290)
         for (int e = rr.deg - 1; e >= 1; --e) {
-            S zj[B];
-            ld<B>(z + (size_t)acol(L, rr, e) * B, zj);
-            blk_matvec_sub<B, S>(L, rr, e, zj, t);
+            const int j = acol(L, rr, e);
+            S zj[B], xj[B];
+            ld<B>(z + (size_t)j * B, zj);
+            ld<B>(x + (size_t)j * B, xj);
+#pragma unroll
+            for (int k = 0; k < B; ++k) xj[k] += zj[k];  // colour-1 x += z ahead of K_R
+            double A[2 * pairs<B>()];
+            ablock<B>(L, rr, e, A);
+#pragma unroll
+            for (int rw = 0; rw < B; ++rw) {
+                S accb = zero<S>(), accm = zero<S>();
+#pragma unroll
+                for (int c = 0; c < B; ++c) {
+                    const double a = A[rw * B + c];
+                    accb += rmul(a, zj[c]);
+                    accm += rmul(a, xj[c]);
+                }
+                t[rw] -= accb;
+                park[((e - 1) * B + rw) * kT + tid] = accm;
+            }
         }
         S lu[B * B];
         int pv[B];
@@ -173,21 +272,14 @@ __global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const double* __re
 #pragma unroll
         for (int k = 0; k < B; ++k) xi[k] += t[k];  // x += z (sparse.hpp:317)
         st<B>(x + (size_t)i * B, xi);
-        // residual row (sparse.hpp:318-319), ascending columns: diagonal first
         S y[B];
 #pragma unroll
         for (int k = 0; k < B; ++k) y[k] = zero<S>();
         const double s = shift ? shift[i] : 0.0;
-        blk_matvec_add<B, S>(L, rr, 0, xi, shift != nullptr, s, y);
-        for (int e = 1; e < rr.deg; ++e) {
-            const int j = acol(L, rr, e);
-            S xj[B], zj[B];
-            ld<B>(x + (size_t)j * B, xj);
-            ld<B>(z + (size_t)j * B, zj);
+        blk_matvec_add<B, S>(L, rr, 0, xi, shift != nullptr, s, y);  // diagonal block first
+        for (int e = 1; e < rr.deg; ++e)
 #pragma unroll
-            for (int k = 0; k < B; ++k) xj[k] += zj[k];  // colour-1 x += z, applied lazily
-            blk_matvec_add<B, S>(L, rr, e, xj, false, 0.0, y);
-        }
+            for (int rw = 0; rw < B; ++rw) y[rw] += park[((e - 1) * B + rw) * kT + tid];
         S bi[B];
         ld<B>(rhs + (size_t)i * B, bi);
 #pragma unroll
@@ -198,17 +290,19 @@ __global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const double* __re
         }
     }
     const double bs = block_sum(loc, red);
-    if (threadIdx.x == 0) partials0[blockIdx.x] = bs;
+    if (tid == 0) partials0[blockIdx.x] = bs;
 }
 
-// ---- K_A: colour 1 rows -----------------------------------------------------
+// ---- K_R: colour 1 residual rows + stopping rule ------------------------------
+// x += z (colour 1), r_i = b_i - sum_e A_e x_col (ascending: lower blocks, then the
+// diagonal), ||r|| over both colours and the stopping decision of this sweep
+// (sparse.hpp:318-328), taken by the last CTA on the device.
 template <int B, class S>
-__global__ void __launch_bounds__(kT) k_rb_colour1(SellDev L, const double* __restrict__ shift,
-                                                   const S* __restrict__ diag_lu, const int* __restrict__ piv,
-                                                   const S* __restrict__ inv0, const S* __restrict__ rhs,
-                                                   S* __restrict__ x, S* __restrict__ z, const S* __restrict__ r,
-                                                   double* __restrict__ partials, int grid0, RbControl* ctl,
-                                                   int sweep, int forward, int max_iter, unsigned int* counter) {
+__global__ void __launch_bounds__(kT) k_rb_resid1(SellDev L, const double* __restrict__ shift,
+                                                  const S* __restrict__ rhs, S* __restrict__ x,
+                                                  const S* __restrict__ z, S* __restrict__ r,
+                                                  double* __restrict__ partials, int grid0, RbControl* ctl,
+                                                  int sweep, int max_iter, unsigned int* counter) {
     __shared__ double red[kT / 32];
     __shared__ bool last;
     if (ctl->done) return;
@@ -216,72 +310,31 @@ __global__ void __launch_bounds__(kT) k_rb_colour1(SellDev L, const double* __re
     double loc = 0.0;
     if (i < L.n) {
         const RowRef rr = row_ref(L, i);
-        const int dg = rr.deg - 1;  // diagonal is the last slot
-        S ri[B];
-        const double s = shift ? shift[i] : 0.0;
-        ld<B>(rhs + (size_t)i * B, ri);
-        if (sweep > 1) {
-            S xi[B], zi[B];
-            ld<B>(x + (size_t)i * B, xi);
-            ld<B>(z + (size_t)i * B, zi);
+        const int dg = rr.deg - 1;
+        S xi[B], zi[B];
+        ld<B>(x + (size_t)i * B, xi);
+        ld<B>(z + (size_t)i * B, zi);
 #pragma unroll
-            for (int k = 0; k < B; ++k) xi[k] += zi[k];
-            st<B>(x + (size_t)i * B, xi);
-            S y[B];
+        for (int k = 0; k < B; ++k) xi[k] += zi[k];
+        st<B>(x + (size_t)i * B, xi);
+        S y[B];
 #pragma unroll
-            for (int k = 0; k < B; ++k) y[k] = zero<S>();
-            for (int e = 0; e < dg; ++e) {
-                S xk[B];
-                ld<B>(x + (size_t)acol(L, rr, e) * B, xk);
-                blk_matvec_add<B, S>(L, rr, e, xk, false, 0.0, y);
-            }
-            blk_matvec_add<B, S>(L, rr, dg, xi, shift != nullptr, s, y);
-#pragma unroll
-            for (int k = 0; k < B; ++k) {
-                ri[k] = ri[k] - y[k];
-                loc += sq(ri[k]);
-            }
+        for (int k = 0; k < B; ++k) y[k] = zero<S>();
+        for (int e = 0; e < dg; ++e) {
+            S xk[B];
+            ld<B>(x + (size_t)acol(L, rr, e) * B, xk);
+            blk_matvec_add<B, S>(L, rr, e, xk, false, 0.0, y);
         }
-        if (forward) {
-            // forward substitution with L_ik = A_ik inv(U_kk), rebuilt in the reference's
-            // order (sparse.cpp:221-232 then dense.hpp:31-39)
-            S zf[B];
+        blk_matvec_add<B, S>(L, rr, dg, xi, shift != nullptr, shift ? shift[i] : 0.0, y);
+        S bi[B];
+        ld<B>(rhs + (size_t)i * B, bi);
 #pragma unroll
-            for (int k = 0; k < B; ++k) zf[k] = ri[k];
-            for (int e = 0; e < dg; ++e) {
-                const int kk = acol(L, rr, e);
-                S zk[B];
-                ld<B>((sweep == 1 ? rhs : r) + (size_t)kk * B, zk);
-                S U[B * B];
-#pragma unroll
-                for (int q = 0; q < B * B; ++q) U[q] = inv0[(size_t)kk * B * B + q];
-#pragma unroll
-                for (int rw = 0; rw < B; ++rw) {
-                    double arow[B];
-#pragma unroll
-                    for (int m = 0; m < B; ++m) arow[m] = aval<B>(L, rr, e, rw * B + m);
-                    S acc = zero<S>();
-#pragma unroll
-                    for (int c = 0; c < B; ++c) {
-                        S lrc = zero<S>();
-#pragma unroll
-                        for (int m = 0; m < B; ++m) lrc += rmul(arow[m], U[m * B + c]);
-                        acc += lrc * zk[c];
-                    }
-                    zf[rw] -= acc;
-                }
-            }
-            S lu[B * B];
-            int pv[B];
-#pragma unroll
-            for (int k = 0; k < B * B; ++k) lu[k] = diag_lu[(size_t)i * B * B + k];
-#pragma unroll
-            for (int k = 0; k < B; ++k) pv[k] = piv[(size_t)i * B + k];
-            lu_solve_reg<B>(lu, pv, zf);  // colour 1 rows have no upper entries
-            st<B>(z + (size_t)i * B, zf);
+        for (int k = 0; k < B; ++k) {
+            const S v = bi[k] - y[k];
+            r[(size_t)i * B + k] = v;
+            loc += sq(v);
         }
     }
-    if (sweep == 1) return;
     const double bs = block_sum(loc, red);
     if (threadIdx.x == 0) {
         partials[grid0 + blockIdx.x] = bs;
@@ -290,11 +343,10 @@ __global__ void __launch_bounds__(kT) k_rb_colour1(SellDev L, const double* __re
     }
     __syncthreads();
     if (!last) return;
-    // stopping rule of sweep - 1 (sparse.hpp:320-328), decided on the device
     const double tot = ordered_sum(partials, grid0 + gridDim.x, red);
     if (threadIdx.x == 0) {
         const double nrm = sqrt(tot);
-        ctl->iterations = sweep - 1;
+        ctl->iterations = sweep;
         ctl->final_residual = nrm;
         if (!isfinite(nrm)) {
             ctl->status = 6;
@@ -302,7 +354,7 @@ __global__ void __launch_bounds__(kT) k_rb_colour1(SellDev L, const double* __re
         } else if (nrm <= ctl->target) {
             ctl->converged = 1;
             ctl->done = 1;
-        } else if (sweep - 1 >= max_iter) {
+        } else if (sweep >= max_iter) {
             ctl->done = 1;
         }
         *counter = 0u;
@@ -379,7 +431,10 @@ __global__ void k_rb_factor1(SellDev L, const int* __restrict__ row_ptr, const l
                 const S a = Lb[r * B + k2];
                 if (is_zero(a)) continue;
 #pragma unroll
-                for (int c = 0; c < B; ++c) Uii[r * B + c] -= a * from_real<S>(Aki[(long long)(k2 * B + c) * 32]);
+                for (int c = 0; c < B; ++c) {
+                    const int kk2 = k2 * B + c;
+                    Uii[r * B + c] -= a * from_real<S>(Aki[(long long)(kk2 >> 1) * 64 + (kk2 & 1)]);
+                }
             }
     }
     int pv[B];
@@ -397,7 +452,7 @@ __global__ void k_to_sell(const double* __restrict__ A, const long long* __restr
     if (t >= nnzb * bb) return;
     const long long e = t / bb;
     const int k = (int)(t % bb);
-    out[map[e] + (long long)k * 32] = A[t];
+    out[map[e] + (long long)(k >> 1) * 64 + (k & 1)] = A[t];
 }
 
 #define RB_DISPATCH(b, ...)                                               \
@@ -481,7 +536,7 @@ RbSystem::RbSystem(const DevicePattern* p, int n0) : p_(p) {
         int r0, r1, md = 0;
         slice_rows(s, r0, r1);
         for (int i = r0; i < r1; ++i) md = std::max(md, deg[i]);
-        sval[s + 1] = sval[s] + (long long)md * b * b * 32;
+        sval[s + 1] = sval[s] + (long long)md * ((b * b + 1) / 2) * 64;
         scol[s + 1] = scol[s] + md * 32;
     }
     L_.total_vals = sval[L_.nslices];
@@ -496,7 +551,7 @@ RbSystem::RbSystem(const DevicePattern* p, int n0) : p_(p) {
             for (int e = 0; e < md; ++e) {
                 const int ce = e < deg[i] ? p->h_col_idx[p->h_row_ptr[i] + e] : i;  // padding: self, zero block
                 cols[scol[s] + e * 32 + lane] = ce;
-                if (e < deg[i]) map[p->h_row_ptr[i] + e] = sval[s] + (long long)e * b * b * 32 + lane;
+                if (e < deg[i]) map[p->h_row_ptr[i] + e] = sval[s] + (long long)e * ((b * b + 1) / 2) * 64 + 2 * lane;
             }
         }
     }
@@ -559,15 +614,21 @@ void rb_smoothed_solve(const RbSystem& A, const double* shift_im, const RbIlu<S>
     double* parts = const_cast<double*>(A.partials.ptr);
     const int gi = std::min(nb((long long)len), 1184);
     k_rb_init<S><<<gi, kT, 0, stm>>>(len, rhs, parts, gi, ctl, tol_rel, counter);
+    const int maxoff = std::max(1, A.pattern()->max_deg - 1);
     RB_DISPATCH(L.b, {
-        for (int s = 1; s <= max_iter; ++s) {
-            k_rb_colour1<B, S><<<A.grid1, kT, 0, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, f.inv0, rhs, x, z, r,
-                                                         parts, A.grid0, ctl, s, 1, max_iter, counter);
-            k_rb_colour0<B, S><<<A.grid0, kT, 0, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, rhs, x, z, r, parts,
-                                                         ctl, s);
+        const std::size_t sm = (std::size_t)maxoff * B * kT * sizeof(S);
+        static bool attr = false;
+        if (!attr) {
+            FNLH_CUDA(cudaFuncSetAttribute(k_rb_colour0<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            attr = true;
         }
-        k_rb_colour1<B, S><<<A.grid1, kT, 0, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, f.inv0, rhs, x, z, r, parts,
-                                                     A.grid0, ctl, max_iter + 1, 0, max_iter, counter);
+        for (int s = 1; s <= max_iter; ++s) {
+            k_rb_forward1<B, S><<<A.grid1, kT, 0, stm>>>(sd, f.diag_lu, f.diag_piv, f.inv0, rhs, r, z, ctl, s);
+            k_rb_colour0<B, S><<<A.grid0, kT, sm, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, rhs, x, z, r, parts,
+                                                          ctl, s);
+            k_rb_resid1<B, S><<<A.grid1, kT, 0, stm>>>(sd, shift_im, rhs, x, z, r, parts, A.grid0, ctl, s, max_iter,
+                                                        counter);
+        }
     });
     FNLH_CUDA(cudaGetLastError());
 }

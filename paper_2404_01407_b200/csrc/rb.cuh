@@ -9,11 +9,11 @@
 // the sweep recomputes L_ik = A_ik * inv(U_kk) from the shared real LHS A5 with the
 // reference's own operation order: the iterates are bitwise those of
 // smoothed_solve (sparse.hpp:295-331), only the residual-norm summation order
-// differs.  One sweep = two fused kernels:
-//   K_B(s)  colour 0: backward substitution + x += z + residual rows (matvec)
-//   K_A(s)  colour 1: x += z of sweep s-1, residual rows of sweep s-1 (matvec),
-//                     norm / stopping decision (last CTA), forward + pivot solve of s
-// so every block of A5 is read from HBM once per sweep.  A5 is stored SELL-32
+// differs.  One sweep = three kernels:
+//   K_F(s)  colour 1: forward substitution with L = A inv(U) + pivot solve
+//   K_B(s)  colour 0: backward substitution + x += z + residual rows, one pass over A
+//   K_R(s)  colour 1: x += z + residual rows + norm / stopping decision (last CTA)
+// (colour-1 blocks are read twice, colour-0 blocks once).  A5 is stored SELL-32
 // (slice of 32 rows, slot-major, lane-minor) so each warp load is 256 contiguous
 // bytes.  The stopping rule is evaluated on the device: no host round trip per sweep.
 #pragma once
