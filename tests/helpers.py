@@ -11,6 +11,25 @@ from paper_2404_01407_b200.mesh import from_faces
 IDX3 = np.array([0, 1, 4])
 
 
+def nozzle_from_golden(path):
+    """RefNozzle-like view of tests/golden/nozzle_nx64_h2.npz (no reference needed)."""
+    import types
+    g = np.load(path, allow_pickle=False)
+    gas = g["gas"]
+    ns = types.SimpleNamespace(**{k: g[k] for k in g.files})
+    ns.n = int(g["n"])
+    ns.nf = len(g["fa"])
+    ns.nnzb = len(g["col_idx"])
+    ns.gamma, ns.gas_constant, ns.p0, ns.T0, ns.p_out, ns.forcing_scale = [float(v) for v in gas]
+
+    def pattern(b=3):
+        diag = np.array([ns.row_ptr[i] + np.searchsorted(ns.col_idx[ns.row_ptr[i]:ns.row_ptr[i + 1]], i)
+                         for i in range(ns.n)], np.int32)
+        return dict(b=b, row_ptr=ns.row_ptr, col_idx=ns.col_idx, diag_idx=diag, partition=np.zeros(ns.n, np.int32))
+    ns.pattern = pattern
+    return ns
+
+
 def line_mesh_from_ref(noz):
     nf = noz.nf
     fn = np.zeros((nf, 3))
