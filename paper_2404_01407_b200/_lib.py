@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfnlh_b200.so")
+LIB_PATH = os.environ.get("FNLH_B200_LIB", os.path.join(HERE, "libfnlh_b200.so"))
 
 _i, _d, _p = C.c_int, C.c_double, C.c_void_p
 

@@ -60,7 +60,6 @@ __device__ __forceinline__ int acol(const SellDev& L, const RowRef& r, int e) { 
 template <int B, class S>
 __device__ __forceinline__ void blk_matvec_add(const SellDev& L, const RowRef& rr, int e, const S (&x)[B],
                                                bool diag, double s, S (&y)[B]) {
-#pragma unroll
     double A[2 * pairs<B>()];
     ablock<B>(L, rr, e, A);
 #pragma unroll
@@ -86,7 +85,6 @@ __device__ __forceinline__ void blk_matvec_add(const SellDev& L, const RowRef& r
 template <int B, class S>
 __device__ __forceinline__ void blk_matvec_sub(const SellDev& L, const RowRef& rr, int e, const S (&x)[B],
                                                S (&y)[B]) {
-#pragma unroll
     double A[2 * pairs<B>()];
     ablock<B>(L, rr, e, A);
 #pragma unroll
