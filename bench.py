@@ -201,7 +201,6 @@ def main():
     from paper_2404_01407_b200.solver import FnlhSolver
 
     require_gpu()
-    lib().fnlh_set_device(local) if hasattr(lib(), "fnlh_set_device") else None
     c = make_case(args.config, scale=args.scale)
     m = c.mesh
     pat = m.pattern()
@@ -218,6 +217,7 @@ def main():
         s.outer_iteration()
     barrier()
     cnt0 = s.counters()
+    launches0 = lib().fnlh_launch_count()
     clocks = ClockSampler(local)
     clocks.start()
     barrier()
@@ -227,6 +227,7 @@ def main():
         dev_ms += s.counters()["last_ms"]
     barrier()
     clk = clocks.stop()
+    launches = int(lib().fnlh_launch_count() - launches0)
     cnt1 = s.counters()
     rows = cnt1["row_updates"] - cnt0["row_updates"]
     sweeps = cnt1["sweeps"] - cnt0["sweeps"]
@@ -274,6 +275,14 @@ def main():
         formula = "sweep_bytes (stored-factor)"
     peak, peak_kind = peaks()
     achieved = bytes_sweep / (sweep_ms * 1e-3) / 1e9
+    traffic = None
+    try:  # dram read + write of the same kernels from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "r1_sweep_ncu_c2.json")) as f:
+            prof = json.load(f)
+        if info["red_black"] and args.config == "c2" and args.scale == 1.0:
+            traffic = prof["traffic_bytes_per_sweep"]
+    except Exception:
+        pass
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
@@ -285,10 +294,10 @@ def main():
                        "sweeps_per_step": sweeps / args.steps, "lhs_bytes": s.lhs_bytes()},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "kernel": kname, "bytes_formula": formula,
+                         "traffic": traffic, "kernel": kname, "bytes_formula": formula,
                          "bytes_per_launch": bytes_sweep, "ms_per_launch": sweep_ms, "peak_kind": peak_kind,
                          "sweep_rows_per_s": n / (sweep_ms * 1e-3)},
-            "clocks": clk, "gpu_launches": None}
+            "clocks": clk, "gpu_launches": launches}
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             line["cpu_baseline"] = cpu_baseline(args.config, args.ref_scale)

@@ -46,6 +46,8 @@ const char* fnlh_last_error(void);
 int fnlh_last_error_node(void);
 int fnlh_last_error_stage(void);
 int fnlh_device_count(void);
+/* number of CUDA kernels this library has launched (monotonic) */
+long long fnlh_launch_count(void);
 
 /* ---- L1: block-sparse LA --------------------------------------------------- */
 

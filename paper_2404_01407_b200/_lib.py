@@ -44,6 +44,7 @@ def lib():
             raise ImportError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
         L = C.CDLL(LIB_PATH)
         L.fnlh_last_error.restype = C.c_char_p
+        L.fnlh_launch_count.restype = C.c_longlong
         _LIB = L
     return _LIB
 

@@ -6,6 +6,10 @@
 #include "capi_util.hpp"
 
 namespace fnlh {
+long long& launch_count() {
+    static long long n = 0;
+    return n;
+}
 ErrorState& last_error() {
     thread_local ErrorState e;
     return e;
@@ -17,6 +21,8 @@ extern "C" {
 const char* fnlh_last_error(void) { return fnlh::last_error().msg.c_str(); }
 int fnlh_last_error_node(void) { return fnlh::last_error().node; }
 int fnlh_last_error_stage(void) { return fnlh::last_error().stage; }
+
+long long fnlh_launch_count(void) { return fnlh::launch_count(); }
 
 int fnlh_device_count(void) {
     int n = 0;

@@ -29,6 +29,10 @@ struct CudaError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
 
+// count of kernel launches issued by this library (bench.py "gpu_launches")
+long long& launch_count();
+inline void note_launch() { ++launch_count(); }
+
 // std::complex<double> layout (re, im), reference arithmetic order.
 struct alignas(16) cplx {
     double re, im;

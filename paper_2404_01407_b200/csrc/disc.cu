@@ -669,16 +669,16 @@ void DeviceDisc::residual(const double* W, const double* wref, int order, int mo
                           const double* skip) {
     const MeshDev& m = view_;
     DISPATCH_B56(m.b, {
-        if (order == 2) k_jst_prepass<B><<<nb(m.n), kT, 0, st>>>(m, W, nu_.ptr, lap_.ptr, skip);
-        k_face_flux<B><<<nb(m.nf), kT, 0, st>>>(m, W, wref, order, mode, forcing, nforcing, need_vis ? 1 : 0,
-                                                nu_.ptr, lap_.ptr, flux_.ptr, vflux_.ptr, err_.ptr, skip);
-        k_node_gather<B><<<nb(m.n), kT, 0, st>>>(m, W, flux_.ptr, vflux_.ptr, need_vis ? 1 : 0, inv, vis, skip);
+        if (order == 2) { ::fnlh::note_launch(); k_jst_prepass<B><<<nb(m.n), kT, 0, st>>>(m, W, nu_.ptr, lap_.ptr, skip); }
+        { ::fnlh::note_launch(); k_face_flux<B><<<nb(m.nf), kT, 0, st>>>(m, W, wref, order, mode, forcing, nforcing, need_vis ? 1 : 0,
+                                                nu_.ptr, lap_.ptr, flux_.ptr, vflux_.ptr, err_.ptr, skip); }
+        { ::fnlh::note_launch(); k_node_gather<B><<<nb(m.n), kT, 0, st>>>(m, W, flux_.ptr, vflux_.ptr, need_vis ? 1 : 0, inv, vis, skip); }
     });
     FNLH_CUDA(cudaGetLastError());
 }
 
 void DeviceDisc::validate(const double* W, cudaStream_t st) {
-    DISPATCH_B56(view_.b, { k_validate<B><<<nb(view_.n), kT, 0, st>>>(view_.n, W, err_.ptr); });
+    DISPATCH_B56(view_.b, { { ::fnlh::note_launch(); k_validate<B><<<nb(view_.n), kT, 0, st>>>(view_.n, W, err_.ptr); } });
     raise_if_err(st, "validate_state");
 }
 
@@ -687,16 +687,16 @@ void DeviceDisc::fd_jacobian(const double* W, double* J, double* P, cudaStream_t
     validate(W, st);
     if (J) FNLH_CUDA(cudaMemsetAsync(J, 0, (std::size_t)pat_->nnzb * m.b * m.b * sizeof(double), st));
     DISPATCH_B56(m.b, {
-        k_umax_init<<<1, 32, 0, st>>>(umax_.ptr, B);
-        k_qscale<B><<<std::min(nb(m.n), 592), kT, 0, st>>>(m.n, m.gamma, W, umax_.ptr);
-        k_qscale_finish<B><<<1, 32, 0, st>>>(umax_.ptr, qscale_.ptr);
-        k_fd_jacobian<B><<<nb((long long)m.n * B), kT, 0, st>>>(m, pat_->diag_idx, e_ab_.ptr, e_ba_.ptr, W,
-                                                                qscale_.ptr, J, P, err_.ptr);
+        { ::fnlh::note_launch(); k_umax_init<<<1, 32, 0, st>>>(umax_.ptr, B); }
+        { ::fnlh::note_launch(); k_qscale<B><<<std::min(nb(m.n), 592), kT, 0, st>>>(m.n, m.gamma, W, umax_.ptr); }
+        { ::fnlh::note_launch(); k_qscale_finish<B><<<1, 32, 0, st>>>(umax_.ptr, qscale_.ptr); }
+        { ::fnlh::note_launch(); k_fd_jacobian<B><<<nb((long long)m.n * B), kT, 0, st>>>(m, pat_->diag_idx, e_ab_.ptr, e_ba_.ptr, W,
+                                                                qscale_.ptr, J, P, err_.ptr); }
     });
     FNLH_CUDA(cudaGetLastError());
     raise_if_err(st, "fd_jacobian");
     if (J) {
-        DISPATCH_B56(m.b, { k_diag_check<B><<<nb(m.n), kT, 0, st>>>(m.n, pat_->diag_idx, J, err_.ptr); });
+        DISPATCH_B56(m.b, { { ::fnlh::note_launch(); k_diag_check<B><<<nb(m.n), kT, 0, st>>>(m.n, pat_->diag_idx, J, err_.ptr); } });
         raise_if_err(st, "fd_jacobian");
     }
 }
@@ -718,19 +718,19 @@ void DeviceDisc::linearized_residual(const double* mean, const cplx* what, doubl
     double* delta = scal_.ptr;
     const int grid = std::min(nb(m.n), 592);
     DISPATCH_B56(m.b, {
-        k_umax_init<<<1, 32, 0, st>>>(umax_.ptr, 3 * B + 2);
-        k_linres_scales<B><<<grid, kT, 0, st>>>(m.n, mean, what, forcing, nforcing, umax_.ptr);
-        k_linres_delta<B><<<1, 32, 0, st>>>(umax_.ptr, m.forcing_scale, delta);
+        { ::fnlh::note_launch(); k_umax_init<<<1, 32, 0, st>>>(umax_.ptr, 3 * B + 2); }
+        { ::fnlh::note_launch(); k_linres_scales<B><<<grid, kT, 0, st>>>(m.n, mean, what, forcing, nforcing, umax_.ptr); }
+        { ::fnlh::note_launch(); k_linres_delta<B><<<1, 32, 0, st>>>(umax_.ptr, m.forcing_scale, delta); }
     });
     const int gs = nb((long long)std::max<std::size_t>(L, (std::size_t)nforcing));
     for (int part = 0; part < 2; ++part) {
-        k_linres_states<<<gs, kT, 0, st>>>(L, mean, what, forcing, nforcing, part, delta, wp, wm, fp, fm);
+        { ::fnlh::note_launch(); k_linres_states<<<gs, kT, 0, st>>>(L, mean, what, forcing, nforcing, part, delta, wp, wm, fp, fm); }
         residual(wp, mean, order, 1, fp, nforcing, need_vis, ip, vp, st, delta + part);
         residual(wm, mean, order, 1, fm, nforcing, need_vis, imn, vm, st, delta + part);
-        k_linres_combine<<<nb(L), kT, 0, st>>>(L, part, delta, ip, imn, inv, part == 0);
-        if (need_vis) k_linres_combine<<<nb(L), kT, 0, st>>>(L, part, delta, vp, vm, vis, part == 0);
+        { ::fnlh::note_launch(); k_linres_combine<<<nb(L), kT, 0, st>>>(L, part, delta, ip, imn, inv, part == 0); }
+        if (need_vis) { ::fnlh::note_launch(); k_linres_combine<<<nb(L), kT, 0, st>>>(L, part, delta, vp, vm, vis, part == 0); }
     }
-    DISPATCH_B56(m.b, { k_spectral<B><<<nb(m.n), kT, 0, st>>>(m.n, m.gamma, omega, vol_.ptr, mean, what, inv); });
+    DISPATCH_B56(m.b, { { ::fnlh::note_launch(); k_spectral<B><<<nb(m.n), kT, 0, st>>>(m.n, m.gamma, omega, vol_.ptr, mean, what, inv); } });
     FNLH_CUDA(cudaGetLastError());
 }
 
@@ -778,7 +778,7 @@ void DeviceDisc::deterministic_flux(const double* mean, const std::vector<const 
     // any nonzero amplitude?  (residual_ops.cpp:133-141)
     DeviceBuffer<int> flag(1);
     FNLH_CUDA(cudaMemsetAsync(flag.ptr, 0, sizeof(int), st));
-    for (int h = 0; h < nh; ++h) k_any_nonzero<<<std::min(nb((long long)L), 592), kT, 0, st>>>(L, amps[h], flag.ptr);
+    for (int h = 0; h < nh; ++h) { ::fnlh::note_launch(); k_any_nonzero<<<std::min(nb((long long)L), 592), kT, 0, st>>>(L, amps[h], flag.ptr); }
     int hflag = 0;
     FNLH_CUDA(cudaMemcpyAsync(&hflag, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
     FNLH_CUDA(cudaStreamSynchronize(st));
@@ -801,13 +801,13 @@ void DeviceDisc::deterministic_flux(const double* mean, const std::vector<const 
     double* inv = scratch_real[1].ptr;
     double* acc = scratch_real[2].ptr;
     for (int k = 0; k < nq; ++k) {
-        k_reconstruct<<<nb((long long)L), kT, 0, st>>>(L, mean, al, nh, dph.ptr + (std::size_t)k * nh, w);
+        { ::fnlh::note_launch(); k_reconstruct<<<nb((long long)L), kT, 0, st>>>(L, mean, al, nh, dph.ptr + (std::size_t)k * nh, w); }
         residual(w, nullptr, 2, 0, nullptr, 0, false, inv, nullptr, st);
-        k_accumulate<<<nb((long long)L), kT, 0, st>>>(L, inv, acc, k == 0);
+        { ::fnlh::note_launch(); k_accumulate<<<nb((long long)L), kT, 0, st>>>(L, inv, acc, k == 0); }
     }
     raise_if_err(st, "deterministic_flux");
     residual(mean, nullptr, 2, 0, nullptr, 0, false, inv, nullptr, st);
-    k_df_finish<<<nb((long long)L), kT, 0, st>>>(L, (double)nq, acc, inv, df, lmax == 0 ? 0 : 1);
+    { ::fnlh::note_launch(); k_df_finish<<<nb((long long)L), kT, 0, st>>>(L, (double)nq, acc, inv, df, lmax == 0 ? 0 : 1); }
     FNLH_CUDA(cudaGetLastError());
     raise_if_err(st, "deterministic_flux");
 }
@@ -815,33 +815,33 @@ void DeviceDisc::deterministic_flux(const double* mean, const std::vector<const 
 // ---------------------------------------------------------------------------
 template <class S>
 void stage_blend(double beta, const S* vf, S* vb, std::size_t len, cudaStream_t st) {
-    k_blend<S><<<nb((long long)len), kT, 0, st>>>(beta, vf, vb, len);
+    { ::fnlh::note_launch(); k_blend<S><<<nb((long long)len), kT, 0, st>>>(beta, vf, vb, len); }
 }
 template <class S>
 void stage_rhs(const S* inv, const S* vb, S* rhs, std::size_t len, cudaStream_t st) {
-    k_rhs<S><<<nb((long long)len), kT, 0, st>>>(inv, vb, rhs, len);
+    { ::fnlh::note_launch(); k_rhs<S><<<nb((long long)len), kT, 0, st>>>(inv, vb, rhs, len); }
 }
 template <class S>
 void scale(S* x, double a, std::size_t len, cudaStream_t st) {
-    k_scale<S><<<nb((long long)len), kT, 0, st>>>(x, a, len);
+    { ::fnlh::note_launch(); k_scale<S><<<nb((long long)len), kT, 0, st>>>(x, a, len); }
 }
 template <class S>
 void add_inplace(S* x, const S* y, std::size_t len, cudaStream_t st) {
-    k_add<S><<<nb((long long)len), kT, 0, st>>>(x, y, len);
+    { ::fnlh::note_launch(); k_add<S><<<nb((long long)len), kT, 0, st>>>(x, y, len); }
 }
 template <class S>
 void check_finite(const S* x, std::size_t len, unsigned long long* err, cudaStream_t st) {
-    k_check_finite<S><<<std::min(nb((long long)len), 592), kT, 0, st>>>(x, len, err);
+    { ::fnlh::note_launch(); k_check_finite<S><<<std::min(nb((long long)len), 592), kT, 0, st>>>(x, len, err); }
 }
 
 void apply_harmonic(int b, int n, double gamma, const double* mean, const cplx* base, const cplx* x, cplx* out,
                     cudaStream_t st) {
-    DISPATCH_B56(b, { k_apply_harmonic<B><<<nb(n), kT, 0, st>>>(n, gamma, mean, base, x, out); });
+    DISPATCH_B56(b, { { ::fnlh::note_launch(); k_apply_harmonic<B><<<nb(n), kT, 0, st>>>(n, gamma, mean, base, x, out); } });
 }
 
 void apply_mean(int b, int n, double gamma, const double* base, const double* x, double* out,
                 unsigned long long* err, cudaStream_t st) {
-    DISPATCH_B56(b, { k_apply_mean<B><<<nb(n), kT, 0, st>>>(n, gamma, base, x, out, err); });
+    DISPATCH_B56(b, { { ::fnlh::note_launch(); k_apply_mean<B><<<nb(n), kT, 0, st>>>(n, gamma, base, x, out, err); } });
 }
 
 #define INST(S)                                                                         \

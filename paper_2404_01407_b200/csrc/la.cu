@@ -509,12 +509,12 @@ void ilu_factorize(const SystemView<S>& A, DeviceIlu<S>& f, Workspace& ws) {
     const int init[2] = {0, 0x7fffffff};
     FNLH_CUDA(cudaMemcpyAsync(ws.status, init, sizeof init, cudaMemcpyHostToDevice, ws.stream));
     FNLH_DISPATCH_B(p.b, {
-        k_ilu_copy<B, S><<<nblocks(p.rows), kThreads, 0, ws.stream>>>(pd, A, f.vals);
+        { ::fnlh::note_launch(); k_ilu_copy<B, S><<<nblocks(p.rows), kThreads, 0, ws.stream>>>(pd, A, f.vals); }
         for (int l = 0; l < p.fwd_levels(); ++l) {
             const int n = p.fwd_ptr[l + 1] - p.fwd_ptr[l];
-            k_ilu_factor<B, S><<<nblocks(n), kThreads, 0, ws.stream>>>(pd, p.fwd_rows + p.fwd_ptr[l], n, f.vals,
+            { ::fnlh::note_launch(); k_ilu_factor<B, S><<<nblocks(n), kThreads, 0, ws.stream>>>(pd, p.fwd_rows + p.fwd_ptr[l], n, f.vals,
                                                                        f.diag_lu, f.diag_piv, f.diag_inv,
-                                                                       ws.status);
+                                                                       ws.status); }
         }
     });
     FNLH_CUDA(cudaGetLastError());
@@ -531,12 +531,12 @@ void ilu_apply(const DeviceIlu<S>& f, const S* rhs, S* x, Workspace& ws, S* x_ac
     FNLH_DISPATCH_B(p.b, {
         for (int l = 0; l < p.fwd_levels(); ++l) {
             const int n = p.fwd_ptr[l + 1] - p.fwd_ptr[l];
-            k_ilu_fwd<B, S><<<nblocks(n), kThreads, 0, ws.stream>>>(pd, p.fwd_rows + p.fwd_ptr[l], n, f.vals, rhs, x);
+            { ::fnlh::note_launch(); k_ilu_fwd<B, S><<<nblocks(n), kThreads, 0, ws.stream>>>(pd, p.fwd_rows + p.fwd_ptr[l], n, f.vals, rhs, x); }
         }
         for (int l = 0; l < p.bwd_levels(); ++l) {
             const int n = p.bwd_ptr[l + 1] - p.bwd_ptr[l];
-            k_ilu_bwd<B, S><<<nblocks(n), kThreads, 0, ws.stream>>>(pd, p.bwd_rows + p.bwd_ptr[l], n, f.vals,
-                                                                    f.diag_lu, f.diag_piv, x, x_accum);
+            { ::fnlh::note_launch(); k_ilu_bwd<B, S><<<nblocks(n), kThreads, 0, ws.stream>>>(pd, p.bwd_rows + p.bwd_ptr[l], n, f.vals,
+                                                                    f.diag_lu, f.diag_piv, x, x_accum); }
         }
     });
     FNLH_CUDA(cudaGetLastError());
@@ -547,9 +547,9 @@ void residual_norm(const SystemView<S>& A, const S* rhs, const S* x, S* r, doubl
     const DevicePattern& p = *A.p;
     const int grid = std::min(nblocks(p.rows), kRedBlocks);
     FNLH_DISPATCH_B(p.b, {
-        k_matvec<B, S><<<grid, kThreads, 0, ws.stream>>>(dev(p), A, x, rhs, r, ws.partials);
+        { ::fnlh::note_launch(); k_matvec<B, S><<<grid, kThreads, 0, ws.stream>>>(dev(p), A, x, rhs, r, ws.partials); }
     });
-    k_finish<<<1, 256, 0, ws.stream>>>(ws.partials, grid, d_norm2);
+    { ::fnlh::note_launch(); k_finish<<<1, 256, 0, ws.stream>>>(ws.partials, grid, d_norm2); }
     FNLH_CUDA(cudaGetLastError());
 }
 
@@ -558,7 +558,7 @@ void matvec(const SystemView<S>& A, const S* x, S* y, Workspace& ws) {
     const DevicePattern& p = *A.p;
     const int grid = std::min(nblocks(p.rows), kRedBlocks);
     FNLH_DISPATCH_B(p.b, {
-        k_matvec<B, S><<<grid, kThreads, 0, ws.stream>>>(dev(p), A, x, nullptr, y, nullptr);
+        { ::fnlh::note_launch(); k_matvec<B, S><<<grid, kThreads, 0, ws.stream>>>(dev(p), A, x, nullptr, y, nullptr); }
     });
     FNLH_CUDA(cudaGetLastError());
 }
@@ -566,8 +566,8 @@ void matvec(const SystemView<S>& A, const S* x, S* y, Workspace& ws) {
 template <class S>
 void norm2_sq(const S* x, std::size_t len, double* d_out, Workspace& ws) {
     const int grid = std::min<long long>(nblocks((long long)len), kRedBlocks);
-    k_sumsq<S><<<grid, kThreads, 0, ws.stream>>>(x, len, ws.partials);
-    k_finish<<<1, 256, 0, ws.stream>>>(ws.partials, grid, d_out);
+    { ::fnlh::note_launch(); k_sumsq<S><<<grid, kThreads, 0, ws.stream>>>(x, len, ws.partials); }
+    { ::fnlh::note_launch(); k_finish<<<1, 256, 0, ws.stream>>>(ws.partials, grid, d_out); }
     FNLH_CUDA(cudaGetLastError());
 }
 
@@ -613,13 +613,13 @@ LinearSolveReport smoothed_solve(const SystemView<S>& A, const S* rhs, const Dev
 
 template <class S>
 void block_diag_solve(int b, int n, const S* lu, const int* piv, const S* rhs, S* x, cudaStream_t st) {
-    FNLH_DISPATCH_B(b, { k_block_diag_solve<B, S><<<nblocks(n), kThreads, 0, st>>>(n, lu, piv, rhs, x); });
+    FNLH_DISPATCH_B(b, { { ::fnlh::note_launch(); k_block_diag_solve<B, S><<<nblocks(n), kThreads, 0, st>>>(n, lu, piv, rhs, x); } });
     FNLH_CUDA(cudaGetLastError());
 }
 
 template <class S>
 void block_diag_factor(int b, int n, S* blocks, int* piv, int* status, cudaStream_t st) {
-    FNLH_DISPATCH_B(b, { k_block_diag_factor<B, S><<<nblocks(n), kThreads, 0, st>>>(n, blocks, piv, status); });
+    FNLH_DISPATCH_B(b, { { ::fnlh::note_launch(); k_block_diag_factor<B, S><<<nblocks(n), kThreads, 0, st>>>(n, blocks, piv, status); } });
     FNLH_CUDA(cudaGetLastError());
 }
 

@@ -576,7 +576,7 @@ RbSystem::RbSystem(const DevicePattern* p, int n0) : p_(p) {
 
 void RbSystem::load(const double* A_csr, cudaStream_t stm) {
     const int bb = L_.b * L_.b;
-    k_to_sell<<<nb((long long)p_->nnzb * bb), kT, 0, stm>>>(A_csr, L_.csr_to_sell.ptr, bb, p_->nnzb, vals_.ptr);
+    { ::fnlh::note_launch(); k_to_sell<<<nb((long long)p_->nnzb * bb), kT, 0, stm>>>(A_csr, L_.csr_to_sell.ptr, bb, p_->nnzb, vals_.ptr); }
     FNLH_CUDA(cudaGetLastError());
 }
 
@@ -587,9 +587,9 @@ void rb_factorize(const RbSystem& A, const double* shift_im, RbIlu<S>& f, Worksp
     const int init[2] = {0, 0x7fffffff};
     FNLH_CUDA(cudaMemcpyAsync(ws.status, init, sizeof init, cudaMemcpyHostToDevice, ws.stream));
     RB_DISPATCH(L.b, {
-        k_rb_factor0<B, S><<<A.grid0, kT, 0, ws.stream>>>(sd, shift_im, f.diag_lu, f.diag_piv, f.inv0, ws.status);
-        k_rb_factor1<B, S><<<A.grid1, kT, 0, ws.stream>>>(sd, A.pattern()->row_ptr, A.trans(), shift_im, f.diag_lu,
-                                                           f.diag_piv, f.inv0, ws.status);
+        { ::fnlh::note_launch(); k_rb_factor0<B, S><<<A.grid0, kT, 0, ws.stream>>>(sd, shift_im, f.diag_lu, f.diag_piv, f.inv0, ws.status); }
+        { ::fnlh::note_launch(); k_rb_factor1<B, S><<<A.grid1, kT, 0, ws.stream>>>(sd, A.pattern()->row_ptr, A.trans(), shift_im, f.diag_lu,
+                                                           f.diag_piv, f.inv0, ws.status); }
     });
     FNLH_CUDA(cudaGetLastError());
     FNLH_CUDA(cudaMemcpyAsync(ws.h_status, ws.status, 2 * sizeof(int), cudaMemcpyDeviceToHost, ws.stream));
@@ -611,7 +611,7 @@ void rb_smoothed_solve(const RbSystem& A, const double* shift_im, const RbIlu<S>
     FNLH_CUDA(cudaMemsetAsync(ctl, 0, sizeof(RbControl), stm));
     double* parts = const_cast<double*>(A.partials.ptr);
     const int gi = std::min(nb((long long)len), 1184);
-    k_rb_init<S><<<gi, kT, 0, stm>>>(len, rhs, parts, gi, ctl, tol_rel, counter);
+    { ::fnlh::note_launch(); k_rb_init<S><<<gi, kT, 0, stm>>>(len, rhs, parts, gi, ctl, tol_rel, counter); }
     const int maxoff = std::max(1, A.pattern()->max_deg - 1);
     RB_DISPATCH(L.b, {
         const std::size_t sm = (std::size_t)maxoff * B * kT * sizeof(S);
@@ -621,11 +621,11 @@ void rb_smoothed_solve(const RbSystem& A, const double* shift_im, const RbIlu<S>
             attr = true;
         }
         for (int s = 1; s <= max_iter; ++s) {
-            k_rb_forward1<B, S><<<A.grid1, kT, 0, stm>>>(sd, f.diag_lu, f.diag_piv, f.inv0, rhs, r, z, ctl, s);
-            k_rb_colour0<B, S><<<A.grid0, kT, sm, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, rhs, x, z, r, parts,
-                                                          ctl, s);
-            k_rb_resid1<B, S><<<A.grid1, kT, 0, stm>>>(sd, shift_im, rhs, x, z, r, parts, A.grid0, ctl, s, max_iter,
-                                                        counter);
+            { ::fnlh::note_launch(); k_rb_forward1<B, S><<<A.grid1, kT, 0, stm>>>(sd, f.diag_lu, f.diag_piv, f.inv0, rhs, r, z, ctl, s); }
+            { ::fnlh::note_launch(); k_rb_colour0<B, S><<<A.grid0, kT, sm, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, rhs, x, z, r, parts,
+                                                          ctl, s); }
+            { ::fnlh::note_launch(); k_rb_resid1<B, S><<<A.grid1, kT, 0, stm>>>(sd, shift_im, rhs, x, z, r, parts, A.grid0, ctl, s, max_iter,
+                                                        counter); }
         }
     });
     FNLH_CUDA(cudaGetLastError());

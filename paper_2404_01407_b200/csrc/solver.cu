@@ -65,16 +65,16 @@ __global__ void k_shifted_blocks(const double* __restrict__ P, const double* __r
 void build_lhs_mean_device(const double* J, double* A, int b, int n, const int* diag_idx, std::size_t nnzb,
                            int implicit, double ga, double inv_es, cudaStream_t st) {
     const std::size_t total = nnzb * b * b;
-    k_build_lhs<<<nb((long long)total), kT, 0, st>>>(J, A, b * b, n, diag_idx, total, implicit, ga, inv_es);
+    { ::fnlh::note_launch(); k_build_lhs<<<nb((long long)total), kT, 0, st>>>(J, A, b * b, n, diag_idx, total, implicit, ga, inv_es); }
     FNLH_CUDA(cudaGetLastError());
 }
 
 void harmonic_shift(const double* vol, int n, double omega, double ga, double* s, cudaStream_t st) {
-    k_shift<<<nb(n), kT, 0, st>>>(vol, n, omega, ga, s);
+    { ::fnlh::note_launch(); k_shift<<<nb(n), kT, 0, st>>>(vol, n, omega, ga, s); }
 }
 
 void shifted_blocks(const double* P, const double* vol, int b, int n, double omega, cplx* out, cudaStream_t st) {
-    k_shifted_blocks<<<nb(n), kT, 0, st>>>(P, vol, b, n, omega, out);
+    { ::fnlh::note_launch(); k_shifted_blocks<<<nb(n), kT, 0, st>>>(P, vol, b, n, omega, out); }
 }
 
 DeviceSolver::DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int* col_idx, const int* partition,
