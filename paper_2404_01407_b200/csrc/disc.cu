@@ -438,9 +438,13 @@ __global__ void k_accumulate(std::size_t len, const double* __restrict__ x, doub
 }
 
 __global__ void k_df_finish(std::size_t len, double nq, const double* __restrict__ acc, const double* __restrict__ inv,
-                            double* __restrict__ df, int divide) {
+                            double* __restrict__ df, int divide, const int* __restrict__ any) {
     const std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x;
     if (t >= len) return;
+    if (!*any) {  // all amplitudes zero: DF is exactly zero (residual_ops.cpp:139-141)
+        df[t] = 0.0;
+        return;
+    }
     const double a = divide ? acc[t] / nq : acc[t];
     df[t] = a - inv[t];
 }
@@ -671,7 +675,7 @@ void DeviceDisc::residual(const double* W, const double* wref, int order, int mo
     DISPATCH_B56(m.b, {
         if (order == 2) { ::fnlh::note_launch(); k_jst_prepass<B><<<nb(m.n), kT, 0, st>>>(m, W, nu_.ptr, lap_.ptr, skip); }
         { ::fnlh::note_launch(); k_face_flux<B><<<nb(m.nf), kT, 0, st>>>(m, W, wref, order, mode, forcing, nforcing, need_vis ? 1 : 0,
-                                                nu_.ptr, lap_.ptr, flux_.ptr, vflux_.ptr, err_.ptr, skip); }
+                                                nu_.ptr, lap_.ptr, flux_.ptr, vflux_.ptr, err(), skip); }
         { ::fnlh::note_launch(); k_node_gather<B><<<nb(m.n), kT, 0, st>>>(m, W, flux_.ptr, vflux_.ptr, need_vis ? 1 : 0, inv, vis, skip); }
     });
     FNLH_CUDA(cudaGetLastError());
@@ -768,48 +772,44 @@ void base_frequency(const std::vector<double>& omega, double& base, int& lmax) {
 }  // namespace
 
 void DeviceDisc::deterministic_flux(const double* mean, const std::vector<const cplx*>& amps,
-                                    const std::vector<double>& omega, double* df, cudaStream_t st) {
+                                    const std::vector<double>& omega, double* df, cudaStream_t st, bool deferred) {
     const std::size_t L = len();
     const int nh = static_cast<int>(amps.size());
     if (nh > 64) throw ConfigError("deterministic_flux: at most 64 harmonics");
     double base;
     int lmax;
     base_frequency(omega, base, lmax);
-    // any nonzero amplitude?  (residual_ops.cpp:133-141)
-    DeviceBuffer<int> flag(1);
-    FNLH_CUDA(cudaMemsetAsync(flag.ptr, 0, sizeof(int), st));
-    for (int h = 0; h < nh; ++h) { ::fnlh::note_launch(); k_any_nonzero<<<std::min(nb((long long)L), 592), kT, 0, st>>>(L, amps[h], flag.ptr); }
-    int hflag = 0;
-    FNLH_CUDA(cudaMemcpyAsync(&hflag, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
-    FNLH_CUDA(cudaStreamSynchronize(st));
-    if (!hflag) {
-        FNLH_CUDA(cudaMemsetAsync(df, 0, L * sizeof(double), st));
-        return;
-    }
+    // any nonzero amplitude?  (residual_ops.cpp:133-141) -- decided on the device in k_df_finish
+    if (!df_flag_.ptr) df_flag_.alloc(1);
+    FNLH_CUDA(cudaMemsetAsync(df_flag_.ptr, 0, sizeof(int), st));
+    for (int h = 0; h < nh; ++h) { ::fnlh::note_launch(); k_any_nonzero<<<std::min(nb((long long)L), 592), kT, 0, st>>>(L, amps[h], df_flag_.ptr); }
     AmpList al{};
     for (int h = 0; h < nh; ++h) al.a[h] = amps[h];
     const int nq = lmax == 0 ? 1 : 4 * lmax + 2;
-    std::vector<std::complex<double>> ph((std::size_t)nq * std::max(nh, 1));
-    const double period = lmax == 0 ? 0.0 : 2.0 * std::acos(-1.0) / base;
-    for (int k = 0; k < nq; ++k) {
-        const double t = lmax == 0 ? 0.0 : period * k / nq;
-        for (int h = 0; h < nh; ++h) ph[(std::size_t)k * nh + h] = std::exp(std::complex<double>(0.0, omega[h] * t));
+    if (omega != df_omega_ || !df_ph_.ptr) {
+        std::vector<std::complex<double>> ph((std::size_t)nq * std::max(nh, 1));
+        const double period = lmax == 0 ? 0.0 : 2.0 * std::acos(-1.0) / base;
+        for (int k = 0; k < nq; ++k) {
+            const double t = lmax == 0 ? 0.0 : period * k / nq;
+            for (int h = 0; h < nh; ++h) ph[(std::size_t)k * nh + h] = std::exp(std::complex<double>(0.0, omega[h] * t));
+        }
+        FNLH_CUDA(cudaStreamSynchronize(st));  // the previous phase table may still be in use
+        df_ph_.upload(reinterpret_cast<const cplx*>(ph.data()), ph.size());
+        df_omega_ = omega;
     }
-    DeviceBuffer<cplx> dph;
-    dph.upload(reinterpret_cast<const cplx*>(ph.data()), ph.size());
+    const cplx* dph = df_ph_.ptr;
     double* w = scratch_real[0].ptr;
     double* inv = scratch_real[1].ptr;
     double* acc = scratch_real[2].ptr;
     for (int k = 0; k < nq; ++k) {
-        { ::fnlh::note_launch(); k_reconstruct<<<nb((long long)L), kT, 0, st>>>(L, mean, al, nh, dph.ptr + (std::size_t)k * nh, w); }
+        { ::fnlh::note_launch(); k_reconstruct<<<nb((long long)L), kT, 0, st>>>(L, mean, al, nh, dph + (std::size_t)k * nh, w); }
         residual(w, nullptr, 2, 0, nullptr, 0, false, inv, nullptr, st);
         { ::fnlh::note_launch(); k_accumulate<<<nb((long long)L), kT, 0, st>>>(L, inv, acc, k == 0); }
     }
-    raise_if_err(st, "deterministic_flux");
     residual(mean, nullptr, 2, 0, nullptr, 0, false, inv, nullptr, st);
-    { ::fnlh::note_launch(); k_df_finish<<<nb((long long)L), kT, 0, st>>>(L, (double)nq, acc, inv, df, lmax == 0 ? 0 : 1); }
+    { ::fnlh::note_launch(); k_df_finish<<<nb((long long)L), kT, 0, st>>>(L, (double)nq, acc, inv, df, lmax == 0 ? 0 : 1, df_flag_.ptr); }
     FNLH_CUDA(cudaGetLastError());
-    raise_if_err(st, "deterministic_flux");
+    if (!deferred) raise_if_err(st, "deterministic_flux");
 }
 
 // ---------------------------------------------------------------------------

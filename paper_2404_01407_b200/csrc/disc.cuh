@@ -32,7 +32,9 @@ public:
     std::size_t len() const { return (std::size_t)view_.n * view_.b; }
 
     // device error word: (key << 4) | code, ~0 when clean
-    unsigned long long* err() const { return err_.ptr; }
+    unsigned long long* err() const { return cur_err_ ? cur_err_ : err_.ptr; }
+    // route error records of subsequent launches to another device word (nullptr: the default)
+    void redirect_err(unsigned long long* p) { cur_err_ = p; }
     void reset_err(cudaStream_t st);
     // 0 or the reference status code of the first recorded error (synchronizes)
     int read_err(cudaStream_t st, long long* key = nullptr);
@@ -49,10 +51,12 @@ public:
     // linearized_residual (mean is the perturbation reference); complex vectors as cplx
     void linearized_residual(const double* mean, const cplx* what, double omega, const cplx* forcing, int nforcing,
                              int order, bool need_vis, cplx* inv, cplx* vis, cudaStream_t st);
-    // deterministic_flux; amps: nh device pointers; omega/index host
+    // deterministic_flux; amps: nh device pointers; omega/index host.  deferred: enqueue
+    // only (no host synchronization); errors stay in err() for the caller to read
     void deterministic_flux(const double* mean, const std::vector<const cplx*>& amps,
-                            const std::vector<double>& omega, double* df, cudaStream_t st);
+                            const std::vector<double>& omega, double* df, cudaStream_t st, bool deferred = false);
 
+    const int* df_active() const { return df_flag_.ptr; }  // set by the last deterministic_flux
     DeviceBuffer<double> scratch_real[6];  // linres / DF temporaries (len each)
 private:
     MeshDev view_{};
@@ -61,8 +65,12 @@ private:
     DeviceBuffer<double> fn_, farea_, fnh_, fvis_, vol_, closure_, mu_;
     DeviceBuffer<double> nu_, lap_, flux_, vflux_, qscale_, scal_;
     DeviceBuffer<unsigned long long> err_;
+    unsigned long long* cur_err_ = nullptr;
     DeviceBuffer<unsigned long long> umax_;
     DeviceBuffer<double> fwork_;  // forcing perturbation vectors
+    DeviceBuffer<int> df_flag_;   // any nonzero amplitude (residual_ops.cpp:133-141)
+    DeviceBuffer<cplx> df_ph_;    // quadrature phases e^{i omega_h t_k}, cached per omega set
+    std::vector<double> df_omega_;
     std::vector<double> h_nfpad_;
 };
 

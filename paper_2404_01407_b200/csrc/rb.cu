@@ -580,18 +580,27 @@ void RbSystem::load(const double* A_csr, cudaStream_t stm) {
     FNLH_CUDA(cudaGetLastError());
 }
 
+__global__ void k_status_init(int* status) {
+    status[0] = 0;
+    status[1] = 0x7fffffff;
+}
+
 template <class S>
-void rb_factorize(const RbSystem& A, const double* shift_im, RbIlu<S>& f, Workspace& ws) {
+void rb_factorize_async(const RbSystem& A, const double* shift_im, RbIlu<S>& f, int* status, cudaStream_t stm) {
     const SellLayout& L = A.layout();
     const SellDev sd = sell_dev(L, A.vals());
-    const int init[2] = {0, 0x7fffffff};
-    FNLH_CUDA(cudaMemcpyAsync(ws.status, init, sizeof init, cudaMemcpyHostToDevice, ws.stream));
+    { ::fnlh::note_launch(); k_status_init<<<1, 1, 0, stm>>>(status); }
     RB_DISPATCH(L.b, {
-        { ::fnlh::note_launch(); k_rb_factor0<B, S><<<A.grid0, kT, 0, ws.stream>>>(sd, shift_im, f.diag_lu, f.diag_piv, f.inv0, ws.status); }
-        { ::fnlh::note_launch(); k_rb_factor1<B, S><<<A.grid1, kT, 0, ws.stream>>>(sd, A.pattern()->row_ptr, A.trans(), shift_im, f.diag_lu,
-                                                           f.diag_piv, f.inv0, ws.status); }
+        { ::fnlh::note_launch(); k_rb_factor0<B, S><<<A.grid0, kT, 0, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, f.inv0, status); }
+        { ::fnlh::note_launch(); k_rb_factor1<B, S><<<A.grid1, kT, 0, stm>>>(sd, A.pattern()->row_ptr, A.trans(), shift_im, f.diag_lu,
+                                                           f.diag_piv, f.inv0, status); }
     });
     FNLH_CUDA(cudaGetLastError());
+}
+
+template <class S>
+void rb_factorize(const RbSystem& A, const double* shift_im, RbIlu<S>& f, Workspace& ws) {
+    rb_factorize_async<S>(A, shift_im, f, ws.status, ws.stream);
     FNLH_CUDA(cudaMemcpyAsync(ws.h_status, ws.status, 2 * sizeof(int), cudaMemcpyDeviceToHost, ws.stream));
     FNLH_CUDA(cudaStreamSynchronize(ws.stream));
     if (ws.h_status[1] != 0x7fffffff) throw FactorizationError("near-singular ILU pivot block", ws.h_status[1]);
@@ -634,6 +643,8 @@ void rb_smoothed_solve(const RbSystem& A, const double* shift_im, const RbIlu<S>
 template struct RbIlu<double>;
 template struct RbIlu<cplx>;
 template void rb_factorize<double>(const RbSystem&, const double*, RbIlu<double>&, Workspace&);
+template void rb_factorize_async<double>(const RbSystem&, const double*, RbIlu<double>&, int*, cudaStream_t);
+template void rb_factorize_async<cplx>(const RbSystem&, const double*, RbIlu<cplx>&, int*, cudaStream_t);
 template void rb_factorize<cplx>(const RbSystem&, const double*, RbIlu<cplx>&, Workspace&);
 template void rb_smoothed_solve<double>(const RbSystem&, const double*, const RbIlu<double>&, const double*, double,
                                         int, double*, double*, double*, RbControl*, Workspace&);

@@ -97,6 +97,9 @@ public:
 // factorize the (shifted) system into the compact RB factors; throws FactorizationError
 template <class S>
 void rb_factorize(const RbSystem& A, const double* shift_im, RbIlu<S>& f, Workspace& ws);
+// same, enqueued only: status[1] receives the first near-singular pivot row (0x7fffffff when clean)
+template <class S>
+void rb_factorize_async(const RbSystem& A, const double* shift_im, RbIlu<S>& f, int* status, cudaStream_t st);
 
 // enqueue a complete smoothed_solve (no host synchronization); the report lands in *ctl
 // (device); x is overwritten.

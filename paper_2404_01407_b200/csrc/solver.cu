@@ -107,7 +107,7 @@ DeviceSolver::DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int
             rbA_ = std::make_unique<RbSystem>(pat_.get(), n0);
             rb_mean_ = std::make_unique<RbIlu<double>>(pat_.get(), n0);
             rb_h_ = std::make_unique<RbIlu<cplx>>(pat_.get(), n0);  // ONE workspace reused by every harmonic
-            ctl_.alloc(1);
+            ctl_.alloc(5);
             rb_z_.alloc(len);
             rb_r_.alloc(len);
         } else {
@@ -123,6 +123,8 @@ DeviceSolver::DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int
         pcpiv_.alloc(len);
     }
     for (auto& v : rk_) v.alloc(len);
+    stage_err_.alloc(11);
+    fac_status_.alloc(2);
     FNLH_CUDA(cudaEventCreate(&ev0_));
     FNLH_CUDA(cudaEventCreate(&ev1_));
 }
@@ -140,26 +142,21 @@ std::size_t DeviceSolver::lhs_bytes() const {
     return s;
 }
 
-// rk_step (rk.cpp:41-99)
 template <class S>
-LinearSolveReport DeviceSolver::rb_solve(const double* shift, const RbIlu<S>& f, const S* rhs, S* x) {
+void DeviceSolver::rb_solve_async(const double* shift, const RbIlu<S>& f, const S* rhs, S* x, RbControl* ctl) {
     rb_smoothed_solve<S>(*rbA_, shift, f, rhs, sch_.linear_tol, sch_.linear_max_iter, x,
-                         reinterpret_cast<S*>(rb_z_.ptr), reinterpret_cast<S*>(rb_r_.ptr), ctl_.ptr, *ws_);
-    RbControl h;
-    FNLH_CUDA(cudaMemcpyAsync(&h, ctl_.ptr, sizeof h, cudaMemcpyDeviceToHost, ws_->stream));
-    FNLH_CUDA(cudaStreamSynchronize(ws_->stream));
-    if (h.status == 6) throw DivergenceError("non-finite iterate in smoothed_solve", h.iterations, "linear");
-    LinearSolveReport rep;
-    rep.iterations = h.iterations;
-    rep.initial_residual = h.initial_residual;
-    rep.final_residual = h.final_residual;
-    rep.converged = h.converged;
-    return rep;
+                         reinterpret_cast<S*>(rb_z_.ptr), reinterpret_cast<S*>(rb_r_.ptr), ctl, *ws_);
 }
 
+// rk_step (rk.cpp:41-99), enqueued without host round trips: residual-evaluation and
+// update errors land in per-stage device words, the fused solver's reports in per-stage
+// control blocks, the stage-1 norm on the device; one synchronization at the end turns
+// them into the reference's exceptions in stage order.  `solve` returns the report when
+// the solver is host-driven (general path) and false when it is deferred (ctl[k-1]).
 template <class S, class Eval, class Apply, class Solve>
 RkStepResult DeviceSolver::rk_step(S* state, Eval&& eval, Apply&& apply, Solve&& solve, const S* pdiag_lu,
-                                   const int* pdiag_piv, const std::string& field) {
+                                   const int* pdiag_piv, const std::string& field, const int* fac_status,
+                                   bool check_df) {
     cudaStream_t st = ws_->stream;
     const std::size_t len = disc_->len();
     S* state0 = reinterpret_cast<S*>(rk_[0].ptr);
@@ -173,56 +170,86 @@ RkStepResult DeviceSolver::rk_step(S* state, Eval&& eval, Apply&& apply, Solve&&
     FNLH_CUDA(cudaMemcpyAsync(stage, state, len * sizeof(S), cudaMemcpyDeviceToDevice, st));
     FNLH_CUDA(cudaMemsetAsync(vis_blend, 0, len * sizeof(S), st));
     FNLH_CUDA(cudaMemsetAsync(vis_fresh, 0, len * sizeof(S), st));
+    FNLH_CUDA(cudaMemsetAsync(stage_err_.ptr, 0xff, 10 * sizeof(unsigned long long), st));
     RkStepResult res;
+    LinearSolveReport host_rep[5];
+    bool have_host[5] = {false, false, false, false, false};
     const double gfac = sch_.implicit ? 1.0 / sch_.eps_relax : sigma_;  // rk.hpp:34
     for (int k = 1; k <= 5; ++k) {
         const double beta = kBeta[k - 1];
         const bool fresh = beta != 0.0;
-        disc_->reset_err(st);
+        disc_->redirect_err(stage_err_.ptr + (k - 1));
         eval(stage, fresh, inv, vis_fresh);
-        {
-            long long key;
-            const int code = disc_->read_err(st, &key);
-            if (code) {
-                disc_->reset_err(st);
-                if (code == 2)
-                    throw DivergenceError("residual evaluation failed: inadmissible boundary state", k, field);
-                if (code == 4) throw UnsupportedCaseError("supersonic boundary state");
-                throw std::runtime_error("device error during residual evaluation");
-            }
-        }
+        disc_->redirect_err(nullptr);
         if (fresh) {
             ++res.viscous_evaluations;
             stage_blend<S>(beta, vis_fresh, vis_blend, len, st);
         }
         stage_rhs<S>(inv, vis_blend, rhs, len, st);
-        if (k == 1) {
-            norm2_sq<S>(rhs, len, ws_->scalars + 8, *ws_);
-            FNLH_CUDA(cudaMemcpyAsync(ws_->h_scalars + 8, ws_->scalars + 8, sizeof(double), cudaMemcpyDeviceToHost, st));
-            FNLH_CUDA(cudaStreamSynchronize(st));
-            res.stage1_residual_norm = std::sqrt(ws_->h_scalars[8]);
-        }
+        if (k == 1) norm2_sq<S>(rhs, len, ws_->scalars + 8, *ws_);
         if (!sch_.implicit) {
             block_diag_solve<S>(disc_->b(), disc_->n(), pdiag_lu, pdiag_piv, rhs, x, st);
             scale<S>(x, gfac * kAlpha[k - 1], len, st);
         } else {
             scale<S>(rhs, kAlpha[k - 1], len, st);
-            LinearSolveReport rep = solve(rhs, x);
+            LinearSolveReport rep;
+            if (solve(rhs, x, k, rep)) {
+                host_rep[k - 1] = rep;
+                have_host[k - 1] = true;
+            }
+        }
+        disc_->redirect_err(stage_err_.ptr + 5 + (k - 1));
+        apply(state0, x, stage);
+        check_finite<S>(stage, len, disc_->err(), st);
+        disc_->redirect_err(nullptr);
+    }
+    unsigned long long errs[11];
+    RbControl ctls[5];
+    int fac[2] = {0, 0x7fffffff};
+    FNLH_CUDA(cudaMemcpyAsync(errs, stage_err_.ptr, sizeof errs, cudaMemcpyDeviceToHost, st));
+    if (fac_status) FNLH_CUDA(cudaMemcpyAsync(fac, fac_status, sizeof fac, cudaMemcpyDeviceToHost, st));
+    int df_active = 0;
+    if (check_df && disc_->df_active())
+        FNLH_CUDA(cudaMemcpyAsync(&df_active, disc_->df_active(), sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (rbA_ && sch_.implicit) FNLH_CUDA(cudaMemcpyAsync(ctls, ctl_.ptr, sizeof ctls, cudaMemcpyDeviceToHost, st));
+    FNLH_CUDA(cudaMemcpyAsync(ws_->h_scalars + 8, ws_->scalars + 8, sizeof(double), cudaMemcpyDeviceToHost, st));
+    FNLH_CUDA(cudaStreamSynchronize(st));
+    res.stage1_residual_norm = std::sqrt(ws_->h_scalars[8]);
+    // errors raised before the step in the reference: the factorization, then DF
+    if (fac[1] != 0x7fffffff) throw FactorizationError("near-singular ILU pivot block", fac[1]);
+    if (check_df && df_active && errs[10] != ~0ull) {
+        const int code = (int)(errs[10] & 15ull);
+        if (code == 2) throw StateError("deterministic_flux: inadmissible state");
+        if (code == 4) throw UnsupportedCaseError("deterministic_flux: supersonic boundary state");
+        throw std::runtime_error("deterministic_flux: device error " + std::to_string(code));
+    }
+    for (int k = 1; k <= 5; ++k) {
+        const unsigned long long ee = errs[k - 1], ea = errs[5 + k - 1];
+        if (ee != ~0ull) {
+            const int code = (int)(ee & 15ull);
+            if (code == 2) throw DivergenceError("residual evaluation failed: inadmissible boundary state", k, field);
+            if (code == 4) throw UnsupportedCaseError("supersonic boundary state");
+            throw std::runtime_error("device error during residual evaluation");
+        }
+        if (sch_.implicit) {
+            LinearSolveReport rep;
+            if (have_host[k - 1]) {
+                rep = host_rep[k - 1];
+            } else {
+                const RbControl& c = ctls[k - 1];
+                if (c.status == 6) throw DivergenceError("non-finite iterate in smoothed_solve", c.iterations, "linear");
+                rep.iterations = c.iterations;
+                rep.initial_residual = c.initial_residual;
+                rep.final_residual = c.final_residual;
+                rep.converged = c.converged;
+            }
             sweeps += rep.iterations;
             row_updates += (long long)rep.iterations * disc_->n();
             res.linear_reports.push_back(rep);
         }
-        disc_->reset_err(st);
-        apply(state0, x, stage);
-        check_finite<S>(stage, len, disc_->err(), st);
-        {
-            long long key;
-            const int code = disc_->read_err(st, &key);
-            if (code) {
-                disc_->reset_err(st);
-                if (code == 2) throw DivergenceError("update left the admissible set", k, field);
-                throw DivergenceError("non-finite stage state", k, field);
-            }
+        if (ea != ~0ull) {
+            if ((int)(ea & 15ull) == 2) throw DivergenceError("update left the admissible set", k, field);
+            throw DivergenceError("non-finite stage state", k, field);
         }
     }
     FNLH_CUDA(cudaMemcpyAsync(state, stage, len * sizeof(S), cudaMemcpyDeviceToDevice, st));
@@ -285,13 +312,17 @@ ConvergenceEntry DeviceSolver::outer_iteration() {
             Ah.real_vals = A5_.ptr;
             Ah.shift_im = shift_.ptr;
             if (rbA_) {
-                rb_factorize<cplx>(*rbA_, shift_.ptr, *rb_h_, *ws_);
-                auto solve = [&](const cplx* rhs, cplx* x) { return rb_solve<cplx>(shift_.ptr, *rb_h_, rhs, x); };
-                step = rk_step<cplx>(amp, eval, apply, solve, nullptr, nullptr, name);
+                rb_factorize_async<cplx>(*rbA_, shift_.ptr, *rb_h_, fac_status_.ptr, st);
+                auto solve = [&](const cplx* rhs, cplx* x, int k, LinearSolveReport&) {
+                    rb_solve_async<cplx>(shift_.ptr, *rb_h_, rhs, x, ctl_.ptr + (k - 1));
+                    return false;
+                };
+                step = rk_step<cplx>(amp, eval, apply, solve, nullptr, nullptr, name, fac_status_.ptr);
             } else {
                 ilu_factorize<cplx>(Ah, *ilu_h_, *ws_);
-                auto solve = [&](const cplx* rhs, cplx* x) {
-                    return smoothed_solve<cplx>(Ah, rhs, *ilu_h_, sch_.linear_tol, sch_.linear_max_iter, x, *ws_);
+                auto solve = [&](const cplx* rhs, cplx* x, int, LinearSolveReport& rep) {
+                    rep = smoothed_solve<cplx>(Ah, rhs, *ilu_h_, sch_.linear_tol, sch_.linear_max_iter, x, *ws_);
+                    return true;
                 };
                 step = rk_step<cplx>(amp, eval, apply, solve, nullptr, nullptr, name);
             }
@@ -303,7 +334,7 @@ ConvergenceEntry DeviceSolver::outer_iteration() {
             FNLH_CUDA(cudaMemcpyAsync(ws_->h_status, ws_->status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
             FNLH_CUDA(cudaStreamSynchronize(st));
             if (ws_->h_status[1] != 0x7fffffff) throw FactorizationError("singular pivot block", ws_->h_status[1]);
-            auto none = [&](const cplx*, cplx*) { return LinearSolveReport{}; };
+            auto none = [&](const cplx*, cplx*, int, LinearSolveReport&) { return true; };
             step = rk_step<cplx>(amp, eval, apply, none, pclu_.ptr, pcpiv_.ptr, name);
         }
         h_norm[h] = step.stage1_residual_norm;
@@ -313,7 +344,10 @@ ConvergenceEntry DeviceSolver::outer_iteration() {
     // deterministic flux from the fresh harmonic fields (driver.cpp:268-271)
     std::vector<const cplx*> amps;
     for (int h = 0; h < nh_; ++h) amps.push_back(amps_.ptr + (std::size_t)h * len);
-    disc_->deterministic_flux(mean_.ptr, amps, omega_, df_.ptr, st);
+    FNLH_CUDA(cudaMemsetAsync(stage_err_.ptr + 10, 0xff, sizeof(unsigned long long), st));
+    disc_->redirect_err(stage_err_.ptr + 10);
+    disc_->deterministic_flux(mean_.ptr, amps, omega_, df_.ptr, st, /*deferred=*/true);
+    disc_->redirect_err(nullptr);
 
     // mean update including DF (driver.cpp:273-296)
     auto mean_eval = [&](const double* state, bool need_vis, double* inv, double* vis) {
@@ -325,19 +359,23 @@ ConvergenceEntry DeviceSolver::outer_iteration() {
     };
     RkStepResult mstep;
     if (implicit && rbA_) {
-        auto solve = [&](const double* rhs, double* x) { return rb_solve<double>(nullptr, *rb_mean_, rhs, x); };
-        mstep = rk_step<double>(mean_.ptr, mean_eval, mean_apply, solve, nullptr, nullptr, "mean");
+        auto solve = [&](const double* rhs, double* x, int k, LinearSolveReport&) {
+            rb_solve_async<double>(nullptr, *rb_mean_, rhs, x, ctl_.ptr + (k - 1));
+            return false;
+        };
+        mstep = rk_step<double>(mean_.ptr, mean_eval, mean_apply, solve, nullptr, nullptr, "mean", nullptr, true);
     } else if (implicit) {
         SystemView<double> Am;
         Am.p = pat_.get();
         Am.real_vals = A5_.ptr;
-        auto solve = [&](const double* rhs, double* x) {
-            return smoothed_solve<double>(Am, rhs, *ilu_mean_, sch_.linear_tol, sch_.linear_max_iter, x, *ws_);
+        auto solve = [&](const double* rhs, double* x, int, LinearSolveReport& rep) {
+            rep = smoothed_solve<double>(Am, rhs, *ilu_mean_, sch_.linear_tol, sch_.linear_max_iter, x, *ws_);
+            return true;
         };
-        mstep = rk_step<double>(mean_.ptr, mean_eval, mean_apply, solve, nullptr, nullptr, "mean");
+        mstep = rk_step<double>(mean_.ptr, mean_eval, mean_apply, solve, nullptr, nullptr, "mean", nullptr, true);
     } else {
-        auto none = [&](const double*, double*) { return LinearSolveReport{}; };
-        mstep = rk_step<double>(mean_.ptr, mean_eval, mean_apply, none, PLU_.ptr, Ppiv_.ptr, "mean");
+        auto none = [&](const double*, double*, int, LinearSolveReport&) { return true; };
+        mstep = rk_step<double>(mean_.ptr, mean_eval, mean_apply, none, PLU_.ptr, Ppiv_.ptr, "mean", nullptr, true);
     }
     for (auto& r : hreps) reports_.push_back(r);
     for (auto& r : mstep.linear_reports) reports_.push_back(r);

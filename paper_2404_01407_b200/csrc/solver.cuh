@@ -75,9 +75,9 @@ public:
 private:
     template <class S, class Eval, class Apply, class Solve>
     RkStepResult rk_step(S* state, Eval&& eval, Apply&& apply, Solve&& solve, const S* pdiag_lu, const int* pdiag_piv,
-                         const std::string& field);
+                         const std::string& field, const int* fac_status = nullptr, bool check_df = false);
     template <class S>
-    LinearSolveReport rb_solve(const double* shift, const RbIlu<S>& f, const S* rhs, S* x);
+    void rb_solve_async(const double* shift, const RbIlu<S>& f, const S* rhs, S* x, RbControl* ctl);
 
     SchemeConfig sch_;
     double sigma_ = 50.0;
@@ -95,7 +95,9 @@ private:
     std::unique_ptr<RbSystem> rbA_;  // 2-colour fast path (rb.cuh), null when not eligible
     std::unique_ptr<RbIlu<double>> rb_mean_;
     std::unique_ptr<RbIlu<cplx>> rb_h_;
-    DeviceBuffer<RbControl> ctl_;
+    DeviceBuffer<RbControl> ctl_;                 // one per RK stage
+    DeviceBuffer<unsigned long long> stage_err_;  // [0,5) eval, [5,10) apply, [10] deterministic flux
+    DeviceBuffer<int> fac_status_;                // harmonic factorization status (deferred check)
     DeviceBuffer<cplx> rb_z_, rb_r_;
     DeviceBuffer<cplx> rk_[7];  // state0, inv, vis_fresh, vis_blend, rhs, x, stage (complex or reinterpreted real)
     std::vector<LinearSolveReport> reports_;
