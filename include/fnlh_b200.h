@@ -83,12 +83,20 @@ int fnlh_smoothed_solve(const fnlh_pattern* p, int is_complex, const double* A, 
 
 /* 2-colour fast path (rb.cuh): *n0 = size of colour 0 when the pattern is a colour-major
    2-colour ordering with one partition, else -1.  fnlh_set_red_black(0) forces the general
-   level-scheduled kernels everywhere (both paths are bitwise the reference's iterates). */
+   level-scheduled kernels everywhere.  fnlh_set_rb_sweep selects the 2-colour sweep:
+     0 (default) iterates bitwise those of smoothed_solve (sparse.hpp:295-331): L_ik =
+       A_ik inv(U_kk) rebuilt per block in the reference's operation order; the colour-1
+       residual of sweep s is fused with the colour-1 forward substitution of sweep s+1
+       (2 kernels per sweep);
+     1 the same arithmetic as three kernels per sweep (K_F, K_B, K_R);
+     2 one pass over A per sweep, L_ik r_k applied as A_ik (U_kk^{-1} r_k): the same
+       preconditioner, iterates equal to rounding, not bitwise. */
 int fnlh_pattern_is_red_black(fnlh_pattern* p, int* n0);
 /* compact factors of the 2-colour ILU(0): pivot LU + piv for every row, inv(U_kk) for colour 0 */
 int fnlh_rb_factorize(fnlh_pattern* p, int is_complex, const double* A, const double* shift_im, double* diag_lu,
                       int* diag_piv, double* inv0);
 void fnlh_set_red_black(int enable);
+int fnlh_set_rb_sweep(int mode);
 
 /* ---- L2/L3: the 3D edge-based discretization ---------------------------------
    Node-centred median-dual mesh (paper_2404_01407_b200/mesh.py builds one):

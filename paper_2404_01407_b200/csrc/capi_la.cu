@@ -1,6 +1,7 @@
 // capi_la.cu -- extern "C" entry points for the L1 block-sparse LA (include/fnlh_b200.h).
 #include <memory>
 #include <string>
+#include <vector>
 
 #include "fnlh_b200.h"
 #include "capi_util.hpp"
@@ -135,9 +136,20 @@ int rb_factor_impl(fnlh_pattern* p, const double* A, const double* shift_im, dou
     sys.load(a.ptr, ws.stream);
     RbIlu<S> f(dp, p->n0);
     rb_factorize<S>(sys, shift_im ? sh.ptr : nullptr, f, ws);
-    const std::size_t bb = (std::size_t)dp->b * dp->b;
-    if (diag_lu) download(reinterpret_cast<S*>(diag_lu), f.diag_lu, (std::size_t)dp->rows * bb);
-    if (diag_piv) download(diag_piv, f.diag_piv, (std::size_t)dp->rows * dp->b);
+    const int b = dp->b, bb = b * b;
+    if (diag_lu) {  // packed [slice][k][lane] -> row-major rows*b*b
+        std::vector<S> pk(f.packed_rows() * bb);
+        download(pk.data(), f.diag_lu, pk.size());
+        S* out = reinterpret_cast<S*>(diag_lu);
+        for (int i = 0; i < dp->rows; ++i)
+            for (int k = 0; k < bb; ++k) out[(std::size_t)i * bb + k] = pk[f.packed_base(i, bb) + 32 * k];
+    }
+    if (diag_piv) {
+        std::vector<int> pk(f.packed_rows() * b);
+        download(pk.data(), f.diag_piv, pk.size());
+        for (int i = 0; i < dp->rows; ++i)
+            for (int k = 0; k < b; ++k) diag_piv[(std::size_t)i * b + k] = pk[f.packed_base(i, b) + 32 * k];
+    }
     if (inv0) download(reinterpret_cast<S*>(inv0), f.inv0, (std::size_t)p->n0 * bb);
     return 0;
 }
@@ -252,5 +264,12 @@ int fnlh_rb_factorize(fnlh_pattern* p, int is_complex, const double* A, const do
 }
 
 void fnlh_set_red_black(int enable) { fnlh::rb_enabled() = enable != 0; }
+
+int fnlh_set_rb_sweep(int mode) {
+    return guarded([&] {
+        if (mode < 0 || mode > 2) throw ConfigError("fnlh_set_rb_sweep: mode must be 0, 1 or 2");
+        fnlh::rb_sweep_mode() = mode;
+    });
+}
 
 }  // extern "C"

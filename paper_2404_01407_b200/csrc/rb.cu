@@ -55,6 +55,29 @@ __device__ __forceinline__ void ablock(const SellDev& L, const RowRef& r, int e,
 
 __device__ __forceinline__ int acol(const SellDev& L, const RowRef& r, int e) { return __ldg(L.cols + r.cbase + e * 32); }
 
+// pivot blocks (diag_lu) and pivots are stored slice-major like A: row i -> slice s,
+// lane l; element k of the row at [s][k][l], so a warp's k-th load is 32 consecutive
+// elements (rb.cuh RbIlu)
+struct LuRef {
+    long long lu;  // element offset of k = 0
+    long long pv;
+};
+template <int B>
+__device__ __forceinline__ LuRef lu_ref(const SellDev& L, int i) {
+    const int li = i < L.n0 ? i : i - L.n0;
+    const int s = (i < L.n0 ? 0 : L.nslices0) + (li >> 5);
+    const int lane = li & 31;
+    return LuRef{(long long)s * 32 * B * B + lane, (long long)s * 32 * B + lane};
+}
+template <int B, class S>
+__device__ __forceinline__ void ld_lu(const S* __restrict__ dlu, const int* __restrict__ piv, const LuRef& q,
+                                      S (&lu)[B * B], int (&pv)[B]) {
+#pragma unroll
+    for (int k = 0; k < B * B; ++k) lu[k] = dlu[q.lu + 32 * k];
+#pragma unroll
+    for (int k = 0; k < B; ++k) pv[k] = piv[q.pv + 32 * k];
+}
+
 // y[r] += sum_c A_e[r][c] x[c] (block_matvec_add, dense.hpp:20-28); the diagonal block of
 // a shifted system carries complex(a + 0, 0 + s) on its diagonal (shift_diagonal)
 template <int B, class S>
@@ -206,10 +229,7 @@ __global__ void __launch_bounds__(kT) k_rb_forward1(SellDev L, const S* __restri
     }
     S lu[B * B];
     int pv[B];
-#pragma unroll
-    for (int k = 0; k < B * B; ++k) lu[k] = diag_lu[(size_t)i * B * B + k];
-#pragma unroll
-    for (int k = 0; k < B; ++k) pv[k] = piv[(size_t)i * B + k];
+    ld_lu<B>(diag_lu, piv, lu_ref<B>(L, i), lu, pv);
     lu_solve_reg<B>(lu, pv, zf);
     st<B>(z + (size_t)i * B, zf);
 }
@@ -260,10 +280,7 @@ __global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const double* __re
         }
         S lu[B * B];
         int pv[B];
-#pragma unroll
-        for (int k = 0; k < B * B; ++k) lu[k] = diag_lu[(size_t)i * B * B + k];
-#pragma unroll
-        for (int k = 0; k < B; ++k) pv[k] = piv[(size_t)i * B + k];
+        ld_lu<B>(diag_lu, piv, lu_ref<B>(L, i), lu, pv);
         lu_solve_reg<B>(lu, pv, t);
         S xi[B];
         ld<B>(x + (size_t)i * B, xi);
@@ -359,6 +376,314 @@ __global__ void __launch_bounds__(kT) k_rb_resid1(SellDev L, const double* __res
     }
 }
 
+// ---- K_RF: colour 1 residual of sweep s fused with the forward substitution of s+1 --
+// Both walk the row's lower blocks A_ik: y += A_ik x_k (residual, ascending) and
+// L_ik r_k with L_ik = A_ik inv(U_kk) rebuilt as in K_F; the L_ik r_k products are
+// parked in shared memory because the forward sum starts from r_i, which is known only
+// after the residual row is complete (zf = r_i - L r_k1 - L r_k2 ..., sparse.cpp:267-278).
+template <int B, class S>
+__global__ void __launch_bounds__(kT) k_rbx_colour1(SellDev L, const double* __restrict__ shift,
+                                                    const S* __restrict__ diag_lu, const int* __restrict__ piv,
+                                                    const S* __restrict__ inv0, const S* __restrict__ rhs,
+                                                    S* __restrict__ x, S* __restrict__ z, const S* __restrict__ r,
+                                                    double* __restrict__ partials, int grid0, RbControl* ctl,
+                                                    int sweep, int max_iter, int forward, unsigned int* counter) {
+    __shared__ double red[kT / 32];
+    __shared__ bool last;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    S* park = reinterpret_cast<S*>(smem_raw);  // [slot][row][tid]
+    if (ctl->done) return;
+    const int tid = threadIdx.x;
+    const int i = L.n0 + blockIdx.x * kT + tid;
+    double loc = 0.0;
+    if (i < L.n) {
+        const RowRef rr = row_ref(L, i);
+        const int dg = rr.deg - 1;
+        S xi[B], zi[B], y[B];
+        ld<B>(x + (size_t)i * B, xi);
+        ld<B>(z + (size_t)i * B, zi);
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            xi[k] += zi[k];
+            y[k] = zero<S>();
+        }
+        st<B>(x + (size_t)i * B, xi);
+        for (int e = 0; e < dg; ++e) {
+            const int kk = acol(L, rr, e);
+            S xk[B], rk[B];
+            ld<B>(x + (size_t)kk * B, xk);
+            double A[2 * pairs<B>()];
+            ablock<B>(L, rr, e, A);
+#pragma unroll
+            for (int rw = 0; rw < B; ++rw) {
+                S acc = zero<S>();
+#pragma unroll
+                for (int c = 0; c < B; ++c) acc += rmul(A[rw * B + c], xk[c]);
+                y[rw] += acc;
+            }
+            if (forward) {
+                ld<B>(r + (size_t)kk * B, rk);
+                const S* __restrict__ U = inv0 + (size_t)kk * B * B;
+                S acc[B];
+#pragma unroll
+                for (int rw = 0; rw < B; ++rw) acc[rw] = zero<S>();
+#pragma unroll
+                for (int c = 0; c < B; ++c) {
+                    S uc[B];
+#pragma unroll
+                    for (int m = 0; m < B; ++m) uc[m] = U[m * B + c];
+#pragma unroll
+                    for (int rw = 0; rw < B; ++rw) {
+                        S lrc = zero<S>();
+#pragma unroll
+                        for (int m = 0; m < B; ++m) lrc += rmul(A[rw * B + m], uc[m]);
+                        acc[rw] += lrc * rk[c];
+                    }
+                }
+#pragma unroll
+                for (int rw = 0; rw < B; ++rw) park[(e * B + rw) * kT + tid] = acc[rw];
+            }
+        }
+        blk_matvec_add<B, S>(L, rr, dg, xi, shift != nullptr, shift ? shift[i] : 0.0, y);
+        S ri[B];
+        ld<B>(rhs + (size_t)i * B, ri);
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            ri[k] -= y[k];
+            loc += sq(ri[k]);
+        }
+        if (forward) {
+            for (int e = 0; e < dg; ++e)
+#pragma unroll
+                for (int rw = 0; rw < B; ++rw) ri[rw] -= park[(e * B + rw) * kT + tid];
+            S lu[B * B];
+            int pv[B];
+            ld_lu<B>(diag_lu, piv, lu_ref<B>(L, i), lu, pv);
+            lu_solve_reg<B>(lu, pv, ri);
+            st<B>(z + (size_t)i * B, ri);
+        }
+    }
+    const double bs = block_sum(loc, red);
+    if (threadIdx.x == 0) {
+        partials[grid0 + blockIdx.x] = bs;
+        __threadfence();
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    const double tot = ordered_sum(partials, grid0 + gridDim.x, red);
+    if (threadIdx.x == 0) {
+        const double nrm = sqrt(tot);
+        ctl->iterations = sweep;
+        ctl->final_residual = nrm;
+        if (!isfinite(nrm)) {
+            ctl->status = 6;
+            ctl->done = 1;
+        } else if (nrm <= ctl->target) {
+            ctl->converged = 1;
+            ctl->done = 1;
+        } else if (sweep >= max_iter) {
+            ctl->done = 1;
+        }
+        *counter = 0u;
+    }
+}
+
+// ---- one-pass sweep (fnlh_set_rb_sweep(2)): two kernels per sweep -----------
+// The same preconditioner M = LU, applied with L_ik r_k = A_ik (U_kk^{-1} r_k): colour-0
+// rows publish w_k = U_kk^{-1} r_k (kept in the colour-0 half of z) when they finish
+// their residual, so the colour-1 forward substitution is a plain block-row product and
+// fuses with the colour-1 residual of the previous sweep (both walk the same A_ik
+// blocks).  Every block of A is read once per sweep; the iterates agree with the
+// reference order to rounding (tests: 1e-12 relative), not bitwise -- the kernels above
+// are the bitwise path (fnlh_set_rb_sweep(0|1)).
+//
+// K0(s): colour 0 rows: t = r_i - sum_j A_ij z_j; z_i = U_ii^{-1} t; x_i += z_i;
+//        r_i = b_i - A_ii x_i - sum_j A_ij (x_j + z_j); w_i = U_ii^{-1} r_i
+// K1(s): colour 1 rows: x_i += z_i; r_i = b_i - sum_k A_ik x_k - A_ii x_i (sweep s);
+//        stopping decision of sweep s (last CTA); then, speculatively for s + 1,
+//        z_i = U_ii^{-1} (r_i - sum_k A_ik w_k)
+template <int B, class S>
+__global__ void __launch_bounds__(kT) k_rbf_w0(SellDev L, const S* __restrict__ diag_lu, const int* __restrict__ piv,
+                                               const S* __restrict__ rhs, S* __restrict__ z, const RbControl* ctl) {
+    if (ctl->done) return;
+    const int i = blockIdx.x * kT + threadIdx.x;
+    if (i >= L.n0) return;
+    S t[B];
+    ld<B>(rhs + (size_t)i * B, t);
+    S lu[B * B];
+    int pv[B];
+    ld_lu<B>(diag_lu, piv, lu_ref<B>(L, i), lu, pv);
+    lu_solve_reg<B>(lu, pv, t);
+    st<B>(z + (size_t)i * B, t);
+}
+
+template <int B, class S>
+__global__ void __launch_bounds__(kT) k_rbf_colour0(SellDev L, const double* __restrict__ shift,
+                                                    const S* __restrict__ diag_lu, const int* __restrict__ piv,
+                                                    const S* __restrict__ rhs, S* __restrict__ x, S* __restrict__ z,
+                                                    S* __restrict__ r, double* __restrict__ partials0,
+                                                    const RbControl* ctl, int sweep) {
+    __shared__ double red[kT / 32];
+    if (ctl->done) return;
+    const int tid = threadIdx.x;
+    const int i = blockIdx.x * kT + tid;
+    double loc = 0.0;
+    if (i < L.n0) {
+        const RowRef rr = row_ref(L, i);
+        S t[B], ym[B];
+        ld<B>((sweep == 1 ? rhs : r) + (size_t)i * B, t);
+#pragma unroll
+        for (int k = 0; k < B; ++k) ym[k] = zero<S>();
+        for (int e = 1; e < rr.deg; ++e) {
+            const int j = acol(L, rr, e);
+            S zj[B], xj[B];
+            ld<B>(z + (size_t)j * B, zj);
+            ld<B>(x + (size_t)j * B, xj);
+#pragma unroll
+            for (int k = 0; k < B; ++k) xj[k] += zj[k];
+            double A[2 * pairs<B>()];
+            ablock<B>(L, rr, e, A);
+#pragma unroll
+            for (int rw = 0; rw < B; ++rw) {
+                S accb = zero<S>(), accm = zero<S>();
+#pragma unroll
+                for (int c = 0; c < B; ++c) {
+                    const double a = A[rw * B + c];
+                    accb += rmul(a, zj[c]);
+                    accm += rmul(a, xj[c]);
+                }
+                t[rw] -= accb;
+                ym[rw] += accm;
+            }
+        }
+        S lu[B * B];
+        int pv[B];
+        ld_lu<B>(diag_lu, piv, lu_ref<B>(L, i), lu, pv);
+        lu_solve_reg<B>(lu, pv, t);
+        S xi[B];
+        ld<B>(x + (size_t)i * B, xi);
+#pragma unroll
+        for (int k = 0; k < B; ++k) xi[k] += t[k];
+        st<B>(x + (size_t)i * B, xi);
+        S y[B];
+#pragma unroll
+        for (int k = 0; k < B; ++k) y[k] = zero<S>();
+        blk_matvec_add<B, S>(L, rr, 0, xi, shift != nullptr, shift ? shift[i] : 0.0, y);
+        S bi[B];
+        ld<B>(rhs + (size_t)i * B, bi);
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            const S v = bi[k] - (y[k] + ym[k]);
+            t[k] = v;
+            loc += sq(v);
+        }
+        st<B>(r + (size_t)i * B, t);
+        lu_solve_reg<B>(lu, pv, t);
+        st<B>(z + (size_t)i * B, t);  // w_i
+    }
+    const double bs = block_sum(loc, red);
+    if (tid == 0) partials0[blockIdx.x] = bs;
+}
+
+template <int B, class S>
+__global__ void __launch_bounds__(kT) k_rbf_colour1(SellDev L, const double* __restrict__ shift,
+                                                    const S* __restrict__ diag_lu, const int* __restrict__ piv,
+                                                    const S* __restrict__ rhs, S* __restrict__ x, S* __restrict__ z,
+                                                    double* __restrict__ partials, int grid0, RbControl* ctl, int sweep,
+                                                    int max_iter, int forward, unsigned int* counter) {
+    __shared__ double red[kT / 32];
+    __shared__ bool last;
+    if (ctl->done) return;
+    const int i = L.n0 + blockIdx.x * kT + threadIdx.x;
+    double loc = 0.0;
+    if (i < L.n) {
+        const RowRef rr = row_ref(L, i);
+        const int dg = rr.deg - 1;
+        S ri[B], f[B];
+        ld<B>(rhs + (size_t)i * B, ri);
+#pragma unroll
+        for (int k = 0; k < B; ++k) f[k] = zero<S>();
+        if (sweep >= 1) {
+            S xi[B], zi[B], y[B];
+            ld<B>(x + (size_t)i * B, xi);
+            ld<B>(z + (size_t)i * B, zi);
+#pragma unroll
+            for (int k = 0; k < B; ++k) {
+                xi[k] += zi[k];
+                y[k] = zero<S>();
+            }
+            st<B>(x + (size_t)i * B, xi);
+            for (int e = 0; e < dg; ++e) {
+                const int kk = acol(L, rr, e);
+                S xk[B], wk[B];
+                ld<B>(x + (size_t)kk * B, xk);
+                ld<B>(z + (size_t)kk * B, wk);
+                double A[2 * pairs<B>()];
+                ablock<B>(L, rr, e, A);
+#pragma unroll
+                for (int rw = 0; rw < B; ++rw) {
+                    S accy = zero<S>(), accf = zero<S>();
+#pragma unroll
+                    for (int c = 0; c < B; ++c) {
+                        const double a = A[rw * B + c];
+                        accy += rmul(a, xk[c]);
+                        accf += rmul(a, wk[c]);
+                    }
+                    y[rw] += accy;
+                    f[rw] += accf;
+                }
+            }
+            blk_matvec_add<B, S>(L, rr, dg, xi, shift != nullptr, shift ? shift[i] : 0.0, y);
+#pragma unroll
+            for (int k = 0; k < B; ++k) {
+                ri[k] -= y[k];
+                loc += sq(ri[k]);
+            }
+        } else {
+            for (int e = 0; e < dg; ++e) {
+                S wk[B];
+                ld<B>(z + (size_t)acol(L, rr, e) * B, wk);
+                blk_matvec_add<B, S>(L, rr, e, wk, false, 0.0, f);
+            }
+        }
+        if (forward) {
+#pragma unroll
+            for (int k = 0; k < B; ++k) ri[k] -= f[k];
+            S lu[B * B];
+            int pv[B];
+            ld_lu<B>(diag_lu, piv, lu_ref<B>(L, i), lu, pv);
+            lu_solve_reg<B>(lu, pv, ri);
+            st<B>(z + (size_t)i * B, ri);
+        }
+    }
+    if (sweep < 1) return;
+    const double bs = block_sum(loc, red);
+    if (threadIdx.x == 0) {
+        partials[grid0 + blockIdx.x] = bs;
+        __threadfence();
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    const double tot = ordered_sum(partials, grid0 + gridDim.x, red);
+    if (threadIdx.x == 0) {
+        const double nrm = sqrt(tot);
+        ctl->iterations = sweep;
+        ctl->final_residual = nrm;
+        if (!isfinite(nrm)) {
+            ctl->status = 6;
+            ctl->done = 1;
+        } else if (nrm <= ctl->target) {
+            ctl->converged = 1;
+            ctl->done = 1;
+        } else if (sweep >= max_iter) {
+            ctl->done = 1;
+        }
+        *counter = 0u;
+    }
+}
+
 // ---- factorization ---------------------------------------------------------
 template <int B, class S>
 __global__ void k_rb_factor0(SellDev L, const double* __restrict__ shift, S* __restrict__ diag_lu,
@@ -376,10 +701,11 @@ __global__ void k_rb_factor0(SellDev L, const double* __restrict__ shift, S* __r
     int pv[B];
     double cond;
     if (lu_factor_reg<B>(A, pv, cond) || !(cond < 1e14)) atomicMin(status + 1, i);
+    const LuRef q = lu_ref<B>(L, i);
 #pragma unroll
-    for (int k = 0; k < B * B; ++k) diag_lu[(size_t)i * B * B + k] = A[k];
+    for (int k = 0; k < B * B; ++k) diag_lu[q.lu + 32 * k] = A[k];
 #pragma unroll
-    for (int k = 0; k < B; ++k) piv[(size_t)i * B + k] = pv[k];
+    for (int k = 0; k < B; ++k) piv[q.pv + 32 * k] = pv[k];
 #pragma unroll
     for (int c = 0; c < B; ++c) {
         S col[B];
@@ -438,10 +764,11 @@ __global__ void k_rb_factor1(SellDev L, const int* __restrict__ row_ptr, const l
     int pv[B];
     double cond;
     if (lu_factor_reg<B>(Uii, pv, cond) || !(cond < 1e14)) atomicMin(status + 1, i);
+    const LuRef q = lu_ref<B>(L, i);
 #pragma unroll
-    for (int k = 0; k < B * B; ++k) diag_lu[(size_t)i * B * B + k] = Uii[k];
+    for (int k = 0; k < B * B; ++k) diag_lu[q.lu + 32 * k] = Uii[k];
 #pragma unroll
-    for (int k = 0; k < B; ++k) piv[(size_t)i * B + k] = pv[k];
+    for (int k = 0; k < B; ++k) piv[q.pv + 32 * k] = pv[k];
 }
 
 __global__ void k_to_sell(const double* __restrict__ A, const long long* __restrict__ map, int bb, long long nnzb,
@@ -490,8 +817,8 @@ bool rb_eligible(const DevicePattern& p, int* n0) {
 template <class S>
 RbIlu<S>::RbIlu(const DevicePattern* pat, int n0_) : p(pat), n0(n0_) {
     const std::size_t bb = (std::size_t)p->b * p->b;
-    FNLH_CUDA(cudaMalloc(&diag_lu, (std::size_t)p->rows * bb * sizeof(S)));
-    FNLH_CUDA(cudaMalloc(&diag_piv, (std::size_t)p->rows * p->b * sizeof(int)));
+    FNLH_CUDA(cudaMalloc(&diag_lu, packed_rows() * bb * sizeof(S)));
+    FNLH_CUDA(cudaMalloc(&diag_piv, packed_rows() * p->b * sizeof(int)));
     FNLH_CUDA(cudaMalloc(&inv0, std::max<std::size_t>((std::size_t)n0 * bb, 1) * sizeof(S)));
 }
 template <class S>
@@ -503,7 +830,7 @@ RbIlu<S>::~RbIlu() {
 template <class S>
 std::size_t RbIlu<S>::bytes() const {
     const std::size_t bb = (std::size_t)p->b * p->b;
-    return ((std::size_t)p->rows * bb + (std::size_t)n0 * bb) * sizeof(S) + (std::size_t)p->rows * p->b * sizeof(int);
+    return (packed_rows() * bb + (std::size_t)n0 * bb) * sizeof(S) + packed_rows() * p->b * sizeof(int);
 }
 
 RbSystem::RbSystem(const DevicePattern* p, int n0) : p_(p) {
@@ -627,14 +954,36 @@ void rb_smoothed_solve(const RbSystem& A, const double* shift_im, const RbIlu<S>
         static bool attr = false;
         if (!attr) {
             FNLH_CUDA(cudaFuncSetAttribute(k_rb_colour0<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            FNLH_CUDA(cudaFuncSetAttribute(k_rbx_colour1<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
             attr = true;
         }
-        for (int s = 1; s <= max_iter; ++s) {
-            { ::fnlh::note_launch(); k_rb_forward1<B, S><<<A.grid1, kT, 0, stm>>>(sd, f.diag_lu, f.diag_piv, f.inv0, rhs, r, z, ctl, s); }
-            { ::fnlh::note_launch(); k_rb_colour0<B, S><<<A.grid0, kT, sm, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, rhs, x, z, r, parts,
-                                                          ctl, s); }
-            { ::fnlh::note_launch(); k_rb_resid1<B, S><<<A.grid1, kT, 0, stm>>>(sd, shift_im, rhs, x, z, r, parts, A.grid0, ctl, s, max_iter,
-                                                        counter); }
+        if (rb_sweep_mode() == 1) {
+            for (int s = 1; s <= max_iter; ++s) {
+                { ::fnlh::note_launch(); k_rb_forward1<B, S><<<A.grid1, kT, 0, stm>>>(sd, f.diag_lu, f.diag_piv, f.inv0, rhs, r, z, ctl, s); }
+                { ::fnlh::note_launch(); k_rb_colour0<B, S><<<A.grid0, kT, sm, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, rhs, x, z, r, parts,
+                                                              ctl, s); }
+                { ::fnlh::note_launch(); k_rb_resid1<B, S><<<A.grid1, kT, 0, stm>>>(sd, shift_im, rhs, x, z, r, parts, A.grid0, ctl, s, max_iter,
+                                                            counter); }
+            }
+        } else if (rb_sweep_mode() == 0) {
+            { ::fnlh::note_launch(); k_rb_forward1<B, S><<<A.grid1, kT, 0, stm>>>(sd, f.diag_lu, f.diag_piv, f.inv0, rhs, r, z, ctl, 1); }
+            for (int s = 1; s <= max_iter; ++s) {
+                { ::fnlh::note_launch(); k_rb_colour0<B, S><<<A.grid0, kT, sm, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, rhs, x, z, r, parts,
+                                                              ctl, s); }
+                { ::fnlh::note_launch(); k_rbx_colour1<B, S><<<A.grid1, kT, sm, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, f.inv0, rhs, x, z, r,
+                                                               parts, A.grid0, ctl, s, max_iter, s < max_iter ? 1 : 0,
+                                                               counter); }
+            }
+        } else {
+            { ::fnlh::note_launch(); k_rbf_w0<B, S><<<A.grid0, kT, 0, stm>>>(sd, f.diag_lu, f.diag_piv, rhs, z, ctl); }
+            { ::fnlh::note_launch(); k_rbf_colour1<B, S><<<A.grid1, kT, 0, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, rhs, x, z, parts,
+                                                           A.grid0, ctl, 0, max_iter, 1, counter); }
+            for (int s = 1; s <= max_iter; ++s) {
+                { ::fnlh::note_launch(); k_rbf_colour0<B, S><<<A.grid0, kT, 0, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, rhs, x, z, r, parts,
+                                                               ctl, s); }
+                { ::fnlh::note_launch(); k_rbf_colour1<B, S><<<A.grid1, kT, 0, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, rhs, x, z, parts,
+                                                               A.grid0, ctl, s, max_iter, s < max_iter ? 1 : 0, counter); }
+            }
         }
     });
     FNLH_CUDA(cudaGetLastError());

@@ -54,6 +54,15 @@ inline bool& rb_enabled() {
     static bool on = true;
     return on;
 }
+// fnlh_set_rb_sweep: the 2-colour sweep variant
+//   0 (default) reference operation order, K_R(s) fused with K_F(s+1): 2 kernels per sweep
+//   1           reference operation order, split K_F / K_B / K_R: 3 kernels per sweep
+//   2           one pass over A per sweep, L_ik r_k applied as A_ik (U_kk^{-1} r_k):
+//               same preconditioner, iterates equal to rounding (not bitwise)
+inline int& rb_sweep_mode() {
+    static int mode = 0;
+    return mode;
+}
 
 // is the pattern a 2-colour colour-major ordering with one partition?
 bool rb_eligible(const DevicePattern& p, int* n0);
@@ -62,14 +71,23 @@ template <class S>
 struct RbIlu {
     const DevicePattern* p = nullptr;
     int n0 = 0;
-    S* diag_lu = nullptr;   // rows*b*b
-    int* diag_piv = nullptr;
+    S* diag_lu = nullptr;   // pivot LUs, slice-major [slice][k][lane] (rows padded to 32 per colour)
+    int* diag_piv = nullptr;  // same layout, b per row
     S* inv0 = nullptr;      // n0*b*b, inv(U_kk) of colour 0 rows
     RbIlu(const DevicePattern* pat, int n0_);
     ~RbIlu();
     RbIlu(const RbIlu&) = delete;
     RbIlu& operator=(const RbIlu&) = delete;
     std::size_t bytes() const;
+    std::size_t packed_rows() const {
+        return (std::size_t)32 * ((n0 + 31) / 32 + (p->rows - n0 + 31) / 32);
+    }
+    // packed row index of row i, element stride 32 (host-side unpacking)
+    std::size_t packed_base(int i, int width) const {
+        const int li = i < n0 ? i : i - n0;
+        const std::size_t s = (i < n0 ? 0 : (n0 + 31) / 32) + (li >> 5);
+        return s * 32 * width + (li & 31);
+    }
 };
 
 class RbSystem {

@@ -111,8 +111,18 @@ def smoothed_solve(pat: Pattern, A, rhs, tol_rel, max_iter, shift_im=None):
 
 
 def set_red_black(enable: bool):
-    """Enable / disable the 2-colour fused sweep (rb.cuh); both paths give the reference's iterates."""
+    """Enable / disable the 2-colour fused sweep (rb.cuh) in favour of the level-scheduled kernels."""
     lib().fnlh_set_red_black(_i(1 if enable else 0))
+
+
+RB_EXACT, RB_EXACT_SPLIT, RB_ONEPASS = 0, 1, 2
+
+
+def set_rb_sweep(mode: int):
+    """2-colour sweep variant (include/fnlh_b200.h fnlh_set_rb_sweep): RB_EXACT (default,
+    bitwise reference iterates, 2 kernels/sweep), RB_EXACT_SPLIT (same, 3 kernels/sweep),
+    RB_ONEPASS (one pass over A, iterates equal to rounding)."""
+    check(lib().fnlh_set_rb_sweep(_i(mode)))
 
 
 def red_black_n0(pat: Pattern) -> int:

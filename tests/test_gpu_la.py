@@ -53,15 +53,26 @@ def test_ilu_factor_apply_solve(ref, meshes, b, cplx, kind):
     yd = la.matvec(P, A, rhs, shift) if cplx else la.matvec(P, A, rhs)
     assert np.array_equal(yd, yr)
     assert (la.red_black_n0(P) > 0) == (kind == "hex")
-    for rb in (True, False):  # the 2-colour fused sweep and the general level-scheduled path
+    # the 2-colour sweep in reference order (bitwise; fused and split kernels), the one-pass
+    # 2-colour sweep (same preconditioner applied as A_ik (U_kk^-1 r_k): equal to rounding),
+    # and the general level-scheduled path (bitwise)
+    for rb, mode in ((True, la.RB_EXACT), (True, la.RB_EXACT_SPLIT), (True, la.RB_ONEPASS), (False, la.RB_EXACT)):
         la.set_red_black(rb)
+        la.set_rb_sweep(mode)
+        exact = mode != la.RB_ONEPASS or kind == "tet"
         for tol, it in ((1e-2, 10), (1e-12, 6)):
             xr, rr = ref.smoothed_solve(pat, Aref, rhs, tol, it)
             xd, rd = la.smoothed_solve(P, A, rhs, tol, it, shift) if cplx else la.smoothed_solve(P, A, rhs, tol, it)
-            assert np.array_equal(xd, xr), (rb, tol)
             assert rd[0] == rr[0] and rd[3] == rr[3]
-            assert abs(rd[1] / rr[1] - 1) < 1e-14 and abs(rd[2] / rr[2] - 1) < 1e-12
+            assert abs(rd[1] / rr[1] - 1) < 1e-14
+            if exact:
+                assert np.array_equal(xd, xr), (rb, mode, tol)
+                assert abs(rd[2] / rr[2] - 1) < 1e-12
+            else:
+                assert np.abs(xd - xr).max() <= 1e-12 * np.abs(xr).max(), (tol, np.abs(xd - xr).max())
+                assert abs(rd[2] - rr[2]) <= 1e-12 * rr[1]
     la.set_red_black(True)
+    la.set_rb_sweep(la.RB_EXACT)
     if kind == "hex":
         fb = la.rb_factorize(P, A, shift)
         n0 = fb["n0"]
