@@ -139,6 +139,10 @@ typedef struct { /* SchemeConfig (driver.hpp:22-42) */
     int linear_max_iter;
     double target_drop_orders;
     int max_outer_iters;
+    int workers; /* harmonics in flight (driver.cpp:246-265): on the 2-colour path min(workers,
+                    N_h, 8) lanes, each with its own complex ILU workspace, share one read of A5
+                    per batched sweep; > 1 also gives the reference's worker semantics (every
+                    harmonic runs, successful ones commit, the first error by index rethrown) */
 } fnlh_scheme;
 
 typedef struct { /* ConvergenceEntry (driver.hpp:50-58); resid_h returned separately */
@@ -167,6 +171,9 @@ double fnlh_solver_lhs_bytes(const fnlh_solver* s);
 /* time `sweeps` Richardson sweeps (smoothed_solve, sparse.hpp:315-329) of harmonic h's system at
    the current mean; *ms = device time of the loop */
 int fnlh_solver_time_sweeps(fnlh_solver* s, int h, int sweeps, double* ms);
+/* the batched sweep of harmonics [0, P) (P <= lanes), device ms for the whole loop */
+int fnlh_solver_time_sweeps_batch(fnlh_solver* s, int P, int sweeps, double* ms);
+int fnlh_solver_lanes(const fnlh_solver* s);
 /* [red_black (0/1), n0 (colour 0 rows), SELL doubles incl. padding, nnzb] */
 int fnlh_solver_info(const fnlh_solver* s, double* out);
 /* counters: [sweeps, block-row updates, last outer iteration device ms] */

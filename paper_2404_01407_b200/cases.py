@@ -54,7 +54,7 @@ SPECS = {
 
 
 def make_case(name: str, scale: float = 1.0, nh: int | None = None, implicit: bool = True, permute: bool = True,
-              **overrides) -> Case:
+              workers: int = 1, **overrides) -> Case:
     """Build config `name` ('c1'..'c5').  `scale` shrinks the cell counts (parity tests run
     the same configuration at sizes the CPU oracle finishes in seconds)."""
     spec = dict(SPECS[name])
@@ -105,6 +105,6 @@ def make_case(name: str, scale: float = 1.0, nh: int | None = None, implicit: bo
         forcing[h, 3 * inlet + 1] = 1e-3 * p * np.exp(1j * ph)
     scheme = dict(implicit=1 if implicit else 0, sigma_cfl=spec["sigma"] if implicit else -1.0, eps_relax=0.6,
                   linear_tol=spec["tol"], linear_max_iter=spec["max_iter"], target_drop_orders=8.0,
-                  max_outer_iters=spec["steps"])
+                  max_outer_iters=spec["steps"], workers=workers)
     return Case(name=name, mesh=m, scheme=scheme, omegas=omegas, forcing=forcing, mean0=W.reshape(-1),
                 pseudo_steps=spec["steps"], description=spec["desc"])

@@ -149,6 +149,7 @@ int fnlh_solver_create(const fnlh_mesh_desc* m, const int* row_ptr, const int* c
         sc.linear_max_iter = s->linear_max_iter;
         sc.target_drop_orders = s->target_drop_orders;
         sc.max_outer_iters = s->max_outer_iters;
+        sc.workers = s->workers;
         auto h = std::make_unique<fnlh_solver>();
         h->s = std::make_unique<DeviceSolver>(arrays(m), row_ptr, col_idx, partition, sc, nh, index, omega, forcing,
                                               nforcing, mean0);
@@ -201,6 +202,12 @@ int fnlh_solver_get_reports(const fnlh_solver* s, fnlh_linear_report* out) {
 int fnlh_solver_time_sweeps(fnlh_solver* s, int h, int sweeps, double* ms) {
     return guarded([&] { *ms = s->s->time_harmonic_sweeps(h, sweeps); });
 }
+
+int fnlh_solver_time_sweeps_batch(fnlh_solver* s, int P, int sweeps, double* ms) {
+    return guarded([&] { *ms = s->s->time_harmonic_sweeps_batch(P, sweeps); });
+}
+
+int fnlh_solver_lanes(const fnlh_solver* s) { return s->s->lanes(); }
 
 double fnlh_solver_lhs_bytes(const fnlh_solver* s) { return static_cast<double>(s->s->lhs_bytes()); }
 

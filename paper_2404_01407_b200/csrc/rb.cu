@@ -150,24 +150,55 @@ __device__ double ordered_sum(const double* __restrict__ p, int n, double* red) 
     return block_sum(s, red);
 }
 
+// per-member operand table of a batched sweep: P independent systems that share the
+// real A (one per harmonic in flight, driver.cpp:246-265 workers); CTA b serves member
+// b % P, so the P CTAs touching the same slice of A run back to back and A comes from
+// HBM once per sweep of the batch (L2 serves the rest)
+template <class S>
+struct RbTab {
+    const S* diag_lu[kMaxBatch];
+    const int* piv[kMaxBatch];
+    const S* inv0[kMaxBatch];
+    const double* shift[kMaxBatch];
+    const S* rhs[kMaxBatch];
+    S* x[kMaxBatch];
+    S* z[kMaxBatch];
+    S* r[kMaxBatch];
+    RbControl* ctl[kMaxBatch];
+    double* parts[kMaxBatch];
+    int P;
+};
+
 // ---- pre-kernel: ||b||, target, x = 0 --------------------------------------
 template <class S>
-__global__ void k_rb_init(std::size_t len, const S* __restrict__ rhs, double* __restrict__ partials, int nparts,
-                          RbControl* ctl, double tol, unsigned int* counter) {
+__global__ void k_rb_init(std::size_t len, const RbTab<S> T, double tol) {
+    const int P_ = T.P, h_ = blockIdx.x % P_, cta = blockIdx.x / P_;
+    [[maybe_unused]] const int nct = gridDim.x / P_;
+    [[maybe_unused]] const S* __restrict__ diag_lu = T.diag_lu[h_];
+    [[maybe_unused]] const int* __restrict__ piv = T.piv[h_];
+    [[maybe_unused]] const S* __restrict__ inv0 = T.inv0[h_];
+    [[maybe_unused]] const double* __restrict__ shift = T.shift[h_];
+    [[maybe_unused]] const S* __restrict__ rhs = T.rhs[h_];
+    [[maybe_unused]] S* __restrict__ x = T.x[h_];
+    [[maybe_unused]] S* __restrict__ z = T.z[h_];
+    [[maybe_unused]] S* __restrict__ r = T.r[h_];
+    RbControl* ctl = T.ctl[h_];
+    [[maybe_unused]] unsigned int* counter = &ctl->counter;
+    [[maybe_unused]] double* __restrict__ partials = T.parts[h_];
     __shared__ double red[kT / 32];
     __shared__ bool last;
     double loc = 0.0;
-    for (std::size_t t = blockIdx.x * (std::size_t)kT + threadIdx.x; t < len; t += (std::size_t)gridDim.x * kT)
+    for (std::size_t t = cta * (std::size_t)kT + threadIdx.x; t < len; t += (std::size_t)nct * kT)
         loc += sq(rhs[t]);
     const double bs = block_sum(loc, red);
     if (threadIdx.x == 0) {
-        partials[blockIdx.x] = bs;
+        partials[cta] = bs;
         __threadfence();
-        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+        last = atomicAdd(counter, 1u) == nct - 1;
     }
     __syncthreads();
     if (!last) return;
-    const double tot = ordered_sum(partials, gridDim.x, red);
+    const double tot = ordered_sum(partials, nct, red);
     if (threadIdx.x == 0) {
         const double r0 = sqrt(tot);
         ctl->initial_residual = r0;
@@ -179,7 +210,6 @@ __global__ void k_rb_init(std::size_t len, const S* __restrict__ rhs, double* __
         ctl->status = 0;
         *counter = 0u;
     }
-    (void)nparts;
 }
 
 // ---- K_F: colour 1 forward substitution -------------------------------------
@@ -187,12 +217,22 @@ __global__ void k_rb_init(std::size_t len, const S* __restrict__ rhs, double* __
 // rebuilt in the reference's order (sparse.cpp:221-232); colour 1 rows have no upper
 // entries, so the backward step is the pivot solve alone.
 template <int B, class S>
-__global__ void __launch_bounds__(kT) k_rb_forward1(SellDev L, const S* __restrict__ diag_lu,
-                                                    const int* __restrict__ piv, const S* __restrict__ inv0,
-                                                    const S* __restrict__ rhs, const S* __restrict__ r,
-                                                    S* __restrict__ z, const RbControl* ctl, int sweep) {
+__global__ void __launch_bounds__(kT) k_rb_forward1(SellDev L, const RbTab<S> T, int sweep) {
+    const int P_ = T.P, h_ = blockIdx.x % P_, cta = blockIdx.x / P_;
+    [[maybe_unused]] const int nct = gridDim.x / P_;
+    [[maybe_unused]] const S* __restrict__ diag_lu = T.diag_lu[h_];
+    [[maybe_unused]] const int* __restrict__ piv = T.piv[h_];
+    [[maybe_unused]] const S* __restrict__ inv0 = T.inv0[h_];
+    [[maybe_unused]] const double* __restrict__ shift = T.shift[h_];
+    [[maybe_unused]] const S* __restrict__ rhs = T.rhs[h_];
+    [[maybe_unused]] S* __restrict__ x = T.x[h_];
+    [[maybe_unused]] S* __restrict__ z = T.z[h_];
+    [[maybe_unused]] S* __restrict__ r = T.r[h_];
+    RbControl* ctl = T.ctl[h_];
+    [[maybe_unused]] unsigned int* counter = &ctl->counter;
+    [[maybe_unused]] double* __restrict__ partials = T.parts[h_];
     if (ctl->done) return;
-    const int i = L.n0 + blockIdx.x * kT + threadIdx.x;
+    const int i = L.n0 + cta * kT + threadIdx.x;
     if (i >= L.n) return;
     const RowRef rr = row_ref(L, i);
     const int dg = rr.deg - 1;
@@ -240,17 +280,26 @@ __global__ void __launch_bounds__(kT) k_rb_forward1(SellDev L, const S* __restri
 // pivot solve and x += z the residual row is summed in ascending order
 // (sparse.hpp:317-319).  Every block is read from HBM once.
 template <int B, class S>
-__global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const double* __restrict__ shift,
-                                                   const S* __restrict__ diag_lu, const int* __restrict__ piv,
-                                                   const S* __restrict__ rhs, S* __restrict__ x,
-                                                   const S* __restrict__ z, S* __restrict__ r,
-                                                   double* __restrict__ partials0, const RbControl* ctl, int sweep) {
+__global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const RbTab<S> T, int sweep) {
+    const int P_ = T.P, h_ = blockIdx.x % P_, cta = blockIdx.x / P_;
+    [[maybe_unused]] const int nct = gridDim.x / P_;
+    [[maybe_unused]] const S* __restrict__ diag_lu = T.diag_lu[h_];
+    [[maybe_unused]] const int* __restrict__ piv = T.piv[h_];
+    [[maybe_unused]] const S* __restrict__ inv0 = T.inv0[h_];
+    [[maybe_unused]] const double* __restrict__ shift = T.shift[h_];
+    [[maybe_unused]] const S* __restrict__ rhs = T.rhs[h_];
+    [[maybe_unused]] S* __restrict__ x = T.x[h_];
+    [[maybe_unused]] S* __restrict__ z = T.z[h_];
+    [[maybe_unused]] S* __restrict__ r = T.r[h_];
+    RbControl* ctl = T.ctl[h_];
+    [[maybe_unused]] unsigned int* counter = &ctl->counter;
+    [[maybe_unused]] double* __restrict__ partials = T.parts[h_];
     __shared__ double red[kT / 32];
     extern __shared__ __align__(16) unsigned char smem_raw[];
     S* park = reinterpret_cast<S*>(smem_raw);  // [slot][row][tid]
     if (ctl->done) return;
     const int tid = threadIdx.x;
-    const int i = blockIdx.x * kT + tid;
+    const int i = cta * kT + tid;
     double loc = 0.0;
     if (i < L.n0) {
         const RowRef rr = row_ref(L, i);
@@ -305,7 +354,7 @@ __global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const double* __re
         }
     }
     const double bs = block_sum(loc, red);
-    if (tid == 0) partials0[blockIdx.x] = bs;
+    if (tid == 0) partials[cta] = bs;
 }
 
 // ---- K_R: colour 1 residual rows + stopping rule ------------------------------
@@ -313,15 +362,24 @@ __global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const double* __re
 // diagonal), ||r|| over both colours and the stopping decision of this sweep
 // (sparse.hpp:318-328), taken by the last CTA on the device.
 template <int B, class S>
-__global__ void __launch_bounds__(kT) k_rb_resid1(SellDev L, const double* __restrict__ shift,
-                                                  const S* __restrict__ rhs, S* __restrict__ x,
-                                                  const S* __restrict__ z, S* __restrict__ r,
-                                                  double* __restrict__ partials, int grid0, RbControl* ctl,
-                                                  int sweep, int max_iter, unsigned int* counter) {
+__global__ void __launch_bounds__(kT) k_rb_resid1(SellDev L, const RbTab<S> T, int grid0, int sweep, int max_iter) {
+    const int P_ = T.P, h_ = blockIdx.x % P_, cta = blockIdx.x / P_;
+    [[maybe_unused]] const int nct = gridDim.x / P_;
+    [[maybe_unused]] const S* __restrict__ diag_lu = T.diag_lu[h_];
+    [[maybe_unused]] const int* __restrict__ piv = T.piv[h_];
+    [[maybe_unused]] const S* __restrict__ inv0 = T.inv0[h_];
+    [[maybe_unused]] const double* __restrict__ shift = T.shift[h_];
+    [[maybe_unused]] const S* __restrict__ rhs = T.rhs[h_];
+    [[maybe_unused]] S* __restrict__ x = T.x[h_];
+    [[maybe_unused]] S* __restrict__ z = T.z[h_];
+    [[maybe_unused]] S* __restrict__ r = T.r[h_];
+    RbControl* ctl = T.ctl[h_];
+    [[maybe_unused]] unsigned int* counter = &ctl->counter;
+    [[maybe_unused]] double* __restrict__ partials = T.parts[h_];
     __shared__ double red[kT / 32];
     __shared__ bool last;
     if (ctl->done) return;
-    const int i = L.n0 + blockIdx.x * kT + threadIdx.x;
+    const int i = L.n0 + cta * kT + threadIdx.x;
     double loc = 0.0;
     if (i < L.n) {
         const RowRef rr = row_ref(L, i);
@@ -352,13 +410,13 @@ __global__ void __launch_bounds__(kT) k_rb_resid1(SellDev L, const double* __res
     }
     const double bs = block_sum(loc, red);
     if (threadIdx.x == 0) {
-        partials[grid0 + blockIdx.x] = bs;
+        partials[grid0 + cta] = bs;
         __threadfence();
-        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+        last = atomicAdd(counter, 1u) == nct - 1;
     }
     __syncthreads();
     if (!last) return;
-    const double tot = ordered_sum(partials, grid0 + gridDim.x, red);
+    const double tot = ordered_sum(partials, grid0 + nct, red);
     if (threadIdx.x == 0) {
         const double nrm = sqrt(tot);
         ctl->iterations = sweep;
@@ -382,19 +440,27 @@ __global__ void __launch_bounds__(kT) k_rb_resid1(SellDev L, const double* __res
 // parked in shared memory because the forward sum starts from r_i, which is known only
 // after the residual row is complete (zf = r_i - L r_k1 - L r_k2 ..., sparse.cpp:267-278).
 template <int B, class S>
-__global__ void __launch_bounds__(kT) k_rbx_colour1(SellDev L, const double* __restrict__ shift,
-                                                    const S* __restrict__ diag_lu, const int* __restrict__ piv,
-                                                    const S* __restrict__ inv0, const S* __restrict__ rhs,
-                                                    S* __restrict__ x, S* __restrict__ z, const S* __restrict__ r,
-                                                    double* __restrict__ partials, int grid0, RbControl* ctl,
-                                                    int sweep, int max_iter, int forward, unsigned int* counter) {
+__global__ void __launch_bounds__(kT) k_rbx_colour1(SellDev L, const RbTab<S> T, int grid0, int sweep, int max_iter, int forward) {
+    const int P_ = T.P, h_ = blockIdx.x % P_, cta = blockIdx.x / P_;
+    [[maybe_unused]] const int nct = gridDim.x / P_;
+    [[maybe_unused]] const S* __restrict__ diag_lu = T.diag_lu[h_];
+    [[maybe_unused]] const int* __restrict__ piv = T.piv[h_];
+    [[maybe_unused]] const S* __restrict__ inv0 = T.inv0[h_];
+    [[maybe_unused]] const double* __restrict__ shift = T.shift[h_];
+    [[maybe_unused]] const S* __restrict__ rhs = T.rhs[h_];
+    [[maybe_unused]] S* __restrict__ x = T.x[h_];
+    [[maybe_unused]] S* __restrict__ z = T.z[h_];
+    [[maybe_unused]] S* __restrict__ r = T.r[h_];
+    RbControl* ctl = T.ctl[h_];
+    [[maybe_unused]] unsigned int* counter = &ctl->counter;
+    [[maybe_unused]] double* __restrict__ partials = T.parts[h_];
     __shared__ double red[kT / 32];
     __shared__ bool last;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     S* park = reinterpret_cast<S*>(smem_raw);  // [slot][row][tid]
     if (ctl->done) return;
     const int tid = threadIdx.x;
-    const int i = L.n0 + blockIdx.x * kT + tid;
+    const int i = L.n0 + cta * kT + tid;
     double loc = 0.0;
     if (i < L.n) {
         const RowRef rr = row_ref(L, i);
@@ -465,13 +531,13 @@ __global__ void __launch_bounds__(kT) k_rbx_colour1(SellDev L, const double* __r
     }
     const double bs = block_sum(loc, red);
     if (threadIdx.x == 0) {
-        partials[grid0 + blockIdx.x] = bs;
+        partials[grid0 + cta] = bs;
         __threadfence();
-        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+        last = atomicAdd(counter, 1u) == nct - 1;
     }
     __syncthreads();
     if (!last) return;
-    const double tot = ordered_sum(partials, grid0 + gridDim.x, red);
+    const double tot = ordered_sum(partials, grid0 + nct, red);
     if (threadIdx.x == 0) {
         const double nrm = sqrt(tot);
         ctl->iterations = sweep;
@@ -504,10 +570,22 @@ __global__ void __launch_bounds__(kT) k_rbx_colour1(SellDev L, const double* __r
 //        stopping decision of sweep s (last CTA); then, speculatively for s + 1,
 //        z_i = U_ii^{-1} (r_i - sum_k A_ik w_k)
 template <int B, class S>
-__global__ void __launch_bounds__(kT) k_rbf_w0(SellDev L, const S* __restrict__ diag_lu, const int* __restrict__ piv,
-                                               const S* __restrict__ rhs, S* __restrict__ z, const RbControl* ctl) {
+__global__ void __launch_bounds__(kT) k_rbf_w0(SellDev L, const RbTab<S> T) {
+    const int P_ = T.P, h_ = blockIdx.x % P_, cta = blockIdx.x / P_;
+    [[maybe_unused]] const int nct = gridDim.x / P_;
+    [[maybe_unused]] const S* __restrict__ diag_lu = T.diag_lu[h_];
+    [[maybe_unused]] const int* __restrict__ piv = T.piv[h_];
+    [[maybe_unused]] const S* __restrict__ inv0 = T.inv0[h_];
+    [[maybe_unused]] const double* __restrict__ shift = T.shift[h_];
+    [[maybe_unused]] const S* __restrict__ rhs = T.rhs[h_];
+    [[maybe_unused]] S* __restrict__ x = T.x[h_];
+    [[maybe_unused]] S* __restrict__ z = T.z[h_];
+    [[maybe_unused]] S* __restrict__ r = T.r[h_];
+    RbControl* ctl = T.ctl[h_];
+    [[maybe_unused]] unsigned int* counter = &ctl->counter;
+    [[maybe_unused]] double* __restrict__ partials = T.parts[h_];
     if (ctl->done) return;
-    const int i = blockIdx.x * kT + threadIdx.x;
+    const int i = cta * kT + threadIdx.x;
     if (i >= L.n0) return;
     S t[B];
     ld<B>(rhs + (size_t)i * B, t);
@@ -519,15 +597,24 @@ __global__ void __launch_bounds__(kT) k_rbf_w0(SellDev L, const S* __restrict__ 
 }
 
 template <int B, class S>
-__global__ void __launch_bounds__(kT) k_rbf_colour0(SellDev L, const double* __restrict__ shift,
-                                                    const S* __restrict__ diag_lu, const int* __restrict__ piv,
-                                                    const S* __restrict__ rhs, S* __restrict__ x, S* __restrict__ z,
-                                                    S* __restrict__ r, double* __restrict__ partials0,
-                                                    const RbControl* ctl, int sweep) {
+__global__ void __launch_bounds__(kT) k_rbf_colour0(SellDev L, const RbTab<S> T, int sweep) {
+    const int P_ = T.P, h_ = blockIdx.x % P_, cta = blockIdx.x / P_;
+    [[maybe_unused]] const int nct = gridDim.x / P_;
+    [[maybe_unused]] const S* __restrict__ diag_lu = T.diag_lu[h_];
+    [[maybe_unused]] const int* __restrict__ piv = T.piv[h_];
+    [[maybe_unused]] const S* __restrict__ inv0 = T.inv0[h_];
+    [[maybe_unused]] const double* __restrict__ shift = T.shift[h_];
+    [[maybe_unused]] const S* __restrict__ rhs = T.rhs[h_];
+    [[maybe_unused]] S* __restrict__ x = T.x[h_];
+    [[maybe_unused]] S* __restrict__ z = T.z[h_];
+    [[maybe_unused]] S* __restrict__ r = T.r[h_];
+    RbControl* ctl = T.ctl[h_];
+    [[maybe_unused]] unsigned int* counter = &ctl->counter;
+    [[maybe_unused]] double* __restrict__ partials = T.parts[h_];
     __shared__ double red[kT / 32];
     if (ctl->done) return;
     const int tid = threadIdx.x;
-    const int i = blockIdx.x * kT + tid;
+    const int i = cta * kT + tid;
     double loc = 0.0;
     if (i < L.n0) {
         const RowRef rr = row_ref(L, i);
@@ -583,19 +670,28 @@ __global__ void __launch_bounds__(kT) k_rbf_colour0(SellDev L, const double* __r
         st<B>(z + (size_t)i * B, t);  // w_i
     }
     const double bs = block_sum(loc, red);
-    if (tid == 0) partials0[blockIdx.x] = bs;
+    if (tid == 0) partials[cta] = bs;
 }
 
 template <int B, class S>
-__global__ void __launch_bounds__(kT) k_rbf_colour1(SellDev L, const double* __restrict__ shift,
-                                                    const S* __restrict__ diag_lu, const int* __restrict__ piv,
-                                                    const S* __restrict__ rhs, S* __restrict__ x, S* __restrict__ z,
-                                                    double* __restrict__ partials, int grid0, RbControl* ctl, int sweep,
-                                                    int max_iter, int forward, unsigned int* counter) {
+__global__ void __launch_bounds__(kT) k_rbf_colour1(SellDev L, const RbTab<S> T, int grid0, int sweep, int max_iter, int forward) {
+    const int P_ = T.P, h_ = blockIdx.x % P_, cta = blockIdx.x / P_;
+    [[maybe_unused]] const int nct = gridDim.x / P_;
+    [[maybe_unused]] const S* __restrict__ diag_lu = T.diag_lu[h_];
+    [[maybe_unused]] const int* __restrict__ piv = T.piv[h_];
+    [[maybe_unused]] const S* __restrict__ inv0 = T.inv0[h_];
+    [[maybe_unused]] const double* __restrict__ shift = T.shift[h_];
+    [[maybe_unused]] const S* __restrict__ rhs = T.rhs[h_];
+    [[maybe_unused]] S* __restrict__ x = T.x[h_];
+    [[maybe_unused]] S* __restrict__ z = T.z[h_];
+    [[maybe_unused]] S* __restrict__ r = T.r[h_];
+    RbControl* ctl = T.ctl[h_];
+    [[maybe_unused]] unsigned int* counter = &ctl->counter;
+    [[maybe_unused]] double* __restrict__ partials = T.parts[h_];
     __shared__ double red[kT / 32];
     __shared__ bool last;
     if (ctl->done) return;
-    const int i = L.n0 + blockIdx.x * kT + threadIdx.x;
+    const int i = L.n0 + cta * kT + threadIdx.x;
     double loc = 0.0;
     if (i < L.n) {
         const RowRef rr = row_ref(L, i);
@@ -660,13 +756,13 @@ __global__ void __launch_bounds__(kT) k_rbf_colour1(SellDev L, const double* __r
     if (sweep < 1) return;
     const double bs = block_sum(loc, red);
     if (threadIdx.x == 0) {
-        partials[grid0 + blockIdx.x] = bs;
+        partials[grid0 + cta] = bs;
         __threadfence();
-        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+        last = atomicAdd(counter, 1u) == nct - 1;
     }
     __syncthreads();
     if (!last) return;
-    const double tot = ordered_sum(partials, grid0 + gridDim.x, red);
+    const double tot = ordered_sum(partials, grid0 + nct, red);
     if (threadIdx.x == 0) {
         const double nrm = sqrt(tot);
         ctl->iterations = sweep;
@@ -934,21 +1030,34 @@ void rb_factorize(const RbSystem& A, const double* shift_im, RbIlu<S>& f, Worksp
 }
 
 template <class S>
-void rb_smoothed_solve(const RbSystem& A, const double* shift_im, const RbIlu<S>& f, const S* rhs, double tol_rel,
-                       int max_iter, S* x, S* z, S* r, RbControl* ctl, Workspace& ws) {
+void rb_smoothed_solve_batch(const RbSystem& A, const RbMember<S>* mem, int P, double tol_rel, int max_iter,
+                             cudaStream_t stm) {
     if (!(tol_rel > 0.0 && tol_rel < 1.0)) throw ConfigError("smoothed_solve: tol_rel must be in (0,1)");
     if (max_iter < 1) throw ConfigError("smoothed_solve: max_iter must be >= 1");
+    if (P < 1 || P > kMaxBatch) throw ConfigError("rb_smoothed_solve_batch: 1 <= P <= kMaxBatch");
     const SellLayout& L = A.layout();
     const SellDev sd = sell_dev(L, A.vals());
     const std::size_t len = (std::size_t)L.n * L.b;
-    cudaStream_t stm = ws.stream;
-    unsigned int* counter = reinterpret_cast<unsigned int*>(&ctl->counter);
-    FNLH_CUDA(cudaMemsetAsync(x, 0, len * sizeof(S), stm));
-    FNLH_CUDA(cudaMemsetAsync(ctl, 0, sizeof(RbControl), stm));
-    double* parts = const_cast<double*>(A.partials.ptr);
+    RbTab<S> T{};
+    T.P = P;
+    for (int m = 0; m < P; ++m) {
+        T.diag_lu[m] = mem[m].f->diag_lu;
+        T.piv[m] = mem[m].f->diag_piv;
+        T.inv0[m] = mem[m].f->inv0;
+        T.shift[m] = mem[m].shift;
+        T.rhs[m] = mem[m].rhs;
+        T.x[m] = mem[m].x;
+        T.z[m] = mem[m].z;
+        T.r[m] = mem[m].r;
+        T.ctl[m] = mem[m].ctl;
+        T.parts[m] = mem[m].partials;
+        FNLH_CUDA(cudaMemsetAsync(mem[m].x, 0, len * sizeof(S), stm));
+        FNLH_CUDA(cudaMemsetAsync(mem[m].ctl, 0, sizeof(RbControl), stm));
+    }
     const int gi = std::min(nb((long long)len), 1184);
-    { ::fnlh::note_launch(); k_rb_init<S><<<gi, kT, 0, stm>>>(len, rhs, parts, gi, ctl, tol_rel, counter); }
+    { ::fnlh::note_launch(); k_rb_init<S><<<gi * P, kT, 0, stm>>>(len, T, tol_rel); }
     const int maxoff = std::max(1, A.pattern()->max_deg - 1);
+    const int g0 = A.grid0 * P, g1 = A.grid1 * P;
     RB_DISPATCH(L.b, {
         const std::size_t sm = (std::size_t)maxoff * B * kT * sizeof(S);
         static bool attr = false;
@@ -959,34 +1068,33 @@ void rb_smoothed_solve(const RbSystem& A, const double* shift_im, const RbIlu<S>
         }
         if (rb_sweep_mode() == 1) {
             for (int s = 1; s <= max_iter; ++s) {
-                { ::fnlh::note_launch(); k_rb_forward1<B, S><<<A.grid1, kT, 0, stm>>>(sd, f.diag_lu, f.diag_piv, f.inv0, rhs, r, z, ctl, s); }
-                { ::fnlh::note_launch(); k_rb_colour0<B, S><<<A.grid0, kT, sm, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, rhs, x, z, r, parts,
-                                                              ctl, s); }
-                { ::fnlh::note_launch(); k_rb_resid1<B, S><<<A.grid1, kT, 0, stm>>>(sd, shift_im, rhs, x, z, r, parts, A.grid0, ctl, s, max_iter,
-                                                            counter); }
+                { ::fnlh::note_launch(); k_rb_forward1<B, S><<<g1, kT, 0, stm>>>(sd, T, s); }
+                { ::fnlh::note_launch(); k_rb_colour0<B, S><<<g0, kT, sm, stm>>>(sd, T, s); }
+                { ::fnlh::note_launch(); k_rb_resid1<B, S><<<g1, kT, 0, stm>>>(sd, T, A.grid0, s, max_iter); }
             }
         } else if (rb_sweep_mode() == 0) {
-            { ::fnlh::note_launch(); k_rb_forward1<B, S><<<A.grid1, kT, 0, stm>>>(sd, f.diag_lu, f.diag_piv, f.inv0, rhs, r, z, ctl, 1); }
+            { ::fnlh::note_launch(); k_rb_forward1<B, S><<<g1, kT, 0, stm>>>(sd, T, 1); }
             for (int s = 1; s <= max_iter; ++s) {
-                { ::fnlh::note_launch(); k_rb_colour0<B, S><<<A.grid0, kT, sm, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, rhs, x, z, r, parts,
-                                                              ctl, s); }
-                { ::fnlh::note_launch(); k_rbx_colour1<B, S><<<A.grid1, kT, sm, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, f.inv0, rhs, x, z, r,
-                                                               parts, A.grid0, ctl, s, max_iter, s < max_iter ? 1 : 0,
-                                                               counter); }
+                { ::fnlh::note_launch(); k_rb_colour0<B, S><<<g0, kT, sm, stm>>>(sd, T, s); }
+                { ::fnlh::note_launch(); k_rbx_colour1<B, S><<<g1, kT, sm, stm>>>(sd, T, A.grid0, s, max_iter, s < max_iter ? 1 : 0); }
             }
         } else {
-            { ::fnlh::note_launch(); k_rbf_w0<B, S><<<A.grid0, kT, 0, stm>>>(sd, f.diag_lu, f.diag_piv, rhs, z, ctl); }
-            { ::fnlh::note_launch(); k_rbf_colour1<B, S><<<A.grid1, kT, 0, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, rhs, x, z, parts,
-                                                           A.grid0, ctl, 0, max_iter, 1, counter); }
+            { ::fnlh::note_launch(); k_rbf_w0<B, S><<<g0, kT, 0, stm>>>(sd, T); }
+            { ::fnlh::note_launch(); k_rbf_colour1<B, S><<<g1, kT, 0, stm>>>(sd, T, A.grid0, 0, max_iter, 1); }
             for (int s = 1; s <= max_iter; ++s) {
-                { ::fnlh::note_launch(); k_rbf_colour0<B, S><<<A.grid0, kT, 0, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, rhs, x, z, r, parts,
-                                                               ctl, s); }
-                { ::fnlh::note_launch(); k_rbf_colour1<B, S><<<A.grid1, kT, 0, stm>>>(sd, shift_im, f.diag_lu, f.diag_piv, rhs, x, z, parts,
-                                                               A.grid0, ctl, s, max_iter, s < max_iter ? 1 : 0, counter); }
+                { ::fnlh::note_launch(); k_rbf_colour0<B, S><<<g0, kT, 0, stm>>>(sd, T, s); }
+                { ::fnlh::note_launch(); k_rbf_colour1<B, S><<<g1, kT, 0, stm>>>(sd, T, A.grid0, s, max_iter, s < max_iter ? 1 : 0); }
             }
         }
     });
     FNLH_CUDA(cudaGetLastError());
+}
+
+template <class S>
+void rb_smoothed_solve(const RbSystem& A, const double* shift_im, const RbIlu<S>& f, const S* rhs, double tol_rel,
+                       int max_iter, S* x, S* z, S* r, RbControl* ctl, Workspace& ws) {
+    RbMember<S> m{&f, shift_im, rhs, x, z, r, ctl, const_cast<double*>(A.partials.ptr)};
+    rb_smoothed_solve_batch<S>(A, &m, 1, tol_rel, max_iter, ws.stream);
 }
 
 template struct RbIlu<double>;
@@ -999,5 +1107,7 @@ template void rb_smoothed_solve<double>(const RbSystem&, const double*, const Rb
                                         int, double*, double*, double*, RbControl*, Workspace&);
 template void rb_smoothed_solve<cplx>(const RbSystem&, const double*, const RbIlu<cplx>&, const cplx*, double, int,
                                       cplx*, cplx*, cplx*, RbControl*, Workspace&);
+template void rb_smoothed_solve_batch<double>(const RbSystem&, const RbMember<double>*, int, double, int, cudaStream_t);
+template void rb_smoothed_solve_batch<cplx>(const RbSystem&, const RbMember<cplx>*, int, double, int, cudaStream_t);
 
 }  // namespace fnlh

@@ -108,6 +108,7 @@ private:
     DeviceBuffer<long long> trans_;  // per CSR entry (i,k): SELL offset of the (k,i) block
 public:
     DeviceBuffer<double> partials;   // per-CTA norm partials (colour 0 then colour 1)
+    std::size_t partials_len() const { return partials.n; }
     int grid0 = 0, grid1 = 0;
     const long long* trans() const { return trans_.ptr; }
 };
@@ -118,6 +119,28 @@ void rb_factorize(const RbSystem& A, const double* shift_im, RbIlu<S>& f, Worksp
 // same, enqueued only: status[1] receives the first near-singular pivot row (0x7fffffff when clean)
 template <class S>
 void rb_factorize_async(const RbSystem& A, const double* shift_im, RbIlu<S>& f, int* status, cudaStream_t st);
+
+constexpr int kMaxBatch = 8;
+
+// one system of a batched solve: its factors, shift, vectors and control block
+template <class S>
+struct RbMember {
+    const RbIlu<S>* f;
+    const double* shift;  // shift_im (complex systems) or nullptr
+    const S* rhs;
+    S* x;
+    S* z;
+    S* r;
+    RbControl* ctl;
+    double* partials;  // >= RbSystem::partials_len() doubles
+};
+
+// enqueue P independent smoothed_solves on systems sharing A (one CTA stream per member,
+// interleaved so A is fetched from HBM once per batched sweep); each member stops on
+// its own rule; reports land in mem[m].ctl
+template <class S>
+void rb_smoothed_solve_batch(const RbSystem& A, const RbMember<S>* mem, int P, double tol_rel, int max_iter,
+                             cudaStream_t st);
 
 // enqueue a complete smoothed_solve (no host synchronization); the report lands in *ctl
 // (device); x is overwritten.

@@ -1,5 +1,6 @@
 // solver.cu -- host orchestration of the FNLH outer iteration on the device
 // (driver.cpp:157-379, rk.cpp:41-99), calling the sm_100a kernels of la.cu / disc.cu.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 
@@ -125,6 +126,23 @@ DeviceSolver::DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int
     for (auto& v : rk_) v.alloc(len);
     stage_err_.alloc(11);
     fac_status_.alloc(2);
+    if (sch_.workers < 1) throw ConfigError("workers must be >= 1");
+    const int P = std::min(std::min(sch_.workers, nh_), kMaxBatch);
+    if (sch_.implicit && rbA_ && P >= 2) {  // harmonics in flight: one workspace per lane
+        rb_h_.reset();
+        for (int m = 0; m < P; ++m) {
+            auto ln = std::make_unique<HarmonicLane>();
+            ln->f = std::make_unique<RbIlu<cplx>>(pat_.get(), rbA_->n0());
+            ln->shift.alloc(mesh.n);
+            for (auto& v : ln->v) v.alloc(len);
+            ln->ctl.alloc(5);
+            ln->err.alloc(10);
+            ln->fac.alloc(2);
+            ln->parts.alloc(rbA_->partials_len());
+            ln->norm.alloc(1);
+            lanes_.push_back(std::move(ln));
+        }
+    }
     FNLH_CUDA(cudaEventCreate(&ev0_));
     FNLH_CUDA(cudaEventCreate(&ev1_));
 }
@@ -136,10 +154,50 @@ DeviceSolver::~DeviceSolver() {
 
 std::size_t DeviceSolver::lhs_bytes() const {
     std::size_t s = 0;
-    if (sch_.implicit && rbA_) s = A5_.bytes() + rbA_->bytes() + rb_mean_->bytes() + rb_h_->bytes();
+    if (sch_.implicit && rbA_) {
+        s = A5_.bytes() + rbA_->bytes() + rb_mean_->bytes();
+        if (lanes_.empty())
+            s += rb_h_->bytes();
+        else
+            for (const auto& ln : lanes_) s += ln->f->bytes();
+    }
     else if (sch_.implicit) s = A5_.bytes() + ilu_mean_->bytes() + ilu_h_->bytes();
     else s = P_.bytes() + PLU_.bytes() + pclu_.bytes();
     return s;
+}
+
+void DeviceSolver::check_step(const unsigned long long* errs, const RbControl* ctls,
+                              const LinearSolveReport* host_rep, const bool* have_host, const std::string& field,
+                              RkStepResult& res) {
+    for (int k = 1; k <= 5; ++k) {
+        const unsigned long long ee = errs[k - 1], ea = errs[5 + k - 1];
+        if (ee != ~0ull) {
+            const int code = (int)(ee & 15ull);
+            if (code == 2) throw DivergenceError("residual evaluation failed: inadmissible boundary state", k, field);
+            if (code == 4) throw UnsupportedCaseError("supersonic boundary state");
+            throw std::runtime_error("device error during residual evaluation");
+        }
+        if (sch_.implicit) {
+            LinearSolveReport rep;
+            if (have_host && have_host[k - 1]) {
+                rep = host_rep[k - 1];
+            } else {
+                const RbControl& c = ctls[k - 1];
+                if (c.status == 6) throw DivergenceError("non-finite iterate in smoothed_solve", c.iterations, "linear");
+                rep.iterations = c.iterations;
+                rep.initial_residual = c.initial_residual;
+                rep.final_residual = c.final_residual;
+                rep.converged = c.converged;
+            }
+            sweeps += rep.iterations;
+            row_updates += (long long)rep.iterations * disc_->n();
+            res.linear_reports.push_back(rep);
+        }
+        if (ea != ~0ull) {
+            if ((int)(ea & 15ull) == 2) throw DivergenceError("update left the admissible set", k, field);
+            throw DivergenceError("non-finite stage state", k, field);
+        }
+    }
 }
 
 template <class S>
@@ -223,37 +281,88 @@ RkStepResult DeviceSolver::rk_step(S* state, Eval&& eval, Apply&& apply, Solve&&
         if (code == 4) throw UnsupportedCaseError("deterministic_flux: supersonic boundary state");
         throw std::runtime_error("deterministic_flux: device error " + std::to_string(code));
     }
-    for (int k = 1; k <= 5; ++k) {
-        const unsigned long long ee = errs[k - 1], ea = errs[5 + k - 1];
-        if (ee != ~0ull) {
-            const int code = (int)(ee & 15ull);
-            if (code == 2) throw DivergenceError("residual evaluation failed: inadmissible boundary state", k, field);
-            if (code == 4) throw UnsupportedCaseError("supersonic boundary state");
-            throw std::runtime_error("device error during residual evaluation");
-        }
-        if (sch_.implicit) {
-            LinearSolveReport rep;
-            if (have_host[k - 1]) {
-                rep = host_rep[k - 1];
-            } else {
-                const RbControl& c = ctls[k - 1];
-                if (c.status == 6) throw DivergenceError("non-finite iterate in smoothed_solve", c.iterations, "linear");
-                rep.iterations = c.iterations;
-                rep.initial_residual = c.initial_residual;
-                rep.final_residual = c.final_residual;
-                rep.converged = c.converged;
-            }
-            sweeps += rep.iterations;
-            row_updates += (long long)rep.iterations * disc_->n();
-            res.linear_reports.push_back(rep);
-        }
-        if (ea != ~0ull) {
-            if ((int)(ea & 15ull) == 2) throw DivergenceError("update left the admissible set", k, field);
-            throw DivergenceError("non-finite stage state", k, field);
-        }
-    }
+    check_step(errs, ctls, host_rep, have_host, field, res);
     FNLH_CUDA(cudaMemcpyAsync(state, stage, len * sizeof(S), cudaMemcpyDeviceToDevice, st));
     return res;
+}
+
+void DeviceSolver::harmonic_batch(int h0, int P, std::vector<double>& h_norm,
+                                  std::vector<std::vector<LinearSolveReport>>& h_reps,
+                                  std::vector<std::exception_ptr>& herr) {
+    cudaStream_t st = ws_->stream;
+    const int n = disc_->n(), b = disc_->b();
+    const std::size_t len = disc_->len();
+    const double gamma = disc_->view().gamma;
+    const double ga5 = (1.0 / sch_.eps_relax) * kAlpha[4];
+    for (int m = 0; m < P; ++m) {  // build_lhs_harmonic + factorize per lane (driver.cpp:213-216)
+        HarmonicLane& ln = *lanes_[m];
+        const int h = h0 + m;
+        const cplx* amp = amps_.ptr + (std::size_t)h * len;
+        harmonic_shift(disc_->view().vol, n, omega_[h], ga5, ln.shift.ptr, st);
+        rb_factorize_async<cplx>(*rbA_, ln.shift.ptr, *ln.f, ln.fac.ptr, st);
+        FNLH_CUDA(cudaMemcpyAsync(ln.v[0].ptr, amp, len * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+        FNLH_CUDA(cudaMemcpyAsync(ln.v[6].ptr, amp, len * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
+        FNLH_CUDA(cudaMemsetAsync(ln.v[2].ptr, 0, len * sizeof(cplx), st));
+        FNLH_CUDA(cudaMemsetAsync(ln.v[3].ptr, 0, len * sizeof(cplx), st));
+        FNLH_CUDA(cudaMemsetAsync(ln.err.ptr, 0xff, 10 * sizeof(unsigned long long), st));
+    }
+    RbMember<cplx> mem[kMaxBatch];
+    for (int k = 1; k <= 5; ++k) {  // rk_step (rk.cpp:41-99), the lanes interleaved stage by stage
+        const double beta = kBeta[k - 1];
+        const bool fresh = beta != 0.0;
+        for (int m = 0; m < P; ++m) {
+            HarmonicLane& ln = *lanes_[m];
+            const int h = h0 + m;
+            disc_->redirect_err(ln.err.ptr + (k - 1));
+            disc_->linearized_residual(mean_.ptr, ln.v[6].ptr, omega_[h], forcing_.ptr + (std::size_t)h * nforcing_,
+                                       nforcing_, 2, fresh, ln.v[1].ptr, ln.v[2].ptr, st);
+            disc_->redirect_err(nullptr);
+            if (fresh) stage_blend<cplx>(beta, ln.v[2].ptr, ln.v[3].ptr, len, st);
+            stage_rhs<cplx>(ln.v[1].ptr, ln.v[3].ptr, ln.v[4].ptr, len, st);
+            if (k == 1) norm2_sq<cplx>(ln.v[4].ptr, len, ln.norm.ptr, *ws_);
+            scale<cplx>(ln.v[4].ptr, kAlpha[k - 1], len, st);
+            mem[m] = RbMember<cplx>{ln.f.get(), ln.shift.ptr, ln.v[4].ptr, ln.v[5].ptr,
+                                    ln.v[7].ptr, ln.v[8].ptr, ln.ctl.ptr + (k - 1), ln.parts.ptr};
+        }
+        rb_smoothed_solve_batch<cplx>(*rbA_, mem, P, sch_.linear_tol, sch_.linear_max_iter, st);
+        for (int m = 0; m < P; ++m) {
+            HarmonicLane& ln = *lanes_[m];
+            disc_->redirect_err(ln.err.ptr + 5 + (k - 1));
+            apply_harmonic(b, n, gamma, mean_.ptr, ln.v[0].ptr, ln.v[5].ptr, ln.v[6].ptr, st);
+            check_finite<cplx>(ln.v[6].ptr, len, disc_->err(), st);
+            disc_->redirect_err(nullptr);
+        }
+    }
+    struct Rec {
+        unsigned long long errs[10];
+        RbControl ctls[5];
+        int fac[2];
+        double norm;
+    };
+    std::vector<Rec> rec(P);
+    for (int m = 0; m < P; ++m) {
+        HarmonicLane& ln = *lanes_[m];
+        FNLH_CUDA(cudaMemcpyAsync(rec[m].errs, ln.err.ptr, sizeof rec[m].errs, cudaMemcpyDeviceToHost, st));
+        FNLH_CUDA(cudaMemcpyAsync(rec[m].ctls, ln.ctl.ptr, sizeof rec[m].ctls, cudaMemcpyDeviceToHost, st));
+        FNLH_CUDA(cudaMemcpyAsync(rec[m].fac, ln.fac.ptr, sizeof rec[m].fac, cudaMemcpyDeviceToHost, st));
+        FNLH_CUDA(cudaMemcpyAsync(&rec[m].norm, ln.norm.ptr, sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+    FNLH_CUDA(cudaStreamSynchronize(st));
+    for (int m = 0; m < P; ++m) {  // each lane as its own worker: commit or capture (driver.cpp:248-262)
+        const int h = h0 + m;
+        try {
+            if (rec[m].fac[1] != 0x7fffffff) throw FactorizationError("near-singular ILU pivot block", rec[m].fac[1]);
+            RkStepResult res;
+            res.stage1_residual_norm = std::sqrt(rec[m].norm);
+            check_step(rec[m].errs, rec[m].ctls, nullptr, nullptr, "harmonic-" + std::to_string(index_[h]), res);
+            FNLH_CUDA(cudaMemcpyAsync(amps_.ptr + (std::size_t)h * len, lanes_[m]->v[6].ptr, len * sizeof(cplx),
+                                      cudaMemcpyDeviceToDevice, st));
+            h_norm[h] = res.stage1_residual_norm;
+            h_reps[h] = std::move(res.linear_reports);
+        } catch (...) {
+            herr[h] = std::current_exception();
+        }
+    }
 }
 
 ConvergenceEntry DeviceSolver::outer_iteration() {
@@ -292,54 +401,68 @@ ConvergenceEntry DeviceSolver::outer_iteration() {
     }
 
     std::vector<double> h_norm(nh_, 0.0);
-    std::vector<LinearSolveReport> hreps;
-    for (int h = 0; h < nh_; ++h) {
-        cplx* amp = amps_.ptr + (std::size_t)h * len;
-        const double omega = omega_[h];
-        const std::string name = "harmonic-" + std::to_string(index_[h]);
-        const cplx* forcing = forcing_.ptr + (std::size_t)h * nforcing_;
-        auto eval = [&](const cplx* state, bool need_vis, cplx* inv, cplx* vis) {
-            disc_->linearized_residual(mean_.ptr, state, omega, forcing, nforcing_, 2, need_vis, inv, vis, st);
-        };
-        auto apply = [&](const cplx* base, const cplx* x, cplx* out) {
-            apply_harmonic(b, n, gamma, mean_.ptr, base, x, out, st);
-        };
-        RkStepResult step;
-        if (implicit) {
-            harmonic_shift(disc_->view().vol, n, omega, ga5, shift_.ptr, st);
-            SystemView<cplx> Ah;
-            Ah.p = pat_.get();
-            Ah.real_vals = A5_.ptr;
-            Ah.shift_im = shift_.ptr;
-            if (rbA_) {
-                rb_factorize_async<cplx>(*rbA_, shift_.ptr, *rb_h_, fac_status_.ptr, st);
-                auto solve = [&](const cplx* rhs, cplx* x, int k, LinearSolveReport&) {
-                    rb_solve_async<cplx>(shift_.ptr, *rb_h_, rhs, x, ctl_.ptr + (k - 1));
-                    return false;
+    std::vector<std::vector<LinearSolveReport>> h_reps(nh_);
+    std::vector<std::exception_ptr> herr(nh_);
+    const bool parallel = sch_.workers > 1 && nh_ > 1;  // driver.cpp:246-265
+    if (!lanes_.empty()) {
+        const int P = static_cast<int>(lanes_.size());
+        for (int h0 = 0; h0 < nh_; h0 += P) harmonic_batch(h0, std::min(P, nh_ - h0), h_norm, h_reps, herr);
+    } else {
+        for (int h = 0; h < nh_; ++h) {
+            try {
+                cplx* amp = amps_.ptr + (std::size_t)h * len;
+                const double omega = omega_[h];
+                const std::string name = "harmonic-" + std::to_string(index_[h]);
+                const cplx* forcing = forcing_.ptr + (std::size_t)h * nforcing_;
+                auto eval = [&](const cplx* state, bool need_vis, cplx* inv, cplx* vis) {
+                    disc_->linearized_residual(mean_.ptr, state, omega, forcing, nforcing_, 2, need_vis, inv, vis, st);
                 };
-                step = rk_step<cplx>(amp, eval, apply, solve, nullptr, nullptr, name, fac_status_.ptr);
-            } else {
-                ilu_factorize<cplx>(Ah, *ilu_h_, *ws_);
-                auto solve = [&](const cplx* rhs, cplx* x, int, LinearSolveReport& rep) {
-                    rep = smoothed_solve<cplx>(Ah, rhs, *ilu_h_, sch_.linear_tol, sch_.linear_max_iter, x, *ws_);
-                    return true;
+                auto apply = [&](const cplx* base, const cplx* x, cplx* out) {
+                    apply_harmonic(b, n, gamma, mean_.ptr, base, x, out, st);
                 };
-                step = rk_step<cplx>(amp, eval, apply, solve, nullptr, nullptr, name);
+                RkStepResult step;
+                if (implicit) {
+                    harmonic_shift(disc_->view().vol, n, omega, ga5, shift_.ptr, st);
+                    SystemView<cplx> Ah;
+                    Ah.p = pat_.get();
+                    Ah.real_vals = A5_.ptr;
+                    Ah.shift_im = shift_.ptr;
+                    if (rbA_) {
+                        rb_factorize_async<cplx>(*rbA_, shift_.ptr, *rb_h_, fac_status_.ptr, st);
+                        auto solve = [&](const cplx* rhs, cplx* x, int k, LinearSolveReport&) {
+                            rb_solve_async<cplx>(shift_.ptr, *rb_h_, rhs, x, ctl_.ptr + (k - 1));
+                            return false;
+                        };
+                        step = rk_step<cplx>(amp, eval, apply, solve, nullptr, nullptr, name, fac_status_.ptr);
+                    } else {
+                        ilu_factorize<cplx>(Ah, *ilu_h_, *ws_);
+                        auto solve = [&](const cplx* rhs, cplx* x, int, LinearSolveReport& rep) {
+                            rep = smoothed_solve<cplx>(Ah, rhs, *ilu_h_, sch_.linear_tol, sch_.linear_max_iter, x, *ws_);
+                            return true;
+                        };
+                        step = rk_step<cplx>(amp, eval, apply, solve, nullptr, nullptr, name);
+                    }
+                } else {
+                    shifted_blocks(P_.ptr, disc_->view().vol, b, n, omega, pclu_.ptr, st);
+                    const int init[2] = {0, 0x7fffffff};
+                    FNLH_CUDA(cudaMemcpyAsync(ws_->status, init, sizeof init, cudaMemcpyHostToDevice, st));
+                    block_diag_factor<cplx>(b, n, pclu_.ptr, pcpiv_.ptr, ws_->status, st);
+                    FNLH_CUDA(cudaMemcpyAsync(ws_->h_status, ws_->status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+                    FNLH_CUDA(cudaStreamSynchronize(st));
+                    if (ws_->h_status[1] != 0x7fffffff) throw FactorizationError("singular pivot block", ws_->h_status[1]);
+                    auto none = [&](const cplx*, cplx*, int, LinearSolveReport&) { return true; };
+                    step = rk_step<cplx>(amp, eval, apply, none, pclu_.ptr, pcpiv_.ptr, name);
+                }
+                h_norm[h] = step.stage1_residual_norm;
+                h_reps[h] = std::move(step.linear_reports);
+            } catch (...) {
+                if (!parallel) throw;
+                herr[h] = std::current_exception();
             }
-        } else {
-            shifted_blocks(P_.ptr, disc_->view().vol, b, n, omega, pclu_.ptr, st);
-            const int init[2] = {0, 0x7fffffff};
-            FNLH_CUDA(cudaMemcpyAsync(ws_->status, init, sizeof init, cudaMemcpyHostToDevice, st));
-            block_diag_factor<cplx>(b, n, pclu_.ptr, pcpiv_.ptr, ws_->status, st);
-            FNLH_CUDA(cudaMemcpyAsync(ws_->h_status, ws_->status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-            FNLH_CUDA(cudaStreamSynchronize(st));
-            if (ws_->h_status[1] != 0x7fffffff) throw FactorizationError("singular pivot block", ws_->h_status[1]);
-            auto none = [&](const cplx*, cplx*, int, LinearSolveReport&) { return true; };
-            step = rk_step<cplx>(amp, eval, apply, none, pclu_.ptr, pcpiv_.ptr, name);
         }
-        h_norm[h] = step.stage1_residual_norm;
-        for (auto& r : step.linear_reports) hreps.push_back(r);
     }
+    for (int h = 0; h < nh_; ++h)
+        if (herr[h]) std::rethrow_exception(herr[h]);
 
     // deterministic flux from the fresh harmonic fields (driver.cpp:268-271)
     std::vector<const cplx*> amps;
@@ -377,7 +500,8 @@ ConvergenceEntry DeviceSolver::outer_iteration() {
         auto none = [&](const double*, double*, int, LinearSolveReport&) { return true; };
         mstep = rk_step<double>(mean_.ptr, mean_eval, mean_apply, none, PLU_.ptr, Ppiv_.ptr, "mean", nullptr, true);
     }
-    for (auto& r : hreps) reports_.push_back(r);
+    for (const auto& hr : h_reps)
+        for (const auto& r : hr) reports_.push_back(r);
     for (auto& r : mstep.linear_reports) reports_.push_back(r);
 
     FNLH_CUDA(cudaEventRecord(ev1_, st));
@@ -414,9 +538,10 @@ double DeviceSolver::time_harmonic_sweeps(int h, int nsweeps) {
     Ah.p = pat_.get();
     Ah.real_vals = A5_.ptr;
     Ah.shift_im = shift_.ptr;
+    RbIlu<cplx>* fh = rb_h_ ? rb_h_.get() : (lanes_.empty() ? nullptr : lanes_[0]->f.get());
     if (rbA_) {
         rbA_->load(A5_.ptr, st);
-        rb_factorize<cplx>(*rbA_, shift_.ptr, *rb_h_, *ws_);
+        rb_factorize<cplx>(*rbA_, shift_.ptr, *fh, *ws_);
     } else {
         ilu_factorize<cplx>(Ah, *ilu_h_, *ws_);
     }
@@ -428,10 +553,42 @@ double DeviceSolver::time_harmonic_sweeps(int h, int nsweeps) {
     FNLH_CUDA(cudaStreamSynchronize(st));
     FNLH_CUDA(cudaEventRecord(ev0_, st));
     if (rbA_)
-        rb_smoothed_solve<cplx>(*rbA_, shift_.ptr, *rb_h_, rhs, 1e-300, nsweeps, x, rb_z_.ptr, rb_r_.ptr, ctl_.ptr,
+        rb_smoothed_solve<cplx>(*rbA_, shift_.ptr, *fh, rhs, 1e-300, nsweeps, x, rb_z_.ptr, rb_r_.ptr, ctl_.ptr,
                                 *ws_);
     else
         smoothed_solve<cplx>(Ah, rhs, *ilu_h_, 1e-300, nsweeps, x, *ws_);
+    FNLH_CUDA(cudaEventRecord(ev1_, st));
+    FNLH_CUDA(cudaEventSynchronize(ev1_));
+    float ms = 0.0f;
+    FNLH_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    return ms;
+}
+
+double DeviceSolver::time_harmonic_sweeps_batch(int P, int nsweeps) {
+    if (lanes_.empty() || P < 1 || P > (int)lanes_.size() || P > nh_)
+        throw ConfigError("time_harmonic_sweeps_batch: needs workers >= P lanes on the 2-colour path");
+    cudaStream_t st = ws_->stream;
+    const int n = disc_->n(), b = disc_->b();
+    const std::size_t len = disc_->len();
+    const double ga5 = (1.0 / sch_.eps_relax) * kAlpha[4];
+    disc_->fd_jacobian(mean_.ptr, A5_.ptr, nullptr, st);
+    build_lhs_mean_device(A5_.ptr, A5_.ptr, b, n, pat_->diag_idx, pat_->nnzb, 1, ga5, 1.0 / (sch_.eps_relax * sigma_),
+                          st);
+    rbA_->load(A5_.ptr, st);
+    RbMember<cplx> mem[kMaxBatch];
+    for (int m = 0; m < P; ++m) {
+        HarmonicLane& ln = *lanes_[m];
+        harmonic_shift(disc_->view().vol, n, omega_[m], ga5, ln.shift.ptr, st);
+        rb_factorize<cplx>(*rbA_, ln.shift.ptr, *ln.f, *ws_);
+        disc_->linearized_residual(mean_.ptr, amps_.ptr + (std::size_t)m * len, omega_[m],
+                                   forcing_.ptr + (std::size_t)m * nforcing_, nforcing_, 2, false, ln.v[4].ptr, nullptr,
+                                   st);
+        mem[m] = RbMember<cplx>{ln.f.get(), ln.shift.ptr, ln.v[4].ptr, ln.v[5].ptr, ln.v[7].ptr, ln.v[8].ptr,
+                                ln.ctl.ptr, ln.parts.ptr};
+    }
+    FNLH_CUDA(cudaStreamSynchronize(st));
+    FNLH_CUDA(cudaEventRecord(ev0_, st));
+    rb_smoothed_solve_batch<cplx>(*rbA_, mem, P, 1e-300, nsweeps, st);
     FNLH_CUDA(cudaEventRecord(ev1_, st));
     FNLH_CUDA(cudaEventSynchronize(ev1_));
     float ms = 0.0f;

@@ -4,7 +4,9 @@
 // rk_step.  Host code is the reference's orchestration; every array stays in HBM.
 #pragma once
 
+#include <exception>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "disc.cuh"
@@ -21,6 +23,20 @@ struct SchemeConfig {  // driver.hpp:22-42
     int linear_max_iter = 10;
     double target_drop_orders = 8.0;
     int max_outer_iters = 2000;
+    int workers = 1;  // harmonics in flight (driver.cpp:246-265); >1: all run, first error rethrown
+};
+
+// one harmonic in flight on the device (a reference harmonic worker, driver.cpp:246-265):
+// its complex ILU workspace, shift and RK vectors; the batched sweep serves up to
+// kMaxBatch lanes from one read of the shared A5
+struct HarmonicLane {
+    std::unique_ptr<RbIlu<cplx>> f;
+    DeviceBuffer<double> shift;
+    DeviceBuffer<cplx> v[9];  // state0, inv, vis_fresh, vis_blend, rhs, x, stage, z, r
+    DeviceBuffer<RbControl> ctl;             // one per RK stage
+    DeviceBuffer<unsigned long long> err;    // [0,5) eval, [5,10) apply
+    DeviceBuffer<int> fac;                   // factorization status
+    DeviceBuffer<double> parts, norm;        // norm partials, stage-1 ||rhs||^2
 };
 
 struct ConvergenceEntry {  // driver.hpp:50-58
@@ -52,7 +68,10 @@ public:
     void set_state(const double* mean, const double* amps_pairs);
     void get_df(double* df) const;
     const std::vector<LinearSolveReport>& reports() const { return reports_; }
-    std::size_t lhs_bytes() const;  // LHS value storage (A5 + real ILU + ONE complex ILU workspace)
+    std::size_t lhs_bytes() const;  // LHS value storage (A5 + real ILU + one complex ILU workspace per lane)
+    int lanes() const { return lanes_.empty() ? 1 : (int)lanes_.size(); }
+    // time `sweeps` batched Richardson sweeps of harmonics [0, P) (P <= lanes())
+    double time_harmonic_sweeps_batch(int P, int sweeps);
     int n() const { return disc_->n(); }
     int b() const { return disc_->b(); }
     int nh() const { return nh_; }
@@ -78,6 +97,12 @@ private:
                          const std::string& field, const int* fac_status = nullptr, bool check_df = false);
     template <class S>
     void rb_solve_async(const double* shift, const RbIlu<S>& f, const S* rhs, S* x, RbControl* ctl);
+    // device records of one RK step -> the reference's exceptions (stage order) + reports
+    void check_step(const unsigned long long* errs, const RbControl* ctls, const LinearSolveReport* host_rep,
+                    const bool* have_host, const std::string& field, RkStepResult& res);
+    // rk_step of harmonics [h0, h0 + P) interleaved stage by stage, one batched sweep per stage
+    void harmonic_batch(int h0, int P, std::vector<double>& h_norm, std::vector<std::vector<LinearSolveReport>>& h_reps,
+                        std::vector<std::exception_ptr>& herr);
 
     SchemeConfig sch_;
     double sigma_ = 50.0;
@@ -100,6 +125,7 @@ private:
     DeviceBuffer<int> fac_status_;                // harmonic factorization status (deferred check)
     DeviceBuffer<cplx> rb_z_, rb_r_;
     DeviceBuffer<cplx> rk_[7];  // state0, inv, vis_fresh, vis_blend, rhs, x, stage (complex or reinterpreted real)
+    std::vector<std::unique_ptr<HarmonicLane>> lanes_;  // batched harmonic path (workers > 1), else empty
     std::vector<LinearSolveReport> reports_;
     int iter_ = 0;
     double cum_seconds_ = 0.0;

@@ -21,7 +21,7 @@ class MeshDesc(C.Structure):
 
 class Scheme(C.Structure):
     _fields_ = [("implicit", _i), ("sigma_cfl", _d), ("eps_relax", _d), ("linear_tol", _d), ("linear_max_iter", _i),
-                ("target_drop_orders", _d), ("max_outer_iters", _i)]
+                ("target_drop_orders", _d), ("max_outer_iters", _i), ("workers", _i)]
 
 
 class Entry(C.Structure):
@@ -39,7 +39,8 @@ def _desc(m, keep):
 def scheme_struct(s: dict) -> Scheme:
     return Scheme(int(s.get("implicit", 1)), float(s.get("sigma_cfl", -1.0)), float(s.get("eps_relax", 0.6)),
                   float(s.get("linear_tol", 1e-2)), int(s.get("linear_max_iter", 10)),
-                  float(s.get("target_drop_orders", 8.0)), int(s.get("max_outer_iters", 2000)))
+                  float(s.get("target_drop_orders", 8.0)), int(s.get("max_outer_iters", 2000)),
+                  int(s.get("workers", 1)))
 
 
 class Discretization:
@@ -164,6 +165,16 @@ class FnlhSolver:
     def lhs_bytes(self):
         lib().fnlh_solver_lhs_bytes.restype = _d
         return int(lib().fnlh_solver_lhs_bytes(self.h))
+
+    def lanes(self):
+        """Harmonics in flight (min(workers, N_h, 8) on the 2-colour path, else 1)."""
+        return lib().fnlh_solver_lanes(self.h)
+
+    def time_sweeps_batch(self, P, sweeps):
+        """Device ms of `sweeps` batched sweeps of harmonics [0, P)."""
+        ms = _d()
+        check(lib().fnlh_solver_time_sweeps_batch(self.h, _i(P), _i(sweeps), C.byref(ms)))
+        return ms.value
 
     def time_sweeps(self, h, sweeps):
         ms = _d()

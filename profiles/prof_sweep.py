@@ -1,6 +1,7 @@
 """Profiling driver: C2 harmonic sweeps (the roofline kernel), optionally after one
 pseudo-step (--step).  Default: the exact (bitwise) sweep; --onepass the one-pass
-sweep; --all every variant.  Run under ncu with -k regex:k_rb to capture the sweep."""
+sweep; --all every variant; --batch P also times the batched sweep of P harmonic lanes
+(workers = P).  Run under ncu with -k regex:k_rb to capture the sweep kernels."""
 import os
 import sys
 
@@ -9,15 +10,21 @@ from paper_2404_01407_b200 import la  # noqa: E402
 from paper_2404_01407_b200.cases import make_case  # noqa: E402
 from paper_2404_01407_b200.solver import FnlhSolver  # noqa: E402
 
-scale = float(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1][0].isdigit() else 1.0
-c = make_case("c2", scale=scale)
+args = sys.argv[1:]
+scale = float(args[0]) if args and args[0][0].isdigit() else 1.0
+P = int(args[args.index("--batch") + 1]) if "--batch" in args else 1
+c = make_case("c2", scale=scale, workers=P)
 s = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
-if "--step" in sys.argv:
+if "--step" in args:
     s.outer_iteration()
 names = {la.RB_EXACT: "exact", la.RB_EXACT_SPLIT: "exact-split", la.RB_ONEPASS: "one-pass"}
-modes = list(names) if "--all" in sys.argv else [la.RB_ONEPASS if "--onepass" in sys.argv else la.RB_EXACT]
+modes = list(names) if "--all" in args else [la.RB_ONEPASS if "--onepass" in args else la.RB_EXACT]
 for mode in modes:
     la.set_rb_sweep(mode)
     s.time_sweeps(0, 3)
     print(names[mode], "sweep ms", s.time_sweeps(0, 20) / 20)
+    if P > 1:
+        s.time_sweeps_batch(P, 3)
+        t = s.time_sweeps_batch(P, 20) / 20
+        print(f"  {names[mode]} batched x{P}: ms per batched sweep {t:.4f}, per harmonic sweep {t / P:.4f}")
 la.set_rb_sweep(la.RB_EXACT)

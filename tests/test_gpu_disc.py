@@ -110,6 +110,29 @@ def test_outer_iteration_history(orc_dev, name, scale, steps, exact):
         la.set_rb_sweep(la.RB_EXACT)
 
 
+@pytest.mark.parametrize("name,scale,nh", [("c1", 0.5, 3), ("c2", 0.08, 3), ("c2", 0.08, 5)])
+def test_workers_batched_harmonics(name, scale, nh):
+    """workers > 1: the harmonics run as lanes of one batched sweep (one read of A5 per
+    sweep for all lanes); the results are bitwise those of workers = 1, LHS memory grows
+    with the lanes (one complex workspace each, as the reference's workers), not with N_h."""
+    from paper_2404_01407_b200.solver import FnlhSolver
+    runs = {}
+    for workers in (1, 3):
+        c = make_case(name, scale=scale, nh=nh, workers=workers)
+        g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
+        assert g.lanes() == (min(workers, nh) if g.info()["red_black"] else 1)
+        hist = [g.outer_iteration() for _ in range(3)]
+        runs[workers] = (hist, g.state(), g.reports(), g.lhs_bytes())
+    (h1, (m1, a1), r1, b1), (h3, (m3, a3), r3, b3) = runs[1], runs[3]
+    assert np.array_equal(m1, m3) and np.array_equal(a1, a3)
+    assert [e["resid_mean"] for e in h1] == [e["resid_mean"] for e in h3]
+    assert [e["rz"] for e in h1] == [e["rz"] for e in h3]
+    assert r1 == r3
+    if name == "c2":
+        c = make_case(name, scale=scale, nh=nh + 4, workers=3)
+        assert FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0).lhs_bytes() == b3
+
+
 def test_explicit_mode(orc_dev):
     from paper_2404_01407_b200.solver import FnlhSolver
     c = make_case("c5", scale=0.06, implicit=False)
