@@ -104,14 +104,16 @@ def sweep_bytes(n, e, b):
     return 2 * e * b * b * 16 + n * (b * b * 16 + 4 * b) + (n + 2 * e) * b * b * 8 + n * 8 + 5 * n * b * 16
 
 
-def rb_sweep_bytes(n, n0, e, b):
-    """Algorithmic bytes of one complex harmonic sweep on the 2-colour fused path (rb.cuh),
-    every array counted once: real A5 (N+2E) b^2 8, shift N 8, rhs N b 16, x r/w 2 N b 16,
-    z (colour 1) r/w 2 N1 b 16, r (colour 0) r/w 2 N0 b 16, pivot LU + piv N (b^2 16 + 4 b),
-    inv(U_kk) of colour 0 N0 b^2 16."""
+def rb_sweep_bytes(n, n0, e, b, lanes=1):
+    """Algorithmic bytes of one batched complex harmonic sweep on the 2-colour path (rb.cuh)
+    over `lanes` harmonics, every array counted once: the shared real A5 (N+2E) b^2 8 once,
+    and per lane: shift N 8, rhs N b 16, x r/w 2 N b 16, z (colour 1) r/w 2 N1 b 16,
+    r (colour 0) r/w 2 N0 b 16, pivot LU + piv N (b^2 16 + 4 b), inv(U_kk) of colour 0
+    N0 b^2 16."""
     n1 = n - n0
-    return ((n + 2 * e) * b * b * 8 + n * 8 + n * b * 16 + 2 * n * b * 16 + 2 * n1 * b * 16 + 2 * n0 * b * 16
-            + n * (b * b * 16 + 4 * b) + n0 * b * b * 16)
+    per_lane = (n * 8 + n * b * 16 + 2 * n * b * 16 + 2 * n1 * b * 16 + 2 * n0 * b * 16
+                + n * (b * b * 16 + 4 * b) + n0 * b * b * 16)
+    return (n + 2 * e) * b * b * 8 + lanes * per_lane
 
 
 def cpu_baseline(config, scale, seconds_hint=20.0):
@@ -182,6 +184,8 @@ def main():
     ap.add_argument("--ref-scale", type=float, default=0.4)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweeps", type=int, default=10, help="sweeps in the roofline leg")
+    ap.add_argument("--workers", type=int, default=0,
+                    help="harmonic lanes (SchemeConfig::workers); 0 = one per harmonic (<= 8)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -202,6 +206,8 @@ def main():
 
     require_gpu()
     c = make_case(args.config, scale=args.scale)
+    if args.workers != 1:
+        c = make_case(args.config, scale=args.scale, workers=args.workers or min(len(c.omegas), 8))
     m = c.mesh
     pat = m.pattern()
     n, b = m.n, m.b
@@ -262,13 +268,19 @@ def main():
         te = torch.stack([tm[0], te[1]])
     e2e_value = float(te[1]) / float(te[0])
 
-    # roofline leg: the harmonic relaxation sweep
-    sweep_ms = s.time_sweeps(0, args.sweeps) / args.sweeps
+    # roofline leg: the harmonic relaxation sweep as the product path runs it (all lanes)
     info = s.info()
+    lanes = s.lanes()
+    if lanes > 1:
+        s.time_sweeps_batch(lanes, 2)
+        sweep_ms = s.time_sweeps_batch(lanes, args.sweeps) / args.sweeps
+    else:
+        sweep_ms = s.time_sweeps(0, args.sweeps) / args.sweeps
     if info["red_black"]:
-        bytes_sweep = rb_sweep_bytes(n, info["n0"], E, b)
-        kname = "2-colour fused ILU(0)-Richardson sweep (k_rb_colour1 + k_rb_colour0)"
-        formula = "rb_sweep_bytes"
+        bytes_sweep = rb_sweep_bytes(n, info["n0"], E, b, lanes)
+        kname = (f"2-colour ILU(0)-Richardson sweep, reference operation order (k_rb_colour0 + k_rbx_colour1), "
+                 f"{lanes} harmonic lane(s) per launch")
+        formula = f"rb_sweep_bytes(lanes={lanes})"
     else:
         bytes_sweep = sweep_bytes(n, E, b)
         kname = "level-scheduled ILU(0)-Richardson sweep (fwd/bwd levels + matvec)"
@@ -279,7 +291,7 @@ def main():
     try:  # dram read + write of the same kernels from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "r1_sweep_ncu_c2.json")) as f:
             prof = json.load(f)
-        if info["red_black"] and args.config == "c2" and args.scale == 1.0:
+        if info["red_black"] and args.config == "c2" and args.scale == 1.0 and prof.get("lanes", 1) == lanes:
             traffic = prof["traffic_bytes_per_sweep"]
     except Exception:
         pass
@@ -291,12 +303,13 @@ def main():
                        "harmonics": len(c.omegas), "pseudo_step": "outer_iteration (FD J, ILU, RK x (N_h+1), DF)",
                        "l2": f"inputs larger than L2 (LHS {s.lhs_bytes() / 1e9:.2f} GB resident)",
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-                       "sweeps_per_step": sweeps / args.steps, "lhs_bytes": s.lhs_bytes()},
+                       "sweeps_per_step": sweeps / args.steps, "lhs_bytes": s.lhs_bytes(),
+                       "workers": c.scheme.get("workers", 1), "harmonic_lanes": lanes},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": kname, "bytes_formula": formula,
                          "bytes_per_launch": bytes_sweep, "ms_per_launch": sweep_ms, "peak_kind": peak_kind,
-                         "sweep_rows_per_s": n / (sweep_ms * 1e-3)},
+                         "sweep_rows_per_s": lanes * n / (sweep_ms * 1e-3)},
             "clocks": clk, "gpu_launches": launches}
     if rank == 0 and world == 1 and not args.no_cpu:
         try:

@@ -159,6 +159,22 @@ int fnlh_solver_create(const fnlh_mesh_desc* m, const int* row_ptr, const int* c
 void fnlh_solver_destroy(fnlh_solver* s);
 /* FnlhSolver::outer_iteration (driver.cpp:157-333) */
 int fnlh_solver_outer_iteration(fnlh_solver* s, fnlh_entry* e, double* resid_h);
+/* outer_iteration in two halves, for harmonic sharding across GPUs (the
+   reference's harmonic workers, driver.cpp:246-265, one rank per GPU):
+   phase_harmonics: transform/FD Jacobian/A5/mean ILU, then the RK steps of the harmonics
+     with owned[h] != 0 (owned NULL: all); h_norm[h] (nh doubles) receives their stage-1
+     norms.  The caller then makes every harmonic field current on every rank (e.g. one
+     broadcast per harmonic from its owner, fnlh_solver_copy_amps to stage it) and
+   phase_mean: DF from all fields, the mean RK step and the monitor entry, given every
+     harmonic's stage-1 norm and its linear reports (nrep[h] of them, concatenated in
+     harmonic order).  fnlh_solver_outer_iteration == phase_harmonics(NULL) + phase_mean. */
+int fnlh_solver_phase_harmonics(fnlh_solver* s, const int* owned, double* h_norm);
+/* linear reports of harmonic h from the last phase_harmonics (count in *n, at most max copied) */
+int fnlh_solver_harmonic_reports(const fnlh_solver* s, int h, fnlh_linear_report* out, int max, int* n);
+int fnlh_solver_phase_mean(fnlh_solver* s, const double* h_norm, const int* nrep, const fnlh_linear_report* reps,
+                           fnlh_entry* e, double* resid_h);
+/* copy harmonic h's field (N*b complex, device) to (to_dev = 1) or from (0) caller device memory */
+int fnlh_solver_copy_amps(fnlh_solver* s, int h, void* dev, int to_dev);
 /* FnlhSolver::run_to_convergence (driver.cpp:335-379): *reason 0 target-drop, 1 cap, 2 divergence */
 int fnlh_solver_run(fnlh_solver* s, int* reason, int* n_entries, fnlh_entry* entries, int max_entries);
 int fnlh_solver_get_state(const fnlh_solver* s, double* mean, double* amps);

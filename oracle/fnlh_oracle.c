@@ -837,6 +837,8 @@ struct or_solver {
     or_ilu_z wsilu;
     report_list reports;
     int iter;
+    report_list* hrep; /* per harmonic, from the last phase_harmonics */
+    double* hnorm;
 };
 
 static void* xcalloc(size_t n, size_t s) { return calloc(n ? n : 1, s); }
@@ -863,6 +865,8 @@ or_solver* or_solver_create(const or_mesh* m, const or_pattern* p, const or_sche
     memcpy(S_->mean, mean0, sizeof(double) * len);
     S_->amps = (ocplx*)xcalloc((size_t)nh * len, sizeof(ocplx));
     S_->df = (double*)xcalloc(len, sizeof(double));
+    S_->hrep = (report_list*)xcalloc(nh, sizeof(report_list));
+    S_->hnorm = (double*)xcalloc(nh, sizeof(double));
     S_->M = (double*)xcalloc((size_t)n * bb, sizeof(double));
     S_->MLU = (double*)xcalloc((size_t)n * bb, sizeof(double));
     S_->Mpiv = (int*)xcalloc(len, sizeof(int));
@@ -912,6 +916,9 @@ void or_solver_destroy(or_solver* s) {
     free(s->wsilu.diag_piv);
     free(s->wsilu.diag_inv);
     free(s->reports.v);
+    for (int h = 0; h < s->nh; ++h) free(s->hrep[h].v);
+    free(s->hrep);
+    free(s->hnorm);
     free(s);
 }
 
@@ -1005,7 +1012,10 @@ static int apply_mean(rk_ctx* c, const double* base, const double* x, double* ou
 #undef APPLY
 
 /* FnlhSolver::outer_iteration (driver.cpp:157-333), workers = 1, single grid */
-int or_solver_outer_iteration(or_solver* s, or_entry* e, double* resid_h) {
+/* outer_iteration split where harmonic sharding exchanges the fields:
+   phase_harmonics relaxes the harmonics with owned[h] (NULL: all), phase_mean runs DF +
+   the mean step given every harmonic's stage-1 norm and reports (harmonic order). */
+int or_solver_phase_harmonics(or_solver* s, const int* owned, double* hnorm_out) {
     s->iter++;
     const or_mesh* m = &s->mesh;
     const int b = m->b, n = m->n, nh = s->nh;
@@ -1031,12 +1041,17 @@ int or_solver_outer_iteration(or_solver* s, or_entry* e, double* resid_h) {
     }
     const double ga5 = gamma_factor(implicit, s->sigma, s->sch.eps_relax) * kAlpha[4];
 
-    double hnorm[64];
-    report_list hreps = {0};
+    double* hnorm = s->hnorm;
+    for (int h = 0; h < nh; ++h) {
+        s->hrep[h].n = 0;
+        hnorm[h] = 0.0;
+    }
     ocplx* shift = (ocplx*)malloc(sizeof(ocplx) * n);
     ocplx* pclu = implicit ? NULL : (ocplx*)malloc(sizeof(ocplx) * n * bb);
     int* pcpiv = implicit ? NULL : (int*)malloc(sizeof(int) * len);
     for (int h = 0; h < nh && !st; ++h) {
+        if (owned && !owned[h]) continue;
+        report_list hreps = {0};
         rk_ctx c = {s, h};
         rk_result res;
         const double omega = s->omega[h];
@@ -1062,14 +1077,32 @@ int or_solver_outer_iteration(or_solver* s, or_entry* e, double* resid_h) {
                            s->sch.linear_max_iter, p, NULL, NULL, pclu, pcpiv, &res, &hreps);
         }
         if (!st) hnorm[h] = res.stage1_norm;
+        for (int k = 0; k < hreps.n; ++k) reports_push(&s->hrep[h], &hreps.v[k]);
+        free(hreps.v);
     }
     free(shift);
     free(pclu);
     free(pcpiv);
-    if (st) {
-        free(hreps.v);
-        return st;
-    }
+    if (hnorm_out)
+        for (int h = 0; h < nh; ++h) hnorm_out[h] = hnorm[h];
+    return st;
+}
+
+int or_solver_harmonic_reports(const or_solver* s, int h, or_linear_report* out, int max) {
+    for (int k = 0; k < s->hrep[h].n && k < max; ++k) out[k] = s->hrep[h].v[k];
+    return s->hrep[h].n;
+}
+
+int or_solver_phase_mean(or_solver* s, const double* hnorm, const int* nrep, const or_linear_report* reps,
+                         or_entry* e, double* resid_h) {
+    const or_mesh* m = &s->mesh;
+    const int b = m->b, n = m->n, nh = s->nh;
+    const or_pattern* p = &s->pat;
+    const int implicit = s->sch.implicit;
+    int st;
+    report_list hreps = {0};
+    for (int h = 0, q = 0; h < nh; ++h)
+        for (int k = 0; k < nrep[h]; ++k, ++q) reports_push(&hreps, &reps[q]);
     /* deterministic flux from the fresh harmonic fields */
     st = or_deterministic_flux(m, s->mean, nh, s->index, s->omega, s->amps, s->df);
     if (st) {
@@ -1108,6 +1141,20 @@ int or_solver_outer_iteration(or_solver* s, or_entry* e, double* resid_h) {
     e->has_rz = nh > 0;
     e->rz = nh > 0 ? sqrt(acc / nh) : 0.0;
     return OR_OK;
+}
+
+int or_solver_outer_iteration(or_solver* s, or_entry* e, double* resid_h) {
+    int st = or_solver_phase_harmonics(s, NULL, NULL);
+    if (st) return st;
+    int nrep[64];
+    report_list all = {0};
+    for (int h = 0; h < s->nh; ++h) {
+        nrep[h] = s->hrep[h].n;
+        for (int k = 0; k < s->hrep[h].n; ++k) reports_push(&all, &s->hrep[h].v[k]);
+    }
+    st = or_solver_phase_mean(s, s->hnorm, nrep, all.v, e, resid_h);
+    free(all.v);
+    return st;
 }
 
 void or_solver_get_state(const or_solver* s, double* mean, ocplx* amps) {

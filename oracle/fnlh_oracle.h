@@ -171,6 +171,10 @@ or_solver* or_solver_create(const or_mesh* m, const or_pattern* p, const or_sche
                             int nforcing, const double* mean0);
 void or_solver_destroy(or_solver* s);
 int or_solver_outer_iteration(or_solver* s, or_entry* e, double* resid_h);
+int or_solver_phase_harmonics(or_solver* s, const int* owned, double* hnorm_out);
+int or_solver_harmonic_reports(const or_solver* s, int h, or_linear_report* out, int max);
+int or_solver_phase_mean(or_solver* s, const double* hnorm, const int* nrep, const or_linear_report* reps,
+                         or_entry* e, double* resid_h);
 void or_solver_get_state(const or_solver* s, double* mean, ocplx* amps);
 void or_solver_set_state(or_solver* s, const double* mean, const ocplx* amps);
 int or_solver_num_reports(const or_solver* s);

@@ -248,6 +248,37 @@ class OracleSolver:
         return dict(iter=e.iter, resid_mean=e.resid_mean, rz=e.rz, has_rz=bool(e.has_rz),
                     resid_h=rh[: self.nh].copy(), stage1_norm_mean=e.stage1_norm_mean)
 
+    # the two halves of outer_iteration (harmonic sharding)
+    def phase_harmonics(self, owned=None):
+        hn = np.zeros(max(self.nh, 1))
+        own = None if owned is None else np.ascontiguousarray(owned, np.int32)
+        self.o._check(self.o.mode().or_solver_phase_harmonics(_p(self.h), ptr(own), ptr(hn)))
+        return hn[: self.nh].copy()
+
+    def harmonic_reports(self, h):
+        arr = (OrReport * 256)()
+        k = self.o.lib.or_solver_harmonic_reports(_p(self.h), _i(h), arr, _i(256))
+        return [(r.iterations, r.initial_residual, r.final_residual, bool(r.converged)) for r in arr[:k]]
+
+    def phase_mean(self, h_norm, h_reports):
+        reps = [r for hr in h_reports for r in hr]
+        arr = (OrReport * max(len(reps), 1))(*[OrReport(r[0], r[1], r[2], int(r[3])) for r in reps])
+        nrep = np.array([len(hr) for hr in h_reports] + [0], np.int32)
+        e = OrEntry()
+        rh = np.zeros(max(self.nh, 1))
+        self.o._check(self.o.mode().or_solver_phase_mean(_p(self.h), ptr(np.ascontiguousarray(h_norm, np.float64)),
+                                                          ptr(nrep), arr, C.byref(e), ptr(rh)))
+        return dict(iter=e.iter, resid_mean=e.resid_mean, rz=e.rz, has_rz=bool(e.has_rz),
+                    resid_h=rh[: self.nh].copy(), stage1_norm_mean=e.stage1_norm_mean)
+
+    def get_amps(self, h):
+        return self.state()[1][h]
+
+    def put_amps(self, h, a):
+        mean, amps = self.state()
+        amps[h] = a
+        self.set_state(mean, amps)
+
     def state(self):
         n = self.m.n * self.m.b
         mean = np.zeros(n)

@@ -168,6 +168,54 @@ int fnlh_solver_outer_iteration(fnlh_solver* s, fnlh_entry* e, double* resid_h) 
     });
 }
 
+int fnlh_solver_phase_harmonics(fnlh_solver* s, const int* owned, double* h_norm) {
+    return guarded([&] {
+        s->s->phase_harmonics(owned);
+        const auto& hn = s->s->last_h_norm();
+        if (h_norm)
+            for (std::size_t h = 0; h < hn.size(); ++h) h_norm[h] = hn[h];
+    });
+}
+
+int fnlh_solver_harmonic_reports(const fnlh_solver* s, int h, fnlh_linear_report* out, int max, int* n) {
+    return guarded([&] {
+        const auto& hr = s->s->last_h_reports();
+        if (h < 0 || h >= (int)hr.size()) throw ShapeError("harmonic_reports: index out of range");
+        *n = (int)hr[h].size();
+        for (int k = 0; k < *n && k < max; ++k) {
+            const LinearSolveReport& r = hr[h][k];
+            out[k] = fnlh_linear_report{r.iterations, r.initial_residual, r.final_residual, r.converged ? 1 : 0};
+        }
+    });
+}
+
+int fnlh_solver_phase_mean(fnlh_solver* s, const double* h_norm, const int* nrep, const fnlh_linear_report* reps,
+                           fnlh_entry* e, double* resid_h) {
+    return guarded([&] {
+        const int nh = s->s->nh();
+        std::vector<double> hn(h_norm, h_norm + nh);
+        std::vector<std::vector<LinearSolveReport>> hr(nh);
+        std::size_t q = 0;
+        for (int h = 0; h < nh; ++h)
+            for (int k = 0; k < nrep[h]; ++k, ++q) {
+                LinearSolveReport r;
+                r.iterations = reps[q].iterations;
+                r.initial_residual = reps[q].initial_residual;
+                r.final_residual = reps[q].final_residual;
+                r.converged = reps[q].converged != 0;
+                hr[h].push_back(r);
+            }
+        ConvergenceEntry c = s->s->phase_mean(hn, hr);
+        *e = fnlh_entry{c.iter, c.resid_mean, c.rz, c.has_rz, c.seconds};
+        if (resid_h)
+            for (std::size_t k = 0; k < c.resid_h.size(); ++k) resid_h[k] = c.resid_h[k];
+    });
+}
+
+int fnlh_solver_copy_amps(fnlh_solver* s, int h, void* dev, int to_dev) {
+    return guarded([&] { s->s->copy_amps(h, dev, to_dev != 0); });
+}
+
 int fnlh_solver_run(fnlh_solver* s, int* reason, int* n_entries, fnlh_entry* entries, int max_entries) {
     return guarded([&] {
         std::vector<ConvergenceEntry> hist;

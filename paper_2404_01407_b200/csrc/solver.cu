@@ -286,7 +286,7 @@ RkStepResult DeviceSolver::rk_step(S* state, Eval&& eval, Apply&& apply, Solve&&
     return res;
 }
 
-void DeviceSolver::harmonic_batch(int h0, int P, std::vector<double>& h_norm,
+void DeviceSolver::harmonic_batch(const int* hs, int P, std::vector<double>& h_norm,
                                   std::vector<std::vector<LinearSolveReport>>& h_reps,
                                   std::vector<std::exception_ptr>& herr) {
     cudaStream_t st = ws_->stream;
@@ -296,7 +296,7 @@ void DeviceSolver::harmonic_batch(int h0, int P, std::vector<double>& h_norm,
     const double ga5 = (1.0 / sch_.eps_relax) * kAlpha[4];
     for (int m = 0; m < P; ++m) {  // build_lhs_harmonic + factorize per lane (driver.cpp:213-216)
         HarmonicLane& ln = *lanes_[m];
-        const int h = h0 + m;
+        const int h = hs[m];
         const cplx* amp = amps_.ptr + (std::size_t)h * len;
         harmonic_shift(disc_->view().vol, n, omega_[h], ga5, ln.shift.ptr, st);
         rb_factorize_async<cplx>(*rbA_, ln.shift.ptr, *ln.f, ln.fac.ptr, st);
@@ -312,7 +312,7 @@ void DeviceSolver::harmonic_batch(int h0, int P, std::vector<double>& h_norm,
         const bool fresh = beta != 0.0;
         for (int m = 0; m < P; ++m) {
             HarmonicLane& ln = *lanes_[m];
-            const int h = h0 + m;
+            const int h = hs[m];
             disc_->redirect_err(ln.err.ptr + (k - 1));
             disc_->linearized_residual(mean_.ptr, ln.v[6].ptr, omega_[h], forcing_.ptr + (std::size_t)h * nforcing_,
                                        nforcing_, 2, fresh, ln.v[1].ptr, ln.v[2].ptr, st);
@@ -349,7 +349,7 @@ void DeviceSolver::harmonic_batch(int h0, int P, std::vector<double>& h_norm,
     }
     FNLH_CUDA(cudaStreamSynchronize(st));
     for (int m = 0; m < P; ++m) {  // each lane as its own worker: commit or capture (driver.cpp:248-262)
-        const int h = h0 + m;
+        const int h = hs[m];
         try {
             if (rec[m].fac[1] != 0x7fffffff) throw FactorizationError("near-singular ILU pivot block", rec[m].fac[1]);
             RkStepResult res;
@@ -366,6 +366,11 @@ void DeviceSolver::harmonic_batch(int h0, int P, std::vector<double>& h_norm,
 }
 
 ConvergenceEntry DeviceSolver::outer_iteration() {
+    phase_harmonics(nullptr);
+    return phase_mean(h_norm_, h_reps_);
+}
+
+void DeviceSolver::phase_harmonics(const int* owned) {
     cudaStream_t st = ws_->stream;
     FNLH_CUDA(cudaEventRecord(ev0_, st));
     ++iter_;
@@ -400,15 +405,21 @@ ConvergenceEntry DeviceSolver::outer_iteration() {
         if (ws_->h_status[1] != 0x7fffffff) throw FactorizationError("singular pivot block", ws_->h_status[1]);
     }
 
-    std::vector<double> h_norm(nh_, 0.0);
-    std::vector<std::vector<LinearSolveReport>> h_reps(nh_);
+    std::vector<double>& h_norm = h_norm_;
+    std::vector<std::vector<LinearSolveReport>>& h_reps = h_reps_;
+    h_norm.assign(nh_, 0.0);
+    h_reps.assign(nh_, {});
     std::vector<std::exception_ptr> herr(nh_);
     const bool parallel = sch_.workers > 1 && nh_ > 1;  // driver.cpp:246-265
+    std::vector<int> mine;  // harmonics this solver relaxes (all, or this rank's shard)
+    for (int h = 0; h < nh_; ++h)
+        if (!owned || owned[h]) mine.push_back(h);
     if (!lanes_.empty()) {
         const int P = static_cast<int>(lanes_.size());
-        for (int h0 = 0; h0 < nh_; h0 += P) harmonic_batch(h0, std::min(P, nh_ - h0), h_norm, h_reps, herr);
+        for (std::size_t q = 0; q < mine.size(); q += P)
+            harmonic_batch(mine.data() + q, std::min<int>(P, (int)(mine.size() - q)), h_norm, h_reps, herr);
     } else {
-        for (int h = 0; h < nh_; ++h) {
+        for (int h : mine) {
             try {
                 cplx* amp = amps_.ptr + (std::size_t)h * len;
                 const double omega = omega_[h];
@@ -463,7 +474,16 @@ ConvergenceEntry DeviceSolver::outer_iteration() {
     }
     for (int h = 0; h < nh_; ++h)
         if (herr[h]) std::rethrow_exception(herr[h]);
+}
 
+ConvergenceEntry DeviceSolver::phase_mean(const std::vector<double>& h_norm,
+                                          const std::vector<std::vector<LinearSolveReport>>& h_reps) {
+    cudaStream_t st = ws_->stream;
+    const int n = disc_->n(), b = disc_->b();
+    const std::size_t len = disc_->len();
+    const double gamma = disc_->view().gamma;
+    const bool implicit = sch_.implicit != 0;
+    if ((int)h_norm.size() != nh_ || (int)h_reps.size() != nh_) throw ShapeError("phase_mean: one entry per harmonic");
     // deterministic flux from the fresh harmonic fields (driver.cpp:268-271)
     std::vector<const cplx*> amps;
     for (int h = 0; h < nh_; ++h) amps.push_back(amps_.ptr + (std::size_t)h * len);
@@ -522,6 +542,15 @@ ConvergenceEntry DeviceSolver::outer_iteration() {
     e.rz = nh_ > 0 ? std::sqrt(acc / nh_) : 0.0;
     e.seconds = cum_seconds_;
     return e;
+}
+
+void DeviceSolver::copy_amps(int h, void* dev, bool to_dev) {
+    if (h < 0 || h >= nh_) throw ShapeError("copy_amps: harmonic index out of range");
+    const std::size_t bytes = disc_->len() * sizeof(cplx);
+    cplx* a = amps_.ptr + (std::size_t)h * disc_->len();
+    FNLH_CUDA(cudaMemcpyAsync(to_dev ? dev : (void*)a, to_dev ? (const void*)a : dev, bytes, cudaMemcpyDeviceToDevice,
+                              ws_->stream));
+    FNLH_CUDA(cudaStreamSynchronize(ws_->stream));
 }
 
 double DeviceSolver::time_harmonic_sweeps(int h, int nsweeps) {

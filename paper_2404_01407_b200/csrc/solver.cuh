@@ -61,7 +61,18 @@ public:
                  const double* forcing_pairs, int nforcing, const double* mean0);
     ~DeviceSolver();
 
-    ConvergenceEntry outer_iteration();
+    ConvergenceEntry outer_iteration();  // phase_harmonics(all) + phase_mean
+    // the two halves of outer_iteration, split where harmonic sharding exchanges the
+    // harmonic fields: J, A5, mean ILU and the owned harmonics' RK steps
+    // (owned: nh flags, nullptr = all) ...
+    void phase_harmonics(const int* owned);
+    const std::vector<double>& last_h_norm() const { return h_norm_; }
+    const std::vector<std::vector<LinearSolveReport>>& last_h_reports() const { return h_reps_; }
+    // ... then DF from every harmonic field, the mean RK step and the monitor, given every
+    // harmonic's stage-1 norm and reports (in harmonic order)
+    ConvergenceEntry phase_mean(const std::vector<double>& h_norm, const std::vector<std::vector<LinearSolveReport>>& h_reps);
+    // copy harmonic h's field to / from device memory owned by the caller (exchange buffers)
+    void copy_amps(int h, void* dev, bool to_dev);
     int run_to_convergence(std::vector<ConvergenceEntry>& history);  // 0 target, 1 cap, 2 divergence
 
     void get_state(double* mean, double* amps_pairs) const;
@@ -100,9 +111,11 @@ private:
     // device records of one RK step -> the reference's exceptions (stage order) + reports
     void check_step(const unsigned long long* errs, const RbControl* ctls, const LinearSolveReport* host_rep,
                     const bool* have_host, const std::string& field, RkStepResult& res);
-    // rk_step of harmonics [h0, h0 + P) interleaved stage by stage, one batched sweep per stage
-    void harmonic_batch(int h0, int P, std::vector<double>& h_norm, std::vector<std::vector<LinearSolveReport>>& h_reps,
-                        std::vector<std::exception_ptr>& herr);
+    // rk_step of harmonics hs[0..P) interleaved stage by stage, one batched sweep per stage
+    void harmonic_batch(const int* hs, int P, std::vector<double>& h_norm,
+                        std::vector<std::vector<LinearSolveReport>>& h_reps, std::vector<std::exception_ptr>& herr);
+    std::vector<double> h_norm_;
+    std::vector<std::vector<LinearSolveReport>> h_reps_;
 
     SchemeConfig sch_;
     double sigma_ = 50.0;

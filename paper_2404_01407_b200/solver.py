@@ -134,6 +134,33 @@ class FnlhSolver:
         return dict(iter=e.iter, resid_mean=e.resid_mean, rz=e.rz, has_rz=bool(e.has_rz), resid_h=rh[: self.nh].copy(),
                     seconds=e.seconds)
 
+    # the two halves of outer_iteration (harmonic sharding across GPUs, shard.py)
+    def phase_harmonics(self, owned=None):
+        hn = np.zeros(max(self.nh, 1))
+        own = None if owned is None else np.ascontiguousarray(owned, np.int32)
+        check(lib().fnlh_solver_phase_harmonics(self.h, ptr(own), ptr(hn)))
+        return hn[: self.nh].copy()
+
+    def harmonic_reports(self, h):
+        arr = (LinearReport * 256)()
+        n = _i()
+        check(lib().fnlh_solver_harmonic_reports(self.h, _i(h), arr, _i(256), C.byref(n)))
+        return [r.as_tuple() for r in arr[: n.value]]
+
+    def phase_mean(self, h_norm, h_reports):
+        reps = [r for hr in h_reports for r in hr]
+        arr = (LinearReport * max(len(reps), 1))(*[LinearReport(r[0], r[1], r[2], int(r[3])) for r in reps])
+        nrep = np.array([len(hr) for hr in h_reports] + [0], np.int32)
+        e = Entry()
+        rh = np.zeros(max(self.nh, 1))
+        check(lib().fnlh_solver_phase_mean(self.h, ptr(f64(h_norm)), ptr(nrep), arr, C.byref(e), ptr(rh)))
+        return dict(iter=e.iter, resid_mean=e.resid_mean, rz=e.rz, has_rz=bool(e.has_rz), resid_h=rh[: self.nh].copy(),
+                    seconds=e.seconds)
+
+    def copy_amps(self, h, dev_ptr, to_dev):
+        """Device-to-device copy of harmonic h's field to (to_dev) / from caller memory."""
+        check(lib().fnlh_solver_copy_amps(self.h, _i(h), C.c_void_p(dev_ptr), _i(1 if to_dev else 0)))
+
     def run_to_convergence(self, max_entries=100000):
         reason, n = _i(), _i()
         arr = (Entry * max_entries)()

@@ -21,8 +21,9 @@ names = {la.RB_EXACT: "exact", la.RB_EXACT_SPLIT: "exact-split", la.RB_ONEPASS: 
 modes = list(names) if "--all" in args else [la.RB_ONEPASS if "--onepass" in args else la.RB_EXACT]
 for mode in modes:
     la.set_rb_sweep(mode)
-    s.time_sweeps(0, 3)
-    print(names[mode], "sweep ms", s.time_sweeps(0, 20) / 20)
+    if "--only-batch" not in args:
+        s.time_sweeps(0, 3)
+        print(names[mode], "sweep ms", s.time_sweeps(0, 20) / 20)
     if P > 1:
         s.time_sweeps_batch(P, 3)
         t = s.time_sweeps_batch(P, 20) / 20

@@ -177,3 +177,36 @@ def test_nozzle_against_reference(ref):
     mg, ag = g.state()
     assert rel(extract(mg, noz.n), mr) < 1e-12
     assert rel(np.stack([extract(a, noz.n) for a in ag]), ar) < 1e-8
+
+
+@pytest.mark.parametrize("workers", [1, 2])
+def test_phase_split_and_field_exchange(workers):
+    """The device halves of outer_iteration (fnlh_solver_phase_harmonics / _phase_mean) with
+    the fields exchanged through fnlh_solver_copy_amps, as shard.py does across ranks:
+    two solvers owning harmonics {0, 2} and {1} end bitwise equal to one solver."""
+    import torch
+    from paper_2404_01407_b200.solver import FnlhSolver
+    c = make_case("c2", scale=0.08, nh=3, workers=workers)
+    mk = lambda: FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)  # noqa: E731
+    ref, a, b = mk(), mk(), mk()
+    L = c.mesh.n * c.mesh.b
+    buf = torch.empty(2 * L, dtype=torch.float64, device="cuda")
+    own = {id(a): [1, 0, 1], id(b): [0, 1, 0]}
+    for _ in range(3):
+        er = ref.outer_iteration()
+        hn = {id(s): s.phase_harmonics(own[id(s)]) for s in (a, b)}
+        norms, reps = [], []
+        for h in range(3):
+            src, dst = (a, b) if own[id(a)][h] else (b, a)
+            src.copy_amps(h, buf.data_ptr(), True)
+            dst.copy_amps(h, buf.data_ptr(), False)
+            norms.append(hn[id(src)][h])
+            reps.append(src.harmonic_reports(h))
+        for s in (a, b):
+            e = s.phase_mean(norms, reps)
+            assert e["resid_mean"] == er["resid_mean"] and e["rz"] == er["rz"]
+    mr, ar = ref.state()
+    for s in (a, b):
+        m, am = s.state()
+        assert np.array_equal(m, mr) and np.array_equal(am, ar)
+        assert s.reports() == ref.reports()
