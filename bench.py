@@ -184,6 +184,9 @@ def main():
     ap.add_argument("--ref-scale", type=float, default=0.4)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweeps", type=int, default=10, help="sweeps in the roofline leg")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "shard"],
+                    help="N>1: independent C2 replicas per rank (weak scaling) or one C2 instance with its "
+                         "harmonics sharded over the ranks, fields exchanged by NCCL broadcast (strong scaling)")
     ap.add_argument("--workers", type=int, default=0,
                     help="harmonic lanes (SchemeConfig::workers); 0 = one per harmonic (<= 8)")
     args = ap.parse_args()
@@ -213,6 +216,12 @@ def main():
     n, b = m.n, m.b
     E = (len(pat["col_idx"]) - n) // 2
     s = FnlhSolver(m, c.scheme, c.omegas, c.forcing, c.mean0, pattern=pat)
+    shard = args.mode == "shard" and world > 1
+    if shard:
+        from paper_2404_01407_b200.shard import HarmonicShards
+        stepper = HarmonicShards(s, len(c.omegas), n * b, device=f"cuda:{local}")
+    else:
+        stepper = s
 
     def barrier():
         torch.cuda.synchronize()
@@ -220,22 +229,25 @@ def main():
             dist.barrier()
 
     for _ in range(args.warmup):
-        s.outer_iteration()
+        stepper.outer_iteration()
     barrier()
     cnt0 = s.counters()
+    nrep0 = len(s.reports()) if shard else 0
     launches0 = lib().fnlh_launch_count()
     clocks = ClockSampler(local)
     clocks.start()
     barrier()
     dev_ms = 0.0
     for _ in range(args.steps):
-        e = s.outer_iteration()
+        e = stepper.outer_iteration()
         dev_ms += s.counters()["last_ms"]
     barrier()
     clk = clocks.stop()
     launches = int(lib().fnlh_launch_count() - launches0)
     cnt1 = s.counters()
     rows = cnt1["row_updates"] - cnt0["row_updates"]
+    if shard:  # the job's work once: every system's sweeps (identical report list on all ranks) on rank 0
+        rows = sum(r[0] for r in s.reports()[nrep0:]) * n if rank == 0 else 0
     sweeps = cnt1["sweeps"] - cnt0["sweeps"]
     t = torch.tensor([dev_ms, float(rows)], dtype=torch.float64, device="cuda")
     if dist:
@@ -251,15 +263,18 @@ def main():
     h2d = mean_h.nbytes + amps_h.nbytes
     d2h = h2d
     cnt2 = s.counters()
+    nrep2 = len(s.reports()) if shard else 0
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         s.set_state(mean_h, amps_h)
-        s.outer_iteration()
+        stepper.outer_iteration()
         mean_h, amps_h = s.state()
     barrier()
     e2e_s = time.perf_counter() - t0
     rows_e2e = s.counters()["row_updates"] - cnt2["row_updates"]
+    if shard:
+        rows_e2e = sum(r[0] for r in s.reports()[nrep2:]) * n if rank == 0 else 0
     te = torch.tensor([e2e_s, float(rows_e2e)], dtype=torch.float64, device="cuda")
     if dist:
         tm = te.clone()
@@ -298,11 +313,13 @@ def main():
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, cases.py)",
+            "scaling": "strong" if shard else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, cases.py)",
             "config": {"workload": f"{args.config}: {c.description}", "nodes": n, "edges": E, "b": b,
                        "harmonics": len(c.omegas), "pseudo_step": "outer_iteration (FD J, ILU, RK x (N_h+1), DF)",
                        "l2": f"inputs larger than L2 (LHS {s.lhs_bytes() / 1e9:.2f} GB resident)",
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "parallelism": (f"harmonics sharded over {world} ranks (NCCL broadcast of fields)" if shard
+                                       else f"replicas x{world}" if world > 1 else "1 GPU"),
                        "sweeps_per_step": sweeps / args.steps, "lhs_bytes": s.lhs_bytes(),
                        "workers": c.scheme.get("workers", 1), "harmonic_lanes": lanes},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},

@@ -37,12 +37,12 @@ __global__ void k_jst_prepass(MeshDev m, const double* __restrict__ W, double* _
     for (int k = 0; k < B; ++k) L[k] = 0.0;
     prim_to_cons<B>(wi, m.gamma, qi);
     for (int e = m.nf_ptr[i]; e < m.nf_ptr[i + 1]; ++e) {
-        const int f = m.nf_idx[e];
-        if (m.fbc[f] >= 0) {
+        const int code = m.nf_code[e];
+        if (code == kBoundaryFace) {
             den += pi + pi;
             continue;
         }
-        const int j = m.fa[f] == i ? m.fb[f] : m.fa[f];
+        const int j = code >= 0 ? code : -code - 1;
         const double* wj = W + (size_t)j * B;
         const double pj = wj[4];
         num += pj - pi;
@@ -109,11 +109,12 @@ __global__ void k_node_gather(MeshDev m, const double* __restrict__ W, const dou
     }
     for (int e = m.nf_ptr[i]; e < m.nf_ptr[i + 1]; ++e) {
         const int f = m.nf_idx[e];
+        const int code = m.nf_code[e];
         const double* fl = flux + (size_t)f * B;
-        if (m.fbc[f] >= 0 || m.fa[f] == i) {
+        if (code >= 0 || code == kBoundaryFace) {
 #pragma unroll
             for (int k = 0; k < B; ++k) acc[k] += fl[k];
-            if (B == 6 && need_vis && m.fbc[f] < 0) {
+            if (B == 6 && need_vis && code != kBoundaryFace) {
                 const double* vf = vflux + (size_t)f * B;
 #pragma unroll
                 for (int k = 0; k < B; ++k) vacc[k] += vf[k];
@@ -609,6 +610,15 @@ DeviceDisc::DeviceDisc(const MeshArrays& m, const DevicePattern* pattern) : pat_
     nf_ptr_.upload(m.nf_ptr, n + 1);
     nf_idx_.upload(m.nf_idx, m.nf_ptr[n]);
     bflag_.upload(m.bflag, n);
+    {
+        std::vector<int> code(m.nf_ptr[n]);
+        for (int i = 0; i < n; ++i)
+            for (int e = m.nf_ptr[i]; e < m.nf_ptr[i + 1]; ++e) {
+                const int f = m.nf_idx[e];
+                code[e] = m.fbc[f] >= 0 ? kBoundaryFace : m.fa[f] == i ? m.fb[f] : -(m.fa[f] + 1);
+            }
+        nf_code_.upload(code.data(), code.size());
+    }
     // per-face BSR entries of (a,b) and (b,a) for the FD scatter (find, sparse.cpp:42-48)
     std::vector<int> eab(nfc, -1), eba(nfc, -1);
     auto find = [&](int i, int j) {
@@ -627,7 +637,7 @@ DeviceDisc::DeviceDisc(const MeshArrays& m, const DevicePattern* pattern) : pat_
     e_ba_.upload(eba.data(), nfc);
     view_ = MeshDev{n, nfc, m.b, fa_.ptr, fb_.ptr, fbc_.ptr, ford_.ptr, fn_.ptr, farea_.ptr, fnh_.ptr, fvis_.ptr,
                     vol_.ptr, closure_.ptr, mu_.ptr, nf_ptr_.ptr, nf_idx_.ptr, bflag_.ptr, m.gamma, m.gas_constant,
-                    m.p0, m.T0, m.p_out, m.nt_in, m.forcing_scale};
+                    m.p0, m.T0, m.p_out, m.nt_in, m.forcing_scale, nf_code_.ptr};
     nu_.alloc(n);
     lap_.alloc((std::size_t)n * m.b);
     flux_.alloc((std::size_t)nfc * m.b);

@@ -61,7 +61,7 @@ public:
 private:
     MeshDev view_{};
     const DevicePattern* pat_;
-    DeviceBuffer<int> fa_, fb_, fbc_, ford_, nf_ptr_, nf_idx_, bflag_, e_ab_, e_ba_;
+    DeviceBuffer<int> fa_, fb_, fbc_, ford_, nf_ptr_, nf_idx_, nf_code_, bflag_, e_ab_, e_ba_;
     DeviceBuffer<double> fn_, farea_, fnh_, fvis_, vol_, closure_, mu_;
     DeviceBuffer<double> nu_, lap_, flux_, vflux_, qscale_, scal_;
     DeviceBuffer<unsigned long long> err_;

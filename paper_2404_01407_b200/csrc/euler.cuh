@@ -27,7 +27,13 @@ struct MeshDev {
     const int* __restrict__ nf_idx;
     const int* __restrict__ bflag;
     double gamma, gas_constant, p0, T0, p_out, nt_in, forcing_scale;
+    // per node-face incidence e (parallel to nf_idx): kBoundaryFace for a boundary face, else
+    // the other endpoint j as j (this node is fa: the face flux adds) or -(j + 1) (this node
+    // is fb: it subtracts) -- the gathers need no random reads of fa / fb / fbc
+    const int* __restrict__ nf_code;
 };
+
+constexpr int kBoundaryFace = -2147483647 - 1;
 
 constexpr double kKappa2 = 0.5;        // disc_euler.cpp:15
 constexpr double kKappa4 = 1.0 / 32.0; // disc_euler.cpp:16

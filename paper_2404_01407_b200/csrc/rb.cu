@@ -456,8 +456,6 @@ __global__ void __launch_bounds__(kT) k_rbx_colour1(SellDev L, const RbTab<S> T,
     [[maybe_unused]] double* __restrict__ partials = T.parts[h_];
     __shared__ double red[kT / 32];
     __shared__ bool last;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    S* park = reinterpret_cast<S*>(smem_raw);  // [slot][row][tid]
     if (ctl->done) return;
     const int tid = threadIdx.x;
     const int i = L.n0 + cta * kT + tid;
@@ -474,22 +472,30 @@ __global__ void __launch_bounds__(kT) k_rbx_colour1(SellDev L, const RbTab<S> T,
             y[k] = zero<S>();
         }
         st<B>(x + (size_t)i * B, xi);
+        // pass 1: the residual row of sweep s, ascending (lower blocks, then the diagonal)
         for (int e = 0; e < dg; ++e) {
-            const int kk = acol(L, rr, e);
-            S xk[B], rk[B];
-            ld<B>(x + (size_t)kk * B, xk);
-            double A[2 * pairs<B>()];
-            ablock<B>(L, rr, e, A);
+            S xk[B];
+            ld<B>(x + (size_t)acol(L, rr, e) * B, xk);
+            blk_matvec_add<B, S>(L, rr, e, xk, false, 0.0, y);
+        }
+        blk_matvec_add<B, S>(L, rr, dg, xi, shift != nullptr, shift ? shift[i] : 0.0, y);
+        S ri[B];
+        ld<B>(rhs + (size_t)i * B, ri);
 #pragma unroll
-            for (int rw = 0; rw < B; ++rw) {
-                S acc = zero<S>();
-#pragma unroll
-                for (int c = 0; c < B; ++c) acc += rmul(A[rw * B + c], xk[c]);
-                y[rw] += acc;
-            }
-            if (forward) {
+        for (int k = 0; k < B; ++k) {
+            ri[k] -= y[k];
+            loc += sq(ri[k]);
+        }
+        // pass 2: forward substitution of sweep s+1 from r_i, the row's blocks again (now
+        // L2-resident), L_ik = A_ik inv(U_kk) rebuilt in the reference's order
+        if (forward) {
+            for (int e = 0; e < dg; ++e) {
+                const int kk = acol(L, rr, e);
+                S rk[B];
                 ld<B>(r + (size_t)kk * B, rk);
                 const S* __restrict__ U = inv0 + (size_t)kk * B * B;
+                double A[2 * pairs<B>()];
+                ablock<B>(L, rr, e, A);
                 S acc[B];
 #pragma unroll
                 for (int rw = 0; rw < B; ++rw) acc[rw] = zero<S>();
@@ -507,21 +513,8 @@ __global__ void __launch_bounds__(kT) k_rbx_colour1(SellDev L, const RbTab<S> T,
                     }
                 }
 #pragma unroll
-                for (int rw = 0; rw < B; ++rw) park[(e * B + rw) * kT + tid] = acc[rw];
+                for (int rw = 0; rw < B; ++rw) ri[rw] -= acc[rw];
             }
-        }
-        blk_matvec_add<B, S>(L, rr, dg, xi, shift != nullptr, shift ? shift[i] : 0.0, y);
-        S ri[B];
-        ld<B>(rhs + (size_t)i * B, ri);
-#pragma unroll
-        for (int k = 0; k < B; ++k) {
-            ri[k] -= y[k];
-            loc += sq(ri[k]);
-        }
-        if (forward) {
-            for (int e = 0; e < dg; ++e)
-#pragma unroll
-                for (int rw = 0; rw < B; ++rw) ri[rw] -= park[(e * B + rw) * kT + tid];
             S lu[B * B];
             int pv[B];
             ld_lu<B>(diag_lu, piv, lu_ref<B>(L, i), lu, pv);
@@ -1076,7 +1069,7 @@ void rb_smoothed_solve_batch(const RbSystem& A, const RbMember<S>* mem, int P, d
             { ::fnlh::note_launch(); k_rb_forward1<B, S><<<g1, kT, 0, stm>>>(sd, T, 1); }
             for (int s = 1; s <= max_iter; ++s) {
                 { ::fnlh::note_launch(); k_rb_colour0<B, S><<<g0, kT, sm, stm>>>(sd, T, s); }
-                { ::fnlh::note_launch(); k_rbx_colour1<B, S><<<g1, kT, sm, stm>>>(sd, T, A.grid0, s, max_iter, s < max_iter ? 1 : 0); }
+                { ::fnlh::note_launch(); k_rbx_colour1<B, S><<<g1, kT, 0, stm>>>(sd, T, A.grid0, s, max_iter, s < max_iter ? 1 : 0); }
             }
         } else {
             { ::fnlh::note_launch(); k_rbf_w0<B, S><<<g0, kT, 0, stm>>>(sd, T); }

@@ -15,32 +15,28 @@ constexpr double kBeta[5] = {1.0, 0.0, 14.0 / 25.0, 0.0, 11.0 / 25.0};          
 constexpr int kT = 128;
 inline int nb(long long n) { return static_cast<int>((n + kT - 1) / kT); }
 
-// build_lhs_mean (rk.cpp:5-30), in place: A = J/ga; diag += J_ii*inv_es/ga
+// build_lhs_mean (rk.cpp:5-30), in place: A = J/ga; diag += J_ii*inv_es/ga.  One warp
+// per block row: the row's blocks are contiguous, so the warp streams them coalesced and
+// knows the diagonal from diag_idx without a search.
 __global__ void k_build_lhs(const double* __restrict__ J, double* __restrict__ A, int bb, int n,
-                            const int* __restrict__ diag_idx, std::size_t total, int implicit, double ga,
-                            double inv_es) {
-    const std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x;
-    if (t >= total) return;
-    const std::size_t e = t / bb;
-    (void)n;
-    const double j = J[t];
-    // is e a diagonal entry?  diag_idx is ascending; binary search on e
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if ((std::size_t)diag_idx[mid] < e)
-            lo = mid + 1;
-        else
-            hi = mid;
+                            const int* __restrict__ row_ptr, const int* __restrict__ diag_idx, int implicit,
+                            double ga, double inv_es) {
+    const int i = (int)((blockIdx.x * (std::size_t)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const std::size_t t0 = (std::size_t)row_ptr[i] * bb, t1 = (std::size_t)row_ptr[i + 1] * bb;
+    const std::size_t d0 = (std::size_t)diag_idx[i] * bb;
+    for (std::size_t t = t0 + lane; t < t1; t += 32) {
+        const bool diag = t >= d0 && t < d0 + bb;
+        const double j = J[t];
+        if (!implicit) {
+            A[t] = diag ? j / ga : 0.0;
+            continue;
+        }
+        double a = j / ga;
+        if (diag) a += j * inv_es / ga;
+        A[t] = a;
     }
-    const bool diag = lo < n && (std::size_t)diag_idx[lo] == e;
-    if (!implicit) {
-        A[t] = diag ? j / ga : 0.0;
-        return;
-    }
-    double a = j / ga;
-    if (diag) a += j * inv_es / ga;
-    A[t] = a;
 }
 
 __global__ void k_shift(const double* __restrict__ vol, int n, double omega, double ga, double* __restrict__ s) {
@@ -63,10 +59,9 @@ __global__ void k_shifted_blocks(const double* __restrict__ P, const double* __r
 
 }  // namespace
 
-void build_lhs_mean_device(const double* J, double* A, int b, int n, const int* diag_idx, std::size_t nnzb,
+void build_lhs_mean_device(const double* J, double* A, int b, int n, const int* row_ptr, const int* diag_idx,
                            int implicit, double ga, double inv_es, cudaStream_t st) {
-    const std::size_t total = nnzb * b * b;
-    { ::fnlh::note_launch(); k_build_lhs<<<nb((long long)total), kT, 0, st>>>(J, A, b * b, n, diag_idx, total, implicit, ga, inv_es); }
+    { ::fnlh::note_launch(); k_build_lhs<<<(int)(((std::size_t)n * 32 + kT - 1) / kT), kT, 0, st>>>(J, A, b * b, n, row_ptr, diag_idx, implicit, ga, inv_es); }
     FNLH_CUDA(cudaGetLastError());
 }
 
@@ -383,7 +378,7 @@ void DeviceSolver::phase_harmonics(const int* owned) {
     const double ga5 = (implicit ? 1.0 / sch_.eps_relax : sigma_) * kAlpha[4];
     if (implicit) {
         disc_->fd_jacobian(mean_.ptr, A5_.ptr, nullptr, st);  // J, then A5 in place
-        build_lhs_mean_device(A5_.ptr, A5_.ptr, b, n, pat_->diag_idx, pat_->nnzb, 1, ga5,
+        build_lhs_mean_device(A5_.ptr, A5_.ptr, b, n, pat_->row_ptr, pat_->diag_idx, 1, ga5,
                               1.0 / (sch_.eps_relax * sigma_), st);
         if (rbA_) {
             rbA_->load(A5_.ptr, st);
@@ -560,7 +555,7 @@ double DeviceSolver::time_harmonic_sweeps(int h, int nsweeps) {
     const std::size_t len = disc_->len();
     const double ga5 = (1.0 / sch_.eps_relax) * kAlpha[4];
     disc_->fd_jacobian(mean_.ptr, A5_.ptr, nullptr, st);
-    build_lhs_mean_device(A5_.ptr, A5_.ptr, b, n, pat_->diag_idx, pat_->nnzb, 1, ga5, 1.0 / (sch_.eps_relax * sigma_),
+    build_lhs_mean_device(A5_.ptr, A5_.ptr, b, n, pat_->row_ptr, pat_->diag_idx, 1, ga5, 1.0 / (sch_.eps_relax * sigma_),
                           st);
     harmonic_shift(disc_->view().vol, n, omega_[h], ga5, shift_.ptr, st);
     SystemView<cplx> Ah;
@@ -601,7 +596,7 @@ double DeviceSolver::time_harmonic_sweeps_batch(int P, int nsweeps) {
     const std::size_t len = disc_->len();
     const double ga5 = (1.0 / sch_.eps_relax) * kAlpha[4];
     disc_->fd_jacobian(mean_.ptr, A5_.ptr, nullptr, st);
-    build_lhs_mean_device(A5_.ptr, A5_.ptr, b, n, pat_->diag_idx, pat_->nnzb, 1, ga5, 1.0 / (sch_.eps_relax * sigma_),
+    build_lhs_mean_device(A5_.ptr, A5_.ptr, b, n, pat_->row_ptr, pat_->diag_idx, 1, ga5, 1.0 / (sch_.eps_relax * sigma_),
                           st);
     rbA_->load(A5_.ptr, st);
     RbMember<cplx> mem[kMaxBatch];

@@ -145,7 +145,7 @@ private:
     cudaEvent_t ev0_, ev1_;
 };
 
-void build_lhs_mean_device(const double* J, double* A, int b, int n, const int* diag_idx, std::size_t nnzb,
+void build_lhs_mean_device(const double* J, double* A, int b, int n, const int* row_ptr, const int* diag_idx,
                            int implicit, double ga, double inv_es, cudaStream_t st);
 void harmonic_shift(const double* vol, int n, double omega, double ga, double* shift_im, cudaStream_t st);
 void shifted_blocks(const double* P, const double* vol, int b, int n, double omega, cplx* out, cudaStream_t st);
