@@ -238,9 +238,13 @@ def main():
     clocks.start()
     barrier()
     dev_ms = 0.0
+    phase = dict(lhs=0.0, harmonics=0.0, df=0.0, mean=0.0)
     for _ in range(args.steps):
         e = stepper.outer_iteration()
-        dev_ms += s.counters()["last_ms"]
+        cn = s.counters()
+        dev_ms += cn["last_ms"]
+        for k in phase:
+            phase[k] += cn["phase_ms"][k] / args.steps
     barrier()
     clk = clocks.stop()
     launches = int(lib().fnlh_launch_count() - launches0)
@@ -321,7 +325,8 @@ def main():
                        "parallelism": (f"harmonics sharded over {world} ranks (NCCL broadcast of fields)" if shard
                                        else f"replicas x{world}" if world > 1 else "1 GPU"),
                        "sweeps_per_step": sweeps / args.steps, "lhs_bytes": s.lhs_bytes(),
-                       "workers": c.scheme.get("workers", 1), "harmonic_lanes": lanes},
+                       "workers": c.scheme.get("workers", 1), "harmonic_lanes": lanes,
+                       "step_split_ms": {k: round(v, 3) for k, v in phase.items()}},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": kname, "bytes_formula": formula,

@@ -192,7 +192,8 @@ int fnlh_solver_time_sweeps_batch(fnlh_solver* s, int P, int sweeps, double* ms)
 int fnlh_solver_lanes(const fnlh_solver* s);
 /* [red_black (0/1), n0 (colour 0 rows), SELL doubles incl. padding, nnzb] */
 int fnlh_solver_info(const fnlh_solver* s, double* out);
-/* counters: [sweeps, block-row updates, last outer iteration device ms] */
+/* counters (7 doubles): [sweeps, block-row updates, last outer iteration device ms, and its
+   split: J + A5 + mean ILU, harmonic RK steps (+ exchange), DF, mean RK step (ms)] */
 int fnlh_solver_counters(const fnlh_solver* s, double* out);
 
 #ifdef __cplusplus

@@ -267,6 +267,7 @@ int fnlh_solver_counters(const fnlh_solver* s, double* out) {
     out[0] = static_cast<double>(s->s->sweeps);
     out[1] = static_cast<double>(s->s->row_updates);
     out[2] = s->s->last_iteration_ms;
+    for (int k = 0; k < 4; ++k) out[3 + k] = s->s->phase_ms[k];
     return 0;
 }
 

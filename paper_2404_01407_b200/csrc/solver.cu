@@ -140,11 +140,13 @@ DeviceSolver::DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int
     }
     FNLH_CUDA(cudaEventCreate(&ev0_));
     FNLH_CUDA(cudaEventCreate(&ev1_));
+    for (auto& e : evp_) FNLH_CUDA(cudaEventCreate(&e));
 }
 
 DeviceSolver::~DeviceSolver() {
     cudaEventDestroy(ev0_);
     cudaEventDestroy(ev1_);
+    for (auto& e : evp_) cudaEventDestroy(e);
 }
 
 std::size_t DeviceSolver::lhs_bytes() const {
@@ -400,6 +402,7 @@ void DeviceSolver::phase_harmonics(const int* owned) {
         if (ws_->h_status[1] != 0x7fffffff) throw FactorizationError("singular pivot block", ws_->h_status[1]);
     }
 
+    FNLH_CUDA(cudaEventRecord(evp_[0], st));  // phase marks: J + A5 + mean ILU done
     std::vector<double>& h_norm = h_norm_;
     std::vector<std::vector<LinearSolveReport>>& h_reps = h_reps_;
     h_norm.assign(nh_, 0.0);
@@ -480,6 +483,7 @@ ConvergenceEntry DeviceSolver::phase_mean(const std::vector<double>& h_norm,
     const bool implicit = sch_.implicit != 0;
     if ((int)h_norm.size() != nh_ || (int)h_reps.size() != nh_) throw ShapeError("phase_mean: one entry per harmonic");
     // deterministic flux from the fresh harmonic fields (driver.cpp:268-271)
+    FNLH_CUDA(cudaEventRecord(evp_[1], st));  // harmonics done (and exchanged, when sharded)
     std::vector<const cplx*> amps;
     for (int h = 0; h < nh_; ++h) amps.push_back(amps_.ptr + (std::size_t)h * len);
     FNLH_CUDA(cudaMemsetAsync(stage_err_.ptr + 10, 0xff, sizeof(unsigned long long), st));
@@ -487,6 +491,7 @@ ConvergenceEntry DeviceSolver::phase_mean(const std::vector<double>& h_norm,
     disc_->deterministic_flux(mean_.ptr, amps, omega_, df_.ptr, st, /*deferred=*/true);
     disc_->redirect_err(nullptr);
 
+    FNLH_CUDA(cudaEventRecord(evp_[2], st));  // DF done
     // mean update including DF (driver.cpp:273-296)
     auto mean_eval = [&](const double* state, bool need_vis, double* inv, double* vis) {
         disc_->residual(state, nullptr, 2, 0, nullptr, 0, need_vis, inv, vis, st);
@@ -522,6 +527,10 @@ ConvergenceEntry DeviceSolver::phase_mean(const std::vector<double>& h_norm,
     FNLH_CUDA(cudaEventRecord(ev1_, st));
     FNLH_CUDA(cudaEventSynchronize(ev1_));
     FNLH_CUDA(cudaEventElapsedTime(&last_iteration_ms, ev0_, ev1_));
+    {
+        cudaEvent_t marks[5] = {ev0_, evp_[0], evp_[1], evp_[2], ev1_};
+        for (int k = 0; k < 4; ++k) FNLH_CUDA(cudaEventElapsedTime(&phase_ms[k], marks[k], marks[k + 1]));
+    }
     cum_seconds_ += last_iteration_ms * 1e-3;
 
     ConvergenceEntry e;  // driver.cpp:315-332

@@ -94,6 +94,8 @@ public:
     // counters for the bench: total sweeps and block-row updates performed
     long long sweeps = 0, row_updates = 0;
     float last_iteration_ms = 0.0f;
+    // last outer iteration split: J + A5 + mean ILU, harmonics, DF, mean RK (device ms)
+    float phase_ms[4] = {0.0f, 0.0f, 0.0f, 0.0f};
     bool red_black() const { return rbA_ != nullptr; }
     void info(double* out) const {
         out[0] = rbA_ ? 1.0 : 0.0;
@@ -142,7 +144,7 @@ private:
     std::vector<LinearSolveReport> reports_;
     int iter_ = 0;
     double cum_seconds_ = 0.0;
-    cudaEvent_t ev0_, ev1_;
+    cudaEvent_t ev0_, ev1_, evp_[3];
 };
 
 void build_lhs_mean_device(const double* J, double* A, int b, int n, const int* row_ptr, const int* diag_idx,

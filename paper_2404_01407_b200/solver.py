@@ -214,9 +214,10 @@ class FnlhSolver:
         return dict(red_black=bool(out[0]), n0=int(out[1]), sell_vals=int(out[2]), nnzb=int(out[3]))
 
     def counters(self):
-        out = np.zeros(3)
+        out = np.zeros(7)
         lib().fnlh_solver_counters(self.h, ptr(out))
-        return dict(sweeps=int(out[0]), row_updates=int(out[1]), last_ms=float(out[2]))
+        return dict(sweeps=int(out[0]), row_updates=int(out[1]), last_ms=float(out[2]),
+                    phase_ms=dict(lhs=float(out[3]), harmonics=float(out[4]), df=float(out[5]), mean=float(out[6])))
 
 
 __all__ = ["Discretization", "FnlhSolver", "FnlhError"]
