@@ -55,23 +55,19 @@ __device__ __forceinline__ S sys_entry(const SystemView<S>& A, int e, int k, boo
     return v;
 }
 
-// Ilu::factorize copy phase (sparse.cpp:199-209)
+// Ilu::factorize copy phase (sparse.cpp:199-209): one warp per block row, the lanes
+// stream the row's contiguous blocks element by element (coalesced)
 template <int B, class S>
 __global__ void k_ilu_copy(PatDev p, SystemView<S> A, S* __restrict__ vals) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = (int)((blockIdx.x * (std::size_t)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
     if (i >= p.rows) return;
     const int pi = p.part[i];
     const int di = p.diag_idx[i];
-    for (int e = p.row_ptr[i]; e < p.row_ptr[i + 1]; ++e) {
-        const int j = p.col_idx[e];
-        S* dst = vals + (size_t)e * B * B;
-        if (p.part[j] == pi) {
-#pragma unroll
-            for (int k = 0; k < B * B; ++k) dst[k] = sys_entry<B, S>(A, e, k, e == di, i);
-        } else {
-#pragma unroll
-            for (int k = 0; k < B * B; ++k) dst[k] = zero<S>();
-        }
+    const int e0 = p.row_ptr[i], e1 = p.row_ptr[i + 1];
+    for (int t = lane; t < (e1 - e0) * B * B; t += 32) {
+        const int e = e0 + t / (B * B), k = t % (B * B);
+        vals[(size_t)e * B * B + k] = p.part[p.col_idx[e]] == pi ? sys_entry<B, S>(A, e, k, e == di, i) : zero<S>();
     }
 }
 
@@ -91,18 +87,21 @@ __global__ void __launch_bounds__(kThreads) k_ilu_factor(PatDev p, const int* __
         if (k >= i) break;
         if (p.part[k] != pi) continue;
         // L_ik = A_ik * U_kk^{-1}
-        S lik[B * B], tmp[B * B];
-        load_block<B>(vals + (size_t)ek * B * B, lik);
+        S tmp[B * B];
         const S* uinv = diag_inv + (size_t)k * B * B;
 #pragma unroll
-        for (int r = 0; r < B; ++r)
+        for (int r = 0; r < B; ++r) {  // one row of A_ik at a time (register pressure)
+            S lrow[B];
+#pragma unroll
+            for (int m = 0; m < B; ++m) lrow[m] = vals[(size_t)ek * B * B + r * B + m];
 #pragma unroll
             for (int c = 0; c < B; ++c) {
                 S acc = zero<S>();
 #pragma unroll
-                for (int m = 0; m < B; ++m) acc += lik[r * B + m] * uinv[m * B + c];
+                for (int m = 0; m < B; ++m) acc += lrow[m] * uinv[m * B + c];
                 tmp[r * B + c] = acc;
             }
+        }
         store_block<B>(vals + (size_t)ek * B * B, tmp);
         // A_ij -= L_ik U_kj for j > k present in both rows (zero-skip, dense.hpp:47)
         for (int ej = rb; ej < re; ++ej) {
@@ -114,18 +113,21 @@ __global__ void __launch_bounds__(kThreads) k_ilu_factor(PatDev p, const int* __
             if (p.part[k] != p.part[j]) continue;
             const S* u = vals + (size_t)ekj * B * B;
             S* cblk = vals + (size_t)ej * B * B;
-            S cc[B * B];
-            load_block<B>(cblk, cc);
 #pragma unroll
-            for (int r = 0; r < B; ++r)
+            for (int r = 0; r < B; ++r) {  // block_matmul_sub row by row (same operation order)
+                S crow[B];
+#pragma unroll
+                for (int c = 0; c < B; ++c) crow[c] = cblk[r * B + c];
 #pragma unroll
                 for (int kk = 0; kk < B; ++kk) {
                     const S a = tmp[r * B + kk];
                     if (is_zero(a)) continue;
 #pragma unroll
-                    for (int c = 0; c < B; ++c) cc[r * B + c] -= a * u[kk * B + c];
+                    for (int c = 0; c < B; ++c) crow[c] -= a * u[kk * B + c];
                 }
-            store_block<B>(cblk, cc);
+#pragma unroll
+                for (int c = 0; c < B; ++c) cblk[r * B + c] = crow[c];
+            }
         }
     }
     // pivot block: partial-pivot LU, condition check, explicit inverse
@@ -509,7 +511,7 @@ void ilu_factorize(const SystemView<S>& A, DeviceIlu<S>& f, Workspace& ws) {
     const int init[2] = {0, 0x7fffffff};
     FNLH_CUDA(cudaMemcpyAsync(ws.status, init, sizeof init, cudaMemcpyHostToDevice, ws.stream));
     FNLH_DISPATCH_B(p.b, {
-        { ::fnlh::note_launch(); k_ilu_copy<B, S><<<nblocks(p.rows), kThreads, 0, ws.stream>>>(pd, A, f.vals); }
+        { ::fnlh::note_launch(); k_ilu_copy<B, S><<<(int)(((std::size_t)p.rows * 32 + kThreads - 1) / kThreads), kThreads, 0, ws.stream>>>(pd, A, f.vals); }
         for (int l = 0; l < p.fwd_levels(); ++l) {
             const int n = p.fwd_ptr[l + 1] - p.fwd_ptr[l];
             { ::fnlh::note_launch(); k_ilu_factor<B, S><<<nblocks(n), kThreads, 0, ws.stream>>>(pd, p.fwd_rows + p.fwd_ptr[l], n, f.vals,
