@@ -168,8 +168,15 @@ class FnlhSolver:
         hist = [dict(iter=e.iter, resid_mean=e.resid_mean, rz=e.rz) for e in arr[: min(n.value, max_entries)]]
         return ["target-drop", "iteration-cap", "divergence"][reason.value], hist
 
-    def state(self):
+    def state(self, out=None):
+        """(mean, amps); `out` = preallocated (mean [N b] f64, amps [N_h, N b] c128) host
+        arrays (e.g. pinned) to download into."""
         n = self.m.n * self.m.b
+        if out is not None:
+            mean, amps = out
+            assert mean.flags.c_contiguous and amps.flags.c_contiguous and amps.dtype == np.complex128
+            check(lib().fnlh_solver_get_state(self.h, ptr(mean), ptr(amps.reshape(-1).view(np.float64))))
+            return mean, amps
         mean = np.zeros(n)
         amps = np.zeros(max(self.nh, 1) * n, np.complex128)
         check(lib().fnlh_solver_get_state(self.h, ptr(mean), ptr(amps.view(np.float64))))
