@@ -4,6 +4,8 @@
  * Build: gcc -std=gnu11 -O2 -ffp-contract=off -fPIC -shared (no -march), see oracle/Makefile.
  */
 #include "fnlh_oracle.h"
+
+#include <pthread.h>
 #include "cr_pow.h"
 
 #include <math.h>
@@ -11,7 +13,7 @@
 #include <stdlib.h>
 #include <string.h>
 
-static or_error g_err;
+static __thread or_error g_err; /* per thread: harmonic workers copy theirs out */
 static int g_cr_pow = 0; /* 0: glibc pow (reference), 1: correctly rounded (device) */
 
 void or_set_pow_mode(int cr) { g_cr_pow = cr; }
@@ -839,6 +841,10 @@ struct or_solver {
     int iter;
     report_list* hrep; /* per harmonic, from the last phase_harmonics */
     double* hnorm;
+    or_ilu_z* ws_extra; /* per-worker complex workspaces (or_set_workers) */
+    or_error* herr;     /* per harmonic error record of the worker threads */
+    ocplx** wsmat_extra;
+    int n_extra;
 };
 
 static void* xcalloc(size_t n, size_t s) { return calloc(n ? n : 1, s); }
@@ -867,6 +873,7 @@ or_solver* or_solver_create(const or_mesh* m, const or_pattern* p, const or_sche
     S_->df = (double*)xcalloc(len, sizeof(double));
     S_->hrep = (report_list*)xcalloc(nh, sizeof(report_list));
     S_->hnorm = (double*)xcalloc(nh, sizeof(double));
+    S_->herr = (or_error*)xcalloc(nh, sizeof(or_error));
     S_->M = (double*)xcalloc((size_t)n * bb, sizeof(double));
     S_->MLU = (double*)xcalloc((size_t)n * bb, sizeof(double));
     S_->Mpiv = (int*)xcalloc(len, sizeof(int));
@@ -917,6 +924,16 @@ void or_solver_destroy(or_solver* s) {
     free(s->wsilu.diag_inv);
     free(s->reports.v);
     for (int h = 0; h < s->nh; ++h) free(s->hrep[h].v);
+    for (int t = 0; t < s->n_extra; ++t) {
+        free(s->wsmat_extra[t]);
+        free(s->ws_extra[t].vals);
+        free(s->ws_extra[t].diag_lu);
+        free(s->ws_extra[t].diag_piv);
+        free(s->ws_extra[t].diag_inv);
+    }
+    free(s->ws_extra);
+    free(s->wsmat_extra);
+    free(s->herr);
     free(s->hrep);
     free(s->hnorm);
     free(s);
@@ -1012,6 +1029,72 @@ static int apply_mean(rk_ctx* c, const double* base, const double* x, double* ou
 #undef APPLY
 
 /* FnlhSolver::outer_iteration (driver.cpp:157-333), workers = 1, single grid */
+static int g_workers = 1;
+void or_set_workers(int w) { g_workers = w; }
+
+/* one harmonic's build_lhs_harmonic + factorization + rk_step (driver.cpp:193-244) */
+static int run_harmonic(or_solver* s, int h, double ga5, ocplx* wsmat, or_ilu_z* wsilu) {
+    const or_mesh* m = &s->mesh;
+    const int b = m->b, n = m->n;
+    const size_t len = (size_t)n * b, bb = (size_t)b * b;
+    const or_pattern* p = &s->pat;
+    const int implicit = s->sch.implicit;
+    report_list hreps = {0};
+    rk_ctx c = {s, h};
+    rk_result res;
+    const double omega = s->omega[h];
+    int st = OR_OK;
+    if (implicit) {
+        /* build_lhs_harmonic (rk.cpp:32-39) */
+        ocplx* shift = (ocplx*)malloc(sizeof(ocplx) * n);
+        for (int i = 0; i < n; ++i) shift[i] = CMPLX(0.0, omega * m->vol[i] / ga5);
+        or_shift_diagonal(p, s->A5, shift, wsmat);
+        free(shift);
+        if ((st = or_ilu_factorize_z(p, wsmat, wsilu))) return st;
+        st = rk_step_z(&c, s->amps + (size_t)h * len, n, b, 1, s->sigma, s->sch.eps_relax, s->sch.linear_tol,
+                       s->sch.linear_max_iter, p, wsmat, wsilu, NULL, NULL, &res, &hreps);
+    } else {
+        /* shifted_blocks (driver.cpp:48-59) */
+        ocplx* pclu = (ocplx*)malloc(sizeof(ocplx) * n * bb);
+        int* pcpiv = (int*)malloc(sizeof(int) * len);
+        for (int i = 0; i < n && !st; ++i) {
+            const double* src = s->P + (size_t)i * bb;
+            ocplx* dst = pclu + (size_t)i * bb;
+            for (size_t k = 0; k < bb; ++k) dst[k] = CMPLX(src[k], 0.0);
+            const ocplx sh = CMPLX(0.0, omega * m->vol[i]);
+            for (int q = 0; q < b; ++q) dst[(size_t)q * b + q] += sh;
+            st = or_block_lu_factor_z(b, dst, pcpiv + (size_t)i * b, i, NULL);
+        }
+        if (!st)
+            st = rk_step_z(&c, s->amps + (size_t)h * len, n, b, 0, s->sigma, s->sch.eps_relax, s->sch.linear_tol,
+                           s->sch.linear_max_iter, p, NULL, NULL, pclu, pcpiv, &res, &hreps);
+        free(pclu);
+        free(pcpiv);
+    }
+    if (!st) s->hnorm[h] = res.stage1_norm;
+    for (int k = 0; k < hreps.n; ++k) reports_push(&s->hrep[h], &hreps.v[k]);
+    free(hreps.v);
+    return st;
+}
+
+typedef struct {
+    or_solver* s;
+    const int* owned;
+    int* hst;
+    double ga5;
+    int t, W;
+} worker_arg;
+
+static void* harmonic_worker(void* p) {
+    worker_arg* a = (worker_arg*)p;
+    for (int h = a->t; h < a->s->nh; h += a->W) {
+        if (a->owned && !a->owned[h]) continue;
+        a->hst[h] = run_harmonic(a->s, h, a->ga5, a->s->wsmat_extra[a->t], &a->s->ws_extra[a->t]);
+        if (a->hst[h]) a->s->herr[h] = g_err;
+    }
+    return NULL;
+}
+
 /* outer_iteration split where harmonic sharding exchanges the fields:
    phase_harmonics relaxes the harmonics with owned[h] (NULL: all), phase_mean runs DF +
    the mean step given every harmonic's stage-1 norm and reports (harmonic order). */
@@ -1046,43 +1129,45 @@ int or_solver_phase_harmonics(or_solver* s, const int* owned, double* hnorm_out)
         s->hrep[h].n = 0;
         hnorm[h] = 0.0;
     }
-    ocplx* shift = (ocplx*)malloc(sizeof(ocplx) * n);
-    ocplx* pclu = implicit ? NULL : (ocplx*)malloc(sizeof(ocplx) * n * bb);
-    int* pcpiv = implicit ? NULL : (int*)malloc(sizeof(int) * len);
-    for (int h = 0; h < nh && !st; ++h) {
-        if (owned && !owned[h]) continue;
-        report_list hreps = {0};
-        rk_ctx c = {s, h};
-        rk_result res;
-        const double omega = s->omega[h];
-        if (implicit) {
-            /* build_lhs_harmonic (rk.cpp:32-39) */
-            for (int i = 0; i < n; ++i) shift[i] = CMPLX(0.0, omega * m->vol[i] / ga5);
-            or_shift_diagonal(p, s->A5, shift, s->wsmat);
-            if ((st = or_ilu_factorize_z(p, s->wsmat, &s->wsilu))) break;
-            st = rk_step_z(&c, s->amps + (size_t)h * len, n, b, 1, s->sigma, s->sch.eps_relax, s->sch.linear_tol,
-                           s->sch.linear_max_iter, p, s->wsmat, &s->wsilu, NULL, NULL, &res, &hreps);
-        } else {
-            /* shifted_blocks (driver.cpp:48-59) */
-            for (int i = 0; i < n; ++i) {
-                const double* src = s->P + (size_t)i * bb;
-                ocplx* dst = pclu + (size_t)i * bb;
-                for (size_t k = 0; k < bb; ++k) dst[k] = CMPLX(src[k], 0.0);
-                const ocplx sh = CMPLX(0.0, omega * m->vol[i]);
-                for (int q = 0; q < b; ++q) dst[(size_t)q * b + q] += sh;
-                if ((st = or_block_lu_factor_z(b, dst, pcpiv + (size_t)i * b, i, NULL))) break;
-            }
-            if (st) break;
-            st = rk_step_z(&c, s->amps + (size_t)h * len, n, b, 0, s->sigma, s->sch.eps_relax, s->sch.linear_tol,
-                           s->sch.linear_max_iter, p, NULL, NULL, pclu, pcpiv, &res, &hreps);
+    /* harmonic workers (driver.cpp:246-265): with or_set_workers(W > 1) the harmonics run
+       on W OpenMP threads, each with its own complex workspace; every harmonic runs and
+       the first error by harmonic index is returned.  W = 1: sequential, stop at the
+       first error. */
+    const int W = g_workers < 1 ? 1 : (g_workers > nh ? (nh > 0 ? nh : 1) : g_workers);
+    int hst[64] = {0};
+    if (W > 1 && !s->ws_extra) {
+        s->ws_extra = (or_ilu_z*)xcalloc(W, sizeof(or_ilu_z));
+        s->wsmat_extra = (ocplx**)xcalloc(W, sizeof(ocplx*));
+        s->n_extra = W;
+        const size_t nnz = (size_t)p->nnzb * bb;
+        for (int t = 0; t < W; ++t) {
+            s->wsmat_extra[t] = (ocplx*)xcalloc(nnz, sizeof(ocplx));
+            s->ws_extra[t].vals = (ocplx*)xcalloc(nnz, sizeof(ocplx));
+            s->ws_extra[t].diag_lu = (ocplx*)xcalloc((size_t)n * bb, sizeof(ocplx));
+            s->ws_extra[t].diag_piv = (int*)xcalloc(len, sizeof(int));
+            s->ws_extra[t].diag_inv = (ocplx*)xcalloc((size_t)n * bb, sizeof(ocplx));
         }
-        if (!st) hnorm[h] = res.stage1_norm;
-        for (int k = 0; k < hreps.n; ++k) reports_push(&s->hrep[h], &hreps.v[k]);
-        free(hreps.v);
     }
-    free(shift);
-    free(pclu);
-    free(pcpiv);
+    if (W == 1) {
+        for (int h = 0; h < nh; ++h) {
+            if (owned && !owned[h]) continue;
+            if ((hst[h] = run_harmonic(s, h, ga5, s->wsmat, &s->wsilu))) break;  /* stop at the first error */
+        }
+    } else {  /* worker t relaxes harmonics t, t + W, ... (driver.cpp:250) */
+        pthread_t th[64];
+        worker_arg args[64];
+        for (int t = 0; t < W; ++t) {
+            args[t] = (worker_arg){s, owned, hst, ga5, t, W};
+            pthread_create(&th[t], NULL, harmonic_worker, &args[t]);
+        }
+        for (int t = 0; t < W; ++t) pthread_join(th[t], NULL);
+        for (int h = 0; h < nh; ++h)
+            if (hst[h]) {  /* the first error by harmonic index (driver.cpp:263-264) */
+                g_err = s->herr[h];
+                break;
+            }
+    }
+    for (int h = 0; h < nh && !st; ++h) st = hst[h];
     if (hnorm_out)
         for (int h = 0; h < nh; ++h) hnorm_out[h] = hnorm[h];
     return st;

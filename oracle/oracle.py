@@ -86,14 +86,16 @@ class OrError(C.Structure):
 class Oracle:
     """The plain-C restatement (liboracle.so)."""
 
-    def __init__(self, path=ORACLE_SO, pow_mode="glibc"):
+    def __init__(self, path=ORACLE_SO, pow_mode="glibc", workers=1):
         """pow_mode: "glibc" evaluates the boundary-state pow with the reference's libm,
-        "cr" with the device's correctly rounded pow (oracle/cr_pow.h)."""
+        "cr" with the device's correctly rounded pow (oracle/cr_pow.h).  workers: harmonic
+        worker threads (SchemeConfig::workers, driver.cpp:246-265)."""
         if not os.path.exists(path):
             build()
         self.lib = C.CDLL(path)
         L = self.lib
         self.cr = 1 if pow_mode == "cr" else 0
+        self.workers = int(workers)
         L.or_last_error.restype = C.POINTER(OrError)
         L.or_solver_create.restype = _p
         L.or_solver_df.restype = C.POINTER(_d)
@@ -101,6 +103,7 @@ class Oracle:
 
     def mode(self):
         self.lib.or_set_pow_mode(_i(self.cr))
+        self.lib.or_set_workers(_i(self.workers))
         return self.lib
 
     def _check(self, st):

@@ -142,3 +142,19 @@ def test_nozzle_solver_history(ref, orc):
     mo, ao = osv.state()
     assert rel(extract(mo, noz.n), mr) < 1e-12
     assert rel(np.stack([extract(a, noz.n) for a in ao]), ar) < 1e-8
+
+
+def test_oracle_harmonic_workers_bitwise():
+    """The checker's harmonic worker threads (the reference's workers, driver.cpp:246-265,
+    used by the CPU baseline) give bitwise the sequential result."""
+    from oracle.oracle import Oracle
+    from paper_2404_01407_b200.cases import make_case
+    c = make_case("c2", scale=0.05, nh=3)
+    out = []
+    for w in (1, 3):
+        s = Oracle(pow_mode="cr", workers=w).solver(c.mesh, c.mesh.pattern(), c.scheme, c.omegas, c.forcing, c.mean0)
+        hist = [s.outer_iteration() for _ in range(2)]
+        out.append(([(e["resid_mean"], e["rz"]) for e in hist], s.state(), s.reports()))
+    (h1, (m1, a1), r1), (h3, (m3, a3), r3) = out
+    assert h1 == h3 and r1 == r3
+    assert np.array_equal(m1, m3) and np.array_equal(a1, a3)
