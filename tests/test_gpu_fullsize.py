@@ -1,0 +1,80 @@
+"""Parity at BASELINE.json's full C2 size (410,865 nodes, 2,840,273 blocks).
+
+* the outer iteration against the CPU restatement for two pseudo-steps (the oracle runs
+  its harmonic worker threads, bitwise its sequential result);
+* size-independent properties of the harmonic relaxation on the full system: the
+  2-colour sweep and the level-scheduled general path (two independent kernel sets, both
+  the reference's ILU(0)-Richardson) agree bitwise; the reported final residual equals
+  ||b - A x|| recomputed by the separate matvec kernel; the one-pass variant agrees to
+  rounding.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from helpers import rel
+from paper_2404_01407_b200.cases import make_case
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c2():
+    return make_case("c2", workers=3)
+
+
+def test_c2_full_size_history_vs_oracle(c2):
+    from oracle.oracle import Oracle
+    from paper_2404_01407_b200.solver import FnlhSolver
+    c = c2
+    g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
+    o = Oracle(pow_mode="cr", workers=min(3, os.cpu_count() or 1)).solver(c.mesh, c.mesh.pattern(), c.scheme,
+                                                                         c.omegas, c.forcing, c.mean0)
+    for it in range(2):
+        eg, eo = g.outer_iteration(), o.outer_iteration()
+        assert abs(eg["resid_mean"] / eo["resid_mean"] - 1) < 1e-8, (it, eg, eo)
+        assert abs(eg["rz"] / eo["rz"] - 1) < 1e-8, (it, eg, eo)
+        assert np.allclose(eg["resid_h"], eo["resid_h"], rtol=1e-8, atol=0)
+    mg, ag = g.state()
+    mo, ao = o.state()
+    assert rel(mg, mo) < 1e-10 and rel(ag, ao) < 1e-10
+    assert [r[0] for r in g.reports()] == [r[0] for r in o.reports()]
+
+
+def test_c2_full_size_relaxation_properties(c2):
+    from paper_2404_01407_b200 import la
+    from paper_2404_01407_b200.solver import Discretization
+    c = c2
+    m = c.mesh
+    pat = m.pattern()
+    J, _ = Discretization(m).fd_jacobian(c.mean0, want_J=True)
+    # A5 = J / ga + diag(J_ii) inv_es / ga (rk.cpp:5-30) with the C2 scheme, and the
+    # harmonic shift i omega V / ga (rk.cpp:32-39) of the first harmonic
+    eps, sigma = c.scheme["eps_relax"], 50.0
+    ga = (1.0 / eps) * 1.0
+    A = (J / ga).reshape(-1, m.b * m.b)
+    A[pat["diag_idx"]] += J.reshape(-1, m.b * m.b)[pat["diag_idx"]] * (1.0 / (eps * sigma)) / ga
+    A = A.reshape(-1)
+    shift = c.omegas[0] * m.vol / ga
+    rng = np.random.default_rng(7)
+    rhs = rng.standard_normal(m.n * m.b) + 1j * rng.standard_normal(m.n * m.b)
+    P = la.Pattern.from_dict(pat)
+    assert la.red_black_n0(P) > 0
+    try:
+        la.set_rb_sweep(la.RB_EXACT)
+        x_rb, r_rb = la.smoothed_solve(P, A, rhs, 1e-14, 6, shift)
+        la.set_red_black(False)
+        x_gen, r_gen = la.smoothed_solve(P, A, rhs, 1e-14, 6, shift)
+        la.set_red_black(True)
+        la.set_rb_sweep(la.RB_ONEPASS)
+        x_op, r_op = la.smoothed_solve(P, A, rhs, 1e-14, 6, shift)
+    finally:
+        la.set_red_black(True)
+        la.set_rb_sweep(la.RB_EXACT)
+    assert np.array_equal(x_rb, x_gen) and r_rb[0] == r_gen[0] == 6
+    assert abs(r_rb[2] / r_gen[2] - 1) < 1e-12 and abs(r_rb[1] / r_gen[1] - 1) < 1e-14
+    res = rhs - la.matvec(P, A, x_rb, shift)
+    assert abs(np.linalg.norm(res) / r_rb[2] - 1) < 1e-10
+    assert r_rb[2] < r_rb[1]
+    assert np.abs(x_op - x_rb).max() <= 1e-12 * np.abs(x_rb).max()
