@@ -210,3 +210,40 @@ def test_phase_split_and_field_exchange(workers):
         m, am = s.state()
         assert np.array_equal(m, mr) and np.array_equal(am, ar)
         assert s.reports() == ref.reports()
+
+
+@pytest.mark.parametrize("workers", [1, 3])
+def test_harmonic_failure_worker_semantics(orc_dev, workers):
+    """A harmonic whose field is not finite fails its RK step.  workers = 1: the reference's
+    sequential loop stops there (earlier harmonics committed, later ones untouched);
+    workers > 1: every harmonic runs, successful ones commit, the first error by index is
+    raised (driver.cpp:246-265).  Device lanes and the CPU restatement's worker threads
+    agree on the surviving fields bitwise."""
+    from oracle.oracle import CheckerError, Oracle
+    from paper_2404_01407_b200._lib import FnlhError
+    from paper_2404_01407_b200.solver import FnlhSolver
+    c = make_case("c2", scale=0.08, nh=3, workers=workers)
+    g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
+    o = Oracle(pow_mode="cr", workers=workers).solver(c.mesh, c.mesh.pattern(), c.scheme, c.omegas, c.forcing,
+                                                       c.mean0)
+    g.outer_iteration()
+    o.outer_iteration()
+    mean, amps = o.state()
+    amps = amps.copy()
+    amps[1, 7] = np.nan
+    g.set_state(mean, amps)
+    o.set_state(mean, amps)
+    with pytest.raises(FnlhError) as eg:
+        g.outer_iteration()
+    with pytest.raises(CheckerError) as eo:
+        o.outer_iteration()
+    assert eg.value.kind == "DivergenceError" and eo.value.code == 6
+    mg, ag = g.state()
+    mo, ao = o.state()
+    assert np.array_equal(mg, mean) and np.array_equal(mo, mean)  # the mean step never ran
+    assert not np.array_equal(ag[0], amps[0]) and np.array_equal(ag[0], ao[0])  # harmonic 0 committed
+    assert np.isnan(ag[1, 7]) and np.isnan(ao[1, 7])  # the failing harmonic is untouched
+    if workers == 1:
+        assert np.array_equal(ag[2], amps[2]) and np.array_equal(ao[2], amps[2])  # never ran
+    else:
+        assert not np.array_equal(ag[2], amps[2]) and np.array_equal(ag[2], ao[2])  # ran and committed
