@@ -314,6 +314,13 @@ def main():
         formula = "sweep_bytes (stored-factor)"
     peak, peak_kind = peaks()
     achieved = bytes_sweep / (sweep_ms * 1e-3) / 1e9
+    single = None
+    if lanes > 1 and info["red_black"]:  # the same sweep for one harmonic alone, for reference
+        s.time_sweeps(0, 2)
+        ms1 = s.time_sweeps(0, args.sweeps) / args.sweeps
+        b1 = rb_sweep_bytes(n, info["n0"], E, b, 1)
+        single = {"ms_per_launch": ms1, "bytes_per_launch": b1, "achieved": b1 / (ms1 * 1e-3) / 1e9,
+                  "frac": b1 / (ms1 * 1e-3) / 1e9 / peak, "unit": "GB/s"}
     traffic = None
     try:  # dram read + write of the same kernels from the committed ncu --set full capture
         name = "r1_sweep_ncu_c2_lanes3.json" if lanes == 3 else "r1_sweep_ncu_c2.json"
@@ -340,7 +347,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": kname, "bytes_formula": formula,
                          "bytes_per_launch": bytes_sweep, "ms_per_launch": sweep_ms, "peak_kind": peak_kind,
-                         "sweep_rows_per_s": lanes * n / (sweep_ms * 1e-3)},
+                         "sweep_rows_per_s": lanes * n / (sweep_ms * 1e-3), "single_lane": single},
             "clocks": clk, "gpu_launches": launches}
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
