@@ -97,11 +97,12 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def sweep_bytes(n, e, b):
-    """Algorithmic bytes of one complex harmonic sweep, stored-factor ILU:
-    2E b^2 16 (L,U) + N (b^2 16 + 4b) (pivot LU + piv) + (N+2E) b^2 8 (real A5 matvec)
-    + N 8 (shift) + 5 N b 16 (rhs, x r/w, r, z)."""
-    return 2 * e * b * b * 16 + n * (b * b * 16 + 4 * b) + (n + 2 * e) * b * b * 8 + n * 8 + 5 * n * b * 16
+def sweep_bytes(n, e, b, lanes=1):
+    """Algorithmic bytes of one (batched) complex harmonic sweep, stored-factor ILU
+    (SURVEY.md 8(d)): the real A5 of the matvec (N+2E) b^2 8 once, and per lane 2E b^2 16
+    (L,U) + N (b^2 16 + 4b) (pivot LU + piv) + N 8 (shift) + 5 N b 16 (rhs, x r/w, r, z)."""
+    per_lane = 2 * e * b * b * 16 + n * (b * b * 16 + 4 * b) + n * 8 + 5 * n * b * 16
+    return (n + 2 * e) * b * b * 8 + lanes * per_lane
 
 
 def rb_sweep_bytes(n, n0, e, b, lanes=1):
@@ -309,9 +310,9 @@ def main():
                  f"{lanes} harmonic lane(s) per launch")
         formula = f"rb_sweep_bytes(lanes={lanes})"
     else:
-        bytes_sweep = sweep_bytes(n, E, b)
-        kname = "level-scheduled ILU(0)-Richardson sweep (fwd/bwd levels + matvec)"
-        formula = "sweep_bytes (stored-factor)"
+        bytes_sweep = sweep_bytes(n, E, b, lanes)
+        kname = f"level-scheduled ILU(0)-Richardson sweep (fwd/bwd levels + matvec), {lanes} harmonic lane(s)"
+        formula = f"sweep_bytes(stored-factor, lanes={lanes})"
     peak, peak_kind = peaks()
     achieved = bytes_sweep / (sweep_ms * 1e-3) / 1e9
     single = None

@@ -312,6 +312,167 @@ __global__ void k_sumsq(const S* __restrict__ x, std::size_t len, double* __rest
     }
 }
 
+// ---- batched level-scheduled Richardson: P systems sharing the real A (harmonic lanes)
+// CTA b serves lane b % P, so the P CTAs reading the same rows of A run back to back.
+template <class S>
+struct LaLanes {
+    const S* vals[kMaxLanes];
+    const S* diag_lu[kMaxLanes];
+    const int* diag_piv[kMaxLanes];
+    const double* shift[kMaxLanes];
+    const S* rhs[kMaxLanes];
+    S* x[kMaxLanes];
+    S* z[kMaxLanes];
+    S* r[kMaxLanes];
+    double* parts[kMaxLanes];
+    const int* active;  // [P] 1 while the lane iterates
+    int P;
+};
+
+template <int B, class S>
+__global__ void __launch_bounds__(kThreads) k_ilu_fwd_b(PatDev p, const int* __restrict__ rows, int nrows,
+                                                        LaLanes<S> T) {
+    const int lane = blockIdx.x % T.P;
+    if (!T.active[lane]) return;
+    const int t = (blockIdx.x / T.P) * blockDim.x + threadIdx.x;
+    if (t >= nrows) return;
+    const S* __restrict__ vals = T.vals[lane];
+    S* x = T.z[lane];
+    const int i = rows[t];
+    const int pi = p.part[i];
+    S xi[B];
+    load_vec<B>(T.r[lane] + (size_t)i * B, xi);
+    for (int e = p.row_ptr[i]; e < p.row_ptr[i + 1]; ++e) {
+        const int k = p.col_idx[e];
+        if (k >= i) break;
+        if (p.part[k] != pi) continue;
+        const S* blk = vals + (size_t)e * B * B;
+        S xkv[B];
+        load_vec<B>(x + (size_t)k * B, xkv);
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+            S acc = zero<S>();
+#pragma unroll
+            for (int c = 0; c < B; ++c) acc += blk[r * B + c] * xkv[c];
+            xi[r] -= acc;
+        }
+    }
+    store_vec<B>(x + (size_t)i * B, xi);
+}
+
+template <int B, class S>
+__global__ void __launch_bounds__(kThreads) k_ilu_bwd_b(PatDev p, const int* __restrict__ rows, int nrows,
+                                                        LaLanes<S> T) {
+    const int lane = blockIdx.x % T.P;
+    if (!T.active[lane]) return;
+    const int t = (blockIdx.x / T.P) * blockDim.x + threadIdx.x;
+    if (t >= nrows) return;
+    const S* __restrict__ vals = T.vals[lane];
+    S* x = T.z[lane];
+    const int i = rows[t];
+    const int pi = p.part[i];
+    S xi[B];
+    load_vec<B>(x + (size_t)i * B, xi);
+    for (int e = p.row_ptr[i + 1] - 1; e >= p.row_ptr[i]; --e) {
+        const int j = p.col_idx[e];
+        if (j <= i) break;
+        if (p.part[j] != pi) continue;
+        const S* blk = vals + (size_t)e * B * B;
+        S xjv[B];
+        load_vec<B>(x + (size_t)j * B, xjv);
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+            S acc = zero<S>();
+#pragma unroll
+            for (int c = 0; c < B; ++c) acc += blk[r * B + c] * xjv[c];
+            xi[r] -= acc;
+        }
+    }
+    S lu[B * B];
+    int piv[B];
+    load_block<B>(T.diag_lu[lane] + (size_t)i * B * B, lu);
+#pragma unroll
+    for (int k = 0; k < B; ++k) piv[k] = T.diag_piv[lane][(size_t)i * B + k];
+    lu_solve_reg<B>(lu, piv, xi);
+    store_vec<B>(x + (size_t)i * B, xi);
+    S* xa = T.x[lane] + (size_t)i * B;
+#pragma unroll
+    for (int k = 0; k < B; ++k) xa[k] += xi[k];
+}
+
+// r = rhs - (A + i diag(shift)) x per lane (k_matvec's arithmetic), per-CTA |r|^2 partials
+template <int B, class S>
+__global__ void __launch_bounds__(kThreads) k_matvec_b(PatDev p, const double* __restrict__ Areal, LaLanes<S> T) {
+    __shared__ double red[kThreads / 32];
+    const int lane = blockIdx.x % T.P;
+    if (!T.active[lane]) return;
+    const int cta = blockIdx.x / T.P, nct = gridDim.x / T.P;
+    const S* __restrict__ x = T.x[lane];
+    const double* __restrict__ shift = T.shift[lane];
+    double local = 0.0;
+    for (int i = cta * blockDim.x + threadIdx.x; i < p.rows; i += nct * blockDim.x) {
+        S y[B];
+#pragma unroll
+        for (int r = 0; r < B; ++r) y[r] = zero<S>();
+        const int di = p.diag_idx[i];
+        for (int e = p.row_ptr[i]; e < p.row_ptr[i + 1]; ++e) {
+            S xc[B];
+            load_vec<B>(x + (size_t)p.col_idx[e] * B, xc);
+            const bool diag = e == di;
+            const double* blk = Areal + (size_t)e * B * B;
+#pragma unroll
+            for (int r = 0; r < B; ++r) {
+                S acc = zero<S>();
+#pragma unroll
+                for (int c = 0; c < B; ++c) {
+                    if constexpr (sizeof(S) == sizeof(cplx)) {
+                        if (diag && r == c && shift)
+                            acc += mk(blk[r * B + c] + 0.0, 0.0 + shift[i]) * xc[c];
+                        else
+                            acc += rmul(blk[r * B + c], xc[c]);
+                    } else {
+                        acc += rmul(blk[r * B + c], xc[c]);
+                    }
+                }
+                y[r] += acc;
+            }
+        }
+        S* o = T.r[lane] + (size_t)i * B;
+        const S* bb = T.rhs[lane] + (size_t)i * B;
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+            const S v = bb[r] - y[r];
+            o[r] = v;
+            local += sq(v);
+        }
+    }
+    for (int off = 16; off > 0; off >>= 1) local += __shfl_down_sync(0xffffffffu, local, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = local;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kThreads / 32; ++w) s += red[w];
+        T.parts[lane][cta] = s;
+    }
+}
+
+// per-lane fixed-order sum of partials (block l = lane l)
+__global__ void k_finish_b(LaLanes<cplx> Tc, LaLanes<double> Td, int is_cplx, int n, double* __restrict__ out) {
+    __shared__ double red[32];
+    const int lane = blockIdx.x;
+    const double* partials = is_cplx ? Tc.parts[lane] : Td.parts[lane];
+    double s = 0.0;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) s += partials[k];
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        out[lane] = t;
+    }
+}
+
 // fixed-order final reduction of the per-block partials (deterministic run to run)
 __global__ void k_finish(const double* __restrict__ partials, int n, double* __restrict__ out) {
     __shared__ double red[32];
@@ -482,7 +643,7 @@ std::size_t DeviceIlu<S>::bytes() const {
 
 Workspace::Workspace(std::size_t max_len) : vec_len(max_len) {
     FNLH_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-    n_partials = 4096;
+    n_partials = 8192;
     FNLH_CUDA(cudaMalloc(&partials, n_partials * sizeof(double)));
     FNLH_CUDA(cudaMalloc(&scalars, 64 * sizeof(double)));
     FNLH_CUDA(cudaMallocHost(&h_scalars, 64 * sizeof(double)));
@@ -613,6 +774,90 @@ LinearSolveReport smoothed_solve(const SystemView<S>& A, const S* rhs, const Dev
     return rep;
 }
 
+// smoothed_solve (sparse.hpp:295-331) on P systems at once: the level kernels and the
+// residual matvec serve every still-iterating lane in one launch; the stopping rule is
+// taken per lane on the host after each sweep (one synchronization per sweep for all)
+template <class S>
+void smoothed_solve_batch(const DevicePattern& p, const double* A_real, const LaneSystem<S>* sys, int P,
+                          double tol_rel, int max_iter, LaneReport* reps, Workspace& ws) {
+    if (!(tol_rel > 0.0 && tol_rel < 1.0)) throw ConfigError("smoothed_solve: tol_rel must be in (0,1)");
+    if (max_iter < 1) throw ConfigError("smoothed_solve: max_iter must be >= 1");
+    if (P < 1 || P > kMaxLanes) throw ConfigError("smoothed_solve_batch: 1 <= P <= kMaxLanes");
+    const std::size_t len = (std::size_t)p.rows * p.b;
+    const PatDev pd = dev(p);
+    const int grid = std::min(nblocks(p.rows), kRedBlocks);
+    if ((std::size_t)ws.n_partials < (std::size_t)grid * P + 2 * kMaxLanes + 16)
+        throw ConfigError("smoothed_solve_batch: workspace too small");
+    LaLanes<S> T{};
+    T.P = P;
+    int* d_active = reinterpret_cast<int*>(ws.partials + (std::size_t)grid * P);
+    double* d_norm = ws.partials + (std::size_t)grid * P + kMaxLanes;
+    T.active = d_active;
+    std::vector<double> target(P);
+    int h_active[kMaxLanes] = {0};
+    for (int m = 0; m < P; ++m) {
+        T.vals[m] = sys[m].f->vals;
+        T.diag_lu[m] = sys[m].f->diag_lu;
+        T.diag_piv[m] = sys[m].f->diag_piv;
+        T.shift[m] = sys[m].shift;
+        T.rhs[m] = sys[m].rhs;
+        T.x[m] = sys[m].x;
+        T.z[m] = sys[m].z;
+        T.r[m] = sys[m].r;
+        T.parts[m] = ws.partials + (std::size_t)grid * m;
+        FNLH_CUDA(cudaMemsetAsync(sys[m].x, 0, len * sizeof(S), ws.stream));
+        norm2_sq(sys[m].rhs, len, d_norm + m, ws);
+        FNLH_CUDA(cudaMemcpyAsync(sys[m].r, sys[m].rhs, len * sizeof(S), cudaMemcpyDeviceToDevice, ws.stream));
+    }
+    FNLH_CUDA(cudaMemcpyAsync(ws.h_scalars, d_norm, P * sizeof(double), cudaMemcpyDeviceToHost, ws.stream));
+    FNLH_CUDA(cudaStreamSynchronize(ws.stream));
+    int live = 0;
+    for (int m = 0; m < P; ++m) {
+        reps[m] = LaneReport{};
+        reps[m].rep.initial_residual = std::sqrt(ws.h_scalars[m]);
+        reps[m].rep.final_residual = reps[m].rep.initial_residual;
+        target[m] = tol_rel * reps[m].rep.initial_residual;
+        if (reps[m].rep.initial_residual == 0.0)
+            reps[m].rep.converged = 1;
+        else
+            h_active[m] = 1, ++live;
+    }
+    LaLanes<cplx> Tc{};
+    LaLanes<double> Td{};
+    if constexpr (sizeof(S) == sizeof(cplx)) Tc = T; else Td = T;
+    for (int it = 1; it <= max_iter && live; ++it) {
+        FNLH_CUDA(cudaMemcpyAsync(d_active, h_active, P * sizeof(int), cudaMemcpyHostToDevice, ws.stream));
+        FNLH_DISPATCH_B(p.b, {
+            for (int l = 0; l < p.fwd_levels(); ++l) {
+                const int n = p.fwd_ptr[l + 1] - p.fwd_ptr[l];
+                { ::fnlh::note_launch(); k_ilu_fwd_b<B, S><<<nblocks(n) * P, kThreads, 0, ws.stream>>>(pd, p.fwd_rows + p.fwd_ptr[l], n, T); }
+            }
+            for (int l = 0; l < p.bwd_levels(); ++l) {
+                const int n = p.bwd_ptr[l + 1] - p.bwd_ptr[l];
+                { ::fnlh::note_launch(); k_ilu_bwd_b<B, S><<<nblocks(n) * P, kThreads, 0, ws.stream>>>(pd, p.bwd_rows + p.bwd_ptr[l], n, T); }
+            }
+            { ::fnlh::note_launch(); k_matvec_b<B, S><<<grid * P, kThreads, 0, ws.stream>>>(pd, A_real, T); }
+        });
+        { ::fnlh::note_launch(); k_finish_b<<<P, 256, 0, ws.stream>>>(Tc, Td, sizeof(S) == sizeof(cplx) ? 1 : 0, grid, d_norm); }
+        FNLH_CUDA(cudaGetLastError());
+        FNLH_CUDA(cudaMemcpyAsync(ws.h_scalars, d_norm, P * sizeof(double), cudaMemcpyDeviceToHost, ws.stream));
+        FNLH_CUDA(cudaStreamSynchronize(ws.stream));
+        for (int m = 0; m < P; ++m) {
+            if (!h_active[m]) continue;
+            LinearSolveReport& rp = reps[m].rep;
+            rp.iterations = it;
+            rp.final_residual = std::sqrt(ws.h_scalars[m]);
+            if (!std::isfinite(rp.final_residual)) {
+                reps[m].diverged = 1;
+                h_active[m] = 0, --live;
+            } else if (rp.final_residual <= target[m]) {
+                rp.converged = 1;
+                h_active[m] = 0, --live;
+            }
+        }
+    }
+}
+
 template <class S>
 void block_diag_solve(int b, int n, const S* lu, const int* piv, const S* rhs, S* x, cudaStream_t st) {
     FNLH_DISPATCH_B(b, { { ::fnlh::note_launch(); k_block_diag_solve<B, S><<<nblocks(n), kThreads, 0, st>>>(n, lu, piv, rhs, x); } });
@@ -635,6 +880,8 @@ void block_diag_factor(int b, int n, S* blocks, int* piv, int* status, cudaStrea
     template LinearSolveReport smoothed_solve<S>(const SystemView<S>&, const S*, const DeviceIlu<S>&,      \
                                                  double, int, S*, Workspace&);                             \
     template void block_diag_solve<S>(int, int, const S*, const int*, const S*, S*, cudaStream_t);         \
+    template void smoothed_solve_batch<S>(const DevicePattern&, const double*, const LaneSystem<S>*, int, double,  \
+                                          int, LaneReport*, Workspace&);                                          \
     template void block_diag_factor<S>(int, int, S*, int*, int*, cudaStream_t);
 
 FNLH_INST(double)

@@ -82,6 +82,27 @@ struct Workspace {
     Workspace& operator=(const Workspace&) = delete;
 };
 
+// one system of a batched level-scheduled solve (harmonic lanes on the general path)
+constexpr int kMaxLanes = 8;
+template <class S>
+struct LaneSystem {
+    const DeviceIlu<S>* f;
+    const double* shift;  // Im of the per-node diagonal shift (complex systems), or nullptr
+    const S* rhs;
+    S* x;
+    S* z;
+    S* r;
+};
+struct LaneReport {
+    LinearSolveReport rep;
+    int diverged = 0;  // a non-finite residual norm (DivergenceError at rep.iterations)
+};
+// P smoothed_solves on systems sharing the real A (A_real, the pattern's BSR layout) with
+// per-lane shifts and factors; host stopping rule per lane after each sweep
+template <class S>
+void smoothed_solve_batch(const DevicePattern& p, const double* A_real, const LaneSystem<S>* sys, int P,
+                          double tol_rel, int max_iter, LaneReport* reps, Workspace& ws);
+
 // status codes (mirror core.hpp:22-56)
 enum Status : int { kOk = 0, kConfig = 1, kState = 2, kShape = 3, kUnsupported = 4, kFactorization = 5,
                     kDivergence = 6, kCuda = 7 };

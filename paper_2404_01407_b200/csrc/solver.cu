@@ -123,17 +123,22 @@ DeviceSolver::DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int
     fac_status_.alloc(2);
     if (sch_.workers < 1) throw ConfigError("workers must be >= 1");
     const int P = std::min(std::min(sch_.workers, nh_), kMaxBatch);
-    if (sch_.implicit && rbA_ && P >= 2) {  // harmonics in flight: one workspace per lane
+    if (sch_.implicit && P >= 2) {  // harmonics in flight: one workspace per lane
         rb_h_.reset();
+        ilu_h_.reset();
         for (int m = 0; m < P; ++m) {
             auto ln = std::make_unique<HarmonicLane>();
-            ln->f = std::make_unique<RbIlu<cplx>>(pat_.get(), rbA_->n0());
+            if (rbA_) {
+                ln->f = std::make_unique<RbIlu<cplx>>(pat_.get(), rbA_->n0());
+                ln->parts.alloc(rbA_->partials_len());
+            } else {
+                ln->gf = std::make_unique<DeviceIlu<cplx>>(pat_.get());
+            }
             ln->shift.alloc(mesh.n);
             for (auto& v : ln->v) v.alloc(len);
             ln->ctl.alloc(5);
             ln->err.alloc(10);
             ln->fac.alloc(2);
-            ln->parts.alloc(rbA_->partials_len());
             ln->norm.alloc(1);
             lanes_.push_back(std::move(ln));
         }
@@ -157,15 +162,20 @@ std::size_t DeviceSolver::lhs_bytes() const {
             s += rb_h_->bytes();
         else
             for (const auto& ln : lanes_) s += ln->f->bytes();
+    } else if (sch_.implicit) {
+        s = A5_.bytes() + ilu_mean_->bytes();
+        if (lanes_.empty())
+            s += ilu_h_->bytes();
+        else
+            for (const auto& ln : lanes_) s += ln->gf->bytes();
     }
-    else if (sch_.implicit) s = A5_.bytes() + ilu_mean_->bytes() + ilu_h_->bytes();
     else s = P_.bytes() + PLU_.bytes() + pclu_.bytes();
     return s;
 }
 
 void DeviceSolver::check_step(const unsigned long long* errs, const RbControl* ctls,
                               const LinearSolveReport* host_rep, const bool* have_host, const std::string& field,
-                              RkStepResult& res) {
+                              RkStepResult& res, const int* host_div) {
     for (int k = 1; k <= 5; ++k) {
         const unsigned long long ee = errs[k - 1], ea = errs[5 + k - 1];
         if (ee != ~0ull) {
@@ -178,6 +188,8 @@ void DeviceSolver::check_step(const unsigned long long* errs, const RbControl* c
             LinearSolveReport rep;
             if (have_host && have_host[k - 1]) {
                 rep = host_rep[k - 1];
+                if (host_div && host_div[k - 1])
+                    throw DivergenceError("non-finite iterate in smoothed_solve", rep.iterations, "linear");
             } else {
                 const RbControl& c = ctls[k - 1];
                 if (c.status == 6) throw DivergenceError("non-finite iterate in smoothed_solve", c.iterations, "linear");
@@ -291,12 +303,28 @@ void DeviceSolver::harmonic_batch(const int* hs, int P, std::vector<double>& h_n
     const std::size_t len = disc_->len();
     const double gamma = disc_->view().gamma;
     const double ga5 = (1.0 / sch_.eps_relax) * kAlpha[4];
+    std::vector<std::exception_ptr> early(P);  // level-scheduled path: factorization errors
+    LaneReport lrep[kMaxBatch][5];
+    int ldiv[kMaxBatch][5] = {};
+    LinearSolveReport hrep[kMaxBatch][5];
     for (int m = 0; m < P; ++m) {  // build_lhs_harmonic + factorize per lane (driver.cpp:213-216)
         HarmonicLane& ln = *lanes_[m];
         const int h = hs[m];
         const cplx* amp = amps_.ptr + (std::size_t)h * len;
         harmonic_shift(disc_->view().vol, n, omega_[h], ga5, ln.shift.ptr, st);
-        rb_factorize_async<cplx>(*rbA_, ln.shift.ptr, *ln.f, ln.fac.ptr, st);
+        if (rbA_) {
+            rb_factorize_async<cplx>(*rbA_, ln.shift.ptr, *ln.f, ln.fac.ptr, st);
+        } else {
+            SystemView<cplx> Ah;
+            Ah.p = pat_.get();
+            Ah.real_vals = A5_.ptr;
+            Ah.shift_im = ln.shift.ptr;
+            try {
+                ilu_factorize<cplx>(Ah, *ln.gf, *ws_);
+            } catch (...) {  // this lane's worker fails here (driver.cpp:215-216)
+                early[m] = std::current_exception();
+            }
+        }
         FNLH_CUDA(cudaMemcpyAsync(ln.v[0].ptr, amp, len * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
         FNLH_CUDA(cudaMemcpyAsync(ln.v[6].ptr, amp, len * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
         FNLH_CUDA(cudaMemsetAsync(ln.v[2].ptr, 0, len * sizeof(cplx), st));
@@ -308,6 +336,7 @@ void DeviceSolver::harmonic_batch(const int* hs, int P, std::vector<double>& h_n
         const double beta = kBeta[k - 1];
         const bool fresh = beta != 0.0;
         for (int m = 0; m < P; ++m) {
+            if (early[m]) continue;
             HarmonicLane& ln = *lanes_[m];
             const int h = hs[m];
             disc_->redirect_err(ln.err.ptr + (k - 1));
@@ -318,11 +347,32 @@ void DeviceSolver::harmonic_batch(const int* hs, int P, std::vector<double>& h_n
             stage_rhs<cplx>(ln.v[1].ptr, ln.v[3].ptr, ln.v[4].ptr, len, st);
             if (k == 1) norm2_sq<cplx>(ln.v[4].ptr, len, ln.norm.ptr, *ws_);
             scale<cplx>(ln.v[4].ptr, kAlpha[k - 1], len, st);
-            mem[m] = RbMember<cplx>{ln.f.get(), ln.shift.ptr, ln.v[4].ptr, ln.v[5].ptr,
-                                    ln.v[7].ptr, ln.v[8].ptr, ln.ctl.ptr + (k - 1), ln.parts.ptr};
+            if (rbA_)
+                mem[m] = RbMember<cplx>{ln.f.get(), ln.shift.ptr, ln.v[4].ptr, ln.v[5].ptr,
+                                        ln.v[7].ptr, ln.v[8].ptr, ln.ctl.ptr + (k - 1), ln.parts.ptr};
         }
-        rb_smoothed_solve_batch<cplx>(*rbA_, mem, P, sch_.linear_tol, sch_.linear_max_iter, st);
+        if (rbA_) {
+            rb_smoothed_solve_batch<cplx>(*rbA_, mem, P, sch_.linear_tol, sch_.linear_max_iter, st);
+        } else {  // level-scheduled lanes: one launch per level for every live lane
+            LaneSystem<cplx> sys[kMaxBatch];
+            LaneReport out[kMaxBatch];
+            int live[kMaxBatch], nl = 0;
+            for (int m = 0; m < P; ++m)
+                if (!early[m]) {
+                    HarmonicLane& ln = *lanes_[m];
+                    sys[nl] = LaneSystem<cplx>{ln.gf.get(), ln.shift.ptr, ln.v[4].ptr, ln.v[5].ptr, ln.v[7].ptr,
+                                               ln.v[8].ptr};
+                    live[nl++] = m;
+                }
+            if (nl) smoothed_solve_batch<cplx>(*pat_, A5_.ptr, sys, nl, sch_.linear_tol, sch_.linear_max_iter, out, *ws_);
+            for (int q = 0; q < nl; ++q) {
+                lrep[live[q]][k - 1] = out[q];
+                hrep[live[q]][k - 1] = out[q].rep;
+                ldiv[live[q]][k - 1] = out[q].diverged;
+            }
+        }
         for (int m = 0; m < P; ++m) {
+            if (early[m]) continue;
             HarmonicLane& ln = *lanes_[m];
             disc_->redirect_err(ln.err.ptr + 5 + (k - 1));
             apply_harmonic(b, n, gamma, mean_.ptr, ln.v[0].ptr, ln.v[5].ptr, ln.v[6].ptr, st);
@@ -347,11 +397,18 @@ void DeviceSolver::harmonic_batch(const int* hs, int P, std::vector<double>& h_n
     FNLH_CUDA(cudaStreamSynchronize(st));
     for (int m = 0; m < P; ++m) {  // each lane as its own worker: commit or capture (driver.cpp:248-262)
         const int h = hs[m];
+        if (early[m]) {
+            herr[h] = early[m];
+            continue;
+        }
         try {
-            if (rec[m].fac[1] != 0x7fffffff) throw FactorizationError("near-singular ILU pivot block", rec[m].fac[1]);
+            if (rbA_ && rec[m].fac[1] != 0x7fffffff)
+                throw FactorizationError("near-singular ILU pivot block", rec[m].fac[1]);
             RkStepResult res;
             res.stage1_residual_norm = std::sqrt(rec[m].norm);
-            check_step(rec[m].errs, rec[m].ctls, nullptr, nullptr, "harmonic-" + std::to_string(index_[h]), res);
+            const bool all[5] = {true, true, true, true, true};
+            check_step(rec[m].errs, rec[m].ctls, rbA_ ? nullptr : hrep[m], rbA_ ? nullptr : all,
+                       "harmonic-" + std::to_string(index_[h]), res, rbA_ ? nullptr : ldiv[m]);
             FNLH_CUDA(cudaMemcpyAsync(amps_.ptr + (std::size_t)h * len, lanes_[m]->v[6].ptr, len * sizeof(cplx),
                                       cudaMemcpyDeviceToDevice, st));
             h_norm[h] = res.stage1_residual_norm;
@@ -572,11 +629,12 @@ double DeviceSolver::time_harmonic_sweeps(int h, int nsweeps) {
     Ah.real_vals = A5_.ptr;
     Ah.shift_im = shift_.ptr;
     RbIlu<cplx>* fh = rb_h_ ? rb_h_.get() : (lanes_.empty() ? nullptr : lanes_[0]->f.get());
+    DeviceIlu<cplx>* gh = ilu_h_ ? ilu_h_.get() : (lanes_.empty() ? nullptr : lanes_[0]->gf.get());
     if (rbA_) {
         rbA_->load(A5_.ptr, st);
         rb_factorize<cplx>(*rbA_, shift_.ptr, *fh, *ws_);
     } else {
-        ilu_factorize<cplx>(Ah, *ilu_h_, *ws_);
+        ilu_factorize<cplx>(Ah, *gh, *ws_);
     }
     // rhs: the harmonic's current linearized residual direction (any nonzero vector works)
     cplx* rhs = rk_[4].ptr;
@@ -589,7 +647,7 @@ double DeviceSolver::time_harmonic_sweeps(int h, int nsweeps) {
         rb_smoothed_solve<cplx>(*rbA_, shift_.ptr, *fh, rhs, 1e-300, nsweeps, x, rb_z_.ptr, rb_r_.ptr, ctl_.ptr,
                                 *ws_);
     else
-        smoothed_solve<cplx>(Ah, rhs, *ilu_h_, 1e-300, nsweeps, x, *ws_);
+        smoothed_solve<cplx>(Ah, rhs, *gh, 1e-300, nsweeps, x, *ws_);
     FNLH_CUDA(cudaEventRecord(ev1_, st));
     FNLH_CUDA(cudaEventSynchronize(ev1_));
     float ms = 0.0f;
@@ -599,7 +657,7 @@ double DeviceSolver::time_harmonic_sweeps(int h, int nsweeps) {
 
 double DeviceSolver::time_harmonic_sweeps_batch(int P, int nsweeps) {
     if (lanes_.empty() || P < 1 || P > (int)lanes_.size() || P > nh_)
-        throw ConfigError("time_harmonic_sweeps_batch: needs workers >= P lanes on the 2-colour path");
+        throw ConfigError("time_harmonic_sweeps_batch: needs workers >= P harmonic lanes");
     cudaStream_t st = ws_->stream;
     const int n = disc_->n(), b = disc_->b();
     const std::size_t len = disc_->len();
@@ -607,21 +665,38 @@ double DeviceSolver::time_harmonic_sweeps_batch(int P, int nsweeps) {
     disc_->fd_jacobian(mean_.ptr, A5_.ptr, nullptr, st);
     build_lhs_mean_device(A5_.ptr, A5_.ptr, b, n, pat_->row_ptr, pat_->diag_idx, 1, ga5, 1.0 / (sch_.eps_relax * sigma_),
                           st);
-    rbA_->load(A5_.ptr, st);
+    if (rbA_) rbA_->load(A5_.ptr, st);
     RbMember<cplx> mem[kMaxBatch];
+    LaneSystem<cplx> sys[kMaxBatch];
     for (int m = 0; m < P; ++m) {
         HarmonicLane& ln = *lanes_[m];
         harmonic_shift(disc_->view().vol, n, omega_[m], ga5, ln.shift.ptr, st);
-        rb_factorize<cplx>(*rbA_, ln.shift.ptr, *ln.f, *ws_);
+        if (rbA_) {
+            rb_factorize<cplx>(*rbA_, ln.shift.ptr, *ln.f, *ws_);
+        } else {
+            SystemView<cplx> Ah;
+            Ah.p = pat_.get();
+            Ah.real_vals = A5_.ptr;
+            Ah.shift_im = ln.shift.ptr;
+            ilu_factorize<cplx>(Ah, *ln.gf, *ws_);
+        }
         disc_->linearized_residual(mean_.ptr, amps_.ptr + (std::size_t)m * len, omega_[m],
                                    forcing_.ptr + (std::size_t)m * nforcing_, nforcing_, 2, false, ln.v[4].ptr, nullptr,
                                    st);
-        mem[m] = RbMember<cplx>{ln.f.get(), ln.shift.ptr, ln.v[4].ptr, ln.v[5].ptr, ln.v[7].ptr, ln.v[8].ptr,
-                                ln.ctl.ptr, ln.parts.ptr};
+        if (rbA_)
+            mem[m] = RbMember<cplx>{ln.f.get(), ln.shift.ptr, ln.v[4].ptr, ln.v[5].ptr, ln.v[7].ptr, ln.v[8].ptr,
+                                    ln.ctl.ptr, ln.parts.ptr};
+        else
+            sys[m] = LaneSystem<cplx>{ln.gf.get(), ln.shift.ptr, ln.v[4].ptr, ln.v[5].ptr, ln.v[7].ptr, ln.v[8].ptr};
     }
     FNLH_CUDA(cudaStreamSynchronize(st));
     FNLH_CUDA(cudaEventRecord(ev0_, st));
-    rb_smoothed_solve_batch<cplx>(*rbA_, mem, P, 1e-300, nsweeps, st);
+    if (rbA_) {
+        rb_smoothed_solve_batch<cplx>(*rbA_, mem, P, 1e-300, nsweeps, st);
+    } else {
+        LaneReport out[kMaxBatch];
+        smoothed_solve_batch<cplx>(*pat_, A5_.ptr, sys, P, 1e-300, nsweeps, out, *ws_);
+    }
     FNLH_CUDA(cudaEventRecord(ev1_, st));
     FNLH_CUDA(cudaEventSynchronize(ev1_));
     float ms = 0.0f;

@@ -30,7 +30,8 @@ struct SchemeConfig {  // driver.hpp:22-42
 // its complex ILU workspace, shift and RK vectors; the batched sweep serves up to
 // kMaxBatch lanes from one read of the shared A5
 struct HarmonicLane {
-    std::unique_ptr<RbIlu<cplx>> f;
+    std::unique_ptr<RbIlu<cplx>> f;           // 2-colour path
+    std::unique_ptr<DeviceIlu<cplx>> gf;      // level-scheduled path
     DeviceBuffer<double> shift;
     DeviceBuffer<cplx> v[9];  // state0, inv, vis_fresh, vis_blend, rhs, x, stage, z, r
     DeviceBuffer<RbControl> ctl;             // one per RK stage
@@ -112,7 +113,8 @@ private:
     void rb_solve_async(const double* shift, const RbIlu<S>& f, const S* rhs, S* x, RbControl* ctl);
     // device records of one RK step -> the reference's exceptions (stage order) + reports
     void check_step(const unsigned long long* errs, const RbControl* ctls, const LinearSolveReport* host_rep,
-                    const bool* have_host, const std::string& field, RkStepResult& res);
+                    const bool* have_host, const std::string& field, RkStepResult& res,
+                    const int* host_div = nullptr);
     // rk_step of harmonics hs[0..P) interleaved stage by stage, one batched sweep per stage
     void harmonic_batch(const int* hs, int P, std::vector<double>& h_norm,
                         std::vector<std::vector<LinearSolveReport>>& h_reps, std::vector<std::exception_ptr>& herr);
