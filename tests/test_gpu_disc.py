@@ -134,9 +134,10 @@ def test_workers_batched_harmonics(name, scale, nh):
         assert FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0).lhs_bytes() == b3
 
 
-def test_explicit_mode(orc_dev):
+@pytest.mark.parametrize("workers", [1, 3])
+def test_explicit_mode(orc_dev, workers):
     from paper_2404_01407_b200.solver import FnlhSolver
-    c = make_case("c5", scale=0.06, implicit=False)
+    c = make_case("c5", scale=0.06, implicit=False, workers=workers)
     g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
     o = orc_dev.solver(c.mesh, c.mesh.pattern(), c.scheme, c.omegas, c.forcing, c.mean0)
     for it in range(4):
