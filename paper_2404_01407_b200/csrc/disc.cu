@@ -182,6 +182,32 @@ __global__ void k_qscale_finish(const unsigned long long* umax, double* qscale) 
 }
 
 template <int B>
+__device__ __forceinline__ void fd_face_flux_int(const MeshDev& m, int f, int j, const double* wj,
+                                                 const double* __restrict__ W, double* out) {
+    const int a = m.fa[f], c = m.fb[f];
+    double wo[B];
+    if (a == j) {
+        load_vec<B>(W + (size_t)c * B, wo);
+        interior_face_flux<B>(m, f, wj, wo, 1, 0.0, 0.0, false, nullptr, nullptr, out);
+        if (B == 6) {
+            double vf[B];
+            viscous_face_flux<B>(m, f, wj, wo, m.mu[a], m.mu[c], vf);
+#pragma unroll
+            for (int k = 0; k < B; ++k) out[k] += vf[k];
+        }
+    } else {
+        load_vec<B>(W + (size_t)a * B, wo);
+        interior_face_flux<B>(m, f, wo, wj, 1, 0.0, 0.0, false, nullptr, nullptr, out);
+        if (B == 6) {
+            double vf[B];
+            viscous_face_flux<B>(m, f, wo, wj, m.mu[a], m.mu[c], vf);
+#pragma unroll
+            for (int k = 0; k < B; ++k) out[k] += vf[k];
+        }
+    }
+}
+
+template <int B>
 __device__ __forceinline__ int fd_face_flux(const MeshDev& m, int f, int j, const double* wj,
                                             const double* __restrict__ W, double* out) {
     if (m.fbc[f] >= 0) return boundary_face_flux<B>(m, f, wj, nullptr, 0, nullptr, 0, out);
@@ -209,15 +235,22 @@ __device__ __forceinline__ int fd_face_flux(const MeshDev& m, int f, int j, cons
     return 0;
 }
 
-template <int B>
+// PART 0: every face of node j.  When the boundary faces are the tail of the face list
+// (nf_int >= 0) the work is split so the common case carries no boundary-state code:
+// PART 1 walks the interior faces of every node (they come first in ascending face order)
+// and finishes the nodes without boundary faces; PART 2 runs on the boundary nodes only
+// (`bnodes`) and continues the same accumulation over their boundary faces from the
+// partial sums PART 1 left in `dpart`.  Every diagonal entry sees the same sequence.
+template <int B, int PART>
 __global__ void __launch_bounds__(kT) k_fd_jacobian(MeshDev m, const int* __restrict__ diag_idx,
                                                     const int* __restrict__ e_ab, const int* __restrict__ e_ba,
                                                     const double* __restrict__ W, const double* __restrict__ qscale,
                                                     double* __restrict__ J, double* __restrict__ P,
-                                                    unsigned long long* err) {
+                                                    unsigned long long* err, const int* __restrict__ bnodes, int nb_nodes,
+                                                    double* __restrict__ dpart) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= m.n * B) return;
-    const int j = t / B, mm = t % B;
+    if (t >= (PART == 2 ? nb_nodes : m.n) * B) return;
+    const int j = PART == 2 ? bnodes[t / B] : t / B, mm = t % B;
     const double g = m.gamma;
     double qj[B], wp[B], wm[B];
     prim_to_cons<B>(W + (size_t)j * B, g, qj);
@@ -241,13 +274,31 @@ __global__ void __launch_bounds__(kT) k_fd_jacobian(MeshDev m, const int* __rest
     }
     const double inv2d = 1.0 / (2.0 * delta);
     double dacc[B];
+    int e = m.nf_ptr[j];
+    if (PART == 2) {
 #pragma unroll
-    for (int r = 0; r < B; ++r) dacc[r] = 0.0;
-    for (int e = m.nf_ptr[j]; e < m.nf_ptr[j + 1]; ++e) {
+        for (int r = 0; r < B; ++r) dacc[r] = dpart[(size_t)j * B * B + r * B + mm];
+        while (e < m.nf_ptr[j + 1] && m.fbc[m.nf_idx[e]] < 0) ++e;  // PART 1 did these
+    } else {
+#pragma unroll
+        for (int r = 0; r < B; ++r) dacc[r] = 0.0;
+    }
+    for (; e < m.nf_ptr[j + 1]; ++e) {
         const int f = m.nf_idx[e];
+        if (PART == 1 && m.fbc[f] >= 0) {  // the rest are boundary faces: PART 2 continues
+#pragma unroll
+            for (int r = 0; r < B; ++r) dpart[(size_t)j * B * B + r * B + mm] = dacc[r];
+            return;
+        }
         double fp[B], fm[B];
-        st = fd_face_flux<B>(m, f, j, wp, W, fp);
-        if (!st) st = fd_face_flux<B>(m, f, j, wm, W, fm);
+        if (PART == 1) {
+            fd_face_flux_int<B>(m, f, j, wp, W, fp);
+            fd_face_flux_int<B>(m, f, j, wm, W, fm);
+            st = 0;
+        } else {
+            st = fd_face_flux<B>(m, f, j, wp, W, fp);
+            if (!st) st = fd_face_flux<B>(m, f, j, wm, W, fm);
+        }
         if (st) {
             record(err, key, st);
             return;
@@ -609,6 +660,27 @@ DeviceDisc::DeviceDisc(const MeshArrays& m, const DevicePattern* pattern) : pat_
     mu_.upload(m.mu, n);
     nf_ptr_.upload(m.nf_ptr, n + 1);
     nf_idx_.upload(m.nf_idx, m.nf_ptr[n]);
+    {  // boundary faces as the tail of the face list -> the split FD Jacobian
+        int first_b = nfc;
+        for (int f = 0; f < nfc; ++f)
+            if (m.fbc[f] >= 0) {
+                first_b = f;
+                break;
+            }
+        bool tail = true;
+        for (int f = first_b; f < nfc && tail; ++f) tail = m.fbc[f] >= 0;
+        nf_int_ = tail ? first_b : -1;
+        std::vector<int> bn;
+        for (int i = 0; i < n; ++i)
+            for (int e = m.nf_ptr[i]; e < m.nf_ptr[i + 1]; ++e)
+                if (m.fbc[m.nf_idx[e]] >= 0) {
+                    bn.push_back(i);
+                    break;
+                }
+        nbn_ = static_cast<int>(bn.size());
+        if (nbn_) bnodes_.upload(bn.data(), bn.size());
+        if (nf_int_ >= 0) fdpart_.alloc((std::size_t)n * m.b * m.b);
+    }
     bflag_.upload(m.bflag, n);
     {
         std::vector<int> code(m.nf_ptr[n]);
@@ -704,8 +776,16 @@ void DeviceDisc::fd_jacobian(const double* W, double* J, double* P, cudaStream_t
         { ::fnlh::note_launch(); k_umax_init<<<1, 32, 0, st>>>(umax_.ptr, B); }
         { ::fnlh::note_launch(); k_qscale<B><<<std::min(nb(m.n), 592), kT, 0, st>>>(m.n, m.gamma, W, umax_.ptr); }
         { ::fnlh::note_launch(); k_qscale_finish<B><<<1, 32, 0, st>>>(umax_.ptr, qscale_.ptr); }
-        { ::fnlh::note_launch(); k_fd_jacobian<B><<<nb((long long)m.n * B), kT, 0, st>>>(m, pat_->diag_idx, e_ab_.ptr, e_ba_.ptr, W,
-                                                                qscale_.ptr, J, P, err_.ptr); }
+        if (nf_int_ >= 0) {
+            { ::fnlh::note_launch(); k_fd_jacobian<B, 1><<<nb((long long)m.n * B), kT, 0, st>>>(m, pat_->diag_idx, e_ab_.ptr, e_ba_.ptr, W,
+                                                                       qscale_.ptr, J, P, err_.ptr, nullptr, 0, fdpart_.ptr); }
+            if (nbn_ > 0) { ::fnlh::note_launch(); k_fd_jacobian<B, 2><<<nb((long long)nbn_ * B), kT, 0, st>>>(m, pat_->diag_idx, e_ab_.ptr, e_ba_.ptr, W,
+                                                                                    qscale_.ptr, J, P, err_.ptr, bnodes_.ptr, nbn_,
+                                                                                    fdpart_.ptr); }
+        } else {
+            { ::fnlh::note_launch(); k_fd_jacobian<B, 0><<<nb((long long)m.n * B), kT, 0, st>>>(m, pat_->diag_idx, e_ab_.ptr, e_ba_.ptr, W,
+                                                                       qscale_.ptr, J, P, err_.ptr, nullptr, 0, nullptr); }
+        }
     });
     FNLH_CUDA(cudaGetLastError());
     raise_if_err(st, "fd_jacobian");

@@ -66,6 +66,10 @@ private:
     DeviceBuffer<double> nu_, lap_, flux_, vflux_, qscale_, scal_;
     DeviceBuffer<unsigned long long> err_;
     unsigned long long* cur_err_ = nullptr;
+    int nf_int_ = -1;              // boundary faces are the tail [nf_int_, nf) (else -1)
+    int nbn_ = 0;                  // nodes with boundary faces
+    DeviceBuffer<int> bnodes_;
+    DeviceBuffer<double> fdpart_;  // FD Jacobian diagonal partial sums (split kernels)
     DeviceBuffer<unsigned long long> umax_;
     DeviceBuffer<double> fwork_;  // forcing perturbation vectors
     DeviceBuffer<int> df_flag_;   // any nonzero amplitude (residual_ops.cpp:133-141)
