@@ -280,9 +280,12 @@ def main():
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        s.set_state(mean_h, amps_h)
-        stepper.outer_iteration()
-        mean_h, amps_h = s.state(out=(mean_h, amps_h))
+        if shard:
+            s.set_state(mean_h, amps_h)
+            stepper.outer_iteration()
+            mean_h, amps_h = s.state(out=(mean_h, amps_h))
+        else:  # one call on host buffers, transfers overlapped with the step
+            s.outer_iteration_host(mean_h, amps_h)
     barrier()
     e2e_s = time.perf_counter() - t0
     rows_e2e = s.counters()["row_updates"] - cnt2["row_updates"]

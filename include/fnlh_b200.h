@@ -159,6 +159,12 @@ int fnlh_solver_create(const fnlh_mesh_desc* m, const int* row_ptr, const int* c
 void fnlh_solver_destroy(fnlh_solver* s);
 /* FnlhSolver::outer_iteration (driver.cpp:157-333) */
 int fnlh_solver_outer_iteration(fnlh_solver* s, fnlh_entry* e, double* resid_h);
+/* the same on host buffers: set_state(mean_in, amps_in) + outer_iteration + get_state into
+   (mean_out, amps_out), with the transfers overlapped with the step (the harmonic fields
+   go up while the Jacobian is assembled and come back while DF and the mean step run);
+   in and out may alias; pinned host buffers give asynchronous copies */
+int fnlh_solver_outer_iteration_host(fnlh_solver* s, const double* mean_in, const double* amps_in, double* mean_out,
+                                     double* amps_out, fnlh_entry* e, double* resid_h);
 /* outer_iteration in two halves, for harmonic sharding across GPUs (the
    reference's harmonic workers, driver.cpp:246-265, one rank per GPU):
    phase_harmonics: transform/FD Jacobian/A5/mean ILU, then the RK steps of the harmonics

@@ -168,6 +168,17 @@ int fnlh_solver_outer_iteration(fnlh_solver* s, fnlh_entry* e, double* resid_h) 
     });
 }
 
+int fnlh_solver_outer_iteration_host(fnlh_solver* s, const double* mean_in, const double* amps_in, double* mean_out,
+                                     double* amps_out, fnlh_entry* e, double* resid_h) {
+    return guarded([&] {
+        ConvergenceEntry c = s->s->outer_iteration_host(mean_in, reinterpret_cast<const cplx*>(amps_in), mean_out,
+                                                        reinterpret_cast<cplx*>(amps_out));
+        *e = fnlh_entry{c.iter, c.resid_mean, c.rz, c.has_rz, c.seconds};
+        if (resid_h)
+            for (std::size_t k = 0; k < c.resid_h.size(); ++k) resid_h[k] = c.resid_h[k];
+    });
+}
+
 int fnlh_solver_phase_harmonics(fnlh_solver* s, const int* owned, double* h_norm) {
     return guarded([&] {
         s->s->phase_harmonics(owned);

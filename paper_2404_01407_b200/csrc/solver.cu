@@ -146,12 +146,18 @@ DeviceSolver::DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int
     FNLH_CUDA(cudaEventCreate(&ev0_));
     FNLH_CUDA(cudaEventCreate(&ev1_));
     for (auto& e : evp_) FNLH_CUDA(cudaEventCreate(&e));
+    FNLH_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
+    FNLH_CUDA(cudaEventCreateWithFlags(&ev_in_, cudaEventDisableTiming));
+    FNLH_CUDA(cudaEventCreateWithFlags(&ev_h_, cudaEventDisableTiming));
 }
 
 DeviceSolver::~DeviceSolver() {
     cudaEventDestroy(ev0_);
     cudaEventDestroy(ev1_);
     for (auto& e : evp_) cudaEventDestroy(e);
+    cudaEventDestroy(ev_in_);
+    cudaEventDestroy(ev_h_);
+    cudaStreamDestroy(cs_);
 }
 
 std::size_t DeviceSolver::lhs_bytes() const {
@@ -424,6 +430,35 @@ ConvergenceEntry DeviceSolver::outer_iteration() {
     return phase_mean(h_norm_, h_reps_);
 }
 
+ConvergenceEntry DeviceSolver::outer_iteration_host(const double* mean_in, const cplx* amps_in, double* mean_out,
+                                                    cplx* amps_out) {
+    cudaStream_t st = ws_->stream;
+    const std::size_t len = disc_->len();
+    FNLH_CUDA(cudaStreamSynchronize(cs_));
+    FNLH_CUDA(cudaMemcpyAsync(mean_.ptr, mean_in, len * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (nh_) {
+        FNLH_CUDA(cudaMemcpyAsync(amps_.ptr, amps_in, (std::size_t)nh_ * len * sizeof(cplx), cudaMemcpyHostToDevice,
+                                  cs_));
+        FNLH_CUDA(cudaEventRecord(ev_in_, cs_));
+    }
+    struct Reset {
+        DeviceSolver* s;
+        ~Reset() {
+            s->wait_amps_ = false;
+            s->amps_download_ = nullptr;
+            cudaStreamSynchronize(s->cs_);
+        }
+    } reset{this};
+    wait_amps_ = nh_ > 0;
+    amps_download_ = amps_out;
+    phase_harmonics(nullptr);
+    ConvergenceEntry e = phase_mean(h_norm_, h_reps_);
+    FNLH_CUDA(cudaMemcpyAsync(mean_out, mean_.ptr, len * sizeof(double), cudaMemcpyDeviceToHost, st));
+    FNLH_CUDA(cudaStreamSynchronize(st));
+    FNLH_CUDA(cudaStreamSynchronize(cs_));
+    return e;
+}
+
 void DeviceSolver::phase_harmonics(const int* owned) {
     cudaStream_t st = ws_->stream;
     FNLH_CUDA(cudaEventRecord(ev0_, st));
@@ -460,6 +495,7 @@ void DeviceSolver::phase_harmonics(const int* owned) {
     }
 
     FNLH_CUDA(cudaEventRecord(evp_[0], st));  // phase marks: J + A5 + mean ILU done
+    if (wait_amps_) FNLH_CUDA(cudaStreamWaitEvent(st, ev_in_, 0));  // harmonic fields uploaded
     std::vector<double>& h_norm = h_norm_;
     std::vector<std::vector<LinearSolveReport>>& h_reps = h_reps_;
     h_norm.assign(nh_, 0.0);
@@ -529,6 +565,12 @@ void DeviceSolver::phase_harmonics(const int* owned) {
     }
     for (int h = 0; h < nh_; ++h)
         if (herr[h]) std::rethrow_exception(herr[h]);
+    if (amps_download_ && nh_) {  // updated harmonic fields home while DF and the mean step run
+        FNLH_CUDA(cudaEventRecord(ev_h_, st));
+        FNLH_CUDA(cudaStreamWaitEvent(cs_, ev_h_, 0));
+        FNLH_CUDA(cudaMemcpyAsync(amps_download_, amps_.ptr, (std::size_t)nh_ * len * sizeof(cplx),
+                                  cudaMemcpyDeviceToHost, cs_));
+    }
 }
 
 ConvergenceEntry DeviceSolver::phase_mean(const std::vector<double>& h_norm,

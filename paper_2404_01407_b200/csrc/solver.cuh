@@ -63,6 +63,12 @@ public:
     ~DeviceSolver();
 
     ConvergenceEntry outer_iteration();  // phase_harmonics(all) + phase_mean
+    // outer_iteration on host buffers (the reference-facing call): the mean is uploaded
+    // first, the harmonic fields on a copy stream while the Jacobian / A5 / mean ILU run,
+    // and the updated harmonic fields go back on the copy stream while DF and the mean
+    // step run; in/out may alias
+    ConvergenceEntry outer_iteration_host(const double* mean_in, const cplx* amps_in, double* mean_out,
+                                          cplx* amps_out);
     // the two halves of outer_iteration, split where harmonic sharding exchanges the
     // harmonic fields: J, A5, mean ILU and the owned harmonics' RK steps
     // (owned: nh flags, nullptr = all) ...
@@ -147,6 +153,10 @@ private:
     int iter_ = 0;
     double cum_seconds_ = 0.0;
     cudaEvent_t ev0_, ev1_, evp_[3];
+    cudaStream_t cs_ = nullptr;          // copy stream of outer_iteration_host
+    cudaEvent_t ev_in_ = nullptr, ev_h_ = nullptr;
+    bool wait_amps_ = false;             // phase_harmonics waits on ev_in_ before the harmonics
+    cplx* amps_download_ = nullptr;      // host destination of the harmonic fields (or null)
 };
 
 void build_lhs_mean_device(const double* J, double* A, int b, int n, const int* row_ptr, const int* diag_idx,

@@ -134,6 +134,22 @@ class FnlhSolver:
         return dict(iter=e.iter, resid_mean=e.resid_mean, rz=e.rz, has_rz=bool(e.has_rz), resid_h=rh[: self.nh].copy(),
                     seconds=e.seconds)
 
+    def outer_iteration_host(self, mean_in, amps_in, mean_out=None, amps_out=None):
+        """outer_iteration on host buffers (upload, step, download overlapped); the output
+        arrays default to the inputs (in place).  Pinned arrays make the copies async."""
+        mean_out = mean_in if mean_out is None else mean_out
+        amps_out = amps_in if amps_out is None else amps_out
+        for a in (mean_in, amps_in, mean_out, amps_out):
+            assert a.flags.c_contiguous
+        assert mean_in.dtype == np.float64 and amps_in.dtype == np.complex128
+        e = Entry()
+        rh = np.zeros(max(self.nh, 1))
+        check(lib().fnlh_solver_outer_iteration_host(self.h, ptr(mean_in), ptr(amps_in.reshape(-1).view(np.float64)),
+                                                     ptr(mean_out), ptr(amps_out.reshape(-1).view(np.float64)),
+                                                     C.byref(e), ptr(rh)))
+        return dict(iter=e.iter, resid_mean=e.resid_mean, rz=e.rz, has_rz=bool(e.has_rz), resid_h=rh[: self.nh].copy(),
+                    seconds=e.seconds)
+
     # the two halves of outer_iteration (harmonic sharding across GPUs, shard.py)
     def phase_harmonics(self, owned=None):
         hn = np.zeros(max(self.nh, 1))

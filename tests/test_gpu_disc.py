@@ -249,3 +249,27 @@ def test_harmonic_failure_worker_semantics(orc_dev, workers):
         assert np.array_equal(ag[2], amps[2]) and np.array_equal(ao[2], amps[2])  # never ran
     else:
         assert not np.array_equal(ag[2], amps[2]) and np.array_equal(ag[2], ao[2])  # ran and committed
+
+
+def test_outer_iteration_host_buffers():
+    """fnlh_solver_outer_iteration_host (upload / step / download overlapped, in place on
+    pinned host buffers) is bitwise set_state + outer_iteration + get_state."""
+    import torch
+    from paper_2404_01407_b200.solver import FnlhSolver
+    c = make_case("c2", scale=0.08, nh=3, workers=3)
+    a = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
+    b = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
+    a.outer_iteration()
+    mean, amps = a.state()
+    L = c.mesh.n * c.mesh.b
+    mp = torch.empty(L, dtype=torch.float64, pin_memory=True).numpy()
+    ap = torch.empty(3 * L * 2, dtype=torch.float64, pin_memory=True).numpy().view(np.complex128).reshape(3, L)
+    mp[:] = mean
+    ap[:] = amps
+    for _ in range(2):
+        a.set_state(mean, amps)
+        ea = a.outer_iteration()
+        mean, amps = a.state()
+        eb = b.outer_iteration_host(mp, ap)
+        assert ea["resid_mean"] == eb["resid_mean"] and ea["rz"] == eb["rz"]
+        assert np.array_equal(mp, mean) and np.array_equal(ap, amps)
