@@ -710,16 +710,30 @@ DeviceDisc::DeviceDisc(const MeshArrays& m, const DevicePattern* pattern) : pat_
     view_ = MeshDev{n, nfc, m.b, fa_.ptr, fb_.ptr, fbc_.ptr, ford_.ptr, fn_.ptr, farea_.ptr, fnh_.ptr, fvis_.ptr,
                     vol_.ptr, closure_.ptr, mu_.ptr, nf_ptr_.ptr, nf_idx_.ptr, bflag_.ptr, m.gamma, m.gas_constant,
                     m.p0, m.T0, m.p_out, m.nt_in, m.forcing_scale, nf_code_.ptr};
-    nu_.alloc(n);
-    lap_.alloc((std::size_t)n * m.b);
-    flux_.alloc((std::size_t)nfc * m.b);
-    vflux_.alloc((std::size_t)nfc * m.b);
     qscale_.alloc(8);
-    scal_.alloc(16);
+    ensure_contexts(1);
     err_.alloc(1);
     umax_.alloc(64);
-    for (auto& s : scratch_real) s.alloc((std::size_t)n * m.b);
+
     FNLH_CUDA(cudaMemset(err_.ptr, 0xff, sizeof(unsigned long long)));
+}
+
+void DeviceDisc::alloc_scratch(Scratch& c) {
+    const std::size_t n = view_.n, nfc = view_.nf, b = view_.b;
+    c.nu.alloc(n);
+    c.lap.alloc(n * b);
+    c.flux.alloc(nfc * b);
+    c.vflux.alloc(nfc * b);
+    c.scal.alloc(16);
+    c.umax.alloc(64);
+    for (auto& r : c.real) r.alloc(n * b);
+}
+
+void DeviceDisc::ensure_contexts(int k) {
+    while (static_cast<int>(ctx_.size()) < k) {
+        ctx_.push_back(std::make_unique<Scratch>());
+        alloc_scratch(*ctx_.back());
+    }
 }
 
 void DeviceDisc::reset_err(cudaStream_t st) {
@@ -755,10 +769,10 @@ void DeviceDisc::residual(const double* W, const double* wref, int order, int mo
                           const double* skip) {
     const MeshDev& m = view_;
     DISPATCH_B56(m.b, {
-        if (order == 2) { ::fnlh::note_launch(); k_jst_prepass<B><<<nb(m.n), kT, 0, st>>>(m, W, nu_.ptr, lap_.ptr, skip); }
+        if (order == 2) { ::fnlh::note_launch(); k_jst_prepass<B><<<nb(m.n), kT, 0, st>>>(m, W, C().nu.ptr, C().lap.ptr, skip); }
         { ::fnlh::note_launch(); k_face_flux<B><<<nb(m.nf), kT, 0, st>>>(m, W, wref, order, mode, forcing, nforcing, need_vis ? 1 : 0,
-                                                nu_.ptr, lap_.ptr, flux_.ptr, vflux_.ptr, err(), skip); }
-        { ::fnlh::note_launch(); k_node_gather<B><<<nb(m.n), kT, 0, st>>>(m, W, flux_.ptr, vflux_.ptr, need_vis ? 1 : 0, inv, vis, skip); }
+                                                C().nu.ptr, C().lap.ptr, C().flux.ptr, C().vflux.ptr, err(), skip); }
+        { ::fnlh::note_launch(); k_node_gather<B><<<nb(m.n), kT, 0, st>>>(m, W, C().flux.ptr, C().vflux.ptr, need_vis ? 1 : 0, inv, vis, skip); }
     });
     FNLH_CUDA(cudaGetLastError());
 }
@@ -800,21 +814,22 @@ void DeviceDisc::linearized_residual(const double* mean, const cplx* what, doubl
     if (omega < 0.0) throw ConfigError("linearized_residual: negative frequency");
     const MeshDev& m = view_;
     const std::size_t L = len();
-    if (nforcing > 0 && (std::size_t)fwork_.n < 2 * (std::size_t)nforcing) fwork_.alloc(2 * (std::size_t)nforcing);
-    double* wp = scratch_real[0].ptr;
-    double* wm = scratch_real[1].ptr;
-    double* ip = scratch_real[2].ptr;
-    double* vp = scratch_real[3].ptr;
-    double* imn = scratch_real[4].ptr;
-    double* vm = scratch_real[5].ptr;
-    double* fp = nforcing > 0 ? fwork_.ptr : nullptr;
-    double* fm = nforcing > 0 ? fwork_.ptr + nforcing : nullptr;
-    double* delta = scal_.ptr;
+    Scratch& cx = C();
+    if (nforcing > 0 && (std::size_t)cx.fwork.n < 2 * (std::size_t)nforcing) cx.fwork.alloc(2 * (std::size_t)nforcing);
+    double* wp = cx.real[0].ptr;
+    double* wm = cx.real[1].ptr;
+    double* ip = cx.real[2].ptr;
+    double* vp = cx.real[3].ptr;
+    double* imn = cx.real[4].ptr;
+    double* vm = cx.real[5].ptr;
+    double* fp = nforcing > 0 ? cx.fwork.ptr : nullptr;
+    double* fm = nforcing > 0 ? cx.fwork.ptr + nforcing : nullptr;
+    double* delta = cx.scal.ptr;
     const int grid = std::min(nb(m.n), 592);
     DISPATCH_B56(m.b, {
-        { ::fnlh::note_launch(); k_umax_init<<<1, 32, 0, st>>>(umax_.ptr, 3 * B + 2); }
-        { ::fnlh::note_launch(); k_linres_scales<B><<<grid, kT, 0, st>>>(m.n, mean, what, forcing, nforcing, umax_.ptr); }
-        { ::fnlh::note_launch(); k_linres_delta<B><<<1, 32, 0, st>>>(umax_.ptr, m.forcing_scale, delta); }
+        { ::fnlh::note_launch(); k_umax_init<<<1, 32, 0, st>>>(cx.umax.ptr, 3 * B + 2); }
+        { ::fnlh::note_launch(); k_linres_scales<B><<<grid, kT, 0, st>>>(m.n, mean, what, forcing, nforcing, cx.umax.ptr); }
+        { ::fnlh::note_launch(); k_linres_delta<B><<<1, 32, 0, st>>>(cx.umax.ptr, m.forcing_scale, delta); }
     });
     const int gs = nb((long long)std::max<std::size_t>(L, (std::size_t)nforcing));
     for (int part = 0; part < 2; ++part) {
@@ -888,9 +903,9 @@ void DeviceDisc::deterministic_flux(const double* mean, const std::vector<const 
         df_omega_ = omega;
     }
     const cplx* dph = df_ph_.ptr;
-    double* w = scratch_real[0].ptr;
-    double* inv = scratch_real[1].ptr;
-    double* acc = scratch_real[2].ptr;
+    double* w = C().real[0].ptr;
+    double* inv = C().real[1].ptr;
+    double* acc = C().real[2].ptr;
     for (int k = 0; k < nq; ++k) {
         { ::fnlh::note_launch(); k_reconstruct<<<nb((long long)L), kT, 0, st>>>(L, mean, al, nh, dph + (std::size_t)k * nh, w); }
         residual(w, nullptr, 2, 0, nullptr, 0, false, inv, nullptr, st);

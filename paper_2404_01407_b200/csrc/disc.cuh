@@ -5,6 +5,7 @@
 #pragma once
 
 #include <complex>
+#include <memory>
 #include <vector>
 
 #include "capi_util.hpp"
@@ -57,21 +58,33 @@ public:
                             const std::vector<double>& omega, double* df, cudaStream_t st, bool deferred = false);
 
     const int* df_active() const { return df_flag_.ptr; }  // set by the last deterministic_flux
-    DeviceBuffer<double> scratch_real[6];  // linres / DF temporaries (len each)
+    // scratch contexts: the residual / linearized-residual temporaries of context k, so k
+    // independent evaluations can run concurrently on k streams (harmonic lanes)
+    void ensure_contexts(int k);
+    void use_context(int k) { cur_ = k; }
+    int contexts() const { return static_cast<int>(ctx_.size()); }
 private:
+    struct Scratch {
+        DeviceBuffer<double> nu, lap, flux, vflux, scal, fwork;
+        DeviceBuffer<unsigned long long> umax;
+        DeviceBuffer<double> real[6];  // linres / DF temporaries (len each)
+    };
+    std::vector<std::unique_ptr<Scratch>> ctx_;
+    int cur_ = 0;
+    Scratch& C() const { return *ctx_[cur_]; }
+    void alloc_scratch(Scratch& c);
     MeshDev view_{};
     const DevicePattern* pat_;
     DeviceBuffer<int> fa_, fb_, fbc_, ford_, nf_ptr_, nf_idx_, nf_code_, bflag_, e_ab_, e_ba_;
     DeviceBuffer<double> fn_, farea_, fnh_, fvis_, vol_, closure_, mu_;
-    DeviceBuffer<double> nu_, lap_, flux_, vflux_, qscale_, scal_;
+    DeviceBuffer<double> qscale_;
     DeviceBuffer<unsigned long long> err_;
     unsigned long long* cur_err_ = nullptr;
     int nf_int_ = -1;              // boundary faces are the tail [nf_int_, nf) (else -1)
     int nbn_ = 0;                  // nodes with boundary faces
     DeviceBuffer<int> bnodes_;
     DeviceBuffer<double> fdpart_;  // FD Jacobian diagonal partial sums (split kernels)
-    DeviceBuffer<unsigned long long> umax_;
-    DeviceBuffer<double> fwork_;  // forcing perturbation vectors
+    DeviceBuffer<unsigned long long> umax_;  // FD Jacobian scales
     DeviceBuffer<int> df_flag_;   // any nonzero amplitude (residual_ops.cpp:133-141)
     DeviceBuffer<cplx> df_ph_;    // quadrature phases e^{i omega_h t_k}, cached per omega set
     std::vector<double> df_omega_;

@@ -727,6 +727,14 @@ void matvec(const SystemView<S>& A, const S* x, S* y, Workspace& ws) {
 }
 
 template <class S>
+void norm2_sq_on(const S* x, std::size_t len, double* d_out, double* partials, cudaStream_t st) {
+    const int grid = std::min<long long>(nblocks((long long)len), kRedBlocks);
+    { ::fnlh::note_launch(); k_sumsq<S><<<grid, kThreads, 0, st>>>(x, len, partials); }
+    { ::fnlh::note_launch(); k_finish<<<1, 256, 0, st>>>(partials, grid, d_out); }
+    FNLH_CUDA(cudaGetLastError());
+}
+
+template <class S>
 void norm2_sq(const S* x, std::size_t len, double* d_out, Workspace& ws) {
     const int grid = std::min<long long>(nblocks((long long)len), kRedBlocks);
     { ::fnlh::note_launch(); k_sumsq<S><<<grid, kThreads, 0, ws.stream>>>(x, len, ws.partials); }
@@ -877,6 +885,7 @@ void block_diag_factor(int b, int n, S* blocks, int* piv, int* status, cudaStrea
     template void residual_norm<S>(const SystemView<S>&, const S*, const S*, S*, double*, Workspace&);     \
     template void matvec<S>(const SystemView<S>&, const S*, S*, Workspace&);                               \
     template void norm2_sq<S>(const S*, std::size_t, double*, Workspace&);                                 \
+    template void norm2_sq_on<S>(const S*, std::size_t, double*, double*, cudaStream_t);                    \
     template LinearSolveReport smoothed_solve<S>(const SystemView<S>&, const S*, const DeviceIlu<S>&,      \
                                                  double, int, S*, Workspace&);                             \
     template void block_diag_solve<S>(int, int, const S*, const int*, const S*, S*, cudaStream_t);         \

@@ -118,6 +118,9 @@ template <class S>
 void matvec(const SystemView<S>& A, const S* x, S* y, Workspace& ws);
 template <class S>
 void norm2_sq(const S* x, std::size_t len, double* d_out, Workspace& ws);
+// the same on a given stream with caller partials (>= 592 doubles)
+template <class S>
+void norm2_sq_on(const S* x, std::size_t len, double* d_out, double* partials, cudaStream_t st);
 template <class S>
 LinearSolveReport smoothed_solve(const SystemView<S>& A, const S* rhs, const DeviceIlu<S>& f, double tol_rel,
                                  int max_iter, S* x, Workspace& ws);

@@ -140,6 +140,9 @@ DeviceSolver::DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int
             ln->err.alloc(10);
             ln->fac.alloc(2);
             ln->norm.alloc(1);
+            ln->nparts.alloc(1024);
+            FNLH_CUDA(cudaStreamCreateWithFlags(&ln->stream, cudaStreamNonBlocking));
+            FNLH_CUDA(cudaEventCreateWithFlags(&ln->done, cudaEventDisableTiming));
             lanes_.push_back(std::move(ln));
         }
     }
@@ -149,6 +152,8 @@ DeviceSolver::DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int
     FNLH_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
     FNLH_CUDA(cudaEventCreateWithFlags(&ev_in_, cudaEventDisableTiming));
     FNLH_CUDA(cudaEventCreateWithFlags(&ev_h_, cudaEventDisableTiming));
+    FNLH_CUDA(cudaEventCreateWithFlags(&ev_stage_, cudaEventDisableTiming));
+    if (!lanes_.empty()) disc_->ensure_contexts(static_cast<int>(lanes_.size()));
 }
 
 DeviceSolver::~DeviceSolver() {
@@ -157,6 +162,7 @@ DeviceSolver::~DeviceSolver() {
     for (auto& e : evp_) cudaEventDestroy(e);
     cudaEventDestroy(ev_in_);
     cudaEventDestroy(ev_h_);
+    cudaEventDestroy(ev_stage_);
     cudaStreamDestroy(cs_);
 }
 
@@ -341,18 +347,27 @@ void DeviceSolver::harmonic_batch(const int* hs, int P, std::vector<double>& h_n
     for (int k = 1; k <= 5; ++k) {  // rk_step (rk.cpp:41-99), the lanes interleaved stage by stage
         const double beta = kBeta[k - 1];
         const bool fresh = beta != 0.0;
+        // the lanes' stage evaluations are independent: each runs on its own stream with its
+        // own residual scratch (DeviceDisc context m), joined before the batched solve
+        FNLH_CUDA(cudaEventRecord(ev_stage_, st));
         for (int m = 0; m < P; ++m) {
             if (early[m]) continue;
             HarmonicLane& ln = *lanes_[m];
             const int h = hs[m];
+            cudaStream_t sm = ln.stream;
+            FNLH_CUDA(cudaStreamWaitEvent(sm, ev_stage_, 0));
+            disc_->use_context(m);
             disc_->redirect_err(ln.err.ptr + (k - 1));
             disc_->linearized_residual(mean_.ptr, ln.v[6].ptr, omega_[h], forcing_.ptr + (std::size_t)h * nforcing_,
-                                       nforcing_, 2, fresh, ln.v[1].ptr, ln.v[2].ptr, st);
+                                       nforcing_, 2, fresh, ln.v[1].ptr, ln.v[2].ptr, sm);
             disc_->redirect_err(nullptr);
-            if (fresh) stage_blend<cplx>(beta, ln.v[2].ptr, ln.v[3].ptr, len, st);
-            stage_rhs<cplx>(ln.v[1].ptr, ln.v[3].ptr, ln.v[4].ptr, len, st);
-            if (k == 1) norm2_sq<cplx>(ln.v[4].ptr, len, ln.norm.ptr, *ws_);
-            scale<cplx>(ln.v[4].ptr, kAlpha[k - 1], len, st);
+            disc_->use_context(0);
+            if (fresh) stage_blend<cplx>(beta, ln.v[2].ptr, ln.v[3].ptr, len, sm);
+            stage_rhs<cplx>(ln.v[1].ptr, ln.v[3].ptr, ln.v[4].ptr, len, sm);
+            if (k == 1) norm2_sq_on<cplx>(ln.v[4].ptr, len, ln.norm.ptr, ln.nparts.ptr, sm);
+            scale<cplx>(ln.v[4].ptr, kAlpha[k - 1], len, sm);
+            FNLH_CUDA(cudaEventRecord(ln.done, sm));
+            FNLH_CUDA(cudaStreamWaitEvent(st, ln.done, 0));
             if (rbA_)
                 mem[m] = RbMember<cplx>{ln.f.get(), ln.shift.ptr, ln.v[4].ptr, ln.v[5].ptr,
                                         ln.v[7].ptr, ln.v[8].ptr, ln.ctl.ptr + (k - 1), ln.parts.ptr};

@@ -38,6 +38,13 @@ struct HarmonicLane {
     DeviceBuffer<unsigned long long> err;    // [0,5) eval, [5,10) apply
     DeviceBuffer<int> fac;                   // factorization status
     DeviceBuffer<double> parts, norm;        // norm partials, stage-1 ||rhs||^2
+    DeviceBuffer<double> nparts;             // partials of the lane's own ||rhs|| reduction
+    cudaStream_t stream = nullptr;           // the lane's stage evaluations run here concurrently
+    cudaEvent_t done = nullptr;
+    ~HarmonicLane() {
+        if (done) cudaEventDestroy(done);
+        if (stream) cudaStreamDestroy(stream);
+    }
 };
 
 struct ConvergenceEntry {  // driver.hpp:50-58
@@ -154,7 +161,7 @@ private:
     double cum_seconds_ = 0.0;
     cudaEvent_t ev0_, ev1_, evp_[3];
     cudaStream_t cs_ = nullptr;          // copy stream of outer_iteration_host
-    cudaEvent_t ev_in_ = nullptr, ev_h_ = nullptr;
+    cudaEvent_t ev_in_ = nullptr, ev_h_ = nullptr, ev_stage_ = nullptr;
     bool wait_amps_ = false;             // phase_harmonics waits on ev_in_ before the harmonics
     cplx* amps_download_ = nullptr;      // host destination of the harmonic fields (or null)
 };
