@@ -718,6 +718,10 @@ DeviceDisc::DeviceDisc(const MeshArrays& m, const DevicePattern* pattern) : pat_
     FNLH_CUDA(cudaMemset(err_.ptr, 0xff, sizeof(unsigned long long)));
 }
 
+DeviceDisc::~DeviceDisc() {
+    for (auto e : df_ev_) cudaEventDestroy(e);
+}
+
 void DeviceDisc::alloc_scratch(Scratch& c) {
     const std::size_t n = view_.n, nfc = view_.nf, b = view_.b;
     c.nu.alloc(n);
@@ -877,7 +881,8 @@ void base_frequency(const std::vector<double>& omega, double& base, int& lmax) {
 }  // namespace
 
 void DeviceDisc::deterministic_flux(const double* mean, const std::vector<const cplx*>& amps,
-                                    const std::vector<double>& omega, double* df, cudaStream_t st, bool deferred) {
+                                    const std::vector<double>& omega, double* df, cudaStream_t st, bool deferred,
+                                    const std::vector<cudaStream_t>& side) {
     const std::size_t L = len();
     const int nh = static_cast<int>(amps.size());
     if (nh > 64) throw ConfigError("deterministic_flux: at most 64 harmonics");
@@ -903,14 +908,37 @@ void DeviceDisc::deterministic_flux(const double* mean, const std::vector<const 
         df_omega_ = omega;
     }
     const cplx* dph = df_ph_.ptr;
-    double* w = C().real[0].ptr;
-    double* inv = C().real[1].ptr;
-    double* acc = C().real[2].ptr;
-    for (int k = 0; k < nq; ++k) {
-        { ::fnlh::note_launch(); k_reconstruct<<<nb((long long)L), kT, 0, st>>>(L, mean, al, nh, dph + (std::size_t)k * nh, w); }
-        residual(w, nullptr, 2, 0, nullptr, 0, false, inv, nullptr, st);
-        { ::fnlh::note_launch(); k_accumulate<<<nb((long long)L), kT, 0, st>>>(L, inv, acc, k == 0); }
+    const int saved = cur_;
+    double* acc = ctx_[saved]->real[2].ptr;
+    // the nq reconstructions + residuals are independent: up to 1 + side.size() of them run
+    // at once (context c on side stream c-1), the sum is then taken in k order on st
+    const int NC = saved != 0 ? 1 : 1 + static_cast<int>(std::min(side.size(), ctx_.size() - 1));
+    while (static_cast<int>(df_ev_.size()) < NC + 1) {
+        cudaEvent_t e;
+        FNLH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        df_ev_.push_back(e);
     }
+    for (int k0 = 0; k0 < nq; k0 += NC) {
+        FNLH_CUDA(cudaEventRecord(df_ev_[NC], st));  // the previous batch's sums are taken
+        for (int c = 0; c < NC && k0 + c < nq; ++c) {
+            const int k = k0 + c;
+            const int cx = c == 0 ? saved : c;
+            cudaStream_t sc = c == 0 ? st : side[c - 1];
+            if (c > 0) FNLH_CUDA(cudaStreamWaitEvent(sc, df_ev_[NC], 0));
+            cur_ = cx;
+            { ::fnlh::note_launch(); k_reconstruct<<<nb((long long)L), kT, 0, sc>>>(L, mean, al, nh, dph + (std::size_t)k * nh, C().real[0].ptr); }
+            residual(C().real[0].ptr, nullptr, 2, 0, nullptr, 0, false, C().real[1].ptr, nullptr, sc);
+            if (c > 0) FNLH_CUDA(cudaEventRecord(df_ev_[c], sc));
+        }
+        cur_ = saved;
+        for (int c = 0; c < NC && k0 + c < nq; ++c) {
+            const int k = k0 + c;
+            if (c > 0) FNLH_CUDA(cudaStreamWaitEvent(st, df_ev_[c], 0));
+            const double* inv_k = ctx_[c == 0 ? saved : c]->real[1].ptr;
+            { ::fnlh::note_launch(); k_accumulate<<<nb((long long)L), kT, 0, st>>>(L, inv_k, acc, k == 0); }
+        }
+    }
+    double* inv = C().real[1].ptr;
     residual(mean, nullptr, 2, 0, nullptr, 0, false, inv, nullptr, st);
     { ::fnlh::note_launch(); k_df_finish<<<nb((long long)L), kT, 0, st>>>(L, (double)nq, acc, inv, df, lmax == 0 ? 0 : 1, df_flag_.ptr); }
     FNLH_CUDA(cudaGetLastError());

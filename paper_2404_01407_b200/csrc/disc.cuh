@@ -25,6 +25,9 @@ struct MeshArrays {  // host-side description (include/fnlh_b200.h fnlh_disc_cre
 class DeviceDisc {
 public:
     DeviceDisc(const MeshArrays& m, const DevicePattern* pattern);
+    ~DeviceDisc();
+    DeviceDisc(const DeviceDisc&) = delete;
+    DeviceDisc& operator=(const DeviceDisc&) = delete;
     int n() const { return view_.n; }
     int b() const { return view_.b; }
     int nf() const { return view_.nf; }
@@ -54,8 +57,10 @@ public:
                              int order, bool need_vis, cplx* inv, cplx* vis, cudaStream_t st);
     // deterministic_flux; amps: nh device pointers; omega/index host.  deferred: enqueue
     // only (no host synchronization); errors stay in err() for the caller to read
+    // side: extra streams; with scratch contexts 1.. they evaluate quadrature points concurrently
     void deterministic_flux(const double* mean, const std::vector<const cplx*>& amps,
-                            const std::vector<double>& omega, double* df, cudaStream_t st, bool deferred = false);
+                            const std::vector<double>& omega, double* df, cudaStream_t st, bool deferred = false,
+                            const std::vector<cudaStream_t>& side = {});
 
     const int* df_active() const { return df_flag_.ptr; }  // set by the last deterministic_flux
     // scratch contexts: the residual / linearized-residual temporaries of context k, so k
@@ -88,6 +93,7 @@ private:
     DeviceBuffer<int> df_flag_;   // any nonzero amplitude (residual_ops.cpp:133-141)
     DeviceBuffer<cplx> df_ph_;    // quadrature phases e^{i omega_h t_k}, cached per omega set
     std::vector<double> df_omega_;
+    std::vector<cudaEvent_t> df_ev_;
     std::vector<double> h_nfpad_;
 };
 

@@ -602,7 +602,9 @@ ConvergenceEntry DeviceSolver::phase_mean(const std::vector<double>& h_norm,
     for (int h = 0; h < nh_; ++h) amps.push_back(amps_.ptr + (std::size_t)h * len);
     FNLH_CUDA(cudaMemsetAsync(stage_err_.ptr + 10, 0xff, sizeof(unsigned long long), st));
     disc_->redirect_err(stage_err_.ptr + 10);
-    disc_->deterministic_flux(mean_.ptr, amps, omega_, df_.ptr, st, /*deferred=*/true);
+    std::vector<cudaStream_t> side;  // the lanes' streams take quadrature points concurrently
+    for (std::size_t m = 1; m < lanes_.size(); ++m) side.push_back(lanes_[m]->stream);
+    disc_->deterministic_flux(mean_.ptr, amps, omega_, df_.ptr, st, /*deferred=*/true, side);
     disc_->redirect_err(nullptr);
 
     FNLH_CUDA(cudaEventRecord(evp_[2], st));  // DF done
