@@ -319,14 +319,20 @@ void DeviceSolver::harmonic_batch(const int* hs, int P, std::vector<double>& h_n
     LaneReport lrep[kMaxBatch][5];
     int ldiv[kMaxBatch][5] = {};
     LinearSolveReport hrep[kMaxBatch][5];
+    FNLH_CUDA(cudaEventRecord(ev_stage_, st));
     for (int m = 0; m < P; ++m) {  // build_lhs_harmonic + factorize per lane (driver.cpp:213-216)
         HarmonicLane& ln = *lanes_[m];
         const int h = hs[m];
         const cplx* amp = amps_.ptr + (std::size_t)h * len;
-        harmonic_shift(disc_->view().vol, n, omega_[h], ga5, ln.shift.ptr, st);
-        if (rbA_) {
-            rb_factorize_async<cplx>(*rbA_, ln.shift.ptr, *ln.f, ln.fac.ptr, st);
+        if (rbA_) {  // the lanes' factorizations are independent: one per lane stream
+            cudaStream_t sm = ln.stream;
+            FNLH_CUDA(cudaStreamWaitEvent(sm, ev_stage_, 0));
+            harmonic_shift(disc_->view().vol, n, omega_[h], ga5, ln.shift.ptr, sm);
+            rb_factorize_async<cplx>(*rbA_, ln.shift.ptr, *ln.f, ln.fac.ptr, sm);
+            FNLH_CUDA(cudaEventRecord(ln.done, sm));
+            FNLH_CUDA(cudaStreamWaitEvent(st, ln.done, 0));
         } else {
+            harmonic_shift(disc_->view().vol, n, omega_[h], ga5, ln.shift.ptr, st);
             SystemView<cplx> Ah;
             Ah.p = pat_.get();
             Ah.real_vals = A5_.ptr;
