@@ -181,6 +181,12 @@ __global__ void k_qscale_finish(const unsigned long long* umax, double* qscale) 
     qscale[k] = v == 0.0 ? 1.0 : v;
 }
 
+// element k of block e: the reference BSR layout, or (sell_map) the 2-colour SELL copy
+template <int B>
+__device__ __forceinline__ long long fd_addr(const long long* __restrict__ sell_map, int e, int k) {
+    return sell_map ? sell_map[e] + (long long)(k >> 1) * 64 + (k & 1) : (long long)e * B * B + k;
+}
+
 template <int B>
 __device__ __forceinline__ void fd_face_flux_int(const MeshDev& m, int f, int j, const double* wj,
                                                  const double* __restrict__ W, double* out) {
@@ -247,7 +253,8 @@ __global__ void __launch_bounds__(kT) k_fd_jacobian(MeshDev m, const int* __rest
                                                     const double* __restrict__ W, const double* __restrict__ qscale,
                                                     double* __restrict__ J, double* __restrict__ P,
                                                     unsigned long long* err, const int* __restrict__ bnodes, int nb_nodes,
-                                                    double* __restrict__ dpart) {
+                                                    double* __restrict__ dpart, const long long* __restrict__ sell_map,
+                                                    double ga, double inv_es, int to_a5) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= (PART == 2 ? nb_nodes : m.n) * B) return;
     const int j = PART == 2 ? bnodes[t / B] : t / B, mm = t % B;
@@ -312,13 +319,15 @@ __global__ void __launch_bounds__(kT) k_fd_jacobian(MeshDev m, const int* __rest
             if (bnd || isa) {
                 dacc[r] += dflux;
                 if (!bnd && J) {
-                    double* dst = J + (size_t)e_ba[f] * B * B + r * B + mm;
-                    *dst = *dst - dflux;
+                    double* dst = J + fd_addr<B>(sell_map, e_ba[f], r * B + mm);
+                    const double v = *dst - dflux;
+                    *dst = to_a5 ? v / ga : v;  // build_lhs_mean (rk.cpp:23) fused: A = J / ga
                 }
             } else {
                 if (J) {
-                    double* dst = J + (size_t)e_ab[f] * B * B + r * B + mm;
-                    *dst = *dst + dflux;
+                    double* dst = J + fd_addr<B>(sell_map, e_ab[f], r * B + mm);
+                    const double v = *dst + dflux;
+                    *dst = to_a5 ? v / ga : v;
                 }
                 dacc[r] -= dflux;
             }
@@ -335,7 +344,15 @@ __global__ void __launch_bounds__(kT) k_fd_jacobian(MeshDev m, const int* __rest
     }
 #pragma unroll
     for (int r = 0; r < B; ++r) {
-        if (J) J[(size_t)diag_idx[j] * B * B + r * B + mm] = dacc[r];
+        if (J) {
+            double v = dacc[r];
+            if (to_a5) {  // rk.cpp:23,27: A_ii = J_ii / ga + (J_ii inv_es) / ga
+                double a = v / ga;
+                a += v * inv_es / ga;
+                v = a;
+            }
+            J[fd_addr<B>(sell_map, diag_idx[j], r * B + mm)] = v;
+        }
         if (P) P[(size_t)j * B * B + r * B + mm] = dacc[r];
     }
 }
@@ -348,7 +365,7 @@ __global__ void k_diag_check(int n, const int* __restrict__ diag_idx, const doub
     if (i >= n) return;
     double A[B * B];
     int piv[B];
-    load_block<B>(J + (size_t)diag_idx[i] * B * B, A);
+    load_block<B>(J + (diag_idx ? (size_t)diag_idx[i] : (size_t)i) * B * B, A);
     double cond;
     if (lu_factor_reg<B>(A, piv, cond)) record(err, (unsigned long long)i, 5);
 }
@@ -786,29 +803,50 @@ void DeviceDisc::validate(const double* W, cudaStream_t st) {
     raise_if_err(st, "validate_state");
 }
 
-void DeviceDisc::fd_jacobian(const double* W, double* J, double* P, cudaStream_t st) {
+void DeviceDisc::fd_jacobian(const double* W, double* J, double* P, cudaStream_t st, const A5Target* a5) {
     const MeshDev& m = view_;
     validate(W, st);
-    if (J) FNLH_CUDA(cudaMemsetAsync(J, 0, (std::size_t)pat_->nnzb * m.b * m.b * sizeof(double), st));
+    const long long* smap = nullptr;
+    double ga = 1.0, inv_es = 0.0;
+    int to_a5 = 0;
+    if (a5) {  // A5 straight from the FD columns; J_ii kept aside for the singularity check
+        if (J) throw ConfigError("fd_jacobian: J and an A5 target are exclusive");
+        J = a5->vals;
+        smap = a5->sell_map;
+        ga = a5->ga;
+        inv_es = a5->inv_es;
+        to_a5 = 1;
+        if (!P) {
+            if (!fddiag_.ptr) fddiag_.alloc((std::size_t)m.n * m.b * m.b);
+            P = fddiag_.ptr;
+        }
+        FNLH_CUDA(cudaMemsetAsync(J, 0, a5->bytes, st));
+    } else if (J) {
+        FNLH_CUDA(cudaMemsetAsync(J, 0, (std::size_t)pat_->nnzb * m.b * m.b * sizeof(double), st));
+    }
     DISPATCH_B56(m.b, {
         { ::fnlh::note_launch(); k_umax_init<<<1, 32, 0, st>>>(umax_.ptr, B); }
         { ::fnlh::note_launch(); k_qscale<B><<<std::min(nb(m.n), 592), kT, 0, st>>>(m.n, m.gamma, W, umax_.ptr); }
         { ::fnlh::note_launch(); k_qscale_finish<B><<<1, 32, 0, st>>>(umax_.ptr, qscale_.ptr); }
         if (nf_int_ >= 0) {
             { ::fnlh::note_launch(); k_fd_jacobian<B, 1><<<nb((long long)m.n * B), kT, 0, st>>>(m, pat_->diag_idx, e_ab_.ptr, e_ba_.ptr, W,
-                                                                       qscale_.ptr, J, P, err_.ptr, nullptr, 0, fdpart_.ptr); }
+                                                                       qscale_.ptr, J, P, err_.ptr, nullptr, 0, fdpart_.ptr,
+                                                                       smap, ga, inv_es, to_a5); }
             if (nbn_ > 0) { ::fnlh::note_launch(); k_fd_jacobian<B, 2><<<nb((long long)nbn_ * B), kT, 0, st>>>(m, pat_->diag_idx, e_ab_.ptr, e_ba_.ptr, W,
                                                                                     qscale_.ptr, J, P, err_.ptr, bnodes_.ptr, nbn_,
-                                                                                    fdpart_.ptr); }
+                                                                                    fdpart_.ptr, smap, ga, inv_es, to_a5); }
         } else {
             { ::fnlh::note_launch(); k_fd_jacobian<B, 0><<<nb((long long)m.n * B), kT, 0, st>>>(m, pat_->diag_idx, e_ab_.ptr, e_ba_.ptr, W,
-                                                                       qscale_.ptr, J, P, err_.ptr, nullptr, 0, nullptr); }
+                                                                       qscale_.ptr, J, P, err_.ptr, nullptr, 0, nullptr,
+                                                                       smap, ga, inv_es, to_a5); }
         }
     });
     FNLH_CUDA(cudaGetLastError());
     raise_if_err(st, "fd_jacobian");
-    if (J) {
-        DISPATCH_B56(m.b, { { ::fnlh::note_launch(); k_diag_check<B><<<nb(m.n), kT, 0, st>>>(m.n, pat_->diag_idx, J, err_.ptr); } });
+    if (J) {  // diagonal non-singularity check of J (disc.cpp:121-129)
+        const int* didx = a5 ? nullptr : pat_->diag_idx;
+        const double* blocks = a5 ? P : J;
+        DISPATCH_B56(m.b, { { ::fnlh::note_launch(); k_diag_check<B><<<nb(m.n), kT, 0, st>>>(m.n, didx, blocks, err_.ptr); } });
         raise_if_err(st, "fd_jacobian");
     }
 }

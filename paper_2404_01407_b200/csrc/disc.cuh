@@ -22,6 +22,16 @@ struct MeshArrays {  // host-side description (include/fnlh_b200.h fnlh_disc_cre
     double gamma, gas_constant, p0, T0, p_out, nt_in, forcing_scale;
 };
 
+// where fd_jacobian may write A5 = J/ga (+ J_ii inv_es/ga on the diagonal) directly
+// (build_lhs_mean fused, rk.cpp:5-30): the BSR layout (sell_map null) or the 2-colour SELL
+// copy (sell_map = per-CSR-entry element offsets); `bytes` of vals are zeroed first
+struct A5Target {
+    double* vals;
+    const long long* sell_map;
+    double ga, inv_es;
+    std::size_t bytes;
+};
+
 class DeviceDisc {
 public:
     DeviceDisc(const MeshArrays& m, const DevicePattern* pattern);
@@ -49,7 +59,7 @@ public:
     void residual(const double* W, const double* wref, int order, int mode, const double* forcing, int nforcing,
                   bool need_vis, double* inv, double* vis, cudaStream_t st, const double* skip_if_zero = nullptr);
     // J (pattern layout) and/or P (n*b*b); validates W and the diagonal blocks (throws)
-    void fd_jacobian(const double* W, double* J, double* P, cudaStream_t st);
+    void fd_jacobian(const double* W, double* J, double* P, cudaStream_t st, const A5Target* a5 = nullptr);
     // transform_jacobian validation (state.cpp:82-94): throws StateError on an inadmissible mean
     void validate(const double* W, cudaStream_t st);
     // linearized_residual (mean is the perturbation reference); complex vectors as cplx
@@ -89,6 +99,7 @@ private:
     int nbn_ = 0;                  // nodes with boundary faces
     DeviceBuffer<int> bnodes_;
     DeviceBuffer<double> fdpart_;  // FD Jacobian diagonal partial sums (split kernels)
+    DeviceBuffer<double> fddiag_;  // J_ii when fd_jacobian writes A5
     DeviceBuffer<unsigned long long> umax_;  // FD Jacobian scales
     DeviceBuffer<int> df_flag_;   // any nonzero amplitude (residual_ops.cpp:133-141)
     DeviceBuffer<cplx> df_ph_;    // quadrature phases e^{i omega_h t_k}, cached per omega set

@@ -97,6 +97,8 @@ public:
     void load(const double* A_csr, cudaStream_t st);
     const SellLayout& layout() const { return L_; }
     const double* vals() const { return vals_.ptr; }
+    double* vals_mut() { return vals_.ptr; }
+    const long long* sell_map() const { return L_.csr_to_sell.ptr; }
     std::size_t bytes() const { return vals_.bytes(); }
     int n0() const { return L_.n0; }
     const DevicePattern* pattern() const { return p_; }

@@ -15,30 +15,6 @@ constexpr double kBeta[5] = {1.0, 0.0, 14.0 / 25.0, 0.0, 11.0 / 25.0};          
 constexpr int kT = 128;
 inline int nb(long long n) { return static_cast<int>((n + kT - 1) / kT); }
 
-// build_lhs_mean (rk.cpp:5-30), in place: A = J/ga; diag += J_ii*inv_es/ga.  One warp
-// per block row: the row's blocks are contiguous, so the warp streams them coalesced and
-// knows the diagonal from diag_idx without a search.
-__global__ void k_build_lhs(const double* __restrict__ J, double* __restrict__ A, int bb, int n,
-                            const int* __restrict__ row_ptr, const int* __restrict__ diag_idx, int implicit,
-                            double ga, double inv_es) {
-    const int i = (int)((blockIdx.x * (std::size_t)blockDim.x + threadIdx.x) >> 5);
-    const int lane = threadIdx.x & 31;
-    if (i >= n) return;
-    const std::size_t t0 = (std::size_t)row_ptr[i] * bb, t1 = (std::size_t)row_ptr[i + 1] * bb;
-    const std::size_t d0 = (std::size_t)diag_idx[i] * bb;
-    for (std::size_t t = t0 + lane; t < t1; t += 32) {
-        const bool diag = t >= d0 && t < d0 + bb;
-        const double j = J[t];
-        if (!implicit) {
-            A[t] = diag ? j / ga : 0.0;
-            continue;
-        }
-        double a = j / ga;
-        if (diag) a += j * inv_es / ga;
-        A[t] = a;
-    }
-}
-
 __global__ void k_shift(const double* __restrict__ vol, int n, double omega, double ga, double* __restrict__ s) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) s[i] = omega * vol[i] / ga;  // rk.cpp:37 shift = i omega V / ga
@@ -58,12 +34,6 @@ __global__ void k_shifted_blocks(const double* __restrict__ P, const double* __r
 }
 
 }  // namespace
-
-void build_lhs_mean_device(const double* J, double* A, int b, int n, const int* row_ptr, const int* diag_idx,
-                           int implicit, double ga, double inv_es, cudaStream_t st) {
-    { ::fnlh::note_launch(); k_build_lhs<<<(int)(((std::size_t)n * 32 + kT - 1) / kT), kT, 0, st>>>(J, A, b * b, n, row_ptr, diag_idx, implicit, ga, inv_es); }
-    FNLH_CUDA(cudaGetLastError());
-}
 
 void harmonic_shift(const double* vol, int n, double omega, double ga, double* s, cudaStream_t st) {
     { ::fnlh::note_launch(); k_shift<<<nb(n), kT, 0, st>>>(vol, n, omega, ga, s); }
@@ -97,7 +67,7 @@ DeviceSolver::DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int
         FNLH_CUDA(cudaMemcpy(forcing_.ptr, forcing_pairs, (std::size_t)nh * nforcing * sizeof(cplx),
                              cudaMemcpyHostToDevice));
     if (sch_.implicit) {
-        A5_.alloc((std::size_t)pat_->nnzb * mesh.b * mesh.b);
+
         int n0 = 0;
         if (rb_enabled() && rb_eligible(*pat_, &n0)) {
             rbA_ = std::make_unique<RbSystem>(pat_.get(), n0);
@@ -107,6 +77,7 @@ DeviceSolver::DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int
             rb_z_.alloc(len);
             rb_r_.alloc(len);
         } else {
+            A5_.alloc((std::size_t)pat_->nnzb * mesh.b * mesh.b);  // BSR A5 (the 2-colour path keeps only its SELL copy)
             ilu_mean_ = std::make_unique<DeviceIlu<double>>(pat_.get());
             ilu_h_ = std::make_unique<DeviceIlu<cplx>>(pat_.get());  // ONE workspace reused by every harmonic
         }
@@ -451,6 +422,26 @@ ConvergenceEntry DeviceSolver::outer_iteration() {
     return phase_mean(h_norm_, h_reps_);
 }
 
+// FD Jacobian straight into A5 (build_lhs_mean fused into the column kernel): the SELL copy
+// of the 2-colour path, else the BSR A5
+void DeviceSolver::assemble_a5(cudaStream_t st) {
+    const double ga5 = (1.0 / sch_.eps_relax) * kAlpha[4];
+    const double inv_es = 1.0 / (sch_.eps_relax * sigma_);
+    A5Target t{};
+    t.ga = ga5;
+    t.inv_es = inv_es;
+    if (rbA_) {
+        t.vals = rbA_->vals_mut();
+        t.sell_map = rbA_->sell_map();
+        t.bytes = rbA_->bytes();
+    } else {
+        t.vals = A5_.ptr;
+        t.sell_map = nullptr;
+        t.bytes = A5_.bytes();
+    }
+    disc_->fd_jacobian(mean_.ptr, nullptr, nullptr, st, &t);
+}
+
 ConvergenceEntry DeviceSolver::outer_iteration_host(const double* mean_in, const cplx* amps_in, double* mean_out,
                                                     cplx* amps_out) {
     cudaStream_t st = ws_->stream;
@@ -492,11 +483,8 @@ void DeviceSolver::phase_harmonics(const int* owned) {
     const bool implicit = sch_.implicit != 0;
     const double ga5 = (implicit ? 1.0 / sch_.eps_relax : sigma_) * kAlpha[4];
     if (implicit) {
-        disc_->fd_jacobian(mean_.ptr, A5_.ptr, nullptr, st);  // J, then A5 in place
-        build_lhs_mean_device(A5_.ptr, A5_.ptr, b, n, pat_->row_ptr, pat_->diag_idx, 1, ga5,
-                              1.0 / (sch_.eps_relax * sigma_), st);
+        assemble_a5(st);  // J and build_lhs_mean (rk.cpp:5-30) in one pass
         if (rbA_) {
-            rbA_->load(A5_.ptr, st);
             rb_factorize<double>(*rbA_, nullptr, *rb_mean_, *ws_);
         } else {
             SystemView<double> Am;
@@ -685,9 +673,7 @@ double DeviceSolver::time_harmonic_sweeps(int h, int nsweeps) {
     const int n = disc_->n(), b = disc_->b();
     const std::size_t len = disc_->len();
     const double ga5 = (1.0 / sch_.eps_relax) * kAlpha[4];
-    disc_->fd_jacobian(mean_.ptr, A5_.ptr, nullptr, st);
-    build_lhs_mean_device(A5_.ptr, A5_.ptr, b, n, pat_->row_ptr, pat_->diag_idx, 1, ga5, 1.0 / (sch_.eps_relax * sigma_),
-                          st);
+    assemble_a5(st);
     harmonic_shift(disc_->view().vol, n, omega_[h], ga5, shift_.ptr, st);
     SystemView<cplx> Ah;
     Ah.p = pat_.get();
@@ -696,7 +682,6 @@ double DeviceSolver::time_harmonic_sweeps(int h, int nsweeps) {
     RbIlu<cplx>* fh = rb_h_ ? rb_h_.get() : (lanes_.empty() ? nullptr : lanes_[0]->f.get());
     DeviceIlu<cplx>* gh = ilu_h_ ? ilu_h_.get() : (lanes_.empty() ? nullptr : lanes_[0]->gf.get());
     if (rbA_) {
-        rbA_->load(A5_.ptr, st);
         rb_factorize<cplx>(*rbA_, shift_.ptr, *fh, *ws_);
     } else {
         ilu_factorize<cplx>(Ah, *gh, *ws_);
@@ -727,10 +712,7 @@ double DeviceSolver::time_harmonic_sweeps_batch(int P, int nsweeps) {
     const int n = disc_->n(), b = disc_->b();
     const std::size_t len = disc_->len();
     const double ga5 = (1.0 / sch_.eps_relax) * kAlpha[4];
-    disc_->fd_jacobian(mean_.ptr, A5_.ptr, nullptr, st);
-    build_lhs_mean_device(A5_.ptr, A5_.ptr, b, n, pat_->row_ptr, pat_->diag_idx, 1, ga5, 1.0 / (sch_.eps_relax * sigma_),
-                          st);
-    if (rbA_) rbA_->load(A5_.ptr, st);
+    assemble_a5(st);
     RbMember<cplx> mem[kMaxBatch];
     LaneSystem<cplx> sys[kMaxBatch];
     for (int m = 0; m < P; ++m) {

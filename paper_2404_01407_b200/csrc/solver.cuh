@@ -129,6 +129,7 @@ private:
                     const bool* have_host, const std::string& field, RkStepResult& res,
                     const int* host_div = nullptr);
     // rk_step of harmonics hs[0..P) interleaved stage by stage, one batched sweep per stage
+    void assemble_a5(cudaStream_t st);
     void harmonic_batch(const int* hs, int P, std::vector<double>& h_norm,
                         std::vector<std::vector<LinearSolveReport>>& h_reps, std::vector<std::exception_ptr>& herr);
     std::vector<double> h_norm_;
@@ -166,8 +167,6 @@ private:
     cplx* amps_download_ = nullptr;      // host destination of the harmonic fields (or null)
 };
 
-void build_lhs_mean_device(const double* J, double* A, int b, int n, const int* row_ptr, const int* diag_idx,
-                           int implicit, double ga, double inv_es, cudaStream_t st);
 void harmonic_shift(const double* vol, int n, double omega, double ga, double* shift_im, cudaStream_t st);
 void shifted_blocks(const double* P, const double* vol, int b, int n, double omega, cplx* out, cudaStream_t st);
 
