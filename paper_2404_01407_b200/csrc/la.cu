@@ -665,22 +665,30 @@ Workspace::~Workspace() {
 // ---------------------------------------------------------------------------
 // operations
 // ---------------------------------------------------------------------------
+__global__ void k_status_reset(int* status) {
+    status[0] = 0;
+    status[1] = 0x7fffffff;
+}
+
 template <class S>
-void ilu_factorize(const SystemView<S>& A, DeviceIlu<S>& f, Workspace& ws) {
+void ilu_factorize_async(const SystemView<S>& A, DeviceIlu<S>& f, int* status, cudaStream_t st) {
     const DevicePattern& p = *f.p;
     const PatDev pd = dev(p);
-    const int init[2] = {0, 0x7fffffff};
-    FNLH_CUDA(cudaMemcpyAsync(ws.status, init, sizeof init, cudaMemcpyHostToDevice, ws.stream));
+    { ::fnlh::note_launch(); k_status_reset<<<1, 1, 0, st>>>(status); }
     FNLH_DISPATCH_B(p.b, {
-        { ::fnlh::note_launch(); k_ilu_copy<B, S><<<(int)(((std::size_t)p.rows * 32 + kThreads - 1) / kThreads), kThreads, 0, ws.stream>>>(pd, A, f.vals); }
+        { ::fnlh::note_launch(); k_ilu_copy<B, S><<<(int)(((std::size_t)p.rows * 32 + kThreads - 1) / kThreads), kThreads, 0, st>>>(pd, A, f.vals); }
         for (int l = 0; l < p.fwd_levels(); ++l) {
             const int n = p.fwd_ptr[l + 1] - p.fwd_ptr[l];
-            { ::fnlh::note_launch(); k_ilu_factor<B, S><<<nblocks(n), kThreads, 0, ws.stream>>>(pd, p.fwd_rows + p.fwd_ptr[l], n, f.vals,
-                                                                       f.diag_lu, f.diag_piv, f.diag_inv,
-                                                                       ws.status); }
+            { ::fnlh::note_launch(); k_ilu_factor<B, S><<<nblocks(n), kThreads, 0, st>>>(pd, p.fwd_rows + p.fwd_ptr[l], n, f.vals,
+                                                                       f.diag_lu, f.diag_piv, f.diag_inv, status); }
         }
     });
     FNLH_CUDA(cudaGetLastError());
+}
+
+template <class S>
+void ilu_factorize(const SystemView<S>& A, DeviceIlu<S>& f, Workspace& ws) {
+    ilu_factorize_async<S>(A, f, ws.status, ws.stream);
     FNLH_CUDA(cudaMemcpyAsync(ws.h_status, ws.status, 2 * sizeof(int), cudaMemcpyDeviceToHost, ws.stream));
     FNLH_CUDA(cudaStreamSynchronize(ws.stream));
     if (ws.h_status[1] != 0x7fffffff)
@@ -881,6 +889,7 @@ void block_diag_factor(int b, int n, S* blocks, int* piv, int* status, cudaStrea
 #define FNLH_INST(S)                                                                                       \
     template struct DeviceIlu<S>;                                                                          \
     template void ilu_factorize<S>(const SystemView<S>&, DeviceIlu<S>&, Workspace&);                       \
+    template void ilu_factorize_async<S>(const SystemView<S>&, DeviceIlu<S>&, int*, cudaStream_t);          \
     template void ilu_apply<S>(const DeviceIlu<S>&, const S*, S*, Workspace&, S*);                         \
     template void residual_norm<S>(const SystemView<S>&, const S*, const S*, S*, double*, Workspace&);     \
     template void matvec<S>(const SystemView<S>&, const S*, S*, Workspace&);                               \

@@ -109,7 +109,10 @@ enum Status : int { kOk = 0, kConfig = 1, kState = 2, kShape = 3, kUnsupported =
 
 // --- operations (all asynchronous on ws.stream unless they return host values) -------
 template <class S>
-void ilu_factorize(const SystemView<S>& A, DeviceIlu<S>& f, Workspace& ws);  // throws FactorizationError
+void ilu_factorize(const SystemView<S>& A, DeviceIlu<S>& f, Workspace& ws);
+// the same, enqueued only: status[1] receives the first near-singular pivot row (0x7fffffff when clean)
+template <class S>
+void ilu_factorize_async(const SystemView<S>& A, DeviceIlu<S>& f, int* status, cudaStream_t st);  // throws FactorizationError
 template <class S>
 void ilu_apply(const DeviceIlu<S>& f, const S* rhs, S* x, Workspace& ws, S* x_accum = nullptr);
 template <class S>

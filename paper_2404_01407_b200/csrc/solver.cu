@@ -302,17 +302,17 @@ void DeviceSolver::harmonic_batch(const int* hs, int P, std::vector<double>& h_n
             rb_factorize_async<cplx>(*rbA_, ln.shift.ptr, *ln.f, ln.fac.ptr, sm);
             FNLH_CUDA(cudaEventRecord(ln.done, sm));
             FNLH_CUDA(cudaStreamWaitEvent(st, ln.done, 0));
-        } else {
-            harmonic_shift(disc_->view().vol, n, omega_[h], ga5, ln.shift.ptr, st);
+        } else {  // likewise on the level-scheduled path (the status is checked after the step)
+            cudaStream_t sm = ln.stream;
+            FNLH_CUDA(cudaStreamWaitEvent(sm, ev_stage_, 0));
+            harmonic_shift(disc_->view().vol, n, omega_[h], ga5, ln.shift.ptr, sm);
             SystemView<cplx> Ah;
             Ah.p = pat_.get();
             Ah.real_vals = A5_.ptr;
             Ah.shift_im = ln.shift.ptr;
-            try {
-                ilu_factorize<cplx>(Ah, *ln.gf, *ws_);
-            } catch (...) {  // this lane's worker fails here (driver.cpp:215-216)
-                early[m] = std::current_exception();
-            }
+            ilu_factorize_async<cplx>(Ah, *ln.gf, ln.fac.ptr, sm);
+            FNLH_CUDA(cudaEventRecord(ln.done, sm));
+            FNLH_CUDA(cudaStreamWaitEvent(st, ln.done, 0));
         }
         FNLH_CUDA(cudaMemcpyAsync(ln.v[0].ptr, amp, len * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
         FNLH_CUDA(cudaMemcpyAsync(ln.v[6].ptr, amp, len * sizeof(cplx), cudaMemcpyDeviceToDevice, st));
@@ -400,8 +400,7 @@ void DeviceSolver::harmonic_batch(const int* hs, int P, std::vector<double>& h_n
             continue;
         }
         try {
-            if (rbA_ && rec[m].fac[1] != 0x7fffffff)
-                throw FactorizationError("near-singular ILU pivot block", rec[m].fac[1]);
+            if (rec[m].fac[1] != 0x7fffffff) throw FactorizationError("near-singular ILU pivot block", rec[m].fac[1]);
             RkStepResult res;
             res.stage1_residual_norm = std::sqrt(rec[m].norm);
             const bool all[5] = {true, true, true, true, true};
