@@ -820,6 +820,19 @@ static void reports_push(report_list* l, const or_linear_report* r) {
     l->v[l->n++] = *r;
 }
 
+/* a coarse multigrid level (multigrid.hpp:26-32, driver.cpp:104-131): its mesh and
+   pattern, the parent map from the next finer level, its boundary forcing, and the
+   per-level operators of the outer iteration */
+typedef struct {
+    or_mesh mesh;
+    or_pattern pat;
+    const int* parent; /* n of the finer level */
+    ocplx* forcing;    /* nh * nforcing */
+    int nforcing;
+    double *mean, *M, *MLU, *P, *PLU;
+    int *Mpiv, *Ppiv;
+} or_level;
+
 struct or_solver {
     or_mesh mesh;
     or_pattern pat;
@@ -842,6 +855,8 @@ struct or_solver {
     report_list* hrep; /* per harmonic, from the last phase_harmonics */
     double* hnorm;
     or_ilu_z* ws_extra; /* per-worker complex workspaces (or_set_workers) */
+    int nlev;           /* coarse multigrid levels (explicit scheme) */
+    or_level* lev;      /* lev[l - 1] = level l */
     or_error* herr;     /* per harmonic error record of the worker threads */
     ocplx** wsmat_extra;
     int n_extra;
@@ -933,6 +948,18 @@ void or_solver_destroy(or_solver* s) {
     }
     free(s->ws_extra);
     free(s->wsmat_extra);
+    for (int l = 0; l < s->nlev; ++l) {
+        or_level* v = &s->lev[l];
+        free(v->forcing);
+        free(v->mean);
+        free(v->M);
+        free(v->MLU);
+        free(v->P);
+        free(v->PLU);
+        free(v->Mpiv);
+        free(v->Ppiv);
+    }
+    free(s->lev);
     free(s->herr);
     free(s->hrep);
     free(s->hnorm);
@@ -943,18 +970,37 @@ void or_solver_destroy(or_solver* s) {
 typedef struct {
     or_solver* s;
     int h; /* harmonic position */
+    int l; /* multigrid level (0 = finest) */
 } rk_ctx;
 
+/* level accessors (level 0 lives in the solver itself) */
+static const or_mesh* lv_mesh(const or_solver* s, int l) { return l == 0 ? &s->mesh : &s->lev[l - 1].mesh; }
+static double* lv_mean(or_solver* s, int l) { return l == 0 ? s->mean : s->lev[l - 1].mean; }
+static double* lv_M(or_solver* s, int l) { return l == 0 ? s->M : s->lev[l - 1].M; }
+static double* lv_MLU(or_solver* s, int l) { return l == 0 ? s->MLU : s->lev[l - 1].MLU; }
+static int* lv_Mpiv(or_solver* s, int l) { return l == 0 ? s->Mpiv : s->lev[l - 1].Mpiv; }
+static double* lv_P(or_solver* s, int l) { return l == 0 ? s->P : s->lev[l - 1].P; }
+static double* lv_PLU(or_solver* s, int l) { return l == 0 ? s->PLU : s->lev[l - 1].PLU; }
+static int* lv_Ppiv(or_solver* s, int l) { return l == 0 ? s->Ppiv : s->lev[l - 1].Ppiv; }
+static const ocplx* lv_forcing(const or_solver* s, int l, int h) {
+    return l == 0 ? s->forcing + (size_t)h * s->nforcing : s->lev[l - 1].forcing + (size_t)h * s->lev[l - 1].nforcing;
+}
+static int lv_nforcing(const or_solver* s, int l) { return l == 0 ? s->nforcing : s->lev[l - 1].nforcing; }
+
+/* coarse levels run the first-order operator (driver.cpp:199-202,284) */
 static int eval_harmonic(rk_ctx* c, const ocplx* state, int need_vis, ocplx* inv, ocplx* vis) {
     or_solver* s = c->s;
-    return or_linearized_residual(&s->mesh, s->mean, s->M, state, s->omega[c->h],
-                                  s->forcing + (size_t)c->h * s->nforcing, s->nforcing, 2, need_vis, inv, vis);
+    const int l = c->l;
+    return or_linearized_residual(lv_mesh(s, l), lv_mean(s, l), lv_M(s, l), state, s->omega[c->h],
+                                  lv_forcing(s, l, c->h), lv_nforcing(s, l), l == 0 ? 2 : 1, need_vis, inv, vis);
 }
 
 /* add_transform_solve (driver.cpp:32-46) */
 static int apply_harmonic(rk_ctx* c, const ocplx* base, const ocplx* x, ocplx* out) {
     or_solver* s = c->s;
-    const int b = s->mesh.b, n = s->mesh.n;
+    const int b = s->mesh.b, n = lv_mesh(s, c->l)->n;
+    const double* MLU = lv_MLU(s, c->l);
+    const int* Mpiv = lv_Mpiv(s, c->l);
     const size_t bb = (size_t)b * b;
     memcpy(out, base, sizeof(ocplx) * (size_t)n * b);
     double re[6], im[6], yre[6], yim[6];
@@ -964,8 +1010,8 @@ static int apply_harmonic(rk_ctx* c, const ocplx* base, const ocplx* x, ocplx* o
             re[k] = creal(xi[k]);
             im[k] = cimag(xi[k]);
         }
-        or_block_lu_solve_d(b, s->MLU + (size_t)i * bb, s->Mpiv + (size_t)i * b, re, yre);
-        or_block_lu_solve_d(b, s->MLU + (size_t)i * bb, s->Mpiv + (size_t)i * b, im, yim);
+        or_block_lu_solve_d(b, MLU + (size_t)i * bb, Mpiv + (size_t)i * b, re, yre);
+        or_block_lu_solve_d(b, MLU + (size_t)i * bb, Mpiv + (size_t)i * b, im, yim);
         ocplx* oi = out + (size_t)i * b;
         for (int k = 0; k < b; ++k) oi[k] += CMPLX(yre[k], yim[k]);
     }
@@ -974,17 +1020,20 @@ static int apply_harmonic(rk_ctx* c, const ocplx* base, const ocplx* x, ocplx* o
 
 static int eval_mean(rk_ctx* c, const double* state, int need_vis, double* inv, double* vis) {
     or_solver* s = c->s;
-    int st = or_residual(&s->mesh, state, NULL, 2, 0, NULL, 0, need_vis, inv, vis);
+    const int l = c->l;
+    int st = or_residual(lv_mesh(s, l), state, NULL, l == 0 ? 2 : 1, 0, NULL, 0, need_vis, inv, vis);
     if (st) return st;
-    const size_t len = (size_t)s->mesh.n * s->mesh.b;
-    for (size_t k = 0; k < len; ++k) inv[k] += s->df[k];
+    if (l == 0) { /* DF enters the finest level only (driver.cpp:284-285) */
+        const size_t len = (size_t)s->mesh.n * s->mesh.b;
+        for (size_t k = 0; k < len; ++k) inv[k] += s->df[k];
+    }
     return OR_OK;
 }
 
 /* mean_apply (driver.cpp:274-280) */
 static int apply_mean(rk_ctx* c, const double* base, const double* x, double* out) {
     or_solver* s = c->s;
-    const int b = s->mesh.b, n = s->mesh.n;
+    const int b = s->mesh.b, n = lv_mesh(s, c->l)->n;
     const size_t len = (size_t)n * b;
     double* q = (double*)malloc(sizeof(double) * len);
     int st = or_prim_to_cons(b, n, s->mesh.gamma, base, q);
@@ -996,6 +1045,28 @@ static int apply_mean(rk_ctx* c, const double* base, const double* x, double* ou
     return st;
 }
 
+/* LevelOps::full_residual (driver.cpp:230-236 harmonic, 300-306 mean): out = inv + vis
+   (+ DF on the finest mean level) */
+static int fullres_harmonic(rk_ctx* c, const ocplx* state, ocplx* out, ocplx* vis) {
+    int st = eval_harmonic(c, state, 1, out, vis);
+    if (st) return st;
+    const size_t len = (size_t)lv_mesh(c->s, c->l)->n * c->s->mesh.b;
+    for (size_t k = 0; k < len; ++k) out[k] += vis[k];
+    return OR_OK;
+}
+
+static int fullres_mean(rk_ctx* c, const double* state, double* out, double* vis) {
+    or_solver* s = c->s;
+    const int l = c->l;
+    int st = or_residual(lv_mesh(s, l), state, NULL, l == 0 ? 2 : 1, 0, NULL, 0, 1, out, vis);
+    if (st) return st;
+    const size_t len = (size_t)lv_mesh(s, l)->n * s->mesh.b;
+    for (size_t k = 0; k < len; ++k) out[k] += vis[k];
+    if (l == 0)
+        for (size_t k = 0; k < len; ++k) out[k] += s->df[k];
+    return OR_OK;
+}
+
 #define S double
 #define SUF d
 #define ILU_T or_ilu_d
@@ -1003,7 +1074,10 @@ static int apply_mean(rk_ctx* c, const double* base, const double* x, double* ou
 #define FINITE(x) isfinite(x)
 #define EVAL eval_mean
 #define APPLY apply_mean
+#define FULLRES fullres_mean
 #include "rk_tmpl.inc"
+#include "mg_tmpl.inc"
+#undef FULLRES
 #undef S
 #undef SUF
 #undef ILU_T
@@ -1019,7 +1093,10 @@ static int apply_mean(rk_ctx* c, const double* base, const double* x, double* ou
 #define FINITE(x) cfinite(x)
 #define EVAL eval_harmonic
 #define APPLY apply_harmonic
+#define FULLRES fullres_harmonic
 #include "rk_tmpl.inc"
+#include "mg_tmpl.inc"
+#undef FULLRES
 #undef S
 #undef SUF
 #undef ILU_T
@@ -1052,7 +1129,32 @@ static int run_harmonic(or_solver* s, int h, double ga5, ocplx* wsmat, or_ilu_z*
         free(shift);
         if ((st = or_ilu_factorize_z(p, wsmat, wsilu))) return st;
         st = rk_step_z(&c, s->amps + (size_t)h * len, n, b, 1, s->sigma, s->sch.eps_relax, s->sch.linear_tol,
-                       s->sch.linear_max_iter, p, wsmat, wsilu, NULL, NULL, &res, &hreps);
+                       s->sch.linear_max_iter, p, wsmat, wsilu, NULL, NULL, &res, &hreps, NULL);
+    } else if (s->nlev > 0) {
+        /* shifted_blocks per level (driver.cpp:224-229), then the FAS V-cycle (:240) */
+        ocplx* pcl[16];
+        int* pvl[16];
+        for (int l = 0; l <= s->nlev; ++l) {
+            const or_mesh* ml = lv_mesh(s, l);
+            pcl[l] = (ocplx*)malloc(sizeof(ocplx) * (size_t)ml->n * bb);
+            pvl[l] = (int*)malloc(sizeof(int) * (size_t)ml->n * b);
+            const double* Pl = lv_P(s, l);
+            for (int i = 0; i < ml->n && !st; ++i) {
+                const double* src = Pl + (size_t)i * bb;
+                ocplx* dst = pcl[l] + (size_t)i * bb;
+                for (size_t k = 0; k < bb; ++k) dst[k] = CMPLX(src[k], 0.0);
+                const ocplx sh = CMPLX(0.0, omega * ml->vol[i]);
+                for (int q = 0; q < b; ++q) dst[(size_t)q * b + q] += sh;
+                st = or_block_lu_factor_z(b, dst, pvl[l] + (size_t)i * b, i, NULL);
+            }
+        }
+        if (!st)
+            st = mg_vcycle_z(s, h, 0, s->amps + (size_t)h * len, NULL, (const ocplx* const*)pcl, (const int* const*)pvl,
+                             &res);
+        for (int l = 0; l <= s->nlev; ++l) {
+            free(pcl[l]);
+            free(pvl[l]);
+        }
     } else {
         /* shifted_blocks (driver.cpp:48-59) */
         ocplx* pclu = (ocplx*)malloc(sizeof(ocplx) * n * bb);
@@ -1067,7 +1169,7 @@ static int run_harmonic(or_solver* s, int h, double ga5, ocplx* wsmat, or_ilu_z*
         }
         if (!st)
             st = rk_step_z(&c, s->amps + (size_t)h * len, n, b, 0, s->sigma, s->sch.eps_relax, s->sch.linear_tol,
-                           s->sch.linear_max_iter, p, NULL, NULL, pclu, pcpiv, &res, &hreps);
+                           s->sch.linear_max_iter, p, NULL, NULL, pclu, pcpiv, &res, &hreps, NULL);
         free(pclu);
         free(pcpiv);
     }
@@ -1106,21 +1208,35 @@ int or_solver_phase_harmonics(or_solver* s, const int* owned, double* hnorm_out)
     const or_pattern* p = &s->pat;
     int st;
     /* perturbation reference = mean (linearized_residual passes mean as wref); M and its LU */
-    if ((st = or_transform_jacobian(b, n, m->gamma, s->mean, s->M))) return st;
-    memcpy(s->MLU, s->M, sizeof(double) * n * bb);
-    for (int i = 0; i < n; ++i)
-        if ((st = or_block_lu_factor_d(b, s->MLU + (size_t)i * bb, s->Mpiv + (size_t)i * b, i, NULL))) return st;
+    /* mean on every level (driver.cpp:168-171), then M and its LU per level (:172-176) */
+    for (int l = 1; l <= s->nlev; ++l)
+        mg_restrict_state_d(lv_mesh(s, l - 1), s->lev[l - 1].parent, lv_mesh(s, l)->n, b, lv_mean(s, l - 1),
+                            lv_mean(s, l));
+    for (int l = 0; l <= s->nlev; ++l) {
+        const int nl = lv_mesh(s, l)->n;
+        if ((st = or_transform_jacobian(b, nl, m->gamma, lv_mean(s, l), lv_M(s, l)))) return st;
+        memcpy(lv_MLU(s, l), lv_M(s, l), sizeof(double) * nl * bb);
+        for (int i = 0; i < nl; ++i)
+            if ((st = or_block_lu_factor_d(b, lv_MLU(s, l) + (size_t)i * bb, lv_Mpiv(s, l) + (size_t)i * b, i, NULL)))
+                return st;
+    }
 
     const int implicit = s->sch.implicit;
     if (implicit) {
         if ((st = or_fd_jacobian(m, p, s->mean, s->J, NULL))) return st;
         if ((st = or_build_lhs_mean(p, s->J, 1, s->sigma, s->sch.eps_relax, 5, s->A5))) return st;
         if ((st = or_ilu_factorize_d(p, s->A5, &s->ilu_mean))) return st;
-    } else {
-        if ((st = or_fd_jacobian(m, p, s->mean, NULL, s->P))) return st;
-        memcpy(s->PLU, s->P, sizeof(double) * n * bb);
-        for (int i = 0; i < n; ++i)
-            if ((st = or_block_lu_factor_d(b, s->PLU + (size_t)i * bb, s->Ppiv + (size_t)i * b, i, NULL))) return st;
+    } else {  /* assemble_diag_blocks per level (driver.cpp:183-186) */
+        for (int l = 0; l <= s->nlev; ++l) {
+            const int nl = lv_mesh(s, l)->n;
+            const or_pattern* pl = l == 0 ? p : &s->lev[l - 1].pat;
+            if ((st = or_fd_jacobian(lv_mesh(s, l), pl, lv_mean(s, l), NULL, lv_P(s, l)))) return st;
+            memcpy(lv_PLU(s, l), lv_P(s, l), sizeof(double) * nl * bb);
+            for (int i = 0; i < nl; ++i)
+                if ((st = or_block_lu_factor_d(b, lv_PLU(s, l) + (size_t)i * bb, lv_Ppiv(s, l) + (size_t)i * b, i,
+                                               NULL)))
+                    return st;
+        }
     }
     const double ga5 = gamma_factor(implicit, s->sigma, s->sch.eps_relax) * kAlpha[4];
 
@@ -1200,10 +1316,18 @@ int or_solver_phase_mean(or_solver* s, const double* hnorm, const int* nrep, con
     report_list mreps = {0};
     if (implicit)
         st = rk_step_d(&c, s->mean, n, b, 1, s->sigma, s->sch.eps_relax, s->sch.linear_tol, s->sch.linear_max_iter,
-                       p, s->A5, &s->ilu_mean, NULL, NULL, &mres, &mreps);
-    else
+                       p, s->A5, &s->ilu_mean, NULL, NULL, &mres, &mreps, NULL);
+    else if (s->nlev > 0) {  /* FAS V-cycle of the mean (driver.cpp:297-311) */
+        const double* pl[16];
+        const int* pv[16];
+        for (int l = 0; l <= s->nlev; ++l) {
+            pl[l] = lv_PLU(s, l);
+            pv[l] = lv_Ppiv(s, l);
+        }
+        st = mg_vcycle_d(s, -1, 0, s->mean, NULL, pl, pv, &mres);
+    } else
         st = rk_step_d(&c, s->mean, n, b, 0, s->sigma, s->sch.eps_relax, s->sch.linear_tol, s->sch.linear_max_iter,
-                       p, NULL, NULL, s->PLU, s->Ppiv, &mres, &mreps);
+                       p, NULL, NULL, s->PLU, s->Ppiv, &mres, &mreps, NULL);
     if (st) {
         free(hreps.v);
         free(mreps.v);
@@ -1294,4 +1418,32 @@ int or_solver_run(or_solver* s, int* n_entries, or_entry* entries, int max_entri
         }
     }
     return reason;
+}
+
+/* a coarse multigrid level below the current coarsest (explicit scheme; the reference's
+   build_hierarchy + per-level discretization, driver.cpp:104-131): mesh, pattern, parent
+   map from the current coarsest level's nodes, and the level's boundary forcing */
+int or_solver_add_level(or_solver* s, const or_mesh* m, const or_pattern* p, const int* parent, const ocplx* forcing,
+                        int nforcing) {
+    if (s->sch.implicit) return or_fail(OR_CONFIG, -1, -1, "multigrid is available for the explicit scheme only");
+    if (s->nlev >= 15) return or_fail(OR_CONFIG, -1, -1, "too many multigrid levels");
+    s->lev = (or_level*)realloc(s->lev, sizeof(or_level) * (s->nlev + 1));
+    or_level* v = &s->lev[s->nlev];
+    memset(v, 0, sizeof *v);
+    v->mesh = *m;
+    v->pat = *p;
+    v->parent = parent;
+    const size_t n = m->n, b = m->b, bb = b * b;
+    v->nforcing = nforcing;
+    v->forcing = (ocplx*)xcalloc((size_t)s->nh * nforcing, sizeof(ocplx));
+    if (nforcing) memcpy(v->forcing, forcing, sizeof(ocplx) * (size_t)s->nh * nforcing);
+    v->mean = (double*)xcalloc(n * b, sizeof(double));
+    v->M = (double*)xcalloc(n * bb, sizeof(double));
+    v->MLU = (double*)xcalloc(n * bb, sizeof(double));
+    v->P = (double*)xcalloc(n * bb, sizeof(double));
+    v->PLU = (double*)xcalloc(n * bb, sizeof(double));
+    v->Mpiv = (int*)xcalloc(n * b, sizeof(int));
+    v->Ppiv = (int*)xcalloc(n * b, sizeof(int));
+    s->nlev++;
+    return OR_OK;
 }

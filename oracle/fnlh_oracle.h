@@ -174,6 +174,10 @@ int or_solver_outer_iteration(or_solver* s, or_entry* e, double* resid_h);
 int or_solver_phase_harmonics(or_solver* s, const int* owned, double* hnorm_out);
 /* harmonic worker threads (SchemeConfig::workers, driver.cpp:246-265), process-wide */
 void or_set_workers(int w);
+/* append a coarse multigrid level (explicit scheme): parent maps the current coarsest
+   level's nodes to this level's; forcing is nh * nforcing complex */
+int or_solver_add_level(or_solver* s, const or_mesh* m, const or_pattern* p, const int* parent, const ocplx* forcing,
+                        int nforcing);
 int or_solver_harmonic_reports(const or_solver* s, int h, or_linear_report* out, int max);
 int or_solver_phase_mean(or_solver* s, const double* hnorm, const int* nrep, const or_linear_report* reps,
                          or_entry* e, double* resid_h);

@@ -244,6 +244,18 @@ class OracleSolver:
         except Exception:
             pass
 
+    def add_level(self, m, parent, forcing=None):
+        """Append a coarse multigrid level (explicit scheme): Mesh3D m, parent map from the
+        current coarsest level's nodes, the level's boundary forcing [nh, nforcing]."""
+        pat = m.pattern()
+        Mm = self.o.mesh(m)
+        P = self.o.pattern(pat)
+        par = np.ascontiguousarray(parent, np.int32)
+        fz = np.ascontiguousarray(forcing if forcing is not None else np.zeros((self.nh, 0)), np.complex128)
+        nf = fz.shape[-1] if self.nh else 0
+        self._keep += [Mm, P, pat, par, fz]
+        self.o._check(self.o.lib.or_solver_add_level(_p(self.h), C.byref(Mm), C.byref(P), ptr(par), ptr(fz), _i(nf)))
+
     def outer_iteration(self):
         e = OrEntry()
         rh = np.zeros(max(self.nh, 1))
@@ -412,8 +424,9 @@ class RefLib:
     def nozzle(self, case_text):
         return RefNozzle(self, case_text)
 
-    def solver(self, case_text, implicit=1, sigma=-1.0, eps=0.6, tol=1e-2, max_iter=10, drop=8.0, max_outer=2000):
-        return RefSolver(self, case_text, implicit, sigma, eps, tol, max_iter, drop, max_outer)
+    def solver(self, case_text, implicit=1, sigma=-1.0, eps=0.6, tol=1e-2, max_iter=10, drop=8.0, max_outer=2000,
+               mg_levels=1):
+        return RefSolver(self, case_text, implicit, sigma, eps, tol, max_iter, drop, max_outer, mg_levels)
 
 
 class RefNozzle:
@@ -509,10 +522,10 @@ class RefNozzle:
 
 
 class RefSolver:
-    def __init__(self, ref, case_text, implicit, sigma, eps, tol, max_iter, drop, max_outer):
+    def __init__(self, ref, case_text, implicit, sigma, eps, tol, max_iter, drop, max_outer, mg_levels=1):
         self.r = ref
         self.h = ref.lib.ref_solver_create(case_text.encode(), _i(implicit), _d(sigma), _d(eps), _d(tol),
-                                           _i(max_iter), _d(drop), _i(max_outer))
+                                           _i(max_iter), _d(drop), _i(max_outer), _i(mg_levels))
         if not self.h:
             raise CheckerError(1, ref.lib.ref_last_error().decode())
         self.noz = RefNozzle(ref, case_text)

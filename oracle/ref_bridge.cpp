@@ -373,7 +373,7 @@ int ref_nozzle_df(void* h, const double* mean, int nh, const int* index, const d
 // ---- full FnlhSolver (driver.hpp/.cpp) -------------------------------------
 
 void* ref_solver_create(const char* case_text, int implicit, double sigma, double eps, double tol, int max_iter,
-                        double drop_orders, int max_outer) {
+                        double drop_orders, int max_outer, int mg_levels) {
     FnlhSolver* s = nullptr;
     guarded([&] {
         SchemeConfig sc;
@@ -384,6 +384,7 @@ void* ref_solver_create(const char* case_text, int implicit, double sigma, doubl
         sc.linear_max_iter = max_iter;
         sc.target_drop_orders = drop_orders;
         sc.max_outer_iters = max_outer;
+        sc.mg_levels = mg_levels;
         s = new FnlhSolver(parse_case_text(case_text), sc);
     });
     return s;

@@ -51,6 +51,7 @@ class Mesh3D:
     partition: np.ndarray | None = None    # int32 [n]
     coords: np.ndarray | None = None       # float64 [n,3]
     n_boundary: int = 0
+    ijk: np.ndarray | None = None          # int64 [n,3] structured indices (coarsening), if any
 
     # --- sparsity pattern of the block LHS (sparse.cpp:61-117): adjacency + diagonal
     def pattern(self, b: int | None = None):
@@ -292,5 +293,120 @@ def structured_sector(ci, cj, ck, *, geometry="annular", length=2.0, pitch_deg=1
     if mu_range is not None:
         lo_, hi_ = np.log(mu_range[0]), np.log(mu_range[1])
         mu = np.exp(rng.uniform(lo_, hi_, size=n))
-    return from_faces(n, fa, fb, fbc, ford, fnv, vol_node[order], b=b, coords=coords[order], colour=col[order],
-                      mu=mu, nt_in=nt_in, **g)
+    m = from_faces(n, fa, fb, fbc, ford, fnv, vol_node[order], b=b, coords=coords[order], colour=col[order],
+                   mu=mu, nt_in=nt_in, **g)
+    m.ijk = np.stack([In.reshape(-1), Jn.reshape(-1), Kn.reshape(-1)], axis=1)[order].astype(np.int64)
+    return m
+
+
+# ---------------------------------------------------------------------------- multigrid
+def parent_map(ijk) -> np.ndarray:
+    """fine node -> coarse node of the 2x2x2 agglomeration of structured nodes (the 3D
+    counterpart of multigrid.cpp:9-24: pairwise in 1D, 2x2 in 2D).  Coarse nodes are
+    numbered in lexicographic (i, j, k) order of their index triple, so a line mesh gets the
+    reference's parent[i] = i / 2."""
+    c = np.asarray(ijk, np.int64) // 2
+    dims = c.max(axis=0) + 1
+    key = (c[:, 0] * dims[1] + c[:, 1]) * dims[2] + c[:, 2]
+    _, parent = np.unique(key, return_inverse=True)
+    return parent.astype(np.int32)
+
+
+def coarsen(m: Mesh3D, parent, forcing=None):
+    """Agglomerated coarse mesh (multigrid.cpp:41-127 restated for median-dual faces).
+
+    * coarse volume = child volumes summed in ascending fine order; coarse position and
+      eddy viscosity volume-weighted;
+    * coarse interior face between agglomerates P < Q = the fine faces crossing from P to
+      Q, normals summed in fine face order (one fine face per coarse face on a line mesh:
+      the reference's "areas transfer unchanged");
+    * coarse boundary face per (boundary kind, agglomerate), normals summed; its forcing
+      slot is the area-weighted mean of the children's (copied when there is one child);
+    * walls stay implicit: the closure is rebuilt from the coarse faces (from_faces).
+
+    Returns (coarse mesh, coarse forcing [nh, 3 * n_boundary] or None)."""
+    parent = np.asarray(parent, np.int64)
+    nc = int(parent.max()) + 1
+    vol = np.zeros(nc)
+    np.add.at(vol, parent, m.vol)
+    fn = m.fn.reshape(-1, 3)
+    interior = m.fbc < 0
+    P, Q, nrm = parent[m.fa[interior]], parent[m.fb[interior]], fn[interior]
+    keep = P != Q
+    P, Q, nrm = P[keep], Q[keep], nrm[keep]
+    sw = P > Q
+    P, Q = np.where(sw, Q, P), np.where(sw, P, Q)
+    nrm = np.where(sw[:, None], -nrm, nrm)
+    key = P * nc + Q
+    ukey, inv = np.unique(key, return_inverse=True)
+    cfn = np.zeros((len(ukey), 3))
+    np.add.at(cfn, inv, nrm)
+    live = np.any(cfn != 0.0, axis=1)  # a periodic pair of agglomerates can cancel exactly
+    ukey, cfn = ukey[live], cfn[live]
+    ca, cb = (ukey // nc).astype(np.int32), (ukey % nc).astype(np.int32)
+    # boundary faces, grouped per (kind, agglomerate)
+    bidx = np.flatnonzero(~interior)
+    bk, bp = m.fbc[bidx].astype(np.int64), parent[m.fa[bidx]]
+    bkey = bk * nc + bp
+    ubkey, binv = np.unique(bkey, return_inverse=True)
+    bfn = np.zeros((len(ubkey), 3))
+    np.add.at(bfn, binv, fn[bidx])
+    nbc = len(ubkey)
+    fa = np.concatenate([ca, (ubkey % nc).astype(np.int32)])
+    fb = np.concatenate([cb, -np.ones(nbc, np.int32)])
+    fbc = np.concatenate([-np.ones(len(ca), np.int32), (ubkey // nc).astype(np.int32)])
+    ford = np.concatenate([np.zeros(len(ca), np.int32), np.arange(nbc, dtype=np.int32)])
+    coords = None
+    if m.coords is not None:
+        coords = np.zeros((nc, 3))
+        np.add.at(coords, parent, m.coords * m.vol[:, None])
+        coords /= vol[:, None]
+    mu = np.zeros(nc)
+    np.add.at(mu, parent, m.mu * m.vol)
+    mu /= vol
+    c = from_faces(nc, fa, fb, fbc, ford, np.concatenate([cfn, bfn]), vol, b=m.b, gamma=m.gamma,
+                   gas_constant=m.gas_constant, p0=m.p0, T0=m.T0, p_out=m.p_out, nt_in=m.nt_in,
+                   forcing_scale=m.forcing_scale, coords=coords, mu=mu)
+    if m.ijk is not None:
+        ijk = np.zeros((nc, 3), np.int64)
+        ijk[parent] = np.asarray(m.ijk, np.int64) // 2
+        c.ijk = ijk
+    cf = None
+    if forcing is not None:
+        fz = np.asarray(forcing, np.complex128).reshape(len(forcing), -1, 3)  # [nh, n_boundary, 3]
+        ordv = m.ford[bidx]
+        area = m.farea[bidx]
+        cnt = np.bincount(binv, minlength=nbc)
+        num = np.zeros((fz.shape[0], nbc, 3), np.complex128)
+        den = np.zeros(nbc)
+        np.add.at(den, binv, area)
+        for h in range(fz.shape[0]):
+            np.add.at(num[h], binv, fz[h][ordv] * area[:, None])
+        cf = num / den[None, :, None]
+        single = np.flatnonzero(cnt == 1)
+        if len(single):
+            first = np.zeros(nbc, np.int64)
+            first[binv[::-1]] = np.arange(len(binv))[::-1]
+            cf[:, single, :] = fz[:, ordv[first[single]], :]
+        cf = cf.reshape(fz.shape[0], -1)
+    return c, cf
+
+
+def hierarchy(m: Mesh3D, levels: int, forcing=None):
+    """build_hierarchy (multigrid.cpp:129-140): [(mesh, parent-into-next, forcing)] per
+    level, finest first (parent is None on the coarsest)."""
+    if levels < 1:
+        raise ValueError("hierarchy needs at least one level")
+    if levels > 1 and m.ijk is None:
+        raise ValueError("coarsening needs structured node indices (Mesh3D.ijk)")
+    out = []
+    cur, cf = m, forcing
+    for lv in range(levels):
+        if lv + 1 < levels:
+            par = parent_map(cur.ijk)
+            nxt, nf = coarsen(cur, par, cf)
+            out.append((cur, par, cf))
+            cur, cf = nxt, nf
+        else:
+            out.append((cur, None, cf))
+    return out

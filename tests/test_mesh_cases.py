@@ -60,3 +60,42 @@ def test_c5_has_sa_scalar_and_eddy_viscosity():
     c = make_case("c5", scale=0.06)
     assert c.mesh.b == 6
     assert c.mesh.mu.min() >= 1e-6 and c.mesh.mu.max() <= 1e-3
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_agglomeration_hierarchy(name):
+    """2x2x2 agglomeration (mesh.coarsen, the 3D counterpart of multigrid.cpp:9-127):
+    volumes, closures and boundary areas are conserved level to level, every coarse node
+    has at most 8 children, and the coarse forcing is the children's area-weighted mean."""
+    from paper_2404_01407_b200.mesh import hierarchy
+    c = make_case(name, scale=0.08)
+    h = hierarchy(c.mesh, 3, c.forcing)
+    for lv in range(2):
+        mf, par, ff = h[lv]
+        mc, _, fc = h[lv + 1]
+        assert par.min() == 0 and par.max() == mc.n - 1
+        assert np.bincount(par).max() <= 8
+        vs = np.zeros(mc.n)
+        np.add.at(vs, par, mf.vol)
+        assert np.array_equal(vs, mc.vol)
+        cl = np.zeros((mc.n, 3))
+        np.add.at(cl, par, mf.closure.reshape(-1, 3))
+        scale = np.abs(mf.fn).max()
+        assert np.abs(cl - mc.closure.reshape(-1, 3)).max() < 1e-12 * scale
+        for kind in (0, 1):
+            af = mf.farea[mf.fbc == kind].sum()
+            ac = mc.farea[mc.fbc == kind].sum()
+            assert ac <= af * (1 + 1e-12)  # summed normals: equal on planar patches
+        assert fc.shape == (len(c.forcing), 3 * mc.n_boundary)
+        # a uniform forcing stays uniform
+        assert np.abs(np.abs(fc[:, 3 * np.flatnonzero(mc.fbc[mc.fbc >= 0] == 0) + 1]) - 1e-3 / 1.4).max() < 1e-15
+    assert h[2][1] is None
+
+
+def test_hierarchy_needs_structure():
+    from paper_2404_01407_b200.mesh import hierarchy
+    c = make_case("c1", scale=0.25)
+    c.mesh.ijk = None
+    with pytest.raises(ValueError):
+        hierarchy(c.mesh, 2)
+    assert len(hierarchy(c.mesh, 1)) == 1

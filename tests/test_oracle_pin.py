@@ -158,3 +158,35 @@ def test_oracle_harmonic_workers_bitwise():
     (h1, (m1, a1), r1), (h3, (m3, a3), r3) = out
     assert h1 == h3 and r1 == r3
     assert np.array_equal(m1, m3) and np.array_equal(a1, a3)
+
+
+@pytest.mark.parametrize("levels", [1, 2, 3])
+def test_nozzle_explicit_multigrid_history(ref, orc, levels):
+    """The explicit scheme with the FAS V-cycle (multigrid.cpp:142-232, driver.cpp:223-241,
+    297-311): the reference's FnlhSolver with mg_levels vs the restated hierarchy built by
+    mesh.hierarchy on the embedded line mesh (pairwise agglomeration: the reference's
+    coarse meshes, forcing and parent maps)."""
+    from paper_2404_01407_b200.mesh import hierarchy
+    case = NOZZLE_CASE.format(nx=64, nh=2)
+    rs = ref.solver(case, implicit=0, mg_levels=levels, sigma=1.0)  # CFL 2 diverges on this nozzle
+    noz = rs.noz
+    m = line_mesh_from_ref(noz)
+    m.ijk = np.stack([np.arange(noz.n), np.zeros(noz.n, np.int64), np.zeros(noz.n, np.int64)], axis=1)
+    forc = np.stack([forcing_triplets(f) for f in noz.forcing])
+    hier = hierarchy(m, levels, forc)
+    osv = orc.solver(m, noz.pattern(5), dict(implicit=0, sigma_cfl=1.0), noz.omega, forc,
+                     embed(noz.initial_mean(), noz.n))
+    for lv in range(1, levels):
+        mc, _, fc = hier[lv]
+        osv.add_level(mc, hier[lv - 1][1], fc)
+        assert mc.n == noz.n >> lv
+    s = np.sqrt(5 / 3)
+    for it in range(10):
+        er, eo = rs.outer_iteration(), osv.outer_iteration()
+        tol = 1e-12 if it == 0 else 1e-7
+        assert abs(eo["resid_mean"] * s / er["resid_mean"] - 1) < tol, (it, eo, er)
+        assert abs(eo["rz"] * s / er["rz"] - 1) < tol, (it, eo, er)
+    mr, ar = rs.state()
+    mo, ao = osv.state()
+    assert rel(extract(mo, noz.n), mr) < 1e-10
+    assert rel(np.stack([extract(a, noz.n) for a in ao]), ar) < 1e-8
