@@ -157,6 +157,15 @@ int fnlh_solver_create(const fnlh_mesh_desc* m, const int* row_ptr, const int* c
                        const fnlh_scheme* s, int nh, const int* index, const double* omega, const double* forcing,
                        int nforcing, const double* mean0, fnlh_solver** out);
 void fnlh_solver_destroy(fnlh_solver* s);
+/* FAS multigrid, explicit scheme only (SchemeConfig::mg_levels, driver.hpp:24; the levels of
+   build_hierarchy, multigrid.cpp:129-140, driver.cpp:104-131): append a coarse level below
+   the current coarsest -- its mesh and block pattern, parent[i] = its node agglomerating node
+   i of the current coarsest level, and its boundary forcing (nh x nforcing complex pairs).
+   Every level then runs the V-cycle of multigrid.cpp:184-214 (coarse levels first order, DF
+   on the finest level only).  ConfigError on an implicit solver. */
+int fnlh_solver_add_level(fnlh_solver* s, const fnlh_mesh_desc* m, const int* row_ptr, const int* col_idx,
+                          const int* parent, const double* forcing, int nforcing);
+int fnlh_solver_levels(const fnlh_solver* s);
 /* FnlhSolver::outer_iteration (driver.cpp:157-333) */
 int fnlh_solver_outer_iteration(fnlh_solver* s, fnlh_entry* e, double* resid_h);
 /* the same on host buffers: set_state(mean_in, amps_in) + outer_iteration + get_state into

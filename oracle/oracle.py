@@ -237,6 +237,12 @@ class OracleSolver:
         self.h = orc.lib.or_solver_create(C.byref(self.Mm), C.byref(self.P), C.byref(self.S), _i(self.nh),
                                           ptr(self._keep[0]), ptr(self._keep[1]), ptr(self._keep[2]), _i(nf),
                                           ptr(self._keep[3]))
+        levels = int(scheme.get("mg_levels", 1))
+        if levels > 1:  # the same 2x2x2 hierarchy the device solver builds
+            from paper_2404_01407_b200.mesh import hierarchy
+            hier = hierarchy(m, levels, self._keep[2] if self.nh else None)
+            for lv in range(1, levels):
+                self.add_level(hier[lv][0], hier[lv - 1][1], hier[lv][2])
 
     def __del__(self):
         try:

@@ -159,6 +159,13 @@ int fnlh_solver_create(const fnlh_mesh_desc* m, const int* row_ptr, const int* c
 
 void fnlh_solver_destroy(fnlh_solver* s) { delete s; }
 
+int fnlh_solver_add_level(fnlh_solver* s, const fnlh_mesh_desc* m, const int* row_ptr, const int* col_idx,
+                          const int* parent, const double* forcing, int nforcing) {
+    return guarded([&] { s->s->add_level(arrays(m), row_ptr, col_idx, parent, forcing, nforcing); });
+}
+
+int fnlh_solver_levels(const fnlh_solver* s) { return s->s->levels(); }
+
 int fnlh_solver_outer_iteration(fnlh_solver* s, fnlh_entry* e, double* resid_h) {
     return guarded([&] {
         ConvergenceEntry c = s->s->outer_iteration();

@@ -537,6 +537,16 @@ __global__ void k_rhs(const S* __restrict__ inv, const S* __restrict__ vb, S* __
 }
 
 template <class S>
+__global__ void k_rhs_forced(const S* __restrict__ inv, const S* __restrict__ vb, const S* __restrict__ f,
+                             S* __restrict__ rhs, std::size_t len) {
+    const std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x;
+    if (t >= len) return;
+    S r = inv[t] + vb[t];
+    r -= f[t];
+    rhs[t] = -r;
+}
+
+template <class S>
 __global__ void k_scale(S* __restrict__ x, double a, std::size_t len) {
     const std::size_t t = blockIdx.x * (std::size_t)blockDim.x + threadIdx.x;
     if (t >= len) return;
@@ -993,6 +1003,10 @@ void stage_rhs(const S* inv, const S* vb, S* rhs, std::size_t len, cudaStream_t 
     { ::fnlh::note_launch(); k_rhs<S><<<nb((long long)len), kT, 0, st>>>(inv, vb, rhs, len); }
 }
 template <class S>
+void stage_rhs_forced(const S* inv, const S* vb, const S* f, S* rhs, std::size_t len, cudaStream_t st) {
+    { ::fnlh::note_launch(); k_rhs_forced<S><<<nb((long long)len), kT, 0, st>>>(inv, vb, f, rhs, len); }
+}
+template <class S>
 void scale(S* x, double a, std::size_t len, cudaStream_t st) {
     { ::fnlh::note_launch(); k_scale<S><<<nb((long long)len), kT, 0, st>>>(x, a, len); }
 }
@@ -1018,6 +1032,7 @@ void apply_mean(int b, int n, double gamma, const double* base, const double* x,
 #define INST(S)                                                                         \
     template void stage_blend<S>(double, const S*, S*, std::size_t, cudaStream_t);      \
     template void stage_rhs<S>(const S*, const S*, S*, std::size_t, cudaStream_t);      \
+    template void stage_rhs_forced<S>(const S*, const S*, const S*, S*, std::size_t, cudaStream_t); \
     template void scale<S>(S*, double, std::size_t, cudaStream_t);                      \
     template void add_inplace<S>(S*, const S*, std::size_t, cudaStream_t);              \
     template void check_finite<S>(const S*, std::size_t, unsigned long long*, cudaStream_t);

@@ -113,6 +113,9 @@ template <class S>
 void stage_blend(double beta, const S* vis_fresh, S* vis_blend, std::size_t len, cudaStream_t st);
 template <class S>
 void stage_rhs(const S* inv, const S* vis_blend, S* rhs, std::size_t len, cudaStream_t st);
+// rhs = -((inv + vis_blend) - f): the FAS-forced stage right-hand side (coarse levels)
+template <class S>
+void stage_rhs_forced(const S* inv, const S* vis_blend, const S* f, S* rhs, std::size_t len, cudaStream_t st);
 template <class S>
 void scale(S* x, double a, std::size_t len, cudaStream_t st);
 template <class S>

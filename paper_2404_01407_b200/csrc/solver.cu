@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <type_traits>
 
 #include "solver.cuh"
 
@@ -30,6 +31,61 @@ __global__ void k_shifted_blocks(const double* __restrict__ P, const double* __r
         cplx v = mk(P[(size_t)i * b * b + k], 0.0);
         if (k / b == k % b) v = v + s;
         out[(size_t)i * b * b + k] = v;
+    }
+}
+
+// --- FAS multigrid transfers (multigrid.cpp:142-182), one thread per node -----------
+__device__ __forceinline__ double div_real(double a, double v) { return a / v; }
+__device__ __forceinline__ cplx div_real(cplx a, double v) { return mk(a.re / v, a.im / v); }
+
+// restrict_state: volume-weighted mean over the children, summed in ascending fine order
+template <class S>
+__global__ void k_restrict_state(const int* __restrict__ cptr, const int* __restrict__ cidx,
+                                 const double* __restrict__ vol, int b, int nc, const S* __restrict__ wf,
+                                 S* __restrict__ wc) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nc) return;
+    S acc[6];
+    for (int m = 0; m < b; ++m) acc[m] = zero<S>();
+    double v = 0.0;
+    for (int q = cptr[p]; q < cptr[p + 1]; ++q) {
+        const int i = cidx[q];
+        const double vi = vol[i];
+        v += vi;
+        for (int m = 0; m < b; ++m) acc[m] += vi * wf[(std::size_t)i * b + m];
+    }
+    for (int m = 0; m < b; ++m) wc[(std::size_t)p * b + m] = div_real(acc[m], v);
+}
+
+// restrict_residual of (r_f - F_f) and fas_forcing: rstar (= R_c(w_c0) on entry) -= sum
+template <class S>
+__global__ void k_restrict_fas(const int* __restrict__ cptr, const int* __restrict__ cidx, int b, int nc,
+                               const S* __restrict__ rf, const S* __restrict__ ff, S* __restrict__ rstar) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= nc) return;
+    S acc[6];
+    for (int m = 0; m < b; ++m) acc[m] = zero<S>();
+    for (int q = cptr[p]; q < cptr[p + 1]; ++q) {
+        const std::size_t i = (std::size_t)cidx[q] * b;
+        for (int m = 0; m < b; ++m) {
+            S t = rf[i + m];
+            if (ff) t -= ff[i + m];
+            acc[m] += t;
+        }
+    }
+    for (int m = 0; m < b; ++m) rstar[(std::size_t)p * b + m] -= acc[m];
+}
+
+// prolong_add of the coarse correction (injection): w_i += (w_c - w_c0)[parent_i]
+template <class S>
+__global__ void k_prolong(const int* __restrict__ parent, int b, int n, const S* __restrict__ wc,
+                          const S* __restrict__ wc0, S* __restrict__ w) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const std::size_t pc = (std::size_t)parent[i] * b;
+    for (int m = 0; m < b; ++m) {
+        const S dlt = wc[pc + m] - wc0[pc + m];
+        w[(std::size_t)i * b + m] += dlt;
     }
 }
 
@@ -152,7 +208,10 @@ std::size_t DeviceSolver::lhs_bytes() const {
         else
             for (const auto& ln : lanes_) s += ln->gf->bytes();
     }
-    else s = P_.bytes() + PLU_.bytes() + pclu_.bytes();
+    else {
+        s = P_.bytes() + PLU_.bytes() + pclu_.bytes();
+        for (const auto& c : mg_) s += c->P.bytes() + c->PLU.bytes() + c->pclu.bytes();
+    }
     return s;
 }
 
@@ -206,9 +265,10 @@ void DeviceSolver::rb_solve_async(const double* shift, const RbIlu<S>& f, const 
 template <class S, class Eval, class Apply, class Solve>
 RkStepResult DeviceSolver::rk_step(S* state, Eval&& eval, Apply&& apply, Solve&& solve, const S* pdiag_lu,
                                    const int* pdiag_piv, const std::string& field, const int* fac_status,
-                                   bool check_df) {
+                                   bool check_df, int level, const S* mg_forcing) {
     cudaStream_t st = ws_->stream;
-    const std::size_t len = disc_->len();
+    DeviceDisc* d = lv_disc(level);
+    const std::size_t len = d->len();
     S* state0 = reinterpret_cast<S*>(rk_[0].ptr);
     S* inv = reinterpret_cast<S*>(rk_[1].ptr);
     S* vis_fresh = reinterpret_cast<S*>(rk_[2].ptr);
@@ -228,17 +288,20 @@ RkStepResult DeviceSolver::rk_step(S* state, Eval&& eval, Apply&& apply, Solve&&
     for (int k = 1; k <= 5; ++k) {
         const double beta = kBeta[k - 1];
         const bool fresh = beta != 0.0;
-        disc_->redirect_err(stage_err_.ptr + (k - 1));
+        d->redirect_err(stage_err_.ptr + (k - 1));
         eval(stage, fresh, inv, vis_fresh);
-        disc_->redirect_err(nullptr);
+        d->redirect_err(nullptr);
         if (fresh) {
             ++res.viscous_evaluations;
             stage_blend<S>(beta, vis_fresh, vis_blend, len, st);
         }
-        stage_rhs<S>(inv, vis_blend, rhs, len, st);
+        if (mg_forcing)  // FAS forcing R* on coarse levels (multigrid.cpp:184-214)
+            stage_rhs_forced<S>(inv, vis_blend, mg_forcing, rhs, len, st);
+        else
+            stage_rhs<S>(inv, vis_blend, rhs, len, st);
         if (k == 1) norm2_sq<S>(rhs, len, ws_->scalars + 8, *ws_);
         if (!sch_.implicit) {
-            block_diag_solve<S>(disc_->b(), disc_->n(), pdiag_lu, pdiag_piv, rhs, x, st);
+            block_diag_solve<S>(d->b(), d->n(), pdiag_lu, pdiag_piv, rhs, x, st);
             scale<S>(x, gfac * kAlpha[k - 1], len, st);
         } else {
             scale<S>(rhs, kAlpha[k - 1], len, st);
@@ -248,10 +311,10 @@ RkStepResult DeviceSolver::rk_step(S* state, Eval&& eval, Apply&& apply, Solve&&
                 have_host[k - 1] = true;
             }
         }
-        disc_->redirect_err(stage_err_.ptr + 5 + (k - 1));
+        d->redirect_err(stage_err_.ptr + 5 + (k - 1));
         apply(state0, x, stage);
-        check_finite<S>(stage, len, disc_->err(), st);
-        disc_->redirect_err(nullptr);
+        check_finite<S>(stage, len, d->err(), st);
+        d->redirect_err(nullptr);
     }
     unsigned long long errs[11];
     RbControl ctls[5];
@@ -275,6 +338,158 @@ RkStepResult DeviceSolver::rk_step(S* state, Eval&& eval, Apply&& apply, Solve&&
     }
     check_step(errs, ctls, host_rep, have_host, field, res);
     FNLH_CUDA(cudaMemcpyAsync(state, stage, len * sizeof(S), cudaMemcpyDeviceToDevice, st));
+    return res;
+}
+
+void DeviceSolver::add_level(const MeshArrays& mesh, const int* row_ptr, const int* col_idx, const int* parent,
+                             const double* forcing_pairs, int nforcing) {
+    if (sch_.implicit) throw ConfigError("multigrid is available for the explicit scheme only");
+    DeviceDisc* fine = lv_disc(levels() - 1);
+    const int nf = fine->n(), nc = mesh.n;
+    if (mesh.b != disc_->b()) throw ShapeError("add_level: block size differs from the finest level");
+    // children lists of the coarse nodes in ascending fine order (the reference's loops)
+    std::vector<int> cptr(nc + 1, 0), cidx(nf);
+    for (int i = 0; i < nf; ++i) {
+        if (parent[i] < 0 || parent[i] >= nc) throw ShapeError("add_level: parent index out of range");
+        ++cptr[parent[i] + 1];
+    }
+    for (int p = 0; p < nc; ++p) {
+        if (cptr[p + 1] == 0) throw ShapeError("add_level: coarse node without children");
+        cptr[p + 1] += cptr[p];
+    }
+    {
+        std::vector<int> fill(cptr.begin(), cptr.end() - 1);
+        for (int i = 0; i < nf; ++i) cidx[fill[parent[i]]++] = i;
+    }
+    auto L = std::make_unique<MgLevel>();
+    L->pat = std::make_unique<DevicePattern>(mesh.b, mesh.n, row_ptr, col_idx, nullptr);
+    L->disc = std::make_unique<DeviceDisc>(mesh, L->pat.get());
+    L->parent.upload(parent, nf);
+    L->cptr.upload(cptr.data(), cptr.size());
+    L->cidx.upload(cidx.data(), cidx.size());
+    L->nforcing = nforcing;
+    L->forcing.alloc(std::max<std::size_t>((std::size_t)nh_ * nforcing, 1));
+    if (nh_ * nforcing)
+        FNLH_CUDA(cudaMemcpy(L->forcing.ptr, forcing_pairs, (std::size_t)nh_ * nforcing * sizeof(cplx),
+                             cudaMemcpyHostToDevice));
+    const std::size_t len = (std::size_t)nc * mesh.b, bb = (std::size_t)nc * mesh.b * mesh.b;
+    L->mean.alloc(len);
+    L->P.alloc(bb);
+    L->PLU.alloc(bb);
+    L->pclu.alloc(bb);
+    L->Ppiv.alloc(len);
+    L->pcpiv.alloc(len);
+    L->wc0.alloc(len);
+    L->wc.alloc(len);
+    L->rstar.alloc(len);
+    mg_.push_back(std::move(L));
+}
+
+// coarse means (driver.cpp:168-171) and their transform_jacobian validation (:172-176);
+// mg_diag_blocks: assemble_diag_blocks + LU per coarse level (:183-186)
+void DeviceSolver::mg_means() {
+    cudaStream_t st = ws_->stream;
+    for (int l = 1; l < levels(); ++l) {
+        MgLevel& c = *mg_[l - 1];
+        const int nc = c.disc->n();
+        ::fnlh::note_launch();
+        k_restrict_state<double><<<nb(nc), kT, 0, st>>>(c.cptr.ptr, c.cidx.ptr, lv_disc(l - 1)->view().vol, c.disc->b(),
+                                                         nc, lv_mean(l - 1), c.mean.ptr);
+    }
+    for (int l = 1; l < levels(); ++l) mg_[l - 1]->disc->validate(mg_[l - 1]->mean.ptr, st);
+}
+
+void DeviceSolver::mg_diag_blocks() {
+    cudaStream_t st = ws_->stream;
+    for (int l = 1; l < levels(); ++l) {
+        MgLevel& c = *mg_[l - 1];
+        const int nc = c.disc->n(), b = c.disc->b();
+        c.disc->fd_jacobian(c.mean.ptr, nullptr, c.P.ptr, st);
+        FNLH_CUDA(cudaMemcpyAsync(c.PLU.ptr, c.P.ptr, c.P.bytes(), cudaMemcpyDeviceToDevice, st));
+        const int init[2] = {0, 0x7fffffff};
+        FNLH_CUDA(cudaMemcpyAsync(ws_->status, init, sizeof init, cudaMemcpyHostToDevice, st));
+        block_diag_factor<double>(b, nc, c.PLU.ptr, c.Ppiv.ptr, ws_->status, st);
+        FNLH_CUDA(cudaMemcpyAsync(ws_->h_status, ws_->status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        FNLH_CUDA(cudaStreamSynchronize(st));
+        if (ws_->h_status[1] != 0x7fffffff) throw FactorizationError("singular pivot block", ws_->h_status[1]);
+    }
+}
+
+// LevelOps::full_residual (driver.cpp:230-236 harmonic, 300-306 mean): out = inv + vis
+// (+ DF on the finest mean level); raises the evaluation's own error
+template <class S>
+void DeviceSolver::mg_full_residual(int h, int l, const S* state, S* out, S* vis) {
+    cudaStream_t st = ws_->stream;
+    DeviceDisc* d = lv_disc(l);
+    const int order = l == 0 ? 2 : 1;
+    if constexpr (std::is_same<S, cplx>::value) {
+        d->linearized_residual(lv_mean(l), state, omega_[h], lv_forcing(l, h), lv_nforcing(l), order, true, out, vis,
+                               st);
+        add_inplace<cplx>(out, vis, d->len(), st);
+    } else {
+        d->residual(state, nullptr, order, 0, nullptr, 0, true, out, vis, st);
+        add_inplace<double>(out, vis, d->len(), st);
+        if (l == 0) add_inplace<double>(out, df_.ptr, d->len(), st);
+    }
+    d->raise_if_err(st, "full_residual");
+}
+
+// vcycle_level (multigrid.cpp:184-214): pre-smoothing RK step with the FAS forcing, then
+// restriction, the coarse problem, and the injected correction
+template <class S>
+RkStepResult DeviceSolver::mg_vcycle(int h, int l, S* w, const S* forcing, const std::string& field) {
+    cudaStream_t st = ws_->stream;
+    DeviceDisc* d = lv_disc(l);
+    const int n = d->n(), b = d->b();
+    const double gamma = d->view().gamma;
+    const int order = l == 0 ? 2 : 1;
+    const double* mean = lv_mean(l);
+    auto none = [&](const S*, S*, int, LinearSolveReport&) { return true; };
+    RkStepResult res;
+    if constexpr (std::is_same<S, cplx>::value) {
+        const double omega = omega_[h];
+        const cplx* hf = lv_forcing(l, h);
+        const int nfl = lv_nforcing(l);
+        auto eval = [&](const cplx* state, bool need_vis, cplx* inv, cplx* vis) {
+            d->linearized_residual(mean, state, omega, hf, nfl, order, need_vis, inv, vis, st);
+        };
+        auto apply = [&](const cplx* base, const cplx* x, cplx* out) {
+            apply_harmonic(b, n, gamma, mean, base, x, out, st);
+        };
+        res = rk_step<cplx>(w, eval, apply, none, l == 0 ? pclu_.ptr : mg_[l - 1]->pclu.ptr,
+                            l == 0 ? pcpiv_.ptr : mg_[l - 1]->pcpiv.ptr, field, nullptr, false, l, forcing);
+    } else {
+        auto eval = [&](const double* state, bool need_vis, double* inv, double* vis) {
+            d->residual(state, nullptr, order, 0, nullptr, 0, need_vis, inv, vis, st);
+            if (l == 0) add_inplace<double>(inv, df_.ptr, d->len(), st);  // DF on the finest level only
+        };
+        auto apply = [&](const double* base, const double* x, double* out) {
+            apply_mean(b, n, gamma, base, x, out, d->err(), st);
+        };
+        res = rk_step<double>(w, eval, apply, none, l == 0 ? PLU_.ptr : mg_[l - 1]->PLU.ptr,
+                              l == 0 ? Ppiv_.ptr : mg_[l - 1]->Ppiv.ptr, field, nullptr, l == 0, l, forcing);
+    }
+    if (l + 1 >= levels()) return res;
+    MgLevel& c = *mg_[l];
+    const int nc = c.disc->n();
+    S* wc0 = reinterpret_cast<S*>(c.wc0.ptr);
+    S* wc = reinterpret_cast<S*>(c.wc.ptr);
+    S* rstar = reinterpret_cast<S*>(c.rstar.ptr);
+    S* rf = reinterpret_cast<S*>(rk_[1].ptr);  // the RK scratch is free between steps
+    S* vf = reinterpret_cast<S*>(rk_[2].ptr);
+    { ::fnlh::note_launch(); k_restrict_state<S><<<nb(nc), kT, 0, st>>>(c.cptr.ptr, c.cidx.ptr, d->view().vol, b, nc, w, wc0); }
+    mg_full_residual<S>(h, l, w, rf, vf);
+    mg_full_residual<S>(h, l + 1, wc0, rstar, vf);
+    { ::fnlh::note_launch(); k_restrict_fas<S><<<nb(nc), kT, 0, st>>>(c.cptr.ptr, c.cidx.ptr, b, nc, rf, forcing, rstar); }
+    FNLH_CUDA(cudaMemcpyAsync(wc, wc0, (std::size_t)nc * b * sizeof(S), cudaMemcpyDeviceToDevice, st));
+    mg_vcycle<S>(h, l + 1, wc, rstar, field);
+    { ::fnlh::note_launch(); k_prolong<S><<<nb(n), kT, 0, st>>>(c.parent.ptr, b, n, wc, wc0, w); }
+    d->reset_err(st);
+    check_finite<S>(w, d->len(), d->err(), st);
+    if (d->read_err(st)) {
+        d->reset_err(st);
+        throw DivergenceError("non-finite state after coarse-grid correction", 0, field);
+    }
     return res;
 }
 
@@ -492,6 +707,7 @@ void DeviceSolver::phase_harmonics(const int* owned) {
             ilu_factorize<double>(Am, *ilu_mean_, *ws_);
         }
     } else {
+        if (!mg_.empty()) mg_means();
         disc_->fd_jacobian(mean_.ptr, nullptr, P_.ptr, st);  // assemble_diag_blocks (disc.cpp:31-35)
         FNLH_CUDA(cudaMemcpyAsync(PLU_.ptr, P_.ptr, P_.bytes(), cudaMemcpyDeviceToDevice, st));
         const int init[2] = {0, 0x7fffffff};
@@ -500,6 +716,7 @@ void DeviceSolver::phase_harmonics(const int* owned) {
         FNLH_CUDA(cudaMemcpyAsync(ws_->h_status, ws_->status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
         FNLH_CUDA(cudaStreamSynchronize(st));
         if (ws_->h_status[1] != 0x7fffffff) throw FactorizationError("singular pivot block", ws_->h_status[1]);
+        if (!mg_.empty()) mg_diag_blocks();
     }
 
     FNLH_CUDA(cudaEventRecord(evp_[0], st));  // phase marks: J + A5 + mean ILU done
@@ -560,8 +777,23 @@ void DeviceSolver::phase_harmonics(const int* owned) {
                     FNLH_CUDA(cudaMemcpyAsync(ws_->h_status, ws_->status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
                     FNLH_CUDA(cudaStreamSynchronize(st));
                     if (ws_->h_status[1] != 0x7fffffff) throw FactorizationError("singular pivot block", ws_->h_status[1]);
-                    auto none = [&](const cplx*, cplx*, int, LinearSolveReport&) { return true; };
-                    step = rk_step<cplx>(amp, eval, apply, none, pclu_.ptr, pcpiv_.ptr, name);
+                    for (int l = 1; l < levels(); ++l) {  // shifted_blocks per level (driver.cpp:224-229)
+                        MgLevel& c = *mg_[l - 1];
+                        const int nc = c.disc->n();
+                        shifted_blocks(c.P.ptr, c.disc->view().vol, b, nc, omega, c.pclu.ptr, st);
+                        FNLH_CUDA(cudaMemcpyAsync(ws_->status, init, sizeof init, cudaMemcpyHostToDevice, st));
+                        block_diag_factor<cplx>(b, nc, c.pclu.ptr, c.pcpiv.ptr, ws_->status, st);
+                        FNLH_CUDA(cudaMemcpyAsync(ws_->h_status, ws_->status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+                        FNLH_CUDA(cudaStreamSynchronize(st));
+                        if (ws_->h_status[1] != 0x7fffffff)
+                            throw FactorizationError("singular pivot block", ws_->h_status[1]);
+                    }
+                    if (!mg_.empty()) {
+                        step = mg_vcycle<cplx>(h, 0, amp, nullptr, name);
+                    } else {
+                        auto none = [&](const cplx*, cplx*, int, LinearSolveReport&) { return true; };
+                        step = rk_step<cplx>(amp, eval, apply, none, pclu_.ptr, pcpiv_.ptr, name);
+                    }
                 }
                 h_norm[h] = step.stage1_residual_norm;
                 h_reps[h] = std::move(step.linear_reports);
@@ -625,6 +857,8 @@ ConvergenceEntry DeviceSolver::phase_mean(const std::vector<double>& h_norm,
             return true;
         };
         mstep = rk_step<double>(mean_.ptr, mean_eval, mean_apply, solve, nullptr, nullptr, "mean", nullptr, true);
+    } else if (!mg_.empty()) {  // FAS V-cycle of the mean (driver.cpp:297-311)
+        mstep = mg_vcycle<double>(-1, 0, mean_.ptr, nullptr, "mean");
     } else {
         auto none = [&](const double*, double*, int, LinearSolveReport&) { return true; };
         mstep = rk_step<double>(mean_.ptr, mean_eval, mean_apply, none, PLU_.ptr, Ppiv_.ptr, "mean", nullptr, true);

@@ -47,6 +47,23 @@ struct HarmonicLane {
     }
 };
 
+// a coarse multigrid level (multigrid.hpp:26-32; the explicit scheme only, driver.cpp:101-131):
+// its discretization on the agglomerated mesh, the parent map from the next finer level and
+// the children lists of its own nodes (ascending fine index: the reference's summation
+// order), its boundary forcing, the per-level mean / diagonal blocks, and the V-cycle
+// vectors that live across the recursion (complex-sized, reinterpreted for the mean)
+struct MgLevel {
+    std::unique_ptr<DevicePattern> pat;
+    std::unique_ptr<DeviceDisc> disc;
+    DeviceBuffer<int> parent, cptr, cidx;
+    DeviceBuffer<cplx> forcing;  // nh x nforcing
+    int nforcing = 0;
+    DeviceBuffer<double> mean, P, PLU;
+    DeviceBuffer<int> Ppiv, pcpiv;
+    DeviceBuffer<cplx> pclu;
+    DeviceBuffer<cplx> wc0, wc, rstar;
+};
+
 struct ConvergenceEntry {  // driver.hpp:50-58
     int iter = 0;
     double resid_mean = 0.0;
@@ -88,6 +105,11 @@ public:
     // copy harmonic h's field to / from device memory owned by the caller (exchange buffers)
     void copy_amps(int h, void* dev, bool to_dev);
     int run_to_convergence(std::vector<ConvergenceEntry>& history);  // 0 target, 1 cap, 2 divergence
+    // append a coarse level below the current coarsest (explicit scheme): its mesh and
+    // pattern, parent[n of the current coarsest] -> its nodes, its boundary forcing
+    void add_level(const MeshArrays& mesh, const int* row_ptr, const int* col_idx, const int* parent,
+                   const double* forcing_pairs, int nforcing);
+    int levels() const { return 1 + static_cast<int>(mg_.size()); }
 
     void get_state(double* mean, double* amps_pairs) const;
     void set_state(const double* mean, const double* amps_pairs);
@@ -121,7 +143,22 @@ public:
 private:
     template <class S, class Eval, class Apply, class Solve>
     RkStepResult rk_step(S* state, Eval&& eval, Apply&& apply, Solve&& solve, const S* pdiag_lu, const int* pdiag_piv,
-                         const std::string& field, const int* fac_status = nullptr, bool check_df = false);
+                         const std::string& field, const int* fac_status = nullptr, bool check_df = false,
+                         int level = 0, const S* mg_forcing = nullptr);
+    // the FAS V-cycle from level l (multigrid.cpp:184-214); h = harmonic position, -1 = mean
+    template <class S>
+    RkStepResult mg_vcycle(int h, int l, S* w, const S* forcing, const std::string& field);
+    template <class S>
+    void mg_full_residual(int h, int l, const S* state, S* out, S* vis);
+    DeviceDisc* lv_disc(int l) const { return l == 0 ? disc_.get() : mg_[l - 1]->disc.get(); }
+    double* lv_mean(int l) const { return l == 0 ? mean_.ptr : mg_[l - 1]->mean.ptr; }
+    const cplx* lv_forcing(int l, int h) const {
+        return l == 0 ? forcing_.ptr + (std::size_t)h * nforcing_ : mg_[l - 1]->forcing.ptr + (std::size_t)h * mg_[l - 1]->nforcing;
+    }
+    int lv_nforcing(int l) const { return l == 0 ? nforcing_ : mg_[l - 1]->nforcing; }
+    void mg_means();        // coarse means and their validation
+    void mg_diag_blocks();  // P and its LU per coarse level
+    std::vector<std::unique_ptr<MgLevel>> mg_;
     template <class S>
     void rb_solve_async(const double* shift, const RbIlu<S>& f, const S* rhs, S* x, RbControl* ctl);
     // device records of one RK step -> the reference's exceptions (stage order) + reports

@@ -120,6 +120,30 @@ class FnlhSolver:
                                        ptr(pat["partition"]), C.byref(self.scheme), _i(self.nh), ptr(idx), ptr(om),
                                        ptr(forc), _i(nforcing), ptr(f64(mean0)), C.byref(h)))
         self.h = h
+        self.hierarchy = None
+        levels = int(scheme.get("mg_levels", 1))
+        if levels > 1:  # SchemeConfig::mg_levels (driver.hpp:24): 2x2x2 agglomeration, mesh.hierarchy
+            from .mesh import hierarchy
+            self.hierarchy = hierarchy(mesh, levels, fz if self.nh else None)
+            for lv in range(1, levels):
+                self.add_level(self.hierarchy[lv][0], self.hierarchy[lv - 1][1], self.hierarchy[lv][2])
+
+    def add_level(self, mesh, parent, forcing=None):
+        """Append a coarse multigrid level (explicit scheme): its mesh, parent[i] = its node
+        agglomerating node i of the current coarsest level, its boundary forcing [nh, nf]."""
+        pat = mesh.pattern()
+        par = np.ascontiguousarray(parent, np.int32)
+        fz = np.asarray(forcing, np.complex128).reshape(self.nh, -1) if (self.nh and forcing is not None) else \
+            np.zeros((self.nh, 0), np.complex128)
+        forc = as_pairs(fz.reshape(-1)) if fz.size else np.zeros(2)
+        keep = [pat["row_ptr"], pat["col_idx"], par, forc]
+        desc = _desc(mesh, keep)
+        self._keep += keep + [desc]
+        check(lib().fnlh_solver_add_level(self.h, C.byref(desc), ptr(pat["row_ptr"]), ptr(pat["col_idx"]), ptr(par),
+                                          ptr(forc), _i(fz.shape[1] if self.nh else 0)))
+
+    def levels(self):
+        return lib().fnlh_solver_levels(self.h)
 
     def __del__(self):
         try:

@@ -273,3 +273,61 @@ def test_outer_iteration_host_buffers():
         eb = b.outer_iteration_host(mp, ap)
         assert ea["resid_mean"] == eb["resid_mean"] and ea["rz"] == eb["rz"]
         assert np.array_equal(mp, mean) and np.array_equal(ap, amps)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,levels,workers", [("c2", 2, 1), ("c2", 3, 3), ("c5", 2, 1), ("c1", 3, 1)])
+def test_explicit_multigrid(orc_dev, name, levels, workers):
+    """Explicit scheme with the FAS V-cycle (multigrid.cpp:184-214, driver.cpp:223-241,
+    297-311) on the 2x2x2 hierarchy: device levels vs the restated V-cycle."""
+    from paper_2404_01407_b200.solver import FnlhSolver
+    c = make_case(name, scale=0.1, nh=2, implicit=False, workers=workers)
+    c.scheme["sigma_cfl"] = 1.0
+    c.scheme["mg_levels"] = levels
+    g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
+    assert g.levels() == levels
+    o = orc_dev.solver(c.mesh, c.mesh.pattern(), c.scheme, c.omegas, c.forcing, c.mean0)
+    for it in range(4):
+        eg, eo = g.outer_iteration(), o.outer_iteration()
+        assert abs(eg["resid_mean"] / eo["resid_mean"] - 1) < 1e-8, (it, eg, eo)
+        assert abs(eg["rz"] / eo["rz"] - 1) < 1e-8, (it, eg, eo)
+    mg, ag = g.state()
+    mo, ao = o.state()
+    assert rel(mg, mo) < 1e-10 and rel(ag, ao) < 1e-10
+
+
+@pytest.mark.gpu
+def test_multigrid_config_errors():
+    from paper_2404_01407_b200.solver import FnlhSolver
+    from paper_2404_01407_b200.mesh import hierarchy
+    c = make_case("c1", scale=0.25, nh=1)
+    g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)  # implicit
+    h = hierarchy(c.mesh, 2, c.forcing)
+    with pytest.raises(Exception, match="explicit"):
+        g.add_level(h[1][0], h[0][1], h[1][2])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("levels", [2, 3])
+def test_nozzle_multigrid_against_reference(ref, levels):
+    """The reference's FnlhSolver with mg_levels (explicit, CFL 1) vs the device V-cycle on
+    the embedded line mesh: pairwise agglomeration reproduces the reference hierarchy."""
+    from paper_2404_01407_b200.solver import FnlhSolver
+    case = NOZZLE_CASE.format(nx=64, nh=2)
+    rs = ref.solver(case, implicit=0, mg_levels=levels, sigma=1.0)
+    noz = rs.noz
+    m = line_mesh_from_ref(noz)
+    m.ijk = np.stack([np.arange(noz.n), np.zeros(noz.n, np.int64), np.zeros(noz.n, np.int64)], axis=1)
+    forc = np.stack([forcing_triplets(f) for f in noz.forcing])
+    g = FnlhSolver(m, dict(implicit=0, sigma_cfl=1.0, mg_levels=levels), noz.omega, forc,
+                   embed(noz.initial_mean(), noz.n), pattern=noz.pattern(5))
+    s = np.sqrt(5 / 3)
+    for it in range(10):
+        er, eg = rs.outer_iteration(), g.outer_iteration()
+        tol = 1e-12 if it == 0 else 1e-7
+        assert abs(eg["resid_mean"] * s / er["resid_mean"] - 1) < tol, (it, eg, er)
+        assert abs(eg["rz"] * s / er["rz"] - 1) < tol, (it, eg, er)
+    mr, ar = rs.state()
+    mg, ag = g.state()
+    assert rel(extract(mg, noz.n), mr) < 1e-10
+    assert rel(np.stack([extract(a, noz.n) for a in ag]), ar) < 1e-8
