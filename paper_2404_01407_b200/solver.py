@@ -205,7 +205,7 @@ class FnlhSolver:
         reason, n = _i(), _i()
         arr = (Entry * max_entries)()
         check(lib().fnlh_solver_run(self.h, C.byref(reason), C.byref(n), arr, _i(max_entries)))
-        hist = [dict(iter=e.iter, resid_mean=e.resid_mean, rz=e.rz) for e in arr[: min(n.value, max_entries)]]
+        hist = [dict(iter=e.iter, resid_mean=e.resid_mean, rz=e.rz, seconds=e.seconds) for e in arr[: min(n.value, max_entries)]]
         return ["target-drop", "iteration-cap", "divergence"][reason.value], hist
 
     def state(self, out=None):

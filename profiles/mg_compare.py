@@ -1,0 +1,64 @@
+"""Implicit FNLH vs explicit RK(5,3) single grid vs explicit + FAS V-cycle (2, 3 levels):
+outer iterations and device seconds to drop the mean and harmonic residuals by `drop`
+orders (run_to_convergence semantics, driver.cpp:335-379) on one seeded configuration.
+The paper's comparison (PAPER.md: implicit 7-10x faster than explicit multigrid) restated
+on the synthetic C2 geometry at reduced size.  Usage: python profiles/mg_compare.py
+[--scale 0.25] [--drop 3] [--max 4000] [--cfl-explicit 1.0]"""
+import argparse
+import json
+import sys
+import time
+import os
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2404_01407_b200.cases import make_case  # noqa: E402
+from paper_2404_01407_b200.solver import FnlhSolver  # noqa: E402
+
+
+def run(name, scale, nh, scheme_over, drop, cap):
+    c = make_case(name, scale=scale, nh=nh, implicit=scheme_over.get("implicit", 1) == 1)
+    c.scheme.update(scheme_over)
+    c.scheme["target_drop_orders"] = drop
+    c.scheme["max_outer_iters"] = cap
+    t0 = time.time()
+    g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
+    setup = time.time() - t0
+    t0 = time.time()
+    try:
+        reason, hist = g.run_to_convergence()
+    except Exception as ex:  # a non-divergence error ends the run (propagates in the reference)
+        return dict(n=c.mesh.n, levels=g.levels(), reason=f"error: {ex}", iters=None, device_s=None)
+    wall = time.time() - t0
+    last = hist[-1] if hist else {}
+    return dict(n=c.mesh.n, levels=g.levels(), reason=reason, iters=len(hist), device_s=last.get("seconds", 0.0),
+                wall_s=wall, setup_s=setup, r0=hist[0]["resid_mean"] if hist else None,
+                r_end=last.get("resid_mean"), rz_end=last.get("rz"))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", default="c2")
+    ap.add_argument("--scale", type=float, default=0.25)
+    ap.add_argument("--nh", type=int, default=2)
+    ap.add_argument("--drop", type=float, default=3.0)
+    ap.add_argument("--max", type=int, default=4000)
+    ap.add_argument("--cfl-explicit", type=float, default=1.0)
+    ap.add_argument("--arms", default="implicit,explicit_1grid,explicit_mg2,explicit_mg3")
+    a = ap.parse_args()
+    arms = {
+        "implicit": dict(implicit=1, workers=a.nh),
+        "explicit_1grid": dict(implicit=0, sigma_cfl=a.cfl_explicit),
+        "explicit_mg2": dict(implicit=0, sigma_cfl=a.cfl_explicit, mg_levels=2),
+        "explicit_mg3": dict(implicit=0, sigma_cfl=a.cfl_explicit, mg_levels=3),
+    }
+    out = {}
+    for k, v in arms.items():
+        if k not in a.arms.split(","):
+            continue
+        out[k] = run(a.case, a.scale, a.nh, v, a.drop, a.max)
+        print(k, json.dumps(out[k]), flush=True)
+    print(json.dumps(dict(case=a.case, scale=a.scale, nh=a.nh, drop=a.drop, arms=out)))
+
+
+if __name__ == "__main__":
+    main()
