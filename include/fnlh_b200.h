@@ -33,6 +33,7 @@ enum fnlh_status {
 typedef struct fnlh_pattern fnlh_pattern;
 typedef struct fnlh_disc fnlh_disc;
 typedef struct fnlh_solver fnlh_solver;
+typedef struct fnlh_sector_dual fnlh_sector_dual;
 
 /* LinearSolveReport (sparse.hpp:231-236) */
 typedef struct {
@@ -210,6 +211,32 @@ int fnlh_solver_info(const fnlh_solver* s, double* out);
 /* counters (7 doubles): [sweeps, block-row updates, last outer iteration device ms, and its
    split: J + A5 + mean ILU, harmonic RK steps (+ exchange), DF, mean RK step (ms)] */
 int fnlh_solver_counters(const fnlh_solver* s, double* out);
+
+/* ---- device mesh preprocessing (csrc/meshgen.cu) ----------------
+   Median-dual geometry of a structured ci x cj x ck sector (hex cells, or each hex split
+   into 6 Kuhn tets), periodic in j or not.  Xu: unwrapped node coordinates
+   [(ci+1)(cj+1)(ck+1)][3], node (i, j, k) at ((i (cj+1) + j)(ck+1) + k); mesh nodes are
+   (i, j mod nj, k) with nj = cj (periodic) or cj + 1.  Produces the unique edges (ea < eb,
+   ascending), their summed dual-face normals en [ne][3] and the node volumes [n],
+   bitwise equal to paper_2404_01407_b200/mesh.py::_sector_dual_host.  No reference
+   counterpart: the reference's meshes are the quasi-1D nozzle's (mesh.cpp). */
+int fnlh_sector_dual_create(int ci, int cj, int ck, int periodic_j, int tets, const double* Xu, long long* n_edges,
+                            fnlh_sector_dual** out);
+int fnlh_sector_dual_get(const fnlh_sector_dual* h, long long* ea, long long* eb, double* en, double* vol);
+void fnlh_sector_dual_destroy(fnlh_sector_dual* h);
+/* make_pattern (sparse.cpp:91-117) on the device: block-CSR pattern of `rows` rows from the
+   diagonal and both directions of every edge (ea[k], eb[k]), columns sorted and unique per
+   row.  row_ptr [rows+1], col_idx [capacity rows + 2 n_edges], diag_idx [rows]; *nnzb =
+   entries written.  ShapeError on an endpoint outside [0, rows). */
+int fnlh_make_pattern(int rows, long long n_edges, const int* ea, const int* eb, int* row_ptr, int* col_idx,
+                      int* diag_idx, long long* nnzb);
+/* Mesh::build_adjacency (mesh.cpp:44-59) and the derived arrays of mesh.py::from_faces on
+   the device: per face (fa, fb = -1 on boundary faces, fn [nf][3]) the area, unit normal
+   and viscous weight area / |x_fb - x_fa| (0 on boundary faces or without coords); per
+   node its faces in ascending order (nf_ptr [n+1], nf_idx [capacity 2 nf]), the closure
+   sum_f (+-fn_f) accumulated from 0.0 in face order, and the boundary flag. */
+int fnlh_mesh_derive(int n, int nf, const int* fa, const int* fb, const double* fn, const double* coords,
+                     double* farea, double* fnh, double* fvis, int* nf_ptr, int* nf_idx, double* closure, int* bflag);
 
 #ifdef __cplusplus
 }

@@ -348,6 +348,27 @@ class RefLib:
         return (int(pat["b"]), len(pat["row_ptr"]) - 1, ptr(pat["row_ptr"]), ptr(pat["col_idx"]),
                 None if part is None else ptr(part))
 
+    def make_pattern(self, b, rows, ea, eb):
+        """The reference's make_pattern (sparse.cpp:91-117) on an edge list."""
+        ea = np.ascontiguousarray(ea, np.int32)
+        eb = np.ascontiguousarray(eb, np.int32)
+        row_ptr = np.empty(rows + 1, np.int32)
+        col_idx = np.empty(rows + 2 * len(ea), np.int32)
+        diag = np.empty(rows, np.int32)
+        nnz = C.c_longlong()
+        self._check(self.lib.ref_make_pattern(_i(b), _i(rows), C.c_longlong(len(ea)), ptr(ea), ptr(eb), ptr(row_ptr),
+                                              ptr(col_idx), ptr(diag), C.byref(nnz)))
+        return dict(row_ptr=row_ptr, col_idx=col_idx[: nnz.value].copy(), diag_idx=diag)
+
+    def build_adjacency(self, n, fa, fb):
+        """Mesh::build_adjacency (mesh.cpp:44-59) on a face list (fb = -1 on boundary faces)."""
+        fa = np.ascontiguousarray(fa, np.int32)
+        fb = np.ascontiguousarray(fb, np.int32)
+        nf_ptr = np.empty(n + 1, np.int32)
+        nf_idx = np.empty(2 * len(fa), np.int32)
+        self._check(self.lib.ref_build_adjacency(_i(n), _i(len(fa)), ptr(fa), ptr(fb), ptr(nf_ptr), ptr(nf_idx)))
+        return nf_ptr, nf_idx[: nf_ptr[n]].copy()
+
     def ilu_factorize(self, pat, A):
         cplx = np.iscomplexobj(A)
         dt = np.complex128 if cplx else np.float64

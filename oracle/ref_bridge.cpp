@@ -229,6 +229,39 @@ int ref_build_lhs_mean(int b, int rows, const int* row_ptr, const int* col_idx, 
     });
 }
 
+// ---- pattern / adjacency builders (sparse.cpp:91-117, mesh.cpp:44-59) ----------
+
+// make_pattern on an edge list; col_idx capacity rows + 2 ne; returns nnzb in *nnz
+int ref_make_pattern(int b, int rows, long long ne, const int* ea, const int* eb, int* row_ptr, int* col_idx,
+                     int* diag_idx, long long* nnz) {
+    return guarded([&] {
+        std::vector<std::pair<int, int>> edges(ne);
+        for (long long k = 0; k < ne; ++k) edges[k] = {ea[k], eb[k]};
+        PatternPtr p = make_pattern(b, rows, edges, {});
+        std::copy(p->row_ptr.begin(), p->row_ptr.end(), row_ptr);
+        std::copy(p->col_idx.begin(), p->col_idx.end(), col_idx);
+        std::copy(p->diag_idx.begin(), p->diag_idx.end(), diag_idx);
+        *nnz = static_cast<long long>(p->col_idx.size());
+    });
+}
+
+// Mesh::build_adjacency on a face list (fb = -1: boundary face)
+int ref_build_adjacency(int n, int nf, const int* fa, const int* fb, int* nf_ptr, int* nf_idx) {
+    return guarded([&] {
+        Mesh m;
+        m.volume.assign(n, 1.0);
+        m.faces.resize(nf);
+        for (int f = 0; f < nf; ++f) {
+            m.faces[f].a = fa[f];
+            m.faces[f].b = fb[f];
+            m.faces[f].boundary = fb[f] < 0 ? kBoundaryWest : kInterior;
+        }
+        m.build_adjacency();
+        std::copy(m.node_face_ptr.begin(), m.node_face_ptr.end(), nf_ptr);
+        std::copy(m.node_face_idx.begin(), m.node_face_idx.end(), nf_idx);
+    });
+}
+
 // ---- nozzle case (the reference's own quasi-1D Euler discretization) ----------
 
 void* ref_nozzle_create(const char* case_text) {

@@ -54,9 +54,14 @@ class Mesh3D:
     ijk: np.ndarray | None = None          # int64 [n,3] structured indices (coarsening), if any
 
     # --- sparsity pattern of the block LHS (sparse.cpp:61-117): adjacency + diagonal
-    def pattern(self, b: int | None = None):
+    def pattern(self, b: int | None = None, device: bool | None = None):
         n = self.n
         interior = self.fbc < 0
+        if device is None:
+            device = _device_available()
+        if device:
+            return make_pattern_device(n, self.fa[interior], self.fb[interior], self.b if b is None else b,
+                                       self.partition)
         a = self.fa[interior].astype(np.int64)
         c = self.fb[interior].astype(np.int64)
         rows = np.concatenate([np.arange(n), a, c])
@@ -76,20 +81,43 @@ class Mesh3D:
 
 
 def from_faces(n, fa, fb, fbc, ford, fn, vol, *, b=5, gamma=1.4, gas_constant=287.05, p0=101325.0, T0=300.0,
-               p_out=98000.0, nt_in=0.0, forcing_scale=None, coords=None, mu=None, colour=None, partition=None):
+               p_out=98000.0, nt_in=0.0, forcing_scale=None, coords=None, mu=None, colour=None, partition=None,
+               device=None):
     """Assemble the derived arrays (areas, unit normals, node->face CSR in ascending face
-    order as mesh.cpp:44-59, slip-wall closure accumulated in face order)."""
+    order as mesh.cpp:44-59, slip-wall closure accumulated in face order) -- on the device
+    (csrc/meshgen.cu, fnlh_mesh_derive) when one is present, else the host restatement."""
     fa = np.ascontiguousarray(fa, np.int32)
     fb = np.ascontiguousarray(fb, np.int32)
     fbc = np.ascontiguousarray(fbc, np.int32)
     ford = np.ascontiguousarray(ford, np.int32)
     fn = np.ascontiguousarray(np.asarray(fn, np.float64).reshape(-1, 3))
     nf = len(fa)
-    farea = np.sqrt(fn[:, 0] * fn[:, 0] + fn[:, 1] * fn[:, 1] + fn[:, 2] * fn[:, 2])
-    fnh = fn / farea[:, None]
     interior = fbc < 0
+    if device is None:
+        device = _device_available()
+    derive = _derive_device if device else _derive_host
+    farea, fnh, fvis, nf_ptr, nf_idx, closure, bflag = derive(n, fa, np.where(interior, fb, -1).astype(np.int32), fn,
+                                                              coords)
+    m = Mesh3D(n=n, nf=nf, b=b, fa=fa, fb=fb, fbc=fbc, ford=ford, fn=fn.reshape(-1).copy(), farea=farea,
+               fnh=np.ascontiguousarray(fnh.reshape(-1)), fvis=fvis, vol=np.ascontiguousarray(vol, np.float64),
+               closure=closure.reshape(-1).copy(),
+               mu=np.zeros(n) if mu is None else np.ascontiguousarray(mu, np.float64),
+               nf_ptr=nf_ptr, nf_idx=nf_idx, bflag=bflag, gamma=gamma, gas_constant=gas_constant, p0=p0, T0=T0,
+               p_out=p_out, nt_in=nt_in, forcing_scale=p_out if forcing_scale is None else forcing_scale,
+               colour=None if colour is None else np.ascontiguousarray(colour, np.int32),
+               partition=None if partition is None else np.ascontiguousarray(partition, np.int32),
+               coords=coords, n_boundary=int((~interior).sum()))
+    return m
+
+
+def _derive_host(n, fa, fb, fn, coords):
+    """Host restatement of fnlh_mesh_derive (mesh.cpp:44-59 + face/node derived arrays)."""
+    nf = len(fa)
+    farea = np.sqrt((fn[:, 0] * fn[:, 0] + fn[:, 1] * fn[:, 1]) + fn[:, 2] * fn[:, 2])
+    fnh = fn / farea[:, None]
+    interior = fb >= 0
     # node -> face CSR, ascending face index per node (Mesh::build_adjacency)
-    ev_node = np.stack([fa, np.where(interior, fb, -1)], axis=1).reshape(-1)
+    ev_node = np.stack([fa, fb], axis=1).reshape(-1)
     ev_face = np.repeat(np.arange(nf, dtype=np.int32), 2)
     ev_sign = np.tile(np.array([1.0, -1.0]), nf)
     keep = ev_node >= 0
@@ -103,22 +131,45 @@ def from_faces(n, fa, fb, fbc, ford, fn, vol, *, b=5, gamma=1.4, gas_constant=28
     np.add.at(closure, ev_node, fn[ev_face] * ev_sign[:, None])
     bflag = np.zeros(n, np.int32)
     bflag[fa[~interior]] = 1
+    fvis = np.zeros(nf)
     if coords is not None and interior.any():
         d = coords[fb[interior]] - coords[fa[interior]]
-        fvis = np.zeros(nf)
-        fvis[interior] = farea[interior] / np.sqrt((d * d).sum(1))
-    else:
-        fvis = np.zeros(nf)
-    m = Mesh3D(n=n, nf=nf, b=b, fa=fa, fb=fb, fbc=fbc, ford=ford, fn=fn.reshape(-1).copy(), farea=farea,
-               fnh=np.ascontiguousarray(fnh.reshape(-1)), fvis=fvis, vol=np.ascontiguousarray(vol, np.float64),
-               closure=closure.reshape(-1).copy(),
-               mu=np.zeros(n) if mu is None else np.ascontiguousarray(mu, np.float64),
-               nf_ptr=nf_ptr, nf_idx=nf_idx, bflag=bflag, gamma=gamma, gas_constant=gas_constant, p0=p0, T0=T0,
-               p_out=p_out, nt_in=nt_in, forcing_scale=p_out if forcing_scale is None else forcing_scale,
-               colour=None if colour is None else np.ascontiguousarray(colour, np.int32),
-               partition=None if partition is None else np.ascontiguousarray(partition, np.int32),
-               coords=coords, n_boundary=int((~interior).sum()))
-    return m
+        fvis[interior] = farea[interior] / np.sqrt((d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2])
+    return farea, fnh, fvis, nf_ptr, nf_idx, closure, bflag
+
+
+def _derive_device(n, fa, fb, fn, coords):
+    import ctypes as C
+    from ._lib import check, lib, ptr
+    nf = len(fa)
+    farea, fvis = np.empty(nf), np.empty(nf)
+    fnh = np.empty((nf, 3))
+    nf_ptr = np.empty(n + 1, np.int32)
+    nf_idx = np.empty(2 * nf, np.int32)
+    closure = np.empty((n, 3))
+    bflag = np.empty(n, np.int32)
+    X = None if coords is None else np.ascontiguousarray(coords, np.float64)
+    check(lib().fnlh_mesh_derive(C.c_int(n), C.c_int(nf), ptr(np.ascontiguousarray(fa, np.int32)),
+                                 ptr(np.ascontiguousarray(fb, np.int32)), ptr(np.ascontiguousarray(fn)), ptr(X),
+                                 ptr(farea), ptr(fnh), ptr(fvis), ptr(nf_ptr), ptr(nf_idx), ptr(closure), ptr(bflag)))
+    return farea, fnh, fvis, nf_ptr, np.ascontiguousarray(nf_idx[: nf_ptr[n]]), closure, bflag
+
+
+def make_pattern_device(n, ea, eb, b=5, partition=None):
+    """make_pattern (sparse.cpp:91-117) on the device (fnlh_make_pattern)."""
+    import ctypes as C
+    from ._lib import check, lib, ptr
+    ea = np.ascontiguousarray(ea, np.int32)
+    eb = np.ascontiguousarray(eb, np.int32)
+    row_ptr = np.empty(n + 1, np.int32)
+    col_idx = np.empty(n + 2 * len(ea), np.int32)
+    diag = np.empty(n, np.int32)
+    nnz = C.c_longlong()
+    check(lib().fnlh_make_pattern(C.c_int(n), C.c_longlong(len(ea)), ptr(ea), ptr(eb), ptr(row_ptr), ptr(col_idx),
+                                  ptr(diag), C.byref(nnz)))
+    part = partition if partition is not None else np.zeros(n, np.int32)
+    return dict(b=b, row_ptr=row_ptr, col_idx=np.ascontiguousarray(col_idx[: nnz.value]), diag_idx=diag,
+                partition=np.ascontiguousarray(part, np.int32))
 
 
 # ---------------------------------------------------------------------------- generators
@@ -142,14 +193,133 @@ def _hex_edge_faces(p, q):
     return faces
 
 
+def _mean_cols(P, idx):
+    """left-to-right sum of the listed corners / count (the device's order)"""
+    acc = P[:, idx[0]].copy()
+    for q in idx[1:]:
+        acc = acc + P[:, q]
+    return acc / float(len(idx))
+
+
+def _dot3(a, b):
+    return (a[:, 0] * b[:, 0] + a[:, 1] * b[:, 1]) + a[:, 2] * b[:, 2]
+
+
+def _tet_vol(a, b_, c, d):
+    return np.abs(_dot3(b_ - a, _cross(c - a, d - a))) / 6.0
+
+
+def _sector_cells(ci, cj, ck, periodic_j):
+    nj_u, nk = cj + 1, ck + 1
+    nj = cj if periodic_j else cj + 1
+    ic, jc, kc = np.meshgrid(np.arange(ci), np.arange(cj), np.arange(ck), indexing="ij")
+    ic, jc, kc = ic.reshape(-1), jc.reshape(-1), kc.reshape(-1)
+    offs = [(c & 1, (c >> 1) & 1, (c >> 2) & 1) for c in range(8)]
+    corners_u = np.stack([((ic + a) * nj_u + (jc + b)) * nk + (kc + c) for a, b, c in offs], axis=1)
+    corners = np.stack([((ic + a) * nj + (jc + b) % nj) * nk + (kc + c) for a, b, c in offs], axis=1)
+    return corners_u, corners
+
+
+def _sector_dual_host(Xu, ci, cj, ck, periodic_j, tets):
+    """Median-dual geometry of the structured sector (host restatement of csrc/meshgen.cu):
+    per cell and edge the dual-face piece 0.5 (cen - m) x (c2 - c1) oriented along the edge,
+    summed per edge in (template, cell) order; node volumes from the Kuhn tets.  Returns
+    (ea, eb, en [ne, 3], vol [n]) with edges in ascending (ea, eb) order."""
+    nj = cj if periodic_j else cj + 1
+    n = (ci + 1) * nj * (ck + 1)
+    corners_u, corners = _sector_cells(ci, cj, ck, periodic_j)
+    P = Xu[corners_u]                                                # [ncell, 8, 3]
+    e_keys, e_vecs = [], []
+    vol_node = np.zeros(n)
+
+    def add_edge(p_id, q_id, S, xp, xq):
+        sgn = np.sign(_dot3(S, xq - xp))
+        S = S * sgn[:, None]
+        lo = np.minimum(p_id, q_id)
+        hi = np.maximum(p_id, q_id)
+        flip = np.where(p_id < q_id, 1.0, -1.0)
+        e_keys.append(lo.astype(np.int64) * n + hi)
+        e_vecs.append(S * flip[:, None])
+
+    if not tets:
+        cen = _mean_cols(P, list(range(8)))
+        for (p, q) in _HEX_EDGES:
+            f1, f2 = _hex_edge_faces(p, q)
+            m = 0.5 * (P[:, p] + P[:, q])
+            c1 = _mean_cols(P, f1)
+            c2 = _mean_cols(P, f2)
+            add_edge(corners[:, p], corners[:, q], 0.5 * _cross(cen - m, c2 - c1), P[:, p], P[:, q])
+        vc = 0.0
+        for t in _KUHN:
+            vc = vc + _tet_vol(P[:, t[0]], P[:, t[1]], P[:, t[2]], P[:, t[3]])
+        for c in range(8):
+            vol_node += np.bincount(corners[:, c], weights=vc / 8.0, minlength=n)
+    else:
+        for t in _KUHN:
+            T = P[:, list(t)]
+            tid = corners[:, list(t)]
+            cen = _mean_cols(T, [0, 1, 2, 3])
+            vt = _tet_vol(T[:, 0], T[:, 1], T[:, 2], T[:, 3])
+            for c in range(4):
+                vol_node += np.bincount(tid[:, c], weights=vt / 4.0, minlength=n)
+            for (p, q) in itertools.combinations(range(4), 2):
+                r, s = [v for v in range(4) if v not in (p, q)]
+                m = 0.5 * (T[:, p] + T[:, q])
+                c1 = (T[:, p] + T[:, q] + T[:, r]) / 3.0
+                c2 = (T[:, p] + T[:, q] + T[:, s]) / 3.0
+                add_edge(tid[:, p], tid[:, q], 0.5 * _cross(cen - m, c2 - c1), T[:, p], T[:, q])
+    keys = np.concatenate(e_keys)
+    vecs = np.concatenate(e_vecs)
+    ukeys, inv = np.unique(keys, return_inverse=True)
+    en = np.stack([np.bincount(inv, weights=vecs[:, d], minlength=len(ukeys)) for d in range(3)], axis=1)
+    return (ukeys // n).astype(np.int64), (ukeys % n).astype(np.int64), en, vol_node
+
+
+def _device_available():
+    try:
+        from ._lib import lib
+        return lib().fnlh_device_count() > 0
+    except Exception:
+        return False
+
+
+def _sector_dual_device(Xu, ci, cj, ck, periodic_j, tets):
+    """The same geometry from the sm_100a kernels (csrc/meshgen.cu, fnlh_sector_dual_*)."""
+    import ctypes as C
+    from ._lib import check, lib, ptr
+    nj = cj if periodic_j else cj + 1
+    n = (ci + 1) * nj * (ck + 1)
+    X = np.ascontiguousarray(Xu, np.float64)
+    h = C.c_void_p()
+    ne = C.c_longlong()
+    L = lib()
+    check(L.fnlh_sector_dual_create(C.c_int(ci), C.c_int(cj), C.c_int(ck), C.c_int(int(periodic_j)),
+                                    C.c_int(int(tets)), ptr(X), C.byref(ne), C.byref(h)))
+    try:
+        ea = np.empty(ne.value, np.int64)
+        eb = np.empty(ne.value, np.int64)
+        en = np.empty((ne.value, 3))
+        vol = np.empty(n)
+        check(L.fnlh_sector_dual_get(h, ptr(ea), ptr(eb), ptr(en), ptr(vol)))
+    finally:
+        L.fnlh_sector_dual_destroy(h)
+    return ea, eb, en, vol
+
+
 def structured_sector(ci, cj, ck, *, geometry="annular", length=2.0, pitch_deg=10.0, r_in=0.5, r_out=1.0,
                       width=1.0, height=0.5, periodic_j=False, tets=False, jitter=0.0, seed=0, b=5, permute=True,
-                      gas=None, nt_in=0.0, mu_range=None):
+                      gas=None, nt_in=0.0, mu_range=None, device=None):
     """Hex (or Kuhn 6-tet) sector mesh, node-centred median dual.
 
     i: axial (inlet i=0, outlet i=ci), j: pitch, k: span/radius.  Walls (hub, casing,
     non-periodic pitch sides) enter through the closure source.  Returns a Mesh3D in
-    colour-major RCM order (2 colours for hex, 8 for Kuhn tets)."""
+    colour-major RCM order (2 colours for hex, 8 for Kuhn tets).
+
+    device: compute the dual geometry (per-cell dual-face normals, their per-edge sums,
+    node volumes) with the sm_100a kernels of csrc/meshgen.cu (bitwise equal to the host
+    restatement `_sector_dual_host`); None = on the device when one is present."""
+    if device is None:
+        device = _device_available()
     rng = np.random.default_rng(seed)
     ni, nj_u, nk = ci + 1, cj + 1, ck + 1
     nj = cj if periodic_j else cj + 1
@@ -173,57 +343,10 @@ def structured_sector(ci, cj, ck, *, geometry="annular", length=2.0, pitch_deg=1
     coords = np.ascontiguousarray(X[:, :nj, :].reshape(-1, 3))     # gid order (seam copies dropped)
     uid = lambda i, j, k: (i * nj_u + j) * nk + k  # noqa: E731
     # hex cells: corner c = di + 2 dj + 4 dk
-    ic, jc, kc = np.meshgrid(np.arange(ci), np.arange(cj), np.arange(ck), indexing="ij")
-    ic, jc, kc = ic.reshape(-1), jc.reshape(-1), kc.reshape(-1)
-    corners_u = np.stack([uid(ic + (c & 1), jc + ((c >> 1) & 1), kc + ((c >> 2) & 1)) for c in range(8)], axis=1)
-    corners = gid[corners_u]
-    P = Xu[corners_u]                                                # [ncell, 8, 3]
-    e_keys, e_vecs = [], []
-    vol_node = np.zeros(n)
-
-    def tet_vol(a, b_, c, d):
-        return np.abs(np.einsum("ij,ij->i", b_ - a, _cross(c - a, d - a))) / 6.0
-
-    def add_edge(p_id, q_id, S, xp, xq):
-        sgn = np.sign(np.einsum("ij,ij->i", S, xq - xp))
-        S = S * sgn[:, None]
-        lo = np.minimum(p_id, q_id)
-        hi = np.maximum(p_id, q_id)
-        flip = np.where(p_id < q_id, 1.0, -1.0)
-        e_keys.append(lo.astype(np.int64) * n + hi)
-        e_vecs.append(S * flip[:, None])
-
-    if not tets:
-        cen = P.mean(axis=1)
-        for (p, q) in _HEX_EDGES:
-            f1, f2 = _hex_edge_faces(p, q)
-            m = 0.5 * (P[:, p] + P[:, q])
-            c1 = P[:, f1].mean(axis=1)
-            c2 = P[:, f2].mean(axis=1)
-            add_edge(corners[:, p], corners[:, q], 0.5 * _cross(cen - m, c2 - c1), P[:, p], P[:, q])
-        vc = sum(tet_vol(P[:, t[0]], P[:, t[1]], P[:, t[2]], P[:, t[3]]) for t in _KUHN)
-        for c in range(8):
-            vol_node += np.bincount(corners[:, c], weights=vc / 8.0, minlength=n)
+    if device:
+        ea, eb, en, vol_node = _sector_dual_device(Xu, ci, cj, ck, periodic_j, tets)
     else:
-        for t in _KUHN:
-            T = P[:, list(t)]
-            tid = corners[:, list(t)]
-            cen = T.mean(axis=1)
-            vt = tet_vol(T[:, 0], T[:, 1], T[:, 2], T[:, 3])
-            for c in range(4):
-                vol_node += np.bincount(tid[:, c], weights=vt / 4.0, minlength=n)
-            for (p, q) in itertools.combinations(range(4), 2):
-                r, s = [v for v in range(4) if v not in (p, q)]
-                m = 0.5 * (T[:, p] + T[:, q])
-                c1 = (T[:, p] + T[:, q] + T[:, r]) / 3.0
-                c2 = (T[:, p] + T[:, q] + T[:, s]) / 3.0
-                add_edge(tid[:, p], tid[:, q], 0.5 * _cross(cen - m, c2 - c1), T[:, p], T[:, q])
-    keys = np.concatenate(e_keys)
-    vecs = np.concatenate(e_vecs)
-    ukeys, inv = np.unique(keys, return_inverse=True)
-    en = np.stack([np.bincount(inv, weights=vecs[:, d], minlength=len(ukeys)) for d in range(3)], axis=1)
-    ea = (ukeys // n).astype(np.int64)
-    eb = (ukeys % n).astype(np.int64)
+        ea, eb, en, vol_node = _sector_dual_host(Xu, ci, cj, ck, periodic_j, tets)
 
     # inlet (i=0, outward -x) and outlet (i=ci, outward +x) dual boundary areas
     jq, kq = np.meshgrid(np.arange(cj), np.arange(ck), indexing="ij")
@@ -294,7 +417,7 @@ def structured_sector(ci, cj, ck, *, geometry="annular", length=2.0, pitch_deg=1
         lo_, hi_ = np.log(mu_range[0]), np.log(mu_range[1])
         mu = np.exp(rng.uniform(lo_, hi_, size=n))
     m = from_faces(n, fa, fb, fbc, ford, fnv, vol_node[order], b=b, coords=coords[order], colour=col[order],
-                   mu=mu, nt_in=nt_in, **g)
+                   mu=mu, nt_in=nt_in, device=device, **g)
     m.ijk = np.stack([In.reshape(-1), Jn.reshape(-1), Kn.reshape(-1)], axis=1)[order].astype(np.int64)
     return m
 
