@@ -238,6 +238,12 @@ int fnlh_make_pattern(int rows, long long n_edges, const int* ea, const int* eb,
 int fnlh_mesh_derive(int n, int nf, const int* fa, const int* fb, const double* fn, const double* coords,
                      double* farea, double* fnh, double* fvis, int* nf_ptr, int* nf_idx, double* closure, int* bflag);
 
+/* ---- work-unit normalization (workunit.cpp:11-46 restated; host) ---------------------
+   T_ref: best of 3 timings of the fixed 256 x 256, 60-sweep Jacobi stencil on one host
+   core (measured once per process); WU = workers x seconds / T_ref. */
+double fnlh_normalization_kernel_seconds(void);
+double fnlh_work_units(int workers, double seconds, double t_ref);
+
 #ifdef __cplusplus
 }
 #endif
