@@ -6,6 +6,8 @@
 // subsonic inlet/outlet states is the only libm call whose last bit may differ).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include "disc.cuh"
 
@@ -15,6 +17,12 @@ namespace {
 
 constexpr int kT = 128;
 inline int nb(long long n, int t = kT) { return static_cast<int>((n + t - 1) / t); }
+
+// FNLH_PACKED_RESIDUAL=0 keeps the unpacked order-2 kernels (A/B measurement)
+bool packed_disabled() {
+    const char* e = std::getenv("FNLH_PACKED_RESIDUAL");
+    return e && e[0] == '0';
+}
 
 __device__ __forceinline__ void record(unsigned long long* err, unsigned long long key, int code) {
     atomicMin(err, (key << 4) | (unsigned long long)code);
@@ -124,6 +132,186 @@ __global__ void k_node_gather(MeshDev m, const double* __restrict__ W, const dou
             for (int k = 0; k < B; ++k) acc[k] -= fl[k];
             if (B == 6 && need_vis) {
                 const double* vf = vflux + (size_t)f * B;
+#pragma unroll
+                for (int k = 0; k < B; ++k) vacc[k] -= vf[k];
+            }
+        }
+    }
+    double src[B];
+    node_source<B>(m, i, W[(size_t)i * B + 4], src);
+#pragma unroll
+    for (int k = 0; k < B; ++k) inv[(size_t)i * B + k] = acc[k] + src[k];
+    if (need_vis) {
+#pragma unroll
+        for (int k = 0; k < B; ++k) vis[(size_t)i * B + k] = vacc[k];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// packed order-2 residual (boundary faces the tail of the face list): the pre-pass writes
+// one 16-byte-aligned record per node [W(B), nu, lap(B), bflag] that the interior face
+// kernel reads with 16-byte loads, the face geometry is one record [fn, fnh, area,
+// (fa, fb)] per interior face, and flux rows are padded to kFS doubles so the node
+// gather reads them with 16-byte loads too.  Same arithmetic, same order as above.
+// ---------------------------------------------------------------------------
+template <int B>
+struct Rec {
+    static constexpr int R = 2 * B + 2;  // 12 (b = 5) or 14 (b = 6) doubles
+};
+constexpr int kFS = 6;                   // flux row stride (doubles)
+
+__device__ __forceinline__ void ld2(const double* __restrict__ p, double& a, double& b) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(p));
+    a = v.x;
+    b = v.y;
+}
+__device__ __forceinline__ void st2(double* __restrict__ p, double a, double b) {
+    *reinterpret_cast<double2*>(p) = make_double2(a, b);
+}
+
+template <int B>
+__global__ void k_jst_prepass_rec(MeshDev m, const double* __restrict__ W, double* __restrict__ rec,
+                                  const double* skip) {
+    constexpr int R = Rec<B>::R;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m.n) return;
+    if (skip && *skip == 0.0) return;
+    const double* wi = W + (size_t)i * B;
+    double r[R];
+#pragma unroll
+    for (int k = 0; k < B; ++k) r[k] = wi[k];
+    const double pi = r[4];
+    double num = 0.0, den = 0.0;
+    double L[B], qi[B], qj[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) L[k] = 0.0;
+    prim_to_cons<B>(r, m.gamma, qi);
+    for (int e = m.nf_ptr[i]; e < m.nf_ptr[i + 1]; ++e) {
+        const int code = m.nf_code[e];
+        if (code == kBoundaryFace) {
+            den += pi + pi;
+            continue;
+        }
+        const int j = code >= 0 ? code : -code - 1;
+        const double* wj = W + (size_t)j * B;
+        const double pj = wj[4];
+        num += pj - pi;
+        den += pj + pi;
+        prim_to_cons<B>(wj, m.gamma, qj);
+#pragma unroll
+        for (int k = 0; k < B; ++k) L[k] += qj[k] - qi[k];
+    }
+    r[B] = fabs(num) / den;
+#pragma unroll
+    for (int k = 0; k < B; ++k) r[B + 1 + k] = L[k];
+    r[2 * B + 1] = m.bflag[i] ? 1.0 : 0.0;
+    double* o = rec + (size_t)i * R;
+#pragma unroll
+    for (int k = 0; k < R; k += 2) st2(o + k, r[k], r[k + 1]);
+}
+
+template <int B>
+__device__ __forceinline__ void face_int(const MeshDev& m, int f, const double* __restrict__ geo,
+                                         const double* __restrict__ rec, int need_vis, double* __restrict__ flux,
+                                         double* __restrict__ vflux) {
+    constexpr int R = Rec<B>::R;
+    double g8[8];
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) ld2(geo + (size_t)f * 8 + k, g8[k], g8[k + 1]);
+    const long long ab = __double_as_longlong(g8[7]);
+    const int a = (int)(ab & 0xffffffffll), c = (int)(ab >> 32);
+    double ra[R], rc[R];
+#pragma unroll
+    for (int k = 0; k < R; k += 2) {
+        ld2(rec + (size_t)a * R + k, ra[k], ra[k + 1]);
+        ld2(rec + (size_t)c * R + k, rc[k], rc[k + 1]);
+    }
+    double out[kFS];
+    out[kFS - 1] = 0.0;
+    interior_flux_core<B>(m.gamma, g8, g8 + 3, g8[6], ra, rc, 2, ra[B], rc[B], ra[2 * B + 1] != 0.0 || rc[2 * B + 1] != 0.0,
+                          ra + B + 1, rc + B + 1, out);
+    double* o = flux + (size_t)f * kFS;
+#pragma unroll
+    for (int k = 0; k < kFS; k += 2) st2(o + k, out[k], out[k + 1]);
+    if (need_vis && B == 6) {
+        double vo[kFS];
+        viscous_face_flux<B>(m, f, ra, rc, m.mu[a], m.mu[c], vo);
+        double* v = vflux + (size_t)f * kFS;
+#pragma unroll
+        for (int k = 0; k < kFS; k += 2) st2(v + k, vo[k], vo[k + 1]);
+    }
+}
+
+template <int B>
+__device__ __forceinline__ void face_bnd(const MeshDev& m, int f, const double* __restrict__ W,
+                                         const double* __restrict__ wref, int mode, const double* __restrict__ forcing,
+                                         int nforcing, double* __restrict__ flux, unsigned long long* err) {
+    const int a = m.fa[f];
+    double out[kFS];
+    out[kFS - 1] = 0.0;
+    const int st = boundary_face_flux<B>(m, f, W + (size_t)a * B, wref ? wref + (size_t)a * B : nullptr, mode, forcing,
+                                         nforcing, out);
+    if (st) {
+        record(err, (unsigned long long)f, st);
+#pragma unroll
+        for (int k = 0; k < B; ++k) out[k] = 0.0;
+    }
+    double* o = flux + (size_t)f * kFS;
+#pragma unroll
+    for (int k = 0; k < kFS; k += 2) st2(o + k, out[k], out[k + 1]);
+}
+
+// one launch for all faces: the first nbb blocks take the boundary tail (long pow
+// latency, started first), the rest the interior faces
+template <int B>
+__global__ void __launch_bounds__(128) k_face_packed(MeshDev m, int nf_int, int nbb, const double* __restrict__ geo,
+                                                     const double* __restrict__ rec, const double* __restrict__ W,
+                                                     const double* __restrict__ wref, int mode,
+                                                     const double* __restrict__ forcing, int nforcing, int need_vis,
+                                                     double* __restrict__ flux, double* __restrict__ vflux,
+                                                     unsigned long long* err, const double* skip) {
+    if (skip && *skip == 0.0) return;
+    if ((int)blockIdx.x < nbb) {
+        const int f = nf_int + blockIdx.x * blockDim.x + threadIdx.x;
+        if (f < m.nf) face_bnd<B>(m, f, W, wref, mode, forcing, nforcing, flux, err);
+    } else {
+        const int f = (blockIdx.x - nbb) * blockDim.x + threadIdx.x;
+        if (f < nf_int) face_int<B>(m, f, geo, rec, need_vis, flux, vflux);
+    }
+}
+
+template <int B>
+__global__ void k_node_gather_p(MeshDev m, const double* __restrict__ W, const double* __restrict__ flux,
+                                const double* __restrict__ vflux, int need_vis, double* __restrict__ inv,
+                                double* __restrict__ vis, const double* skip) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m.n) return;
+    if (skip && *skip == 0.0) return;
+    double acc[B], vacc[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+        acc[k] = 0.0;
+        vacc[k] = 0.0;
+    }
+    for (int e = m.nf_ptr[i]; e < m.nf_ptr[i + 1]; ++e) {
+        const int f = m.nf_idx[e];
+        const int code = m.nf_code[e];
+        double fl[kFS];
+#pragma unroll
+        for (int k = 0; k < kFS; k += 2) ld2(flux + (size_t)f * kFS + k, fl[k], fl[k + 1]);
+        if (code >= 0 || code == kBoundaryFace) {
+#pragma unroll
+            for (int k = 0; k < B; ++k) acc[k] += fl[k];
+            if (B == 6 && need_vis && code != kBoundaryFace) {
+                const double* vf = vflux + (size_t)f * kFS;
+#pragma unroll
+                for (int k = 0; k < B; ++k) vacc[k] += vf[k];
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < B; ++k) acc[k] -= fl[k];
+            if (B == 6 && need_vis) {
+                const double* vf = vflux + (size_t)f * kFS;
 #pragma unroll
                 for (int k = 0; k < B; ++k) vacc[k] -= vf[k];
             }
@@ -709,6 +897,20 @@ DeviceDisc::DeviceDisc(const MeshArrays& m, const DevicePattern* pattern) : pat_
         if (nf_int_ >= 0) fdpart_.alloc((std::size_t)n * m.b * m.b);
     }
     bflag_.upload(m.bflag, n);
+    if (nf_int_ >= 0 && !packed_disabled()) {  // interior face records of the packed residual
+        std::vector<double> g((std::size_t)nf_int_ * 8);
+        for (int f = 0; f < nf_int_; ++f) {
+            double* r = g.data() + (std::size_t)f * 8;
+            for (int d = 0; d < 3; ++d) {
+                r[d] = m.fn[3 * (std::size_t)f + d];
+                r[3 + d] = m.fnh[3 * (std::size_t)f + d];
+            }
+            r[6] = m.farea[f];
+            const long long ab = ((long long)(unsigned)m.fb[f] << 32) | (long long)(unsigned)m.fa[f];
+            std::memcpy(r + 7, &ab, sizeof ab);
+        }
+        fgeo_.upload(g.data(), g.size());
+    }
     {
         std::vector<int> code(m.nf_ptr[n]);
         for (int i = 0; i < n; ++i)
@@ -753,8 +955,9 @@ void DeviceDisc::alloc_scratch(Scratch& c) {
     const std::size_t n = view_.n, nfc = view_.nf, b = view_.b;
     c.nu.alloc(n);
     c.lap.alloc(n * b);
-    c.flux.alloc(nfc * b);
-    c.vflux.alloc(nfc * b);
+    c.flux.alloc(nfc * std::max<std::size_t>(b, kFS));
+    c.vflux.alloc(nfc * std::max<std::size_t>(b, kFS));
+    if (fgeo_.ptr) c.rec.alloc(n * (2 * b + 2));
     c.scal.alloc(16);
     c.umax.alloc(64);
     for (auto& r : c.real) r.alloc(n * b);
@@ -799,6 +1002,16 @@ void DeviceDisc::residual(const double* W, const double* wref, int order, int mo
                           int nforcing, bool need_vis, double* inv, double* vis, cudaStream_t st,
                           const double* skip) {
     const MeshDev& m = view_;
+    if (order == 2 && fgeo_.ptr) {  // packed records (boundary faces the tail)
+        DISPATCH_B56(m.b, {
+            { ::fnlh::note_launch(); k_jst_prepass_rec<B><<<nb(m.n), kT, 0, st>>>(m, W, C().rec.ptr, skip); }
+            const int nbb = nb(m.nf - nf_int_), nbi = nb(nf_int_);
+            if (nbb + nbi) { ::fnlh::note_launch(); k_face_packed<B><<<nbb + nbi, kT, 0, st>>>(m, nf_int_, nbb, fgeo_.ptr, C().rec.ptr, W, wref, mode, forcing, nforcing, need_vis ? 1 : 0, C().flux.ptr, C().vflux.ptr, err(), skip); }
+            { ::fnlh::note_launch(); k_node_gather_p<B><<<nb(m.n), kT, 0, st>>>(m, W, C().flux.ptr, C().vflux.ptr, need_vis ? 1 : 0, inv, vis, skip); }
+        });
+        FNLH_CUDA(cudaGetLastError());
+        return;
+    }
     DISPATCH_B56(m.b, {
         if (order == 2) { ::fnlh::note_launch(); k_jst_prepass<B><<<nb(m.n), kT, 0, st>>>(m, W, C().nu.ptr, C().lap.ptr, skip); }
         { ::fnlh::note_launch(); k_face_flux<B><<<nb(m.nf), kT, 0, st>>>(m, W, wref, order, mode, forcing, nforcing, need_vis ? 1 : 0,

@@ -80,7 +80,7 @@ public:
     int contexts() const { return static_cast<int>(ctx_.size()); }
 private:
     struct Scratch {
-        DeviceBuffer<double> nu, lap, flux, vflux, scal, fwork;
+        DeviceBuffer<double> nu, lap, flux, vflux, scal, fwork, rec;
         DeviceBuffer<unsigned long long> umax;
         DeviceBuffer<double> real[6];  // linres / DF temporaries (len each)
     };
@@ -92,6 +92,7 @@ private:
     const DevicePattern* pat_;
     DeviceBuffer<int> fa_, fb_, fbc_, ford_, nf_ptr_, nf_idx_, nf_code_, bflag_, e_ab_, e_ba_;
     DeviceBuffer<double> fn_, farea_, fnh_, fvis_, vol_, closure_, mu_;
+    DeviceBuffer<double> fgeo_;    // interior face records of the packed order-2 residual
     DeviceBuffer<double> qscale_;
     DeviceBuffer<unsigned long long> err_;
     unsigned long long* cur_err_ = nullptr;

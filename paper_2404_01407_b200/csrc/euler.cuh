@@ -216,14 +216,13 @@ __device__ __forceinline__ int boundary_face_flux(const MeshDev& m, int f, const
     return 0;
 }
 
-// interior_face_flux (disc_euler.cpp:121-159); order 2 takes the node pre-pass values
+// interior_face_flux (disc_euler.cpp:121-159); order 2 takes the node pre-pass values.
+// The core takes the face geometry by value (n, nh, area: global or register copies).
 template <int B>
-__device__ __forceinline__ void interior_face_flux(const MeshDev& m, int f, const double* wa, const double* wc,
-                                                   int order, double nua, double nub, bool trunc,
-                                                   const double* lapa, const double* lapc, double* out) {
-    const double g = m.gamma;
-    const double* n = m.fn + 3 * (size_t)f;
-    const double* nh = m.fnh + 3 * (size_t)f;
+__device__ __forceinline__ void interior_flux_core(double g, const double* n, const double* nh, double area,
+                                                   const double* wa, const double* wc, int order, double nua,
+                                                   double nub, bool trunc, const double* lapa, const double* lapc,
+                                                   double* out) {
     double fa[6], fb[6], qa[6], qb[6];
     phys_flux<B>(wa, g, n, fa);
     phys_flux<B>(wc, g, n, fb);
@@ -233,7 +232,7 @@ __device__ __forceinline__ void interior_face_flux(const MeshDev& m, int f, cons
     const double ww = 0.5 * (wa[3] + wc[3]);
     const double p = 0.5 * (wa[4] + wc[4]);
     const double cs = sqrt(g * p / rho);
-    const double lam = (fabs(u * nh[0] + v * nh[1] + ww * nh[2]) + cs) * m.farea[f];
+    const double lam = (fabs(u * nh[0] + v * nh[1] + ww * nh[2]) + cs) * area;
     prim_to_cons<B>(wa, g, qa);
     prim_to_cons<B>(wc, g, qb);
 #pragma unroll
@@ -253,6 +252,14 @@ __device__ __forceinline__ void interior_face_flux(const MeshDev& m, int f, cons
         if (s4 > 0.0) d -= s4 * lam * (lapc[k] - lapa[k]);
         out[k] -= d;
     }
+}
+
+template <int B>
+__device__ __forceinline__ void interior_face_flux(const MeshDev& m, int f, const double* wa, const double* wc,
+                                                   int order, double nua, double nub, bool trunc,
+                                                   const double* lapa, const double* lapc, double* out) {
+    interior_flux_core<B>(m.gamma, m.fn + 3 * (size_t)f, m.fnh + 3 * (size_t)f, m.farea[f], wa, wc, order, nua, nub,
+                          trunc, lapa, lapc, out);
 }
 
 // SA-like viscous flux (b = 6 only)
