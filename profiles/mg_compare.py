@@ -30,9 +30,19 @@ def run(name, scale, nh, scheme_over, drop, cap):
         return dict(n=c.mesh.n, levels=g.levels(), reason=f"error: {ex}", iters=None, device_s=None)
     wall = time.time() - t0
     last = hist[-1] if hist else {}
-    return dict(n=c.mesh.n, levels=g.levels(), reason=reason, iters=len(hist), device_s=last.get("seconds", 0.0),
-                wall_s=wall, setup_s=setup, r0=hist[0]["resid_mean"] if hist else None,
-                r_end=last.get("resid_mean"), rz_end=last.get("rz"))
+    out = dict(n=c.mesh.n, levels=g.levels(), reason=reason, iters=len(hist), device_s=last.get("seconds", 0.0),
+               wall_s=wall, setup_s=setup, r0=hist[0]["resid_mean"] if hist else None,
+               r_end=last.get("resid_mean"), rz0=hist[0]["rz"] if hist else None, rz_end=last.get("rz"))
+    # first outer iteration (1-based) and device seconds at which each residual had dropped
+    # by `drop` orders from its first-iteration value (run_to_convergence's test, per field)
+    for key, name in (("resid_mean", "mean"), ("rz", "rz")):
+        if not hist:
+            break
+        tgt = hist[0][key] * 10.0 ** (-drop)
+        hit = next((e for e in hist if e[key] <= tgt), None)
+        out[f"{name}_drop_iter"] = hit["iter"] + 1 if hit else None
+        out[f"{name}_drop_s"] = hit["seconds"] if hit else None
+    return out
 
 
 def main():
