@@ -24,7 +24,7 @@ namespace {
 
 template <class S>
 struct HostSystem {
-    DeviceBuffer<double> real_vals;
+    DeviceBuffer<double> real_vals, sell;
     DeviceBuffer<S> vals;
     DeviceBuffer<double> shift;
     SystemView<S> view;
@@ -37,6 +37,10 @@ struct HostSystem {
         } else {
             real_vals.upload(A, n);
             view.real_vals = real_vals.ptr;
+            sell.alloc(std::max<long long>(p->msell_doubles, 1));  // the matvec operand, as the solver keeps A5
+            sell_from_bsr(*p, real_vals.ptr, sell.ptr, nullptr);
+            FNLH_CUDA(cudaDeviceSynchronize());
+            view.real_sell = sell.ptr;
             if (shift_im) {
                 shift.upload(shift_im, p->rows);
                 view.shift_im = shift.ptr;
@@ -53,11 +57,7 @@ int factorize_impl(const fnlh_pattern* p, const double* A, int A_complex, const 
     Workspace ws(1);
     DeviceIlu<S> f(dp);
     ilu_factorize(sys.view, f, ws);
-    const std::size_t bb = (std::size_t)dp->b * dp->b;
-    if (vals) download(reinterpret_cast<S*>(vals), f.vals, (std::size_t)dp->nnzb * bb);
-    if (diag_lu) download(reinterpret_cast<S*>(diag_lu), f.diag_lu, (std::size_t)dp->rows * bb);
-    if (diag_piv) download(diag_piv, f.diag_piv, (std::size_t)dp->rows * dp->b);
-    if (diag_inv) download(reinterpret_cast<S*>(diag_inv), f.diag_inv, (std::size_t)dp->rows * bb);
+    f.download(reinterpret_cast<S*>(vals), reinterpret_cast<S*>(diag_lu), diag_piv, reinterpret_cast<S*>(diag_inv));
     return 0;
 }
 

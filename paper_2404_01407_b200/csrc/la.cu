@@ -25,9 +25,46 @@ struct PatDev {
     const int* __restrict__ col_idx;
     const int* __restrict__ diag_idx;
     const int* __restrict__ part;
+    // sliced factor layout (la.cuh DevicePattern)
+    const long long* __restrict__ ent;
+    const long long* __restrict__ lbase;
+    const long long* __restrict__ ubase;
+    const int* __restrict__ lcolb;
+    const int* __restrict__ ucolb;
+    const int* __restrict__ nlow;
+    const int* __restrict__ nup;
+    const int* __restrict__ lcols;
+    const int* __restrict__ ucols;
+    const int* __restrict__ dpos;
+    const int* __restrict__ blk_e;
+    const int* __restrict__ blk_row;
+    const long long* __restrict__ mbase;
+    const int* __restrict__ mcolb;
+    const int* __restrict__ mcols;
 };
 
-PatDev dev(const DevicePattern& p) { return PatDev{p.b, p.rows, p.nnzb, p.row_ptr, p.col_idx, p.diag_idx, p.part}; }
+PatDev dev(const DevicePattern& p) {
+    return PatDev{p.b, p.rows, p.nnzb, p.row_ptr, p.col_idx, p.diag_idx, p.part, p.ent, p.lbase, p.ubase,
+                  p.lcolb, p.ucolb, p.nlow, p.nup, p.lcols, p.ucols, p.dpos, p.blk_e, p.blk_row,
+                  p.mbase, p.mcolb, p.mcols};
+}
+
+// b x b block at g with element stride 32 (sliced layout)
+template <int B, class S>
+__device__ __forceinline__ void load_blk32(const S* __restrict__ g, S (&A)[B * B]) {
+#pragma unroll
+    for (int k = 0; k < B * B; ++k) A[k] = g[(std::size_t)k * 32];
+}
+template <int B, class S>
+__device__ __forceinline__ void store_blk32(S* __restrict__ g, const S (&A)[B * B]) {
+#pragma unroll
+    for (int k = 0; k < B * B; ++k) g[(std::size_t)k * 32] = A[k];
+}
+// element offsets of row i's pivot LU (element stride 32) and pivots in the pivot layout
+__device__ __forceinline__ long long dlu_off(const PatDev& p, int i, int bb) {
+    const int d = p.dpos[i];
+    return (long long)(d >> 5) * bb * 32 + (d & 31);
+}
 
 inline int nblocks(long long n, int t = kThreads) { return static_cast<int>((n + t - 1) / t); }
 
@@ -55,20 +92,21 @@ __device__ __forceinline__ S sys_entry(const SystemView<S>& A, int e, int k, boo
     return v;
 }
 
-// Ilu::factorize copy phase (sparse.cpp:199-209): one warp per block row, the lanes
-// stream the row's contiguous blocks element by element (coalesced)
+// Ilu::factorize copy phase (sparse.cpp:199-209): one thread per block position of the
+// sliced layout (blk_e / blk_row: source entry and row, -1 for padding), so each element
+// store of a warp is 32 consecutive lanes
 template <int B, class S>
-__global__ void k_ilu_copy(PatDev p, SystemView<S> A, S* __restrict__ vals) {
-    const int i = (int)((blockIdx.x * (std::size_t)blockDim.x + threadIdx.x) >> 5);
-    const int lane = threadIdx.x & 31;
-    if (i >= p.rows) return;
-    const int pi = p.part[i];
-    const int di = p.diag_idx[i];
-    const int e0 = p.row_ptr[i], e1 = p.row_ptr[i + 1];
-    for (int t = lane; t < (e1 - e0) * B * B; t += 32) {
-        const int e = e0 + t / (B * B), k = t % (B * B);
-        vals[(size_t)e * B * B + k] = p.part[p.col_idx[e]] == pi ? sys_entry<B, S>(A, e, k, e == di, i) : zero<S>();
-    }
+__global__ void k_ilu_copy(PatDev p, SystemView<S> A, S* __restrict__ vals, long long npos) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= npos) return;
+    const int e = p.blk_e[t];
+    if (e < 0) return;
+    const int i = p.blk_row[t];
+    const bool keep = p.part[p.col_idx[e]] == p.part[i];
+    const bool diag = e == p.diag_idx[i];
+    S* dst = vals + (t >> 5) * (long long)(B * B) * 32 + (t & 31);
+#pragma unroll
+    for (int k = 0; k < B * B; ++k) dst[(long long)k * 32] = keep ? sys_entry<B, S>(A, e, k, diag, i) : zero<S>();
 }
 
 // Ilu::factorize elimination + pivot phase for the rows of one level (sparse.cpp:214-255)
@@ -89,11 +127,12 @@ __global__ void __launch_bounds__(kThreads) k_ilu_factor(PatDev p, const int* __
         // L_ik = A_ik * U_kk^{-1}
         S tmp[B * B];
         const S* uinv = diag_inv + (size_t)k * B * B;
+        S* const lik = vals + p.ent[ek];
 #pragma unroll
         for (int r = 0; r < B; ++r) {  // one row of A_ik at a time (register pressure)
             S lrow[B];
 #pragma unroll
-            for (int m = 0; m < B; ++m) lrow[m] = vals[(size_t)ek * B * B + r * B + m];
+            for (int m = 0; m < B; ++m) lrow[m] = lik[(r * B + m) * 32];
 #pragma unroll
             for (int c = 0; c < B; ++c) {
                 S acc = zero<S>();
@@ -102,7 +141,7 @@ __global__ void __launch_bounds__(kThreads) k_ilu_factor(PatDev p, const int* __
                 tmp[r * B + c] = acc;
             }
         }
-        store_block<B>(vals + (size_t)ek * B * B, tmp);
+        store_blk32<B>(lik, tmp);
         // A_ij -= L_ik U_kj for j > k present in both rows (zero-skip, dense.hpp:47)
         for (int ej = rb; ej < re; ++ej) {
             const int j = p.col_idx[ej];
@@ -111,35 +150,37 @@ __global__ void __launch_bounds__(kThreads) k_ilu_factor(PatDev p, const int* __
             const int ekj = find_entry(p, k, j);
             if (ekj < 0) continue;
             if (p.part[k] != p.part[j]) continue;
-            const S* u = vals + (size_t)ekj * B * B;
-            S* cblk = vals + (size_t)ej * B * B;
+            const S* u = vals + p.ent[ekj];
+            S* cblk = vals + p.ent[ej];
 #pragma unroll
             for (int r = 0; r < B; ++r) {  // block_matmul_sub row by row (same operation order)
                 S crow[B];
 #pragma unroll
-                for (int c = 0; c < B; ++c) crow[c] = cblk[r * B + c];
+                for (int c = 0; c < B; ++c) crow[c] = cblk[(r * B + c) * 32];
 #pragma unroll
                 for (int kk = 0; kk < B; ++kk) {
                     const S a = tmp[r * B + kk];
                     if (is_zero(a)) continue;
 #pragma unroll
-                    for (int c = 0; c < B; ++c) crow[c] -= a * u[kk * B + c];
+                    for (int c = 0; c < B; ++c) crow[c] -= a * u[(kk * B + c) * 32];
                 }
 #pragma unroll
-                for (int c = 0; c < B; ++c) cblk[r * B + c] = crow[c];
+                for (int c = 0; c < B; ++c) cblk[(r * B + c) * 32] = crow[c];
             }
         }
     }
     // pivot block: partial-pivot LU, condition check, explicit inverse
     S lu[B * B];
     int piv[B];
-    load_block<B>(vals + (size_t)p.diag_idx[i] * B * B, lu);
+    load_blk32<B>(vals + p.ent[p.diag_idx[i]], lu);
     double cond = 0.0;
     const int sing = lu_factor_reg<B>(lu, piv, cond);
     if (sing || !(cond < 1e14)) atomicMin(status + 1, i);
-    store_block<B>(diag_lu + (size_t)i * B * B, lu);
+    const long long dl = dlu_off(p, i, B * B);
+    store_blk32<B>(diag_lu + dl, lu);
+    const long long dp = dlu_off(p, i, B);
 #pragma unroll
-    for (int k = 0; k < B; ++k) diag_piv[(size_t)i * B + k] = piv[k];
+    for (int k = 0; k < B; ++k) diag_piv[dp + k * 32] = piv[k];
     S* inv = diag_inv + (size_t)i * B * B;
 #pragma unroll
     for (int c = 0; c < B; ++c) {
@@ -163,11 +204,12 @@ __global__ void __launch_bounds__(kThreads) k_ilu_fwd(PatDev p, const int* __res
     const int pi = p.part[i];
     S xi[B];
     load_vec<B>(rhs + (size_t)i * B, xi);
-    for (int e = p.row_ptr[i]; e < p.row_ptr[i + 1]; ++e) {
-        const int k = p.col_idx[e];
-        if (k >= i) break;
+    const long long lb = p.lbase[i];
+    const int cb = p.lcolb[i], nl = p.nlow[i];
+    for (int s = 0; s < nl; ++s) {  // lower entries, ascending column (slots of the sliced layout)
+        const int k = p.lcols[cb + s * 32];
         if (p.part[k] != pi) continue;
-        const S* blk = vals + (size_t)e * B * B;
+        const S* blk = vals + lb + (long long)s * B * B * 32;
         const S* xk = x + (size_t)k * B;
         S xkv[B];
         load_vec<B>(xk, xkv);
@@ -175,7 +217,7 @@ __global__ void __launch_bounds__(kThreads) k_ilu_fwd(PatDev p, const int* __res
         for (int r = 0; r < B; ++r) {  // block_matvec_sub (dense.hpp:31-39)
             S acc = zero<S>();
 #pragma unroll
-            for (int c = 0; c < B; ++c) acc += blk[r * B + c] * xkv[c];
+            for (int c = 0; c < B; ++c) acc += blk[(r * B + c) * 32] * xkv[c];
             xi[r] -= acc;
         }
     }
@@ -194,26 +236,28 @@ __global__ void __launch_bounds__(kThreads) k_ilu_bwd(PatDev p, const int* __res
     const int pi = p.part[i];
     S xi[B];
     load_vec<B>(x + (size_t)i * B, xi);
-    for (int e = p.row_ptr[i + 1] - 1; e >= p.row_ptr[i]; --e) {
-        const int j = p.col_idx[e];
-        if (j <= i) break;
+    const long long ub = p.ubase[i];
+    const int cb = p.ucolb[i], nu = p.nup[i];
+    for (int s = 0; s < nu; ++s) {  // upper entries, descending column
+        const int j = p.ucols[cb + s * 32];
         if (p.part[j] != pi) continue;
-        const S* blk = vals + (size_t)e * B * B;
+        const S* blk = vals + ub + (long long)s * B * B * 32;
         S xjv[B];
         load_vec<B>(x + (size_t)j * B, xjv);
 #pragma unroll
         for (int r = 0; r < B; ++r) {
             S acc = zero<S>();
 #pragma unroll
-            for (int c = 0; c < B; ++c) acc += blk[r * B + c] * xjv[c];
+            for (int c = 0; c < B; ++c) acc += blk[(r * B + c) * 32] * xjv[c];
             xi[r] -= acc;
         }
     }
     S lu[B * B];
     int piv[B];
-    load_block<B>(diag_lu + (size_t)i * B * B, lu);
+    load_blk32<B>(diag_lu + dlu_off(p, i, B * B), lu);
+    const long long dp = dlu_off(p, i, B);
 #pragma unroll
-    for (int k = 0; k < B; ++k) piv[k] = diag_piv[(size_t)i * B + k];
+    for (int k = 0; k < B; ++k) piv[k] = diag_piv[dp + k * 32];
     lu_solve_reg<B>(lu, piv, xi);
     store_vec<B>(x + (size_t)i * B, xi);
     if (x_accum) {
@@ -221,6 +265,59 @@ __global__ void __launch_bounds__(kThreads) k_ilu_bwd(PatDev p, const int* __res
 #pragma unroll
         for (int k = 0; k < B; ++k) xa[k] += xi[k];
     }
+}
+
+// y_i = sum over the row's entries (ascending) of A_e x_col(e) from the sliced copy of the
+// real A (16-byte element pairs, lane-minor), the diagonal block carrying the complex shift
+// (shift_diagonal): k_matvec's arithmetic, operation by operation
+template <int B, class S>
+__device__ __forceinline__ void sell_row_matvec(const PatDev& p, const double* __restrict__ sell, int i,
+                                                const S* __restrict__ x, const double* __restrict__ shift,
+                                                S (&y)[B]) {
+    constexpr int NP = (B * B + 1) / 2;
+    const double2* base = reinterpret_cast<const double2*>(sell + p.mbase[i]);
+    const int cb = p.mcolb[i], deg = p.row_ptr[i + 1] - p.row_ptr[i], dq = p.diag_idx[i] - p.row_ptr[i];
+#pragma unroll
+    for (int r = 0; r < B; ++r) y[r] = zero<S>();
+    for (int q = 0; q < deg; ++q) {
+        S xc[B];
+        load_vec<B>(x + (size_t)p.mcols[cb + q * 32] * B, xc);
+        double blk[2 * NP];
+#pragma unroll
+        for (int t = 0; t < NP; ++t) {
+            const double2 v = __ldg(base + (long long)(q * NP + t) * 32);
+            blk[2 * t] = v.x;
+            blk[2 * t + 1] = v.y;
+        }
+        const bool diag = q == dq;
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+            S acc = zero<S>();
+#pragma unroll
+            for (int c = 0; c < B; ++c) {
+                if constexpr (sizeof(S) == sizeof(cplx)) {
+                    if (diag && r == c && shift)
+                        acc += mk(blk[r * B + c] + 0.0, 0.0 + shift[i]) * xc[c];
+                    else
+                        acc += rmul(blk[r * B + c], xc[c]);
+                } else {
+                    acc += rmul(blk[r * B + c], xc[c]);
+                }
+            }
+            y[r] += acc;
+        }
+    }
+}
+
+__global__ void k_sell_copy(const int* __restrict__ mblk_e, long long npos, int bb, const double* __restrict__ bsr,
+                            double* __restrict__ sell) {
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (t >= npos) return;
+    const int e = mblk_e[t];
+    if (e < 0) return;
+    const int np = (bb + 1) / 2;
+    double* dst = sell + (t >> 5) * np * 64 + 2 * (t & 31);
+    for (int k = 0; k < bb; ++k) dst[(k >> 1) * 64 + (k & 1)] = bsr[(long long)e * bb + k];
 }
 
 // y_i = sum_e A_e x_col(e) (Bsr::matvec, sparse.hpp:259-270); with rhs: r = rhs - y
@@ -236,7 +333,8 @@ __global__ void __launch_bounds__(kThreads) k_matvec(PatDev p, SystemView<S> A, 
 #pragma unroll
         for (int r = 0; r < B; ++r) y[r] = zero<S>();
         const int di = p.diag_idx[i];
-        for (int e = p.row_ptr[i]; e < p.row_ptr[i + 1]; ++e) {
+        if (!A.vals && A.real_sell) sell_row_matvec<B, S>(p, A.real_sell, i, x, A.shift_im, y);
+        else for (int e = p.row_ptr[i]; e < p.row_ptr[i + 1]; ++e) {
             S xc[B];
             load_vec<B>(x + (size_t)p.col_idx[e] * B, xc);
             const bool diag = e == di;
@@ -342,18 +440,19 @@ __global__ void __launch_bounds__(kThreads) k_ilu_fwd_b(PatDev p, const int* __r
     const int pi = p.part[i];
     S xi[B];
     load_vec<B>(T.r[lane] + (size_t)i * B, xi);
-    for (int e = p.row_ptr[i]; e < p.row_ptr[i + 1]; ++e) {
-        const int k = p.col_idx[e];
-        if (k >= i) break;
+    const long long lb = p.lbase[i];
+    const int cb = p.lcolb[i], nl = p.nlow[i];
+    for (int s = 0; s < nl; ++s) {  // lower entries, ascending column (slots of the sliced layout)
+        const int k = p.lcols[cb + s * 32];
         if (p.part[k] != pi) continue;
-        const S* blk = vals + (size_t)e * B * B;
+        const S* blk = vals + lb + (long long)s * B * B * 32;
         S xkv[B];
         load_vec<B>(x + (size_t)k * B, xkv);
 #pragma unroll
         for (int r = 0; r < B; ++r) {
             S acc = zero<S>();
 #pragma unroll
-            for (int c = 0; c < B; ++c) acc += blk[r * B + c] * xkv[c];
+            for (int c = 0; c < B; ++c) acc += blk[(r * B + c) * 32] * xkv[c];
             xi[r] -= acc;
         }
     }
@@ -373,26 +472,28 @@ __global__ void __launch_bounds__(kThreads) k_ilu_bwd_b(PatDev p, const int* __r
     const int pi = p.part[i];
     S xi[B];
     load_vec<B>(x + (size_t)i * B, xi);
-    for (int e = p.row_ptr[i + 1] - 1; e >= p.row_ptr[i]; --e) {
-        const int j = p.col_idx[e];
-        if (j <= i) break;
+    const long long ub = p.ubase[i];
+    const int cb = p.ucolb[i], nu = p.nup[i];
+    for (int s = 0; s < nu; ++s) {  // upper entries, descending column
+        const int j = p.ucols[cb + s * 32];
         if (p.part[j] != pi) continue;
-        const S* blk = vals + (size_t)e * B * B;
+        const S* blk = vals + ub + (long long)s * B * B * 32;
         S xjv[B];
         load_vec<B>(x + (size_t)j * B, xjv);
 #pragma unroll
         for (int r = 0; r < B; ++r) {
             S acc = zero<S>();
 #pragma unroll
-            for (int c = 0; c < B; ++c) acc += blk[r * B + c] * xjv[c];
+            for (int c = 0; c < B; ++c) acc += blk[(r * B + c) * 32] * xjv[c];
             xi[r] -= acc;
         }
     }
     S lu[B * B];
     int piv[B];
-    load_block<B>(T.diag_lu[lane] + (size_t)i * B * B, lu);
+    load_blk32<B>(T.diag_lu[lane] + dlu_off(p, i, B * B), lu);
+    const long long dp = dlu_off(p, i, B);
 #pragma unroll
-    for (int k = 0; k < B; ++k) piv[k] = T.diag_piv[lane][(size_t)i * B + k];
+    for (int k = 0; k < B; ++k) piv[k] = T.diag_piv[lane][dp + k * 32];
     lu_solve_reg<B>(lu, piv, xi);
     store_vec<B>(x + (size_t)i * B, xi);
     S* xa = T.x[lane] + (size_t)i * B;
@@ -402,7 +503,8 @@ __global__ void __launch_bounds__(kThreads) k_ilu_bwd_b(PatDev p, const int* __r
 
 // r = rhs - (A + i diag(shift)) x per lane (k_matvec's arithmetic), per-CTA |r|^2 partials
 template <int B, class S>
-__global__ void __launch_bounds__(kThreads) k_matvec_b(PatDev p, const double* __restrict__ Areal, LaLanes<S> T) {
+__global__ void __launch_bounds__(kThreads) k_matvec_b(PatDev p, const double* __restrict__ Areal,
+                                                       const double* __restrict__ Asell, LaLanes<S> T) {
     __shared__ double red[kThreads / 32];
     const int lane = blockIdx.x % T.P;
     if (!T.active[lane]) return;
@@ -415,7 +517,8 @@ __global__ void __launch_bounds__(kThreads) k_matvec_b(PatDev p, const double* _
 #pragma unroll
         for (int r = 0; r < B; ++r) y[r] = zero<S>();
         const int di = p.diag_idx[i];
-        for (int e = p.row_ptr[i]; e < p.row_ptr[i + 1]; ++e) {
+        if (Asell) sell_row_matvec<B, S>(p, Asell, i, x, shift, y);
+        else for (int e = p.row_ptr[i]; e < p.row_ptr[i + 1]; ++e) {
             S xc[B];
             load_vec<B>(x + (size_t)p.col_idx[e] * B, xc);
             const bool diag = e == di;
@@ -453,6 +556,94 @@ __global__ void __launch_bounds__(kThreads) k_matvec_b(PatDev p, const double* _
         double s = 0.0;
         for (int w = 0; w < kThreads / 32; ++w) s += red[w];
         T.parts[lane][cta] = s;
+    }
+}
+
+// k_matvec_b on the sliced A with one thread per row serving a group of up to kLG lanes:
+// each block of A is loaded once into registers and applied to every lane's gathered x
+// (the lanes' operations interleave, each lane's sum keeps k_matvec's order); rows, CTAs
+// and per-lane partials exactly as k_matvec_b / k_matvec (same grid of CTAs per lane)
+constexpr int kLG = 5;
+template <int B, class S>
+__global__ void __launch_bounds__(kThreads) k_matvec_lg(PatDev p, const double* __restrict__ sell, int lg,
+                                                        LaLanes<S> T) {
+    constexpr int NP = (B * B + 1) / 2;
+    __shared__ double red[kLG][kThreads / 32];
+    const int ng = (T.P + lg - 1) / lg;
+    const int g = blockIdx.x % ng, cta = blockIdx.x / ng, nct = gridDim.x / ng;
+    const int l0 = g * lg, nl = min(lg, T.P - l0);
+    bool act[kLG];
+#pragma unroll
+    for (int q = 0; q < kLG; ++q) act[q] = q < nl && T.active[l0 + q];
+    double local[kLG];
+#pragma unroll
+    for (int q = 0; q < kLG; ++q) local[q] = 0.0;
+    for (int i = cta * blockDim.x + threadIdx.x; i < p.rows; i += nct * blockDim.x) {
+        S y[kLG][B];
+#pragma unroll
+        for (int q = 0; q < kLG; ++q)
+#pragma unroll
+            for (int r = 0; r < B; ++r) y[q][r] = zero<S>();
+        const double2* base = reinterpret_cast<const double2*>(sell + p.mbase[i]);
+        const int cb = p.mcolb[i], deg = p.row_ptr[i + 1] - p.row_ptr[i], dq = p.diag_idx[i] - p.row_ptr[i];
+        for (int e = 0; e < deg; ++e) {
+            const int col = p.mcols[cb + e * 32];
+            double blk[2 * NP];
+#pragma unroll
+            for (int t = 0; t < NP; ++t) {
+                const double2 v = __ldg(base + (long long)(e * NP + t) * 32);
+                blk[2 * t] = v.x;
+                blk[2 * t + 1] = v.y;
+            }
+            const bool diag = e == dq;
+#pragma unroll
+            for (int q = 0; q < kLG; ++q) {
+                if (!act[q]) continue;
+                S xc[B];
+                load_vec<B>(T.x[l0 + q] + (size_t)col * B, xc);
+                const double* shift = T.shift[l0 + q];
+#pragma unroll
+                for (int r = 0; r < B; ++r) {
+                    S acc = zero<S>();
+#pragma unroll
+                    for (int c = 0; c < B; ++c) {
+                        if constexpr (sizeof(S) == sizeof(cplx)) {
+                            if (diag && r == c && shift)
+                                acc += mk(blk[r * B + c] + 0.0, 0.0 + shift[i]) * xc[c];
+                            else
+                                acc += rmul(blk[r * B + c], xc[c]);
+                        } else {
+                            acc += rmul(blk[r * B + c], xc[c]);
+                        }
+                    }
+                    y[q][r] += acc;
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kLG; ++q) {
+            if (!act[q]) continue;
+            S* o = T.r[l0 + q] + (size_t)i * B;
+            const S* bb = T.rhs[l0 + q] + (size_t)i * B;
+#pragma unroll
+            for (int r = 0; r < B; ++r) {
+                const S v = bb[r] - y[q][r];
+                o[r] = v;
+                local[q] += sq(v);
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kLG; ++q) {
+        double v = local[q];
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+        if ((threadIdx.x & 31) == 0) red[q][threadIdx.x >> 5] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < kLG && act[threadIdx.x]) {
+        double s = 0.0;
+        for (int w = 0; w < kThreads / 32; ++w) s += red[threadIdx.x][w];
+        T.parts[l0 + threadIdx.x][cta] = s;
     }
 }
 
@@ -596,9 +787,127 @@ DevicePattern::DevicePattern(int b_, int rows_, const int* row_ptr_, const int* 
         return out;
     };
     std::vector<int> fr = group(lf, nf, fwd_ptr), br = group(lb, nb, bwd_ptr);
+    // sliced factor layout (la.cuh): per-row lower / upper entry counts; rows of a level by
+    // descending count (stable) so a slice's rows have similar slot counts
+    const int bb = b * b;
+    std::vector<int> nl(rows), nu(rows);
+    for (int i = 0; i < rows; ++i) {
+        nl[i] = h_diag_idx[i] - h_row_ptr[i];
+        nu[i] = h_row_ptr[i + 1] - 1 - h_diag_idx[i];
+    }
+    auto by_count = [&](std::vector<int>& order, const std::vector<int>& ptr, const std::vector<int>& cnt) {
+        for (std::size_t l = 0; l + 1 < ptr.size(); ++l)
+            std::stable_sort(order.begin() + ptr[l], order.begin() + ptr[l + 1],
+                             [&](int x, int y) { return cnt[x] > cnt[y]; });
+    };
+    by_count(fr, fwd_ptr, nl);
+    by_count(br, bwd_ptr, nu);
+    // slices of 32 consecutive rows of one level; returns per-row (slice, lane) and the
+    // per-slice max count
+    auto slices = [&](const std::vector<int>& order, const std::vector<int>& ptr, const std::vector<int>& cnt,
+                      std::vector<int>& sl_of, std::vector<int>& lane_of, std::vector<int>& smax) {
+        sl_of.assign(rows, 0);
+        lane_of.assign(rows, 0);
+        smax.clear();
+        for (std::size_t l = 0; l + 1 < ptr.size(); ++l)
+            for (int t = ptr[l]; t < ptr[l + 1]; ++t) {
+                const int q = t - ptr[l];
+                if ((q & 31) == 0) smax.push_back(0);
+                const int i = order[t];
+                sl_of[i] = (int)smax.size() - 1;
+                lane_of[i] = q & 31;
+                smax.back() = std::max(smax.back(), cnt[i]);
+            }
+    };
+    std::vector<int> fsl, flane, fmax, bsl, blane, bmax;
+    slices(fr, fwd_ptr, nl, fsl, flane, fmax);
+    slices(br, bwd_ptr, nu, bsl, blane, bmax);
+    n_dslices = (int)bmax.size();
+    // element offsets: [L region][U region][diagonal entries (backward slices)]
+    std::vector<long long> fv(fmax.size() + 1, 0), bv(bmax.size() + 1, 0);
+    std::vector<int> fc(fmax.size() + 1, 0), bc(bmax.size() + 1, 0);
+    for (std::size_t k = 0; k < fmax.size(); ++k) {
+        fv[k + 1] = fv[k] + (long long)fmax[k] * bb * 32;
+        fc[k + 1] = fc[k] + fmax[k] * 32;
+    }
+    for (std::size_t k = 0; k < bmax.size(); ++k) {
+        bv[k + 1] = bv[k] + (long long)bmax[k] * bb * 32;
+        bc[k + 1] = bc[k] + bmax[k] * 32;
+    }
+    const long long u0 = fv.back(), d0 = u0 + bv.back();
+    sell_elems = d0 + (long long)n_dslices * bb * 32;
+    std::vector<long long> hl(rows), hu(rows);
+    std::vector<int> hlc(rows), huc(rows), lcs(std::max(fc.back(), 1), 0), ucs(std::max(bc.back(), 1), 0);
+    h_ent.assign(nnzb, 0);
+    h_dpos.assign(rows, 0);
+    for (int i = 0; i < rows; ++i) {
+        hl[i] = fv[fsl[i]] + flane[i];
+        hlc[i] = fc[fsl[i]] + flane[i];
+        hu[i] = u0 + bv[bsl[i]] + blane[i];
+        huc[i] = bc[bsl[i]] + blane[i];
+        h_dpos[i] = bsl[i] * 32 + blane[i];
+        for (int q = 0; q < nl[i]; ++q) {
+            const int e = h_row_ptr[i] + q;
+            h_ent[e] = hl[i] + (long long)q * bb * 32;
+            lcs[hlc[i] + q * 32] = h_col_idx[e];
+        }
+        for (int q = 0; q < nu[i]; ++q) {  // slot q = q-th entry from the row end
+            const int e = h_row_ptr[i + 1] - 1 - q;
+            h_ent[e] = hu[i] + (long long)q * bb * 32;
+            ucs[huc[i] + q * 32] = h_col_idx[e];
+        }
+        h_ent[h_diag_idx[i]] = d0 + (long long)bsl[i] * bb * 32 + blane[i];
+    }
+    // natural 32-row slices of the matvec copy
+    {
+        const int np = (bb + 1) / 2, ns = (rows + 31) / 32;
+        std::vector<long long> so(ns + 1, 0);
+        std::vector<int> co(ns + 1, 0);
+        for (int q = 0; q < ns; ++q) {
+            int md = 0;
+            for (int i = q * 32; i < std::min(rows, q * 32 + 32); ++i) md = std::max(md, h_row_ptr[i + 1] - h_row_ptr[i]);
+            so[q + 1] = so[q] + (long long)md * np * 64;
+            co[q + 1] = co[q] + md * 32;
+        }
+        msell_doubles = so[ns];
+        std::vector<long long> mb(rows);
+        std::vector<int> mc(rows), mcs(std::max(co[ns], 1), 0), mbe(std::max<long long>(so[ns] / (np * 2), 1), -1);
+        for (int i = 0; i < rows; ++i) {
+            const int q = i >> 5, l = i & 31;
+            mb[i] = so[q] + 2 * l;
+            mc[i] = co[q] + l;
+            for (int t = 0; t < h_row_ptr[i + 1] - h_row_ptr[i]; ++t) {
+                mcs[mc[i] + t * 32] = h_col_idx[h_row_ptr[i] + t];
+                mbe[(so[q] / (np * 64) + t) * 32 + l] = h_row_ptr[i] + t;
+            }
+        }
+        auto upl2 = [](long long** d, const std::vector<long long>& h) {
+            FNLH_CUDA(cudaMalloc(d, std::max<std::size_t>(h.size(), 1) * sizeof(long long)));
+            if (!h.empty()) FNLH_CUDA(cudaMemcpy(*d, h.data(), h.size() * sizeof(long long), cudaMemcpyHostToDevice));
+        };
+        auto up2 = [](int** d, const std::vector<int>& h) {
+            FNLH_CUDA(cudaMalloc(d, std::max<std::size_t>(h.size(), 1) * sizeof(int)));
+            if (!h.empty()) FNLH_CUDA(cudaMemcpy(*d, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice));
+        };
+        upl2(&mbase, mb);
+        up2(&mcolb, mc);
+        up2(&mcols, mcs);
+        up2(&mblk_e, mbe);
+    }
+    std::vector<int> be(sell_elems / bb, -1), br_(sell_elems / bb, -1);
+    for (int i = 0; i < rows; ++i)
+        for (int e = h_row_ptr[i]; e < h_row_ptr[i + 1]; ++e) {
+            const long long pos = h_ent[e] / ((long long)bb * 32) * 32 + h_ent[e] % 32;
+            be[pos] = e;
+            br_[pos] = i;
+        }
     auto up = [](int** d, const std::vector<int>& h) {
         FNLH_CUDA(cudaMalloc(d, std::max<std::size_t>(h.size(), 1) * sizeof(int)));
         if (!h.empty()) FNLH_CUDA(cudaMemcpy(*d, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice));
+    };
+    auto upl = [](long long** d, const std::vector<long long>& h) {
+        FNLH_CUDA(cudaMalloc(d, std::max<std::size_t>(h.size(), 1) * sizeof(long long)));
+        if (!h.empty()) FNLH_CUDA(cudaMemcpy(*d, h.data(), h.size() * sizeof(long long), cudaMemcpyHostToDevice));
     };
     up(&row_ptr, h_row_ptr);
     up(&col_idx, h_col_idx);
@@ -606,6 +915,18 @@ DevicePattern::DevicePattern(int b_, int rows_, const int* row_ptr_, const int* 
     up(&part, h_part);
     up(&fwd_rows, fr);
     up(&bwd_rows, br);
+    upl(&ent, h_ent);
+    upl(&lbase, hl);
+    upl(&ubase, hu);
+    up(&lcolb, hlc);
+    up(&ucolb, huc);
+    up(&nlow, nl);
+    up(&nup, nu);
+    up(&lcols, lcs);
+    up(&ucols, ucs);
+    up(&dpos, h_dpos);
+    up(&blk_e, be);
+    up(&blk_row, br_);
 }
 
 DevicePattern::~DevicePattern() {
@@ -615,15 +936,22 @@ DevicePattern::~DevicePattern() {
     cudaFree(part);
     cudaFree(fwd_rows);
     cudaFree(bwd_rows);
+    for (void* q : {(void*)ent, (void*)lbase, (void*)ubase, (void*)lcolb, (void*)ucolb, (void*)nlow, (void*)nup,
+                    (void*)lcols, (void*)ucols, (void*)dpos, (void*)blk_e, (void*)blk_row, (void*)mbase,
+                    (void*)mcolb, (void*)mcols, (void*)mblk_e})
+        cudaFree(q);
 }
 
 template <class S>
 DeviceIlu<S>::DeviceIlu(const DevicePattern* pat) : p(pat) {
     const std::size_t bb = (std::size_t)p->b * p->b;
-    FNLH_CUDA(cudaMalloc(&vals, (std::size_t)p->nnzb * bb * sizeof(S)));
-    FNLH_CUDA(cudaMalloc(&diag_lu, (std::size_t)p->rows * bb * sizeof(S)));
-    FNLH_CUDA(cudaMalloc(&diag_piv, (std::size_t)p->rows * p->b * sizeof(int)));
+    const std::size_t dr = (std::size_t)p->n_dslices * 32;
+    FNLH_CUDA(cudaMalloc(&vals, std::max<std::size_t>(p->sell_elems, 1) * sizeof(S)));
+    FNLH_CUDA(cudaMalloc(&diag_lu, std::max<std::size_t>(dr * bb, 1) * sizeof(S)));
+    FNLH_CUDA(cudaMalloc(&diag_piv, std::max<std::size_t>(dr * p->b, 1) * sizeof(int)));
     FNLH_CUDA(cudaMalloc(&diag_inv, (std::size_t)p->rows * bb * sizeof(S)));
+    // padding slots stay zero (never read as live entries)
+    FNLH_CUDA(cudaMemset(vals, 0, std::max<std::size_t>(p->sell_elems, 1) * sizeof(S)));
 }
 
 template <class S>
@@ -637,8 +965,36 @@ DeviceIlu<S>::~DeviceIlu() {
 template <class S>
 std::size_t DeviceIlu<S>::bytes() const {
     const std::size_t bb = (std::size_t)p->b * p->b;
-    return ((std::size_t)p->nnzb * bb + 2 * (std::size_t)p->rows * bb) * sizeof(S) +
-           (std::size_t)p->rows * p->b * sizeof(int);
+    const std::size_t dr = (std::size_t)p->n_dslices * 32;
+    return ((std::size_t)p->sell_elems + dr * bb + (std::size_t)p->rows * bb) * sizeof(S) + dr * p->b * sizeof(int);
+}
+
+template <class S>
+void DeviceIlu<S>::download(S* vals_out, S* diag_lu_out, int* diag_piv_out, S* diag_inv_out) const {
+    const int b = p->b, bb = b * b;
+    const std::size_t dr = (std::size_t)p->n_dslices * 32;
+    FNLH_CUDA(cudaDeviceSynchronize());
+    if (vals_out) {
+        std::vector<S> h(std::max<std::size_t>(p->sell_elems, 1));
+        FNLH_CUDA(cudaMemcpy(h.data(), vals, h.size() * sizeof(S), cudaMemcpyDeviceToHost));
+        for (int e = 0; e < p->nnzb; ++e)
+            for (int k = 0; k < bb; ++k) vals_out[(std::size_t)e * bb + k] = h[p->h_ent[e] + (long long)k * 32];
+    }
+    auto off = [&](int i, int w) { return (long long)(p->h_dpos[i] >> 5) * w * 32 + (p->h_dpos[i] & 31); };
+    if (diag_lu_out) {
+        std::vector<S> h(std::max<std::size_t>(dr * bb, 1));
+        FNLH_CUDA(cudaMemcpy(h.data(), diag_lu, h.size() * sizeof(S), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < p->rows; ++i)
+            for (int k = 0; k < bb; ++k) diag_lu_out[(std::size_t)i * bb + k] = h[off(i, bb) + (long long)k * 32];
+    }
+    if (diag_piv_out) {
+        std::vector<int> h(std::max<std::size_t>(dr * b, 1));
+        FNLH_CUDA(cudaMemcpy(h.data(), diag_piv, h.size() * sizeof(int), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < p->rows; ++i)
+            for (int k = 0; k < b; ++k) diag_piv_out[(std::size_t)i * b + k] = h[off(i, b) + (long long)k * 32];
+    }
+    if (diag_inv_out)
+        FNLH_CUDA(cudaMemcpy(diag_inv_out, diag_inv, (std::size_t)p->rows * bb * sizeof(S), cudaMemcpyDeviceToHost));
 }
 
 Workspace::Workspace(std::size_t max_len) : vec_len(max_len) {
@@ -676,7 +1032,8 @@ void ilu_factorize_async(const SystemView<S>& A, DeviceIlu<S>& f, int* status, c
     const PatDev pd = dev(p);
     { ::fnlh::note_launch(); k_status_reset<<<1, 1, 0, st>>>(status); }
     FNLH_DISPATCH_B(p.b, {
-        { ::fnlh::note_launch(); k_ilu_copy<B, S><<<(int)(((std::size_t)p.rows * 32 + kThreads - 1) / kThreads), kThreads, 0, st>>>(pd, A, f.vals); }
+        const long long npos = p.sell_elems / (B * B);
+        { ::fnlh::note_launch(); k_ilu_copy<B, S><<<nblocks(npos), kThreads, 0, st>>>(pd, A, f.vals, npos); }
         for (int l = 0; l < p.fwd_levels(); ++l) {
             const int n = p.fwd_ptr[l + 1] - p.fwd_ptr[l];
             { ::fnlh::note_launch(); k_ilu_factor<B, S><<<nblocks(n), kThreads, 0, st>>>(pd, p.fwd_rows + p.fwd_ptr[l], n, f.vals,
@@ -795,7 +1152,7 @@ LinearSolveReport smoothed_solve(const SystemView<S>& A, const S* rhs, const Dev
 // taken per lane on the host after each sweep (one synchronization per sweep for all)
 template <class S>
 void smoothed_solve_batch(const DevicePattern& p, const double* A_real, const LaneSystem<S>* sys, int P,
-                          double tol_rel, int max_iter, LaneReport* reps, Workspace& ws) {
+                          double tol_rel, int max_iter, LaneReport* reps, Workspace& ws, const double* A_sell) {
     if (!(tol_rel > 0.0 && tol_rel < 1.0)) throw ConfigError("smoothed_solve: tol_rel must be in (0,1)");
     if (max_iter < 1) throw ConfigError("smoothed_solve: max_iter must be >= 1");
     if (P < 1 || P > kMaxLanes) throw ConfigError("smoothed_solve_batch: 1 <= P <= kMaxLanes");
@@ -852,7 +1209,12 @@ void smoothed_solve_batch(const DevicePattern& p, const double* A_real, const La
                 const int n = p.bwd_ptr[l + 1] - p.bwd_ptr[l];
                 { ::fnlh::note_launch(); k_ilu_bwd_b<B, S><<<nblocks(n) * P, kThreads, 0, ws.stream>>>(pd, p.bwd_rows + p.bwd_ptr[l], n, T); }
             }
-            { ::fnlh::note_launch(); k_matvec_b<B, S><<<grid * P, kThreads, 0, ws.stream>>>(pd, A_real, T); }
+            if (A_sell && sizeof(S) == sizeof(cplx)) {
+                const int ng = (P + kLG - 1) / kLG, lg = (P + ng - 1) / ng;
+                { ::fnlh::note_launch(); k_matvec_lg<B, S><<<grid * ng, kThreads, 0, ws.stream>>>(pd, A_sell, lg, T); }
+            } else {
+                { ::fnlh::note_launch(); k_matvec_b<B, S><<<grid * P, kThreads, 0, ws.stream>>>(pd, A_real, A_sell, T); }
+            }
         });
         { ::fnlh::note_launch(); k_finish_b<<<P, 256, 0, ws.stream>>>(Tc, Td, sizeof(S) == sizeof(cplx) ? 1 : 0, grid, d_norm); }
         FNLH_CUDA(cudaGetLastError());
@@ -872,6 +1234,13 @@ void smoothed_solve_batch(const DevicePattern& p, const double* A_real, const La
             }
         }
     }
+}
+
+void sell_from_bsr(const DevicePattern& p, const double* bsr, double* sell, cudaStream_t st) {
+    const int bb = p.b * p.b;
+    const long long npos = p.msell_doubles / (((bb + 1) / 2) * 2);
+    { ::fnlh::note_launch(); k_sell_copy<<<nblocks(npos), kThreads, 0, st>>>(p.mblk_e, npos, bb, bsr, sell); }
+    FNLH_CUDA(cudaGetLastError());
 }
 
 template <class S>
@@ -899,7 +1268,7 @@ void block_diag_factor(int b, int n, S* blocks, int* piv, int* status, cudaStrea
                                                  double, int, S*, Workspace&);                             \
     template void block_diag_solve<S>(int, int, const S*, const int*, const S*, S*, cudaStream_t);         \
     template void smoothed_solve_batch<S>(const DevicePattern&, const double*, const LaneSystem<S>*, int, double,  \
-                                          int, LaneReport*, Workspace&);                                          \
+                                          int, LaneReport*, Workspace&, const double*);                                          \
     template void block_diag_factor<S>(int, int, S*, int*, int*, cudaStream_t);
 
 FNLH_INST(double)

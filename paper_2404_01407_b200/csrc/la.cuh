@@ -31,6 +31,34 @@ struct DevicePattern {
     int max_deg = 0;
     bool single_partition = true;
 
+    // Sliced-ELL storage of the ILU factor values (DeviceIlu), so that the threads of a
+    // level kernel (one row each) read their rows' blocks coalesced: the rows of one
+    // forward level are cut into slices of 32 (rows of a level ordered by descending
+    // lower-entry count, stable), and slot s (the s-th lower entry, ascending column)
+    // element k of the row in lane l sits at lbase + (s*b*b + k)*32 with lbase = slice
+    // offset + l.  Upper entries likewise over the backward levels, slots in descending
+    // column order (the backward loop's order); diagonal entries and the pivot LUs /
+    // pivots over backward-level slices too.  ent[e] = element-0 offset of CSR entry e
+    // (element stride 32), used by the factorization; host unpacking uses h_ent / h_dpos.
+    long long* ent = nullptr;
+    long long* lbase = nullptr;
+    long long* ubase = nullptr;
+    int *lcolb = nullptr, *ucolb = nullptr, *nlow = nullptr, *nup = nullptr;
+    int *lcols = nullptr, *ucols = nullptr;
+    int* dpos = nullptr;  // slice*32 + lane of row i in the pivot (diag_lu / diag_piv) layout
+    int *blk_e = nullptr, *blk_row = nullptr;  // per block position (sell_elems / b^2): CSR entry, row; -1 = padding
+    long long sell_elems = 0;  // elements of DeviceIlu::vals
+    int n_dslices = 0;         // slices of the pivot layout
+    std::vector<long long> h_ent;
+    std::vector<int> h_dpos;
+    // Sliced-ELL copy of a real BSR on this pattern (the matvec operand A5, sell_from_bsr):
+    // slices of 32 consecutive rows, slot s = the row's s-th entry, element pairs of a block
+    // as 16-byte words, lane-minor: row i (lane l) slot s pair q at mbase[i] + (s*pairs + q)*64
+    // (doubles), mbase = slice offset + 2l; columns at mcols[mcolb[i] + 32 s]
+    long long* mbase = nullptr;
+    int *mcolb = nullptr, *mcols = nullptr, *mblk_e = nullptr;
+    long long msell_doubles = 0;
+
     DevicePattern(int b, int rows, const int* row_ptr, const int* col_idx, const int* partition);
     ~DevicePattern();
     DevicePattern(const DevicePattern&) = delete;
@@ -39,7 +67,9 @@ struct DevicePattern {
     int bwd_levels() const { return static_cast<int>(bwd_ptr.size()) - 1; }
 };
 
-// Ilu<S> storage (sparse.hpp:180-205): vals nnzb*b*b, diag_lu / diag_inv rows*b*b, piv rows*b
+// Ilu<S> storage (sparse.hpp:180-205) in the pattern's sliced layout: vals (sell_elems),
+// diag_lu / diag_piv over n_dslices*32 rows, diag_inv rows*b*b (row-major, gathered by the
+// factorization only)
 template <class S>
 struct DeviceIlu {
     const DevicePattern* p = nullptr;
@@ -52,6 +82,9 @@ struct DeviceIlu {
     DeviceIlu(const DeviceIlu&) = delete;
     DeviceIlu& operator=(const DeviceIlu&) = delete;
     std::size_t bytes() const;
+    // the reference layout (Ilu<S>: vals nnzb*b*b, diag_lu rows*b*b, diag_piv rows*b, diag_inv
+    // rows*b*b); any pointer may be null
+    void download(S* vals_out, S* diag_lu_out, int* diag_piv_out, S* diag_inv_out) const;
 };
 
 // A system matrix as the reference sees it: either a stored S-valued BSR, or a real
@@ -63,7 +96,11 @@ struct SystemView {
     const double* real_vals = nullptr;  // used when vals == nullptr
     const S* vals = nullptr;
     const double* shift_im = nullptr;   // per node Im(s_i) (Re(s_i) = 0), complex systems only
+    const double* real_sell = nullptr;  // optional sliced copy of real_vals (sell_from_bsr): matvec operand
 };
+
+// real BSR (pattern layout) -> the pattern's sliced matvec layout (msell_doubles)
+void sell_from_bsr(const DevicePattern& p, const double* bsr, double* sell, cudaStream_t st);
 
 // Scratch for reductions and the Richardson loop, one per stream.
 struct Workspace {
@@ -101,7 +138,8 @@ struct LaneReport {
 // per-lane shifts and factors; host stopping rule per lane after each sweep
 template <class S>
 void smoothed_solve_batch(const DevicePattern& p, const double* A_real, const LaneSystem<S>* sys, int P,
-                          double tol_rel, int max_iter, LaneReport* reps, Workspace& ws);
+                          double tol_rel, int max_iter, LaneReport* reps, Workspace& ws,
+                          const double* A_sell = nullptr);
 
 // status codes (mirror core.hpp:22-56)
 enum Status : int { kOk = 0, kConfig = 1, kState = 2, kShape = 3, kUnsupported = 4, kFactorization = 5,

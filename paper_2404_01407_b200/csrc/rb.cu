@@ -888,11 +888,12 @@ SellDev sell_dev(const SellLayout& L, const double* vals) {
 bool rb_eligible(const DevicePattern& p, int* n0) {
     if (!p.single_partition || p.fwd_levels() != 2 || p.bwd_levels() != 2) return false;
     const int c0 = p.fwd_ptr[1];
-    // level 0 must be exactly rows [0, c0) (colour-major); level 1 rows [c0, n)
+    // level 0 must be exactly the rows [0, c0) (colour-major; in any order within the level);
+    // level 1 then holds [c0, n)
     std::vector<int> rows(p.rows);
     FNLH_CUDA(cudaMemcpy(rows.data(), p.fwd_rows, p.rows * sizeof(int), cudaMemcpyDeviceToHost));
-    for (int k = 0; k < p.rows; ++k)
-        if (rows[k] != k) return false;
+    for (int k = 0; k < c0; ++k)
+        if (rows[k] >= c0) return false;
     // no edges inside a colour
     for (int i = 0; i < p.rows; ++i)
         for (int e = p.h_row_ptr[i]; e < p.h_row_ptr[i + 1]; ++e) {

@@ -134,6 +134,7 @@ DeviceSolver::DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int
             rb_r_.alloc(len);
         } else {
             A5_.alloc((std::size_t)pat_->nnzb * mesh.b * mesh.b);  // BSR A5 (the 2-colour path keeps only its SELL copy)
+            A5s_.alloc(std::max<long long>(pat_->msell_doubles, 1));  // sliced copy: the matvec operand (la.cuh)
             ilu_mean_ = std::make_unique<DeviceIlu<double>>(pat_.get());
             ilu_h_ = std::make_unique<DeviceIlu<cplx>>(pat_.get());  // ONE workspace reused by every harmonic
         }
@@ -202,7 +203,7 @@ std::size_t DeviceSolver::lhs_bytes() const {
         else
             for (const auto& ln : lanes_) s += ln->f->bytes();
     } else if (sch_.implicit) {
-        s = A5_.bytes() + ilu_mean_->bytes();
+        s = A5_.bytes() + A5s_.bytes() + ilu_mean_->bytes();
         if (lanes_.empty())
             s += ilu_h_->bytes();
         else
@@ -524,6 +525,7 @@ void DeviceSolver::harmonic_batch(const int* hs, int P, std::vector<double>& h_n
             SystemView<cplx> Ah;
             Ah.p = pat_.get();
             Ah.real_vals = A5_.ptr;
+            Ah.real_sell = A5s_.ptr;
             Ah.shift_im = ln.shift.ptr;
             ilu_factorize_async<cplx>(Ah, *ln.gf, ln.fac.ptr, sm);
             FNLH_CUDA(cudaEventRecord(ln.done, sm));
@@ -577,7 +579,7 @@ void DeviceSolver::harmonic_batch(const int* hs, int P, std::vector<double>& h_n
                                                ln.v[8].ptr};
                     live[nl++] = m;
                 }
-            if (nl) smoothed_solve_batch<cplx>(*pat_, A5_.ptr, sys, nl, sch_.linear_tol, sch_.linear_max_iter, out, *ws_);
+            if (nl) smoothed_solve_batch<cplx>(*pat_, A5_.ptr, sys, nl, sch_.linear_tol, sch_.linear_max_iter, out, *ws_, A5s_.ptr);
             for (int q = 0; q < nl; ++q) {
                 lrep[live[q]][k - 1] = out[q];
                 hrep[live[q]][k - 1] = out[q].rep;
@@ -654,6 +656,7 @@ void DeviceSolver::assemble_a5(cudaStream_t st) {
         t.bytes = A5_.bytes();
     }
     disc_->fd_jacobian(mean_.ptr, nullptr, nullptr, st, &t);
+    if (!rbA_) sell_from_bsr(*pat_, A5_.ptr, A5s_.ptr, st);
 }
 
 ConvergenceEntry DeviceSolver::outer_iteration_host(const double* mean_in, const cplx* amps_in, double* mean_out,
@@ -704,6 +707,7 @@ void DeviceSolver::phase_harmonics(const int* owned) {
             SystemView<double> Am;
             Am.p = pat_.get();
             Am.real_vals = A5_.ptr;
+            Am.real_sell = A5s_.ptr;
             ilu_factorize<double>(Am, *ilu_mean_, *ws_);
         }
     } else {
@@ -753,6 +757,7 @@ void DeviceSolver::phase_harmonics(const int* owned) {
                     SystemView<cplx> Ah;
                     Ah.p = pat_.get();
                     Ah.real_vals = A5_.ptr;
+                    Ah.real_sell = A5s_.ptr;
                     Ah.shift_im = shift_.ptr;
                     if (rbA_) {
                         rb_factorize_async<cplx>(*rbA_, shift_.ptr, *rb_h_, fac_status_.ptr, st);
@@ -852,6 +857,7 @@ ConvergenceEntry DeviceSolver::phase_mean(const std::vector<double>& h_norm,
         SystemView<double> Am;
         Am.p = pat_.get();
         Am.real_vals = A5_.ptr;
+        Am.real_sell = A5s_.ptr;
         auto solve = [&](const double* rhs, double* x, int, LinearSolveReport& rep) {
             rep = smoothed_solve<double>(Am, rhs, *ilu_mean_, sch_.linear_tol, sch_.linear_max_iter, x, *ws_);
             return true;
@@ -911,6 +917,7 @@ double DeviceSolver::time_harmonic_sweeps(int h, int nsweeps) {
     SystemView<cplx> Ah;
     Ah.p = pat_.get();
     Ah.real_vals = A5_.ptr;
+    Ah.real_sell = A5s_.ptr;
     Ah.shift_im = shift_.ptr;
     RbIlu<cplx>* fh = rb_h_ ? rb_h_.get() : (lanes_.empty() ? nullptr : lanes_[0]->f.get());
     DeviceIlu<cplx>* gh = ilu_h_ ? ilu_h_.get() : (lanes_.empty() ? nullptr : lanes_[0]->gf.get());
@@ -957,6 +964,7 @@ double DeviceSolver::time_harmonic_sweeps_batch(int P, int nsweeps) {
             SystemView<cplx> Ah;
             Ah.p = pat_.get();
             Ah.real_vals = A5_.ptr;
+            Ah.real_sell = A5s_.ptr;
             Ah.shift_im = ln.shift.ptr;
             ilu_factorize<cplx>(Ah, *ln.gf, *ws_);
         }
@@ -975,7 +983,7 @@ double DeviceSolver::time_harmonic_sweeps_batch(int P, int nsweeps) {
         rb_smoothed_solve_batch<cplx>(*rbA_, mem, P, 1e-300, nsweeps, st);
     } else {
         LaneReport out[kMaxBatch];
-        smoothed_solve_batch<cplx>(*pat_, A5_.ptr, sys, P, 1e-300, nsweeps, out, *ws_);
+        smoothed_solve_batch<cplx>(*pat_, A5_.ptr, sys, P, 1e-300, nsweeps, out, *ws_, A5s_.ptr);
     }
     FNLH_CUDA(cudaEventRecord(ev1_, st));
     FNLH_CUDA(cudaEventSynchronize(ev1_));

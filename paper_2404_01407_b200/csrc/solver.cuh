@@ -180,7 +180,7 @@ private:
     std::unique_ptr<DevicePattern> pat_;
     std::unique_ptr<DeviceDisc> disc_;
     std::unique_ptr<Workspace> ws_;
-    DeviceBuffer<double> mean_, df_, A5_, P_, PLU_, shift_;
+    DeviceBuffer<double> mean_, df_, A5_, A5s_, P_, PLU_, shift_;
     DeviceBuffer<int> Ppiv_, pcpiv_;
     DeviceBuffer<cplx> amps_, forcing_, pclu_;
     std::unique_ptr<DeviceIlu<double>> ilu_mean_;

@@ -1,4 +1,4 @@
-"""Profiling driver: C2 harmonic sweeps (the roofline kernel), optionally after one
+"""Profiling driver: C2 (or --case cN) harmonic sweeps (the roofline kernel), optionally after one
 pseudo-step (--step).  Default: the exact (bitwise) sweep; --onepass the one-pass
 sweep; --all every variant; --batch P also times the batched sweep of P harmonic lanes
 (workers = P).  Run under ncu with -k regex:k_rb to capture the sweep kernels."""
@@ -13,7 +13,8 @@ from paper_2404_01407_b200.solver import FnlhSolver  # noqa: E402
 args = sys.argv[1:]
 scale = float(args[0]) if args and args[0][0].isdigit() else 1.0
 P = int(args[args.index("--batch") + 1]) if "--batch" in args else 1
-c = make_case("c2", scale=scale, workers=P)
+case = args[args.index("--case") + 1] if "--case" in args else "c2"
+c = make_case(case, scale=scale, workers=P)
 s = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
 if "--step" in args:
     s.outer_iteration()
