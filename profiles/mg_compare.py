@@ -42,6 +42,14 @@ def run(name, scale, nh, scheme_over, drop, cap):
         hit = next((e for e in hist if e[key] <= tgt), None)
         out[f"{name}_drop_iter"] = hit["iter"] + 1 if hit else None
         out[f"{name}_drop_s"] = hit["seconds"] if hit else None
+        # every whole order on the way: [orders, iteration, device seconds]
+        orders = []
+        for o in range(1, int(drop) + 1):
+            h = next((e for e in hist if e[key] <= hist[0][key] * 10.0 ** (-o)), None)
+            if h is None:
+                break
+            orders.append([o, h["iter"] + 1, round(h["seconds"], 3)])
+        out[f"{name}_orders"] = orders
     return out
 
 
