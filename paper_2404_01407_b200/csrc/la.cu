@@ -17,7 +17,8 @@ namespace fnlh {
 namespace {
 
 constexpr int kThreads = 128;
-constexpr int kRedBlocks = 592;  // 4 x 148 SMs
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs (norm reductions; callers' partial buffers hold 592)
+constexpr int kMvBlocks = 2368;  // 16 x 148: matvec-residual grid (rows per thread ~ N / 303k; enough warps in flight)
 
 struct PatDev {
     int b, rows, nnzb;
@@ -999,7 +1000,7 @@ void DeviceIlu<S>::download(S* vals_out, S* diag_lu_out, int* diag_piv_out, S* d
 
 Workspace::Workspace(std::size_t max_len) : vec_len(max_len) {
     FNLH_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-    n_partials = 8192;
+    n_partials = 32768;  // >= kMvBlocks * kMaxLanes + 2 kMaxLanes + 16
     FNLH_CUDA(cudaMalloc(&partials, n_partials * sizeof(double)));
     FNLH_CUDA(cudaMalloc(&scalars, 64 * sizeof(double)));
     FNLH_CUDA(cudaMallocHost(&h_scalars, 64 * sizeof(double)));
@@ -1073,7 +1074,7 @@ void ilu_apply(const DeviceIlu<S>& f, const S* rhs, S* x, Workspace& ws, S* x_ac
 template <class S>
 void residual_norm(const SystemView<S>& A, const S* rhs, const S* x, S* r, double* d_norm2, Workspace& ws) {
     const DevicePattern& p = *A.p;
-    const int grid = std::min(nblocks(p.rows), kRedBlocks);
+    const int grid = std::min(nblocks(p.rows), kMvBlocks);
     FNLH_DISPATCH_B(p.b, {
         { ::fnlh::note_launch(); k_matvec<B, S><<<grid, kThreads, 0, ws.stream>>>(dev(p), A, x, rhs, r, ws.partials); }
     });
@@ -1084,7 +1085,7 @@ void residual_norm(const SystemView<S>& A, const S* rhs, const S* x, S* r, doubl
 template <class S>
 void matvec(const SystemView<S>& A, const S* x, S* y, Workspace& ws) {
     const DevicePattern& p = *A.p;
-    const int grid = std::min(nblocks(p.rows), kRedBlocks);
+    const int grid = std::min(nblocks(p.rows), kMvBlocks);
     FNLH_DISPATCH_B(p.b, {
         { ::fnlh::note_launch(); k_matvec<B, S><<<grid, kThreads, 0, ws.stream>>>(dev(p), A, x, nullptr, y, nullptr); }
     });
@@ -1158,7 +1159,7 @@ void smoothed_solve_batch(const DevicePattern& p, const double* A_real, const La
     if (P < 1 || P > kMaxLanes) throw ConfigError("smoothed_solve_batch: 1 <= P <= kMaxLanes");
     const std::size_t len = (std::size_t)p.rows * p.b;
     const PatDev pd = dev(p);
-    const int grid = std::min(nblocks(p.rows), kRedBlocks);
+    const int grid = std::min(nblocks(p.rows), kMvBlocks);
     if ((std::size_t)ws.n_partials < (std::size_t)grid * P + 2 * kMaxLanes + 16)
         throw ConfigError("smoothed_solve_batch: workspace too small");
     LaLanes<S> T{};
