@@ -27,7 +27,8 @@ enum fnlh_status {
     FNLH_UNSUPPORTED = 4,   /* UnsupportedCaseError */
     FNLH_FACTORIZATION = 5, /* FactorizationError(node) */
     FNLH_DIVERGENCE = 6,    /* DivergenceError(stage, field) */
-    FNLH_CUDA = 7           /* device / runtime failure */
+    FNLH_CUDA = 7,          /* device / runtime failure */
+    FNLH_NONCONVERGENCE = 8 /* NonConvergenceError (core.hpp:54-56): the URANS oracle's period cap */
 };
 
 typedef struct fnlh_pattern fnlh_pattern;
@@ -211,6 +212,22 @@ int fnlh_solver_info(const fnlh_solver* s, double* out);
 /* counters (7 doubles): [sweeps, block-row updates, last outer iteration device ms, and its
    split: J + A5 + mean ILU, harmonic RK steps (+ exchange), DF, mean RK step (ms)] */
 int fnlh_solver_counters(const fnlh_solver* s, double* out);
+
+/* ---- time-accurate reference solver (SPEC oracle_urans; declared by oracle.hpp:28-52,
+   `unsteady_solve`, which the reference does not implement) -------------------------------
+   Classical 4-stage explicit time-accurate integration of V dQ/dt = -R(W, t) at a global
+   stable step (cfl * min_i V_i / sum_f lambda_f at the steady state, then shrunk so a period
+   is a whole number of steps and of samples), from `steady` (N*b, primitive; NULL = the
+   solver's current mean) under the periodic boundary forcing
+   sum_l 2 Re(forcing_l e^{i omega_l t}) in perturbation mode referenced to `steady`
+   (order 2, the FNLH residual itself), marched period by period until the period-to-period
+   relative L2 change of the state is below periodic_tol (after at least min_periods), then
+   one period sampled uniformly into samples (samples_per_period * N*b doubles; the count is
+   raised to 4 l_max + 2 when smaller and returned in info[0]).
+   info (5 doubles): [samples, steps per period, dt, periods marched, last relative change].
+   NonConvergenceError when max_periods pass first (the last period is still sampled). */
+int fnlh_solver_unsteady(fnlh_solver* s, const double* steady, int samples_per_period, double cfl,
+                         double periodic_tol, int max_periods, int min_periods, double* samples, double* info);
 
 /* ---- device mesh preprocessing (csrc/meshgen.cu) ----------------
    Median-dual geometry of a structured ci x cj x ck sector (hex cells, or each hex split

@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("FNLH_B200_LIB", os.path.join(HERE, "libfnlh_b200.so")
 _i, _d, _p = C.c_int, C.c_double, C.c_void_p
 
 STATUS = {1: "ConfigError", 2: "StateError", 3: "ShapeError", 4: "UnsupportedCaseError",
-          5: "FactorizationError", 6: "DivergenceError", 7: "CudaError"}
+          5: "FactorizationError", 6: "DivergenceError", 7: "CudaError", 8: "NonConvergenceError"}
 
 
 class FnlhError(RuntimeError):

@@ -256,6 +256,13 @@ int fnlh_solver_get_df(const fnlh_solver* s, double* df) {
     return guarded([&] { s->s->get_df(df); });
 }
 
+int fnlh_solver_unsteady(fnlh_solver* s, const double* steady, int samples_per_period, double cfl,
+                         double periodic_tol, int max_periods, int min_periods, double* samples, double* info) {
+    return guarded([&] {
+        s->s->unsteady_solve(steady, samples_per_period, cfl, periodic_tol, max_periods, min_periods, samples, info);
+    });
+}
+
 int fnlh_solver_num_reports(const fnlh_solver* s) { return static_cast<int>(s->s->reports().size()); }
 
 int fnlh_solver_get_reports(const fnlh_solver* s, fnlh_linear_report* out) {

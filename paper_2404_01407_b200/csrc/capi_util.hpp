@@ -46,6 +46,9 @@ int guarded(F&& f) {
         e.msg = x.what();
         e.stage = x.stage;
         return 6;
+    } catch (const NonConvergenceError& x) {
+        e.msg = x.what();
+        return 8;
     } catch (const std::exception& x) {
         e.msg = x.what();
         return 7;

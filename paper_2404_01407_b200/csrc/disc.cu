@@ -1108,7 +1108,6 @@ void DeviceDisc::linearized_residual(const double* mean, const cplx* what, doubl
     FNLH_CUDA(cudaGetLastError());
 }
 
-namespace {
 // HarmonicSpec::base_frequency / max_multiple (case.cpp:10-44)
 void base_frequency(const std::vector<double>& omega, double& base, int& lmax) {
     const double rel_tol = 1e-9;
@@ -1139,7 +1138,6 @@ void base_frequency(const std::vector<double>& omega, double& base, int& lmax) {
     for (double w : omega)
         if (w > 0.0) lmax = std::max(lmax, static_cast<int>(std::llround(w / g)));
 }
-}  // namespace
 
 void DeviceDisc::deterministic_flux(const double* mean, const std::vector<const cplx*>& amps,
                                     const std::vector<double>& omega, double* df, cudaStream_t st, bool deferred,

@@ -109,6 +109,10 @@ private:
     std::vector<double> h_nfpad_;
 };
 
+// HarmonicSpec::base_frequency / max_multiple (case.cpp:10-44): base = 0, lmax = 0 without
+// positive frequencies; ConfigError when incommensurate
+void base_frequency(const std::vector<double>& omega, double& base, int& lmax);
+
 // --- RK stage / update kernels (rk.cpp:41-99) ---------------------------------
 template <class S>
 void stage_blend(double beta, const S* vis_fresh, S* vis_blend, std::size_t len, cudaStream_t st);

@@ -34,5 +34,8 @@ struct DivergenceError : std::runtime_error {
           stage(stage_idx),
           field(std::move(field_name)) {}
 };
+struct NonConvergenceError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
 
 }  // namespace fnlh

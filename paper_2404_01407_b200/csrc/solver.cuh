@@ -119,6 +119,10 @@ public:
     int lanes() const { return lanes_.empty() ? 1 : (int)lanes_.size(); }
     // time `sweeps` batched Richardson sweeps of harmonics [0, P) (P <= lanes())
     double time_harmonic_sweeps_batch(int P, int sweeps);
+    // time-accurate reference solver (SPEC oracle_urans; oracle.hpp:28-52; urans.cu):
+    // include/fnlh_b200.h fnlh_solver_unsteady
+    void unsteady_solve(const double* steady_host, int samples_per_period, double cfl, double periodic_tol,
+                        int max_periods, int min_periods, double* samples_host, double* info);
     int n() const { return disc_->n(); }
     int b() const { return disc_->b(); }
     int nh() const { return nh_; }

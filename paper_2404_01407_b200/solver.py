@@ -120,6 +120,7 @@ class FnlhSolver:
                                        ptr(pat["partition"]), C.byref(self.scheme), _i(self.nh), ptr(idx), ptr(om),
                                        ptr(forc), _i(nforcing), ptr(f64(mean0)), C.byref(h)))
         self.h = h
+        self.omegas = np.array(om)
         self.hierarchy = None
         levels = int(scheme.get("mg_levels", 1))
         if levels > 1:  # SchemeConfig::mg_levels (driver.hpp:24): 2x2x2 agglomeration, mesh.hierarchy

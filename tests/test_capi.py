@@ -41,4 +41,4 @@ def test_no_cpu_fallback():
 def test_error_taxonomy_matches_reference():
     from paper_2404_01407_b200._lib import STATUS
     assert STATUS == {1: "ConfigError", 2: "StateError", 3: "ShapeError", 4: "UnsupportedCaseError",
-                      5: "FactorizationError", 6: "DivergenceError", 7: "CudaError"}
+                      5: "FactorizationError", 6: "DivergenceError", 7: "CudaError", 8: "NonConvergenceError"}
