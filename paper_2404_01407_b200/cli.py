@@ -1,4 +1,4 @@
-"""Command-line entry point (SPEC.md cli module): run / compare / bench with the
+"""Command-line entry point (SPEC.md cli module): run / oracle / compare / bench with the
 machine-readable outputs the specification lists -- a fully materialized manifest, the
 convergence CSV (iter, resid_mean, resid_h0..h{N_h-1}, R_z, seconds, WU), optional
 final-field CSVs and a key-value summary.  The reference specifies these but ships no
@@ -7,6 +7,7 @@ CLI; the solver underneath is the device FnlhSolver.
     python -m paper_2404_01407_b200 run c2 --max-iters 50 --out runs/c2
     python -m paper_2404_01407_b200 run case.cfg --mode explicit --mg-levels 3
     python -m paper_2404_01407_b200 compare runs/a runs/b --bound 1e-8
+    python -m paper_2404_01407_b200 oracle c1 --scale 0.5 --harmonics 1 --out runs/c1_oracle
     python -m paper_2404_01407_b200 bench memory-audit
 
 Config files are plain-text `key = value` lines (# comments); keys: case (c1..c5),
@@ -157,6 +158,77 @@ def read_kv(path):
     return out
 
 
+def write_manifest(out, r, c, tr, extra=()):
+    write_kv(os.path.join(out, "manifest.txt"),
+             [("case", r["case"]), ("description", c.description), ("nodes", c.mesh.n), ("block_size", c.mesh.b)] +
+             [(k, r[k]) for k in ("scale", "harmonics", "mode", "cfl", "eps", "tol", "sweeps", "mg_levels",
+                                  "partitions", "workers", "target_drop", "max_iters")] +
+             [("omegas", " ".join(repr(float(w)) for w in c.omegas)), ("output_dir", os.path.abspath(out)),
+              ("t_ref_seconds", repr(tr)), ("data", "synthetic (seeded, cases.py)")] + list(extra))
+
+
+def write_fields(out, mean, amps, b):
+    np.savetxt(os.path.join(out, "field_mean.csv"), np.asarray(mean).reshape(-1, b), delimiter=",",
+               header=",".join(f"w{k}" for k in range(b)), comments="", fmt="%.17g")
+    for h in range(len(amps)):
+        a = np.asarray(amps[h]).reshape(-1, b)
+        np.savetxt(os.path.join(out, f"field_h{h}.csv"), np.concatenate([a.real, a.imag], axis=1), delimiter=",",
+                   header=",".join([f"re{k}" for k in range(b)] + [f"im{k}" for k in range(b)]), comments="",
+                   fmt="%.17g")
+
+
+def cmd_oracle(args) -> int:
+    """SPEC oracle_urans through the CLI: run_to_convergence, then the time-accurate march
+    (urans.unsteady_solve) from the converged mean.  Writes the oracle's fields (time mean,
+    DFT amplitudes) in the run layout, so `compare <run dir> <oracle dir>` applies, plus
+    amplitude_errors.csv (compare_amplitudes: interior nodes) against the FNLH fields of
+    the same run.  Exit 0, or 3 when either the FNLH run or the march hits its cap, 4 on
+    divergence."""
+    from . import urans
+    from ._lib import FnlhError
+    r = resolve(args)
+    out = args.out or os.path.join("runs", f"{r['case']}_oracle")
+    os.makedirs(out, exist_ok=True)
+    tr = t_ref()
+    c, g = build_solver(r)
+    hist, reason, msg = run_loop(g, r)
+    if reason == "divergence":
+        print(f"oracle: the FNLH run diverged ({msg})", file=sys.stderr)
+        return EXIT[reason]
+    mean_f, amps_f = g.state()
+    opt = urans.OracleOptions(samples_per_period=args.samples, cfl=args.oracle_cfl, max_periods=args.max_periods)
+    t0 = time.time()
+    code = 0
+    try:
+        ts = urans.unsteady_solve(g, mean_f, opt)
+    except FnlhError as ex:
+        if ex.kind != "NonConvergenceError":
+            raise
+        ts, code = ex.timeseries, 3
+        print(f"oracle: {ex}", file=sys.stderr)
+    wall = time.time() - t0
+    mean_t, amps_t = urans.extract_harmonics(ts, g.omegas)
+    write_manifest(out, r, c, tr, [("kind", "oracle_urans")])
+    write_fields(out, mean_t, amps_t, c.mesh.b)
+    errs = urans.compare_amplitudes(amps_f, amps_t, c.mesh)
+    with open(os.path.join(out, "amplitude_errors.csv"), "w") as f:
+        f.write("harmonic,omega,rel_l2_interior\n")
+        for (l, e), om in zip(errs, g.omegas):
+            f.write(f"{l},{float(om)!r},{e!r}\n")
+    write_kv(os.path.join(out, "summary.txt"),
+             [("case", r["case"]), ("fnlh_reason", reason), ("fnlh_iterations", len(hist)),
+              ("samples", ts.info["samples"]), ("steps_per_period", ts.info["steps_per_period"]),
+              ("dt", repr(ts.info["dt"])), ("periods", ts.info["periods"]),
+              ("last_change", repr(ts.info["last_change"])), ("march_wall_seconds", f"{wall:.3f}"),
+              ("periodic", int(code == 0))] + [(f"amp_error_h{l}", repr(e)) for l, e in errs])
+    for l, e in errs:
+        print(f"harmonic {l}: FNLH vs time-accurate relative L2 (interior) {e:.3e}")
+    print(f"-> {out}")
+    if code == 0 and reason != "target-drop":
+        code = EXIT[reason]
+    return code
+
+
 def cmd_run(args) -> int:
     r = resolve(args)
     out = args.out or os.path.join("runs", f"{r['case']}_{r['mode']}")
@@ -165,12 +237,7 @@ def cmd_run(args) -> int:
     t0 = time.time()
     c, g = build_solver(r)
     setup = time.time() - t0
-    write_kv(os.path.join(out, "manifest.txt"),
-             [("case", r["case"]), ("description", c.description), ("nodes", c.mesh.n), ("block_size", c.mesh.b)] +
-             [(k, r[k]) for k in ("scale", "harmonics", "mode", "cfl", "eps", "tol", "sweeps", "mg_levels",
-                                  "partitions", "workers", "target_drop", "max_iters")] +
-             [("omegas", " ".join(repr(float(w)) for w in c.omegas)), ("output_dir", os.path.abspath(out)),
-              ("t_ref_seconds", repr(tr)), ("data", "synthetic (seeded, cases.py)")])
+    write_manifest(out, r, c, tr)
     nh = r["harmonics"]
     fcsv = open(os.path.join(out, "convergence.csv"), "w", newline="")
     w = csv.writer(fcsv)
@@ -185,15 +252,7 @@ def cmd_run(args) -> int:
     hist, reason, msg = run_loop(g, r, row)
     fcsv.close()
     if args.fields:
-        mean, amps = g.state()
-        b = c.mesh.b
-        np.savetxt(os.path.join(out, "field_mean.csv"), mean.reshape(-1, b), delimiter=",",
-                   header=",".join(f"w{k}" for k in range(b)), comments="", fmt="%.17g")
-        for h in range(nh):
-            a = amps[h].reshape(-1, b)
-            np.savetxt(os.path.join(out, f"field_h{h}.csv"), np.concatenate([a.real, a.imag], axis=1), delimiter=",",
-                       header=",".join([f"re{k}" for k in range(b)] + [f"im{k}" for k in range(b)]), comments="",
-                       fmt="%.17g")
+        write_fields(out, *g.state(), c.mesh.b)
     last = hist[-1] if hist else dict(resid_mean=float("nan"), rz=float("nan"), seconds=0.0)
     write_kv(os.path.join(out, "summary.txt"),
              [("case", r["case"]), ("mode", r["mode"]), ("sigma_cfl", r["cfl"]), ("mg_levels", r["mg_levels"]),
@@ -305,6 +364,19 @@ def main(argv=None) -> int:
     pr.add_argument("--scale", type=float)
     pr.add_argument("--out")
     pr.add_argument("--fields", action="store_true", help="write the final fields as CSV")
+    po = sub.add_parser("oracle", help="FNLH run, then the time-accurate reference march (SPEC oracle_urans)")
+    po.add_argument("config")
+    for k in ("--cfl", "--eps", "--tol", "--scale"):
+        po.add_argument(k, type=float)
+    for k, d in (("--sweeps", "sweeps"), ("--harmonics", "harmonics"), ("--workers", "workers"),
+                 ("--max-iters", "max_iters"), ("--mg-levels", "mg_levels"), ("--partitions", "partitions")):
+        po.add_argument(k, dest=d, type=int)
+    po.add_argument("--mode", choices=["implicit", "explicit"])
+    po.add_argument("--target-drop", dest="target_drop", type=float)
+    po.add_argument("--samples", type=int, default=32, help="samples per period (raised to 4 l_max + 2)")
+    po.add_argument("--oracle-cfl", dest="oracle_cfl", type=float, default=0.7)
+    po.add_argument("--max-periods", dest="max_periods", type=int, default=200)
+    po.add_argument("--out")
     pc = sub.add_parser("compare", help="per-field error report between two runs")
     pc.add_argument("a")
     pc.add_argument("b")
@@ -324,6 +396,8 @@ def main(argv=None) -> int:
             return cmd_run(a)
         if a.cmd == "compare":
             return cmd_compare(a)
+        if a.cmd == "oracle":
+            return cmd_oracle(a)
         return cmd_bench(a)
     except ConfigParseError as ex:
         print(f"error: {ex}", file=sys.stderr)

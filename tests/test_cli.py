@@ -56,3 +56,20 @@ def test_run_compare_bench(tmp_path):
     with open(out) as f:
         mem = list(csv.DictReader(f))
     assert len({r["peak_lhs_bytes"] for r in mem}) == 1
+
+
+@pytest.mark.gpu
+def test_oracle_command(tmp_path):
+    """`oracle`: FNLH run + the time-accurate march; fields in the run layout (so `compare`
+    applies between a run and its oracle), amplitude errors on interior nodes."""
+    o, a = str(tmp_path / "o"), str(tmp_path / "a")
+    args = ["c1", "--scale", "0.5", "--harmonics", "1", "--max-iters", "400", "--target-drop", "8", "--tol", "0.01",
+            "--sweeps", "10"]
+    assert main(["oracle"] + args + ["--out", o]) in (0, 3)
+    summ = read_kv(os.path.join(o, "summary.txt"))
+    assert summ["periodic"] == "1" and float(summ["amp_error_h0"]) < 0.02
+    with open(os.path.join(o, "amplitude_errors.csv")) as f:
+        rows = list(csv.DictReader(f))
+    assert len(rows) == 1 and float(rows[0]["rel_l2_interior"]) < 0.02
+    assert main(["run"] + args + ["--out", a, "--fields"]) in (0, 3)
+    assert main(["compare", a, o, "--bound", "0.05"]) == 0
