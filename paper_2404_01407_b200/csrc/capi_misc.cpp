@@ -6,8 +6,8 @@
 #include "capi_util.hpp"
 
 namespace fnlh {
-long long& launch_count() {
-    static long long n = 0;
+std::atomic<long long>& launch_count() {
+    static std::atomic<long long> n{0};
     return n;
 }
 ErrorState& last_error() {
@@ -22,7 +22,7 @@ const char* fnlh_last_error(void) { return fnlh::last_error().msg.c_str(); }
 int fnlh_last_error_node(void) { return fnlh::last_error().node; }
 int fnlh_last_error_stage(void) { return fnlh::last_error().stage; }
 
-long long fnlh_launch_count(void) { return fnlh::launch_count(); }
+long long fnlh_launch_count(void) { return fnlh::launch_count().load(); }
 
 int fnlh_device_count(void) {
     int n = 0;

@@ -87,7 +87,10 @@ struct DeviceBuffer {
     }
     void upload(const T* h, std::size_t count) {
         alloc(count);
-        if (count) FNLH_CUDA(cudaMemcpy(ptr, h, count * sizeof(T), cudaMemcpyHostToDevice));
+        if (count) {
+            FNLH_CUDA(cudaMemcpy(ptr, h, count * sizeof(T), cudaMemcpyHostToDevice));
+            legacy_sync();
+        }
     }
     std::size_t bytes() const { return n * sizeof(T); }
 };

@@ -6,6 +6,7 @@
 // multiplies and adds reproduce its arithmetic bit for bit.
 #pragma once
 
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <math.h>
@@ -29,9 +30,17 @@ struct CudaError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
 
-// count of kernel launches issued by this library (bench.py "gpu_launches")
-long long& launch_count();
-inline void note_launch() { ++launch_count(); }
+// Setup transfers and memsets go through the legacy default stream, which the library's
+// non-blocking work streams do not wait for (and a pageable upload may return before its
+// DMA lands).  Wait for it before any work stream can read the data: with several host
+// threads driving distinct handles, another thread's legacy-stream traffic can otherwise
+// delay it past the first kernels.
+inline void legacy_sync() { FNLH_CUDA(cudaStreamSynchronize(cudaStreamLegacy)); }
+
+// count of kernel launches issued by this library (bench.py "gpu_launches"); atomic: the
+// C ABI may be called concurrently from several host threads with distinct handles
+std::atomic<long long>& launch_count();
+inline void note_launch() { launch_count().fetch_add(1, std::memory_order_relaxed); }
 
 // std::complex<double> layout (re, im), reference arithmetic order.
 struct alignas(16) cplx {

@@ -945,6 +945,7 @@ DeviceDisc::DeviceDisc(const MeshArrays& m, const DevicePattern* pattern) : pat_
     umax_.alloc(64);
 
     FNLH_CUDA(cudaMemset(err_.ptr, 0xff, sizeof(unsigned long long)));
+    legacy_sync();
 }
 
 DeviceDisc::~DeviceDisc() {

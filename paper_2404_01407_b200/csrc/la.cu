@@ -928,6 +928,7 @@ DevicePattern::DevicePattern(int b_, int rows_, const int* row_ptr_, const int* 
     up(&dpos, h_dpos);
     up(&blk_e, be);
     up(&blk_row, br_);
+    legacy_sync();
 }
 
 DevicePattern::~DevicePattern() {
@@ -953,6 +954,7 @@ DeviceIlu<S>::DeviceIlu(const DevicePattern* pat) : p(pat) {
     FNLH_CUDA(cudaMalloc(&diag_inv, (std::size_t)p->rows * bb * sizeof(S)));
     // padding slots stay zero (never read as live entries)
     FNLH_CUDA(cudaMemset(vals, 0, std::max<std::size_t>(p->sell_elems, 1) * sizeof(S)));
+    legacy_sync();
 }
 
 template <class S>

@@ -986,6 +986,7 @@ RbSystem::RbSystem(const DevicePattern* p, int n0) : p_(p) {
     trans_.upload(trans.data(), trans.size());
     vals_.alloc(std::max<long long>(L_.total_vals, 1));
     FNLH_CUDA(cudaMemset(vals_.ptr, 0, vals_.bytes()));
+    legacy_sync();
     grid0 = nb(n0);
     grid1 = nb(n - n0);
     partials.alloc(std::max(grid0 + grid1, nb((long long)n * b)) + 8);
@@ -1054,12 +1055,12 @@ void rb_smoothed_solve_batch(const RbSystem& A, const RbMember<S>* mem, int P, d
     const int g0 = A.grid0 * P, g1 = A.grid1 * P;
     RB_DISPATCH(L.b, {
         const std::size_t sm = (std::size_t)maxoff * B * kT * sizeof(S);
-        static bool attr = false;
-        if (!attr) {
+        static const bool attr = [] {  // once per instantiation (thread-safe static initialization)
             FNLH_CUDA(cudaFuncSetAttribute(k_rb_colour0<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
             FNLH_CUDA(cudaFuncSetAttribute(k_rbx_colour1<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            attr = true;
-        }
+            return true;
+        }();
+        (void)attr;
         if (rb_sweep_mode() == 1) {
             for (int s = 1; s <= max_iter; ++s) {
                 { ::fnlh::note_launch(); k_rb_forward1<B, S><<<g1, kT, 0, stm>>>(sd, T, s); }

@@ -50,8 +50,8 @@ struct RbControl {  // device-side Richardson control block
 };
 
 // global switch (fnlh_set_red_black) so tests can force the general level-scheduled path
-inline bool& rb_enabled() {
-    static bool on = true;
+inline std::atomic<bool>& rb_enabled() {
+    static std::atomic<bool> on{true};
     return on;
 }
 // fnlh_set_rb_sweep: the 2-colour sweep variant
@@ -59,8 +59,8 @@ inline bool& rb_enabled() {
 //   1           reference operation order, split K_F / K_B / K_R: 3 kernels per sweep
 //   2           one pass over A per sweep, L_ik r_k applied as A_ik (U_kk^{-1} r_k):
 //               same preconditioner, iterates equal to rounding (not bitwise)
-inline int& rb_sweep_mode() {
-    static int mode = 0;
+inline std::atomic<int>& rb_sweep_mode() {
+    static std::atomic<int> mode{0};
     return mode;
 }
 

@@ -122,6 +122,7 @@ DeviceSolver::DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int
     if (nh * nforcing)
         FNLH_CUDA(cudaMemcpy(forcing_.ptr, forcing_pairs, (std::size_t)nh * nforcing * sizeof(cplx),
                              cudaMemcpyHostToDevice));
+    legacy_sync();  // the memsets and uploads above complete before any work stream runs
     if (sch_.implicit) {
 
         int n0 = 0;
@@ -373,6 +374,7 @@ void DeviceSolver::add_level(const MeshArrays& mesh, const int* row_ptr, const i
     if (nh_ * nforcing)
         FNLH_CUDA(cudaMemcpy(L->forcing.ptr, forcing_pairs, (std::size_t)nh_ * nforcing * sizeof(cplx),
                              cudaMemcpyHostToDevice));
+    legacy_sync();
     const std::size_t len = (std::size_t)nc * mesh.b, bb = (std::size_t)nc * mesh.b * mesh.b;
     L->mean.alloc(len);
     L->P.alloc(bb);
@@ -1028,6 +1030,7 @@ void DeviceSolver::set_state(const double* mean, const double* amps_pairs) {
     if (mean) FNLH_CUDA(cudaMemcpy(mean_.ptr, mean, len * sizeof(double), cudaMemcpyHostToDevice));
     if (amps_pairs && nh_)
         FNLH_CUDA(cudaMemcpy(amps_.ptr, amps_pairs, (std::size_t)nh_ * len * sizeof(cplx), cudaMemcpyHostToDevice));
+    legacy_sync();
 }
 
 void DeviceSolver::get_df(double* df) const {

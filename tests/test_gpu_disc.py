@@ -331,3 +331,41 @@ def test_nozzle_multigrid_against_reference(ref, levels):
     mg, ag = g.state()
     assert rel(extract(mg, noz.n), mr) < 1e-10
     assert rel(np.stack([extract(a, noz.n) for a in ag]), ar) < 1e-8
+
+
+def test_concurrent_handles_from_host_threads():
+    """SURVEY 8(b) threading contract: the C ABI is callable concurrently with distinct
+    handles (each solver owns its streams and workspaces; A5 / pattern per handle).  Four
+    host threads drive four solvers (hex 2-colour and tet level-scheduled paths, implicit
+    and explicit) at once; every history and final state is bitwise the sequential run's."""
+    import threading
+    from paper_2404_01407_b200.solver import FnlhSolver
+    specs = [("c1", 0.5, True, 1), ("c2", 0.08, True, 3), ("c3", 0.06, True, 3), ("c5", 0.06, False, 1)]
+    cases = [make_case(n, scale=s, implicit=imp, workers=w) for n, s, imp, w in specs]
+
+    def drive(c, out, k):
+        g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
+        hist = [g.outer_iteration() for _ in range(3)]
+        out[k] = ([(e["resid_mean"], e["rz"]) for e in hist], g.state())
+
+    seq, par = {}, {}
+    for k, c in enumerate(cases):
+        drive(c, seq, k)
+    errors = []
+
+    def guarded(c, k):
+        try:
+            drive(c, par, k)
+        except Exception as ex:  # surfaced below
+            errors.append(ex)
+
+    ts = [threading.Thread(target=guarded, args=(c, k)) for k, c in enumerate(cases)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    for k in range(len(cases)):
+        (hs, (ms, as_)), (hp, (mp, ap)) = seq[k], par[k]
+        assert hs == hp, specs[k]
+        assert np.array_equal(ms, mp) and np.array_equal(as_, ap), specs[k]
