@@ -126,3 +126,21 @@ def test_c3_full_size_relaxation_vs_reference(ref, c3, cplx):
     assert abs(rd[1] / rr[1] - 1) < 1e-12 and abs(rd[2] / rr[2] - 1) < 1e-12
     res = rhs - (la.matvec(P, A, xd, shift) if cplx else la.matvec(P, A, xd))
     assert abs(np.linalg.norm(res) / rd[2] - 1) < 1e-10
+
+
+def test_c4_full_size_memory_contract():
+    """BASELINE configs[3] at full size (4,276,737 nodes, 29.8 M blocks): the LHS bytes with
+    10 harmonics equal those with 1 (one reused complex workspace, workers = 1; PAPER's
+    memory-saving idea); one outer iteration with all 10 harmonics runs."""
+    import math
+    from paper_2404_01407_b200.solver import FnlhSolver
+    lhs = {}
+    for nh in (1, 10):
+        c = make_case("c4", nh=nh, workers=1)
+        g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
+        lhs[nh] = g.lhs_bytes()
+        if nh == 10:
+            e = g.outer_iteration()
+            assert math.isfinite(e["resid_mean"]) and math.isfinite(e["rz"]) and len(e["resid_h"]) == 10
+        del g
+    assert lhs[1] == lhs[10]
