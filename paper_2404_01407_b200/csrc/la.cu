@@ -665,6 +665,39 @@ __global__ void k_finish_b(LaLanes<cplx> Tc, LaLanes<double> Td, int is_cplx, in
     }
 }
 
+// device-side stopping rule of smoothed_solve (sparse.hpp:305-328) per lane: control block
+// [initial, final, target, iterations, converged, diverged] (8 doubles per lane)
+__global__ void k_lane_init(int P, const double* __restrict__ norm_sq, double tol, int* __restrict__ active,
+                            double* __restrict__ ctl) {
+    const int l = threadIdx.x;
+    if (l >= P) return;
+    const double r0 = sqrt(norm_sq[l]);
+    double* c = ctl + 8 * l;
+    c[0] = r0;
+    c[1] = r0;
+    c[2] = tol * r0;
+    c[3] = 0.0;
+    c[4] = r0 == 0.0 ? 1.0 : 0.0;
+    c[5] = 0.0;
+    active[l] = r0 == 0.0 ? 0 : 1;
+}
+__global__ void k_lane_stop(int P, int it, const double* __restrict__ norm_sq, int* __restrict__ active,
+                            double* __restrict__ ctl) {
+    const int l = threadIdx.x;
+    if (l >= P || !active[l]) return;
+    const double nrm = sqrt(norm_sq[l]);
+    double* c = ctl + 8 * l;
+    c[1] = nrm;
+    c[3] = it;
+    if (!isfinite(nrm)) {
+        c[5] = 1.0;
+        active[l] = 0;
+    } else if (nrm <= c[2]) {
+        c[4] = 1.0;
+        active[l] = 0;
+    }
+}
+
 // fixed-order final reduction of the per-block partials (deterministic run to run)
 __global__ void k_finish(const double* __restrict__ partials, int n, double* __restrict__ out) {
     __shared__ double red[32];
@@ -1120,6 +1153,13 @@ LinearSolveReport smoothed_solve(const SystemView<S>& A, const S* rhs, const Dev
     const std::size_t len = (std::size_t)p.rows * p.b;
     S* r = static_cast<S*>(ws.vec[0]);
     S* z = static_cast<S*>(ws.vec[1]);
+    if (!A.vals) {  // real A (+ per-node shift): the lane kernels with one lane, stopping rule on the device
+        const LaneSystem<S> sys{&f, A.shift_im, rhs, x, z, r};
+        LaneReport lr;
+        smoothed_solve_batch<S>(p, A.real_vals, &sys, 1, tol_rel, max_iter, &lr, ws, A.real_sell);
+        if (lr.diverged) throw DivergenceError("non-finite iterate in smoothed_solve", lr.rep.iterations, "linear");
+        return lr.rep;
+    }
     FNLH_CUDA(cudaMemsetAsync(x, 0, len * sizeof(S), ws.stream));
     LinearSolveReport rep;
     norm2_sq(rhs, len, ws.scalars, ws);
@@ -1152,7 +1192,8 @@ LinearSolveReport smoothed_solve(const SystemView<S>& A, const S* rhs, const Dev
 
 // smoothed_solve (sparse.hpp:295-331) on P systems at once: the level kernels and the
 // residual matvec serve every still-iterating lane in one launch; the stopping rule is
-// taken per lane on the host after each sweep (one synchronization per sweep for all)
+// taken per lane on the device after each sweep (k_lane_stop), one host synchronization
+// per solve
 template <class S>
 void smoothed_solve_batch(const DevicePattern& p, const double* A_real, const LaneSystem<S>* sys, int P,
                           double tol_rel, int max_iter, LaneReport* reps, Workspace& ws, const double* A_sell) {
@@ -1162,15 +1203,16 @@ void smoothed_solve_batch(const DevicePattern& p, const double* A_real, const La
     const std::size_t len = (std::size_t)p.rows * p.b;
     const PatDev pd = dev(p);
     const int grid = std::min(nblocks(p.rows), kMvBlocks);
-    if ((std::size_t)ws.n_partials < (std::size_t)grid * P + 2 * kMaxLanes + 16)
+    // partials layout: [lanes' matvec partials grid*P][active][norms][control blocks][norm scratch 592]
+    const std::size_t scratch = (std::size_t)grid * P + 10 * kMaxLanes + 16;
+    if ((std::size_t)ws.n_partials < scratch + kRedBlocks)
         throw ConfigError("smoothed_solve_batch: workspace too small");
     LaLanes<S> T{};
     T.P = P;
     int* d_active = reinterpret_cast<int*>(ws.partials + (std::size_t)grid * P);
     double* d_norm = ws.partials + (std::size_t)grid * P + kMaxLanes;
+    double* d_ctl = d_norm + kMaxLanes;
     T.active = d_active;
-    std::vector<double> target(P);
-    int h_active[kMaxLanes] = {0};
     for (int m = 0; m < P; ++m) {
         T.vals[m] = sys[m].f->vals;
         T.diag_lu[m] = sys[m].f->diag_lu;
@@ -1182,27 +1224,16 @@ void smoothed_solve_batch(const DevicePattern& p, const double* A_real, const La
         T.r[m] = sys[m].r;
         T.parts[m] = ws.partials + (std::size_t)grid * m;
         FNLH_CUDA(cudaMemsetAsync(sys[m].x, 0, len * sizeof(S), ws.stream));
-        norm2_sq(sys[m].rhs, len, d_norm + m, ws);
+        norm2_sq_on(sys[m].rhs, len, d_norm + m, ws.partials + scratch, ws.stream);
         FNLH_CUDA(cudaMemcpyAsync(sys[m].r, sys[m].rhs, len * sizeof(S), cudaMemcpyDeviceToDevice, ws.stream));
     }
-    FNLH_CUDA(cudaMemcpyAsync(ws.h_scalars, d_norm, P * sizeof(double), cudaMemcpyDeviceToHost, ws.stream));
-    FNLH_CUDA(cudaStreamSynchronize(ws.stream));
-    int live = 0;
-    for (int m = 0; m < P; ++m) {
-        reps[m] = LaneReport{};
-        reps[m].rep.initial_residual = std::sqrt(ws.h_scalars[m]);
-        reps[m].rep.final_residual = reps[m].rep.initial_residual;
-        target[m] = tol_rel * reps[m].rep.initial_residual;
-        if (reps[m].rep.initial_residual == 0.0)
-            reps[m].rep.converged = 1;
-        else
-            h_active[m] = 1, ++live;
-    }
+    { ::fnlh::note_launch(); k_lane_init<<<1, 32, 0, ws.stream>>>(P, d_norm, tol_rel, d_active, d_ctl); }
     LaLanes<cplx> Tc{};
     LaLanes<double> Td{};
     if constexpr (sizeof(S) == sizeof(cplx)) Tc = T; else Td = T;
-    for (int it = 1; it <= max_iter && live; ++it) {
-        FNLH_CUDA(cudaMemcpyAsync(d_active, h_active, P * sizeof(int), cudaMemcpyHostToDevice, ws.stream));
+    // every sweep is enqueued; a lane whose stopping rule fired is skipped by the kernels
+    // (active[lane] == 0), so the loop needs no host synchronization
+    for (int it = 1; it <= max_iter; ++it) {
         FNLH_DISPATCH_B(p.b, {
             for (int l = 0; l < p.fwd_levels(); ++l) {
                 const int n = p.fwd_ptr[l + 1] - p.fwd_ptr[l];
@@ -1220,22 +1251,19 @@ void smoothed_solve_batch(const DevicePattern& p, const double* A_real, const La
             }
         });
         { ::fnlh::note_launch(); k_finish_b<<<P, 256, 0, ws.stream>>>(Tc, Td, sizeof(S) == sizeof(cplx) ? 1 : 0, grid, d_norm); }
+        { ::fnlh::note_launch(); k_lane_stop<<<1, 32, 0, ws.stream>>>(P, it, d_norm, d_active, d_ctl); }
         FNLH_CUDA(cudaGetLastError());
-        FNLH_CUDA(cudaMemcpyAsync(ws.h_scalars, d_norm, P * sizeof(double), cudaMemcpyDeviceToHost, ws.stream));
-        FNLH_CUDA(cudaStreamSynchronize(ws.stream));
-        for (int m = 0; m < P; ++m) {
-            if (!h_active[m]) continue;
-            LinearSolveReport& rp = reps[m].rep;
-            rp.iterations = it;
-            rp.final_residual = std::sqrt(ws.h_scalars[m]);
-            if (!std::isfinite(rp.final_residual)) {
-                reps[m].diverged = 1;
-                h_active[m] = 0, --live;
-            } else if (rp.final_residual <= target[m]) {
-                rp.converged = 1;
-                h_active[m] = 0, --live;
-            }
-        }
+    }
+    FNLH_CUDA(cudaMemcpyAsync(ws.h_scalars, d_ctl, 8 * P * sizeof(double), cudaMemcpyDeviceToHost, ws.stream));
+    FNLH_CUDA(cudaStreamSynchronize(ws.stream));
+    for (int m = 0; m < P; ++m) {
+        const double* c = ws.h_scalars + 8 * m;
+        reps[m] = LaneReport{};
+        reps[m].rep.initial_residual = c[0];
+        reps[m].rep.final_residual = c[1];
+        reps[m].rep.iterations = (int)c[3];
+        reps[m].rep.converged = c[4] != 0.0 ? 1 : 0;
+        reps[m].diverged = c[5] != 0.0 ? 1 : 0;
     }
 }
 

@@ -135,7 +135,7 @@ struct LaneReport {
     int diverged = 0;  // a non-finite residual norm (DivergenceError at rep.iterations)
 };
 // P smoothed_solves on systems sharing the real A (A_real, the pattern's BSR layout) with
-// per-lane shifts and factors; host stopping rule per lane after each sweep
+// per-lane shifts and factors; device-side stopping rule per lane after each sweep (one host synchronization per solve)
 template <class S>
 void smoothed_solve_batch(const DevicePattern& p, const double* A_real, const LaneSystem<S>* sys, int P,
                           double tol_rel, int max_iter, LaneReport* reps, Workspace& ws,
