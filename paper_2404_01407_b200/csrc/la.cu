@@ -42,12 +42,14 @@ struct PatDev {
     const long long* __restrict__ mbase;
     const int* __restrict__ mcolb;
     const int* __restrict__ mcols;
+    const long long* __restrict__ kjo;
+    const long long* __restrict__ kj;
 };
 
 PatDev dev(const DevicePattern& p) {
     return PatDev{p.b, p.rows, p.nnzb, p.row_ptr, p.col_idx, p.diag_idx, p.part, p.ent, p.lbase, p.ubase,
                   p.lcolb, p.ucolb, p.nlow, p.nup, p.lcols, p.ucols, p.dpos, p.blk_e, p.blk_row,
-                  p.mbase, p.mcolb, p.mcols};
+                  p.mbase, p.mcolb, p.mcols, p.kjo, p.kj};
 }
 
 // b x b block at g with element stride 32 (sliced layout)
@@ -93,6 +95,24 @@ __device__ __forceinline__ S sys_entry(const SystemView<S>& A, int e, int k, boo
     return v;
 }
 
+// the factorization's (k, j) lookups (find_entry, sparse.cpp:42-48), once per pattern: for
+// row i, each lower entry ek and each later entry ej of the row, the sliced offset of
+// U_kj = entry (k, col ej), or -1
+__global__ void k_build_kj(PatDev p, long long* __restrict__ kj) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.rows) return;
+    const int rb = p.row_ptr[i], re = p.row_ptr[i + 1];
+    long long pos = p.kjo[i];
+    for (int ek = rb; ek < re; ++ek) {
+        const int k = p.col_idx[ek];
+        if (k >= i) break;
+        for (int ej = ek + 1; ej < re; ++ej) {
+            const int e = find_entry(p, k, p.col_idx[ej]);
+            kj[pos++] = e < 0 ? -1 : p.ent[e];
+        }
+    }
+}
+
 // Ilu::factorize copy phase (sparse.cpp:199-209): one thread per block position of the
 // sliced layout (blk_e / blk_row: source entry and row, -1 for padding), so each element
 // store of a warp is 32 consecutive lanes
@@ -121,9 +141,12 @@ __global__ void __launch_bounds__(kThreads) k_ilu_factor(PatDev p, const int* __
     const int i = rows[t];
     const int pi = p.part[i];
     const int rb = p.row_ptr[i], re = p.row_ptr[i + 1];
+    long long pos = p.kjo[i];  // (ek, ej > ek) -> offset of U_kj, precomputed (la.cuh kj)
     for (int ek = rb; ek < re; ++ek) {
         const int k = p.col_idx[ek];
         if (k >= i) break;
+        const long long kb = pos;
+        pos += re - ek - 1;
         if (p.part[k] != pi) continue;
         // L_ik = A_ik * U_kk^{-1}
         S tmp[B * B];
@@ -144,14 +167,13 @@ __global__ void __launch_bounds__(kThreads) k_ilu_factor(PatDev p, const int* __
         }
         store_blk32<B>(lik, tmp);
         // A_ij -= L_ik U_kj for j > k present in both rows (zero-skip, dense.hpp:47)
-        for (int ej = rb; ej < re; ++ej) {
+        for (int ej = ek + 1; ej < re; ++ej) {  // columns ascend: exactly the entries with j > k
+            const long long uo = p.kj[kb + (ej - ek - 1)];
             const int j = p.col_idx[ej];
-            if (j <= k) continue;
             if (p.part[j] != pi) continue;
-            const int ekj = find_entry(p, k, j);
-            if (ekj < 0) continue;
+            if (uo < 0) continue;  // (k, j) not in the pattern (find, sparse.cpp:42-48)
             if (p.part[k] != p.part[j]) continue;
-            const S* u = vals + p.ent[ekj];
+            const S* u = vals + uo;
             S* cblk = vals + p.ent[ej];
 #pragma unroll
             for (int r = 0; r < B; ++r) {  // block_matmul_sub row by row (same operation order)
@@ -961,6 +983,18 @@ DevicePattern::DevicePattern(int b_, int rows_, const int* row_ptr_, const int* 
     up(&dpos, h_dpos);
     up(&blk_e, be);
     up(&blk_row, br_);
+    {
+        std::vector<long long> ko(rows + 1, 0);
+        for (int i = 0; i < rows; ++i) {
+            long long c = 0;
+            for (int e = h_row_ptr[i]; e < h_row_ptr[i + 1] && h_col_idx[e] < i; ++e) c += h_row_ptr[i + 1] - e - 1;
+            ko[i + 1] = ko[i] + c;
+        }
+        upl(&kjo, ko);
+        FNLH_CUDA(cudaMalloc(&kj, std::max<long long>(ko[rows], 1) * sizeof(long long)));
+        if (rows) { ::fnlh::note_launch(); k_build_kj<<<nblocks(rows), kThreads>>>(dev(*this), kj); }
+        FNLH_CUDA(cudaGetLastError());
+    }
     legacy_sync();
 }
 
@@ -973,7 +1007,7 @@ DevicePattern::~DevicePattern() {
     cudaFree(bwd_rows);
     for (void* q : {(void*)ent, (void*)lbase, (void*)ubase, (void*)lcolb, (void*)ucolb, (void*)nlow, (void*)nup,
                     (void*)lcols, (void*)ucols, (void*)dpos, (void*)blk_e, (void*)blk_row, (void*)mbase,
-                    (void*)mcolb, (void*)mcols, (void*)mblk_e})
+                    (void*)mcolb, (void*)mcols, (void*)mblk_e, (void*)kjo, (void*)kj})
         cudaFree(q);
 }
 

@@ -58,6 +58,10 @@ struct DevicePattern {
     long long* mbase = nullptr;
     int *mcolb = nullptr, *mcols = nullptr, *mblk_e = nullptr;
     long long msell_doubles = 0;
+    // the factorization's (k, j) lookups, precomputed: for row i, lower entry ek and each
+    // later entry ej, the sliced offset of U_kj = entry (col ek, col ej) or -1, at
+    // kj[kjo[i] + ...] in loop order (the reference's find, sparse.cpp:42-48, done once)
+    long long *kjo = nullptr, *kj = nullptr;
 
     DevicePattern(int b, int rows, const int* row_ptr, const int* col_idx, const int* partition);
     ~DevicePattern();
