@@ -1075,6 +1075,8 @@ Workspace::Workspace(std::size_t max_len) : vec_len(max_len) {
     FNLH_CUDA(cudaMallocHost(&h_scalars, 64 * sizeof(double)));
     FNLH_CUDA(cudaMalloc(&status, 8 * sizeof(int)));
     FNLH_CUDA(cudaMallocHost(&h_status, 8 * sizeof(int)));
+    FNLH_CUDA(cudaMallocHost(&h_flags, 2 * kMaxLanes * sizeof(int)));
+    for (auto& e : flag_ev) FNLH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& v : vec) FNLH_CUDA(cudaMalloc(&v, std::max<std::size_t>(max_len, 1) * sizeof(cplx)));
 }
 
@@ -1085,6 +1087,9 @@ Workspace::~Workspace() {
     cudaFreeHost(h_scalars);
     cudaFree(status);
     cudaFreeHost(h_status);
+    cudaFreeHost(h_flags);
+    for (auto& e : flag_ev)
+        if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -1287,6 +1292,24 @@ void smoothed_solve_batch(const DevicePattern& p, const double* A_real, const La
         { ::fnlh::note_launch(); k_finish_b<<<P, 256, 0, ws.stream>>>(Tc, Td, sizeof(S) == sizeof(cplx) ? 1 : 0, grid, d_norm); }
         { ::fnlh::note_launch(); k_lane_stop<<<1, 32, 0, ws.stream>>>(P, it, d_norm, d_active, d_ctl); }
         FNLH_CUDA(cudaGetLastError());
+        // non-blocking look-behind: once the flags of an earlier sweep have landed and every
+        // lane had stopped, no further sweep is enqueued (a deep level schedule launches
+        // 2 x levels kernels per sweep; the kernels of a stopped lane return at once anyway)
+        const int slot = it & 1;
+        FNLH_CUDA(cudaMemcpyAsync(ws.h_flags + slot * kMaxLanes, d_active, P * sizeof(int), cudaMemcpyDeviceToHost,
+                                  ws.stream));
+        FNLH_CUDA(cudaEventRecord(ws.flag_ev[slot], ws.stream));
+        // a deep schedule (a natural-order chain: hundreds of tiny launches per sweep) waits
+        // for this sweep's flags, a shallow one only looks at the previous sweep's
+        const bool deep = p.fwd_levels() + p.bwd_levels() > 32;
+        if (deep) FNLH_CUDA(cudaEventSynchronize(ws.flag_ev[slot]));
+        const int seen = deep ? slot : slot ^ 1;
+        if ((deep || it > 1) && cudaEventQuery(ws.flag_ev[seen]) == cudaSuccess) {
+            const int* f = ws.h_flags + seen * kMaxLanes;
+            bool any = false;
+            for (int m = 0; m < P; ++m) any |= f[m] != 0;
+            if (!any) break;
+        }
     }
     FNLH_CUDA(cudaMemcpyAsync(ws.h_scalars, d_ctl, 8 * P * sizeof(double), cudaMemcpyDeviceToHost, ws.stream));
     FNLH_CUDA(cudaStreamSynchronize(ws.stream));

@@ -114,6 +114,8 @@ struct Workspace {
     double* h_scalars = nullptr; // pinned mirror
     int* status = nullptr;       // device status words [code, node]
     int* h_status = nullptr;
+    int* h_flags = nullptr;             // pinned: lanes' active flags after a sweep, two slots
+    cudaEvent_t flag_ev[2] = {nullptr, nullptr};
     void* vec[4] = {nullptr, nullptr, nullptr, nullptr};  // r, z, ax, spare (len * sizeof(cplx))
     std::size_t vec_len = 0;
     int n_partials = 0;
