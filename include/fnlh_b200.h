@@ -247,6 +247,13 @@ void fnlh_sector_dual_destroy(fnlh_sector_dual* h);
    entries written.  ShapeError on an endpoint outside [0, rows). */
 int fnlh_make_pattern(int rows, long long n_edges, const int* ea, const int* eb, int* row_ptr, int* col_idx,
                       int* diag_idx, long long* nnzb);
+/* Reverse Cuthill-McKee ordering of the graph of a CSR pattern (row_ptr [n+1], col_idx with
+   the diagonal in every row or in none), on the device: perm[position] = node.  Each
+   component is seeded by the first unvisited node of `starts` (NULL: nodes by ascending
+   degree, stable); with starts = np.argsort(degree) it equals
+   scipy.sparse.csgraph.reverse_cuthill_mckee(graph, symmetric_mode=True) (the ordering step
+   of the configurations' mesh generator).  Degrees must be <= 255. */
+int fnlh_rcm(int n, const int* row_ptr, const int* col_idx, const int* starts, int* perm);
 /* Mesh::build_adjacency (mesh.cpp:44-59) and the derived arrays of mesh.py::from_faces on
    the device: per face (fa, fb = -1 on boundary faces, fn [nf][3]) the area, unit normal
    and viscous weight area / |x_fb - x_fa| (0 on boundary faces or without coords); per

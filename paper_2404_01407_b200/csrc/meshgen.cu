@@ -371,6 +371,62 @@ struct SectorDual {
     DeviceBuffer<double> en, vol;
 };
 
+
+// ---- Reverse Cuthill-McKee (scipy.sparse.csgraph.reverse_cuthill_mckee, the host
+// ordering step of mesh.py::structured_sector) as a level-synchronous BFS.  Sequential
+// Cuthill-McKee appends, for each dequeued node u in order, its unvisited neighbours by
+// ascending degree (stable in CSR order); a node is taken by the first u that sees it.  So
+// level L+1 is exactly its nodes sorted by (position of the claiming parent, degree, CSR
+// slot in that parent), the claim being the minimum (parent position, slot): one
+// atomicMin per (frontier node, neighbour), one radix sort per level.
+__global__ void k_rcm_claim(int nf, const int* __restrict__ frontier, const long long* __restrict__ pos,
+                            const int* __restrict__ row_ptr, const int* __restrict__ col_idx,
+                            const int* __restrict__ visited, unsigned long long* __restrict__ claim,
+                            int* __restrict__ mark, int* __restrict__ next, int* __restrict__ nnext) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nf) return;
+    const int u = frontier[t];
+    const unsigned long long pu = (unsigned long long)pos[u];
+    for (int e = row_ptr[u], slot = 0; e < row_ptr[u + 1]; ++e, ++slot) {
+        const int v = col_idx[e];
+        if (visited[v]) continue;
+        atomicMin(claim + v, (pu << 8) | (unsigned long long)slot);
+        if (atomicExch(mark + v, 1) == 0) next[atomicAdd(nnext, 1)] = v;
+    }
+}
+__global__ void k_rcm_keys(int nn, const int* __restrict__ next, const unsigned long long* __restrict__ claim,
+                           const int* __restrict__ row_ptr, unsigned long long* __restrict__ keys) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nn) return;
+    const int v = next[t];
+    const unsigned long long c = claim[v];
+    const unsigned long long deg = (unsigned long long)(row_ptr[v + 1] - row_ptr[v]);
+    keys[t] = ((c >> 8) << 16) | (deg << 8) | (c & 255ull);
+}
+__global__ void k_rcm_assign(int nn, const int* __restrict__ sorted, long long base, long long* __restrict__ pos,
+                             int* __restrict__ visited, int* __restrict__ order) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nn) return;
+    const int v = sorted[t];
+    pos[v] = base + t;
+    visited[v] = 1;
+    order[base + t] = v;
+}
+__global__ void k_rcm_degree(int n, const int* __restrict__ row_ptr, unsigned int* __restrict__ deg,
+                             int* __restrict__ idx) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    deg[i] = (unsigned int)(row_ptr[i + 1] - row_ptr[i]);
+    idx[i] = i;
+}
+__global__ void k_rcm_start(int v, long long base, long long* __restrict__ pos, int* __restrict__ visited,
+                            int* __restrict__ order, int* __restrict__ frontier) {
+    pos[v] = base;
+    visited[v] = 1;
+    order[base] = v;
+    frontier[0] = v;
+}
+
 }  // namespace fnlh
 
 using namespace fnlh;
@@ -504,6 +560,76 @@ int fnlh_make_pattern(int rows, long long n_edges, const int* ea, const int* eb,
         download(col_idx, ci.ptr, (std::size_t)nnz);
         download(diag_idx, di.ptr, (std::size_t)rows);
         *nnzb = nnz;
+    });
+}
+
+int fnlh_rcm(int n, const int* row_ptr, const int* col_idx, const int* starts, int* perm) {
+    return guarded([&] {
+        if (n < 1) throw ShapeError("rcm: n must be >= 1");
+        for (int i = 0; i < n; ++i)
+            if (row_ptr[i + 1] - row_ptr[i] > 255) throw ShapeError("rcm: degree above 255");
+        cudaStream_t st = 0;
+        const long long nnz = row_ptr[n];
+        DeviceBuffer<int> rp, ci, visited(n), mark(n), order(n), frontier(n), next(n), sorted(n), nnext(1), idx(n),
+            idx_s(n);
+        DeviceBuffer<long long> pos(n);
+        DeviceBuffer<unsigned long long> claim(n), keys(n), keys_s(n);
+        DeviceBuffer<unsigned int> deg(n), deg_s(n);
+        rp.upload(row_ptr, (std::size_t)n + 1);
+        ci.upload(col_idx, (std::size_t)nnz);
+        FNLH_CUDA(cudaMemset(visited.ptr, 0, n * sizeof(int)));
+        FNLH_CUDA(cudaMemset(mark.ptr, 0, n * sizeof(int)));
+        FNLH_CUDA(cudaMemset(claim.ptr, 0xff, n * sizeof(unsigned long long)));
+        // component starts: nodes by ascending degree, stable (scipy's argsort of degrees)
+        note_launch();
+        k_rcm_degree<<<nb(n), kT, 0, st>>>(n, rp.ptr, deg.ptr, idx.ptr);
+        std::size_t tb = 0, tb2 = 0;
+        FNLH_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, deg.ptr, deg_s.ptr, idx.ptr, idx_s.ptr, n, 0, 9, st));
+        FNLH_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, keys.ptr, keys_s.ptr, next.ptr, sorted.ptr, n, 0, 64, st));
+        DeviceBuffer<unsigned char> tmp(std::max(tb, tb2));
+        FNLH_CUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, tb, deg.ptr, deg_s.ptr, idx.ptr, idx_s.ptr, n, 0, 9, st));
+        std::vector<int> by_deg(n), vis(n);
+        if (starts) {  // the caller's seed order (scipy: np.argsort(degree), an unstable sort)
+            std::copy(starts, starts + n, by_deg.begin());
+        } else {
+            FNLH_CUDA(cudaMemcpyAsync(by_deg.data(), idx_s.ptr, n * sizeof(int), cudaMemcpyDeviceToHost, st));
+            FNLH_CUDA(cudaStreamSynchronize(st));
+        }
+        const int kbits = 64;
+        long long base = 0;
+        std::size_t cursor = 0;
+        while (base < n) {
+            FNLH_CUDA(cudaMemcpyAsync(vis.data(), visited.ptr, n * sizeof(int), cudaMemcpyDeviceToHost, st));
+            FNLH_CUDA(cudaStreamSynchronize(st));
+            while (vis[by_deg[cursor]]) ++cursor;
+            note_launch();
+            k_rcm_start<<<1, 1, 0, st>>>(by_deg[cursor], base, pos.ptr, visited.ptr, order.ptr, frontier.ptr);
+            ++base;
+            int nf = 1;
+            while (nf > 0) {
+                FNLH_CUDA(cudaMemsetAsync(nnext.ptr, 0, sizeof(int), st));
+                note_launch();
+                k_rcm_claim<<<nb(nf), kT, 0, st>>>(nf, frontier.ptr, pos.ptr, rp.ptr, ci.ptr, visited.ptr, claim.ptr,
+                                                   mark.ptr, next.ptr, nnext.ptr);
+                int nn = 0;
+                FNLH_CUDA(cudaMemcpyAsync(&nn, nnext.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
+                FNLH_CUDA(cudaStreamSynchronize(st));
+                if (nn == 0) break;
+                note_launch();
+                k_rcm_keys<<<nb(nn), kT, 0, st>>>(nn, next.ptr, claim.ptr, rp.ptr, keys.ptr);
+                std::size_t tbl = tb2;
+                FNLH_CUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, tbl, keys.ptr, keys_s.ptr, next.ptr, sorted.ptr, nn,
+                                                          0, kbits, st));
+                note_launch();
+                k_rcm_assign<<<nb(nn), kT, 0, st>>>(nn, sorted.ptr, base, pos.ptr, visited.ptr, order.ptr);
+                base += nn;
+                std::swap(frontier.ptr, sorted.ptr);
+                nf = nn;
+            }
+        }
+        std::vector<int> cm(n);
+        download(cm.data(), order.ptr, (std::size_t)n);
+        for (int i = 0; i < n; ++i) perm[i] = cm[n - 1 - i];  // reversed: perm[position] = node
     });
 }
 

@@ -283,6 +283,29 @@ def _device_available():
         return False
 
 
+def rcm_order(n, ea, eb, device=None):
+    """Reverse Cuthill-McKee order of the graph with edges (ea, eb): rcm[position] = node.
+    On the device (fnlh_rcm: level-synchronous BFS over the device-built pattern, equal to
+    scipy's sequential algorithm) when one is present, else scipy.sparse.csgraph."""
+    if device is None:
+        device = _device_available()
+    if device:
+        from ._lib import check, lib, ptr
+        pat = make_pattern_device(n, ea, eb)
+        # component seeds exactly as scipy picks them: np.argsort of the int32 degrees
+        # (numpy's default, unstable sort; the diagonal's +1 does not change the order)
+        starts = np.ascontiguousarray(np.argsort(np.diff(pat["row_ptr"]).astype(np.int32)), np.int32)
+        out = np.empty(n, np.int32)
+        check(lib().fnlh_rcm(n, ptr(pat["row_ptr"]), ptr(pat["col_idx"]), ptr(starts), ptr(out)))
+        return out.astype(np.int64)
+    from scipy.sparse import coo_matrix
+    from scipy.sparse.csgraph import reverse_cuthill_mckee
+    ea = np.asarray(ea, np.int64)
+    eb = np.asarray(eb, np.int64)
+    G = coo_matrix((np.ones(2 * len(ea)), (np.concatenate([ea, eb]), np.concatenate([eb, ea]))), shape=(n, n)).tocsr()
+    return np.asarray(reverse_cuthill_mckee(G, symmetric_mode=True), np.int64)
+
+
 def _sector_dual_device(Xu, ci, cj, ck, periodic_j, tets):
     """The same geometry from the sm_100a kernels (csrc/meshgen.cu, fnlh_sector_dual_*)."""
     import ctypes as C
@@ -385,11 +408,8 @@ def structured_sector(ci, cj, ck, *, geometry="annular", length=2.0, pitch_deg=1
     perm0 = rng.permutation(n) if permute else np.arange(n)        # perm0[new] = old
     inv0 = np.empty(n, np.int64)
     inv0[perm0] = np.arange(n)
-    from scipy.sparse import coo_matrix
-    from scipy.sparse.csgraph import reverse_cuthill_mckee
     ra, rb = inv0[ea], inv0[eb]
-    G = coo_matrix((np.ones(2 * len(ra)), (np.concatenate([ra, rb]), np.concatenate([rb, ra]))), shape=(n, n)).tocsr()
-    rcm = np.asarray(reverse_cuthill_mckee(G, symmetric_mode=True), np.int64)   # rcm[pos] = permuted id
+    rcm = rcm_order(n, ra, rb, device)                               # rcm[pos] = permuted id
     rank = np.empty(n, np.int64)
     rank[perm0[rcm]] = np.arange(n)                                  # rank[old] = RCM position
     order = np.lexsort((rank, col))                                  # order[new] = old

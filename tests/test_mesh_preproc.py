@@ -74,3 +74,47 @@ def test_device_sector_c4_size():
     assert m.n == 257 * 129 * 129
     assert (m.vol > 0).all() and (m.farea > 0).all()
     print(f"C4 sector mesh on the device: {dt:.1f} s")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["hex", "tet", "periodic", "components"])
+def test_device_rcm_equals_scipy(kind):
+    """fnlh_rcm (level-synchronous Cuthill-McKee on the device) reproduces
+    scipy.sparse.csgraph.reverse_cuthill_mckee exactly: hex / jittered-tet / periodic sector
+    graphs in a seeded random numbering, and a graph of several components (starts by
+    ascending degree, stable)."""
+    from paper_2404_01407_b200.mesh import rcm_order, structured_sector
+    rng = np.random.default_rng(17)
+    if kind == "components":
+        n = 300
+        ea = rng.integers(0, n, 500)
+        eb = rng.integers(0, n, 500)
+        keep = (ea != eb) & ((ea < 100) == (eb < 100)) & ((ea < 200) == (eb < 200))
+        ea, eb = ea[keep], eb[keep]
+    else:
+        kw = dict(tets=True, jitter=0.05) if kind == "tet" else dict(periodic_j=True) if kind == "periodic" else {}
+        m = structured_sector(12, 8, 6, seed=2, **kw)
+        inter = m.fbc < 0
+        p = rng.permutation(m.n)
+        n, ea, eb = m.n, p[m.fa[inter]], p[m.fb[inter]]
+    assert np.array_equal(rcm_order(n, ea, eb, device=True), rcm_order(n, ea, eb, device=False))
+
+
+@pytest.mark.gpu
+def test_device_rcm_c4_size():
+    """The full C4 graph (4.28 M nodes, 12.7 M edges): equal to scipy."""
+    import time
+    from paper_2404_01407_b200.mesh import rcm_order, _sector_dual_device, structured_sector  # noqa: F401
+    ci, cj, ck = 256, 128, 128
+    ni, nj, nk = ci + 1, cj + 1, ck + 1
+    idx = np.arange(ni * nj * nk).reshape(ni, nj, nk)
+    ea = np.concatenate([idx[:-1].ravel(), idx[:, :-1].ravel(), idx[:, :, :-1].ravel()])
+    eb = np.concatenate([idx[1:].ravel(), idx[:, 1:].ravel(), idx[:, :, 1:].ravel()])
+    p = np.random.default_rng(3).permutation(idx.size)
+    t0 = time.time()
+    d = rcm_order(idx.size, p[ea], p[eb], device=True)
+    t1 = time.time()
+    h = rcm_order(idx.size, p[ea], p[eb], device=False)
+    t2 = time.time()
+    print(f"rcm at C4 size: device {t1 - t0:.2f} s, scipy {t2 - t1:.2f} s")
+    assert np.array_equal(d, h)
