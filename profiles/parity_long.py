@@ -1,0 +1,45 @@
+"""Full-size, full-length parity of the outer iteration against the CPU restatement (whose
+linear algebra is bitwise the reference's): BASELINE C1 (20 pseudo-steps) and C2 (50), the
+device path as bench.py runs it (C2: 3 harmonic lanes), the restatement with the
+reference's harmonic worker threads.  Prints per-step relative differences of the mean and
+harmonic residual norms, the linear-iteration counts, and the final state difference.
+Usage: python profiles/parity_long.py [c1 c2]"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from oracle.oracle import Oracle  # noqa: E402
+from paper_2404_01407_b200.cases import make_case  # noqa: E402
+from paper_2404_01407_b200.solver import FnlhSolver  # noqa: E402
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+for name in (sys.argv[1:] or ["c1", "c2"]):
+    c = make_case(name, workers=3)
+    g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
+    o = Oracle(pow_mode="cr", workers=min(3, os.cpu_count() or 1)).solver(c.mesh, c.mesh.pattern(), c.scheme,
+                                                                         c.omegas, c.forcing, c.mean0)
+    worst_m = worst_z = 0.0
+    t0 = time.time()
+    for it in range(c.pseudo_steps):
+        eg, eo = g.outer_iteration(), o.outer_iteration()
+        dm = abs(eg["resid_mean"] / eo["resid_mean"] - 1)
+        dz = abs(eg["rz"] / eo["rz"] - 1) if eo["rz"] else 0.0
+        worst_m, worst_z = max(worst_m, dm), max(worst_z, dz)
+        print(f"{name} step {it + 1:3d} resid_mean {eg['resid_mean']:.6e} rel {dm:.2e}  R_z {eg['rz']:.6e} rel {dz:.2e}",
+              flush=True)
+    mg, ag = g.state()
+    mo, ao = o.state()
+    same_iters = [r[0] for r in g.reports()] == [r[0] for r in o.reports()]
+    print(json.dumps(dict(case=name, nodes=c.mesh.n, steps=c.pseudo_steps, max_rel_resid_mean=worst_m,
+                          max_rel_rz=worst_z, final_mean_rel=rel(mg, mo), final_amps_rel=rel(ag, ao),
+                          identical_linear_iteration_counts=same_iters, wall_s=round(time.time() - t0, 1))),
+          flush=True)
