@@ -3,7 +3,8 @@ linear algebra is bitwise the reference's): BASELINE C1 (20 pseudo-steps) and C2
 device path as bench.py runs it (C2: 3 harmonic lanes), the restatement with the
 reference's harmonic worker threads.  Prints per-step relative differences of the mean and
 harmonic residual norms, the linear-iteration counts, and the final state difference.
-Usage: python profiles/parity_long.py [c1 c2]"""
+Usage: python profiles/parity_long.py [c1 c2 c3:2 ...]   (name[:steps], default the
+BASELINE step count)"""
 import json
 import os
 import sys
@@ -22,10 +23,13 @@ def rel(a, b):
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
 
 
-for name in (sys.argv[1:] or ["c1", "c2"]):
+for arg in (sys.argv[1:] or ["c1", "c2"]):
+    name, _, k = arg.partition(":")
     c = make_case(name, workers=3)
+    c.pseudo_steps = int(k) if k else c.pseudo_steps
+    nw = min(len(c.omegas), os.cpu_count() or 1)
     g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
-    o = Oracle(pow_mode="cr", workers=min(3, os.cpu_count() or 1)).solver(c.mesh, c.mesh.pattern(), c.scheme,
+    o = Oracle(pow_mode="cr", workers=nw).solver(c.mesh, c.mesh.pattern(), c.scheme,
                                                                          c.omegas, c.forcing, c.mean0)
     worst_m = worst_z = 0.0
     t0 = time.time()
