@@ -208,11 +208,12 @@ def main():
     else:
         dist = None
     os.environ.setdefault("CUDA_VISIBLE_DEVICES_LOCAL", str(local))
-    from paper_2404_01407_b200._lib import lib, require_gpu
+    from paper_2404_01407_b200._lib import check, lib, require_gpu
     from paper_2404_01407_b200.cases import make_case
     from paper_2404_01407_b200.solver import FnlhSolver
 
     require_gpu()
+    check(lib().fnlh_set_device(local))  # this rank's GPU for the library's own runtime calls
     c = make_case(args.config, scale=args.scale)
     if args.workers != 1:
         c = make_case(args.config, scale=args.scale, workers=args.workers or min(len(c.omegas), 8))

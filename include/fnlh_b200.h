@@ -48,6 +48,8 @@ const char* fnlh_last_error(void);
 int fnlh_last_error_node(void);
 int fnlh_last_error_stage(void);
 int fnlh_device_count(void);
+/* make `device` current for the calling host thread (one process per GPU: the local rank) */
+int fnlh_set_device(int device);
 /* number of CUDA kernels this library has launched (monotonic) */
 long long fnlh_launch_count(void);
 

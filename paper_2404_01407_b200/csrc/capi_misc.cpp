@@ -24,6 +24,10 @@ int fnlh_last_error_stage(void) { return fnlh::last_error().stage; }
 
 long long fnlh_launch_count(void) { return fnlh::launch_count().load(); }
 
+int fnlh_set_device(int device) {
+    return fnlh::guarded([&] { FNLH_CUDA(cudaSetDevice(device)); });
+}
+
 int fnlh_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
