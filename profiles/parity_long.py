@@ -3,8 +3,8 @@ linear algebra is bitwise the reference's): BASELINE C1 (20 pseudo-steps) and C2
 device path as bench.py runs it (C2: 3 harmonic lanes), the restatement with the
 reference's harmonic worker threads.  Prints per-step relative differences of the mean and
 harmonic residual norms, the linear-iteration counts, and the final state difference.
-Usage: python profiles/parity_long.py [c1 c2 c3:2 ...]   (name[:steps], default the
-BASELINE step count)"""
+Usage: python profiles/parity_long.py [c1 c2 c3:2 c4:1:3 ...]   (name[:steps[:oracle
+workers]], default the BASELINE step count and one worker per harmonic)"""
 import json
 import os
 import sys
@@ -24,10 +24,11 @@ def rel(a, b):
 
 
 for arg in (sys.argv[1:] or ["c1", "c2"]):
-    name, _, k = arg.partition(":")
+    name, _, rest = arg.partition(":")
+    k, _, w = rest.partition(":")  # name[:steps[:oracle workers]] (C4: each worker holds 24 GB)
     c = make_case(name, workers=3)
     c.pseudo_steps = int(k) if k else c.pseudo_steps
-    nw = min(len(c.omegas), os.cpu_count() or 1)
+    nw = int(w) if w else min(len(c.omegas), os.cpu_count() or 1)
     g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
     o = Oracle(pow_mode="cr", workers=nw).solver(c.mesh, c.mesh.pattern(), c.scheme,
                                                                          c.omegas, c.forcing, c.mean0)
