@@ -50,6 +50,15 @@ int fnlh_last_error_stage(void);
 int fnlh_device_count(void);
 /* make `device` current for the calling host thread (one process per GPU: the local rank) */
 int fnlh_set_device(int device);
+/* Boundary-state pow (disc_euler.cpp:179-180,187).  0: glibc's pow restated bit for bit
+   (its tables located in the libm this process loaded and the restatement checked against
+   ::pow on a fixed sample at first use, csrc/libm_pow.cuh) -- the device then rounds every
+   boundary state as the reference does; 1: correctly rounded (tables absent, the check
+   failed, or FNLH_POW=cr in the environment).  fnlh_pow evaluates the selected routine on
+   the host (for tests). */
+int fnlh_pow_mode(void);
+const char* fnlh_pow_mode_info(void);
+double fnlh_pow(double x, double y);
 /* number of CUDA kernels this library has launched (monotonic) */
 long long fnlh_launch_count(void);
 

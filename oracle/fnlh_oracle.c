@@ -333,7 +333,7 @@ static int boundary_face_flux(const or_mesh* m, int f, const double* W, const do
 
 /* interior_face_flux (disc_euler.cpp:121-159); nu/lap are the node pre-pass (order 2) */
 static void interior_face_flux(const or_mesh* m, int f, const double* W, int order, const double* nu,
-                               const double* lap, double* out) {
+                               const double* lap, int line, double* out) {
     const int b = m->b;
     const double g = m->gamma;
     const int a = m->fa[f], c = m->fb[f];
@@ -362,12 +362,44 @@ static void interior_face_flux(const or_mesh* m, int f, const double* W, int ord
     const double s2 = kKappa2 * (nua > nub ? nua : nub);
     double s4 = kKappa4 - s2;
     if (!(s4 > 0.0)) s4 = 0.0; /* std::max(0.0, kKappa4 - s2) */
+    if (line) {
+        /* line mesh: the reference's own stencil (a-1, a, b, b+1), disc_euler.cpp:145-157;
+           lap holds Q per node here (jst_prepass), the 4th difference in its operation order */
+        const int im1 = a - 1, ip2 = c + 1;
+        if (im1 < 0 || ip2 >= m->n) s4 = 0.0; /* stencil truncated at boundaries */
+        for (int k = 0; k < b; ++k) {
+            double d = s2 * lam * (qb[k] - qa[k]);
+            if (s4 > 0.0)
+                d -= s4 * lam * (lap[(size_t)ip2 * b + k] - 3.0 * qb[k] + 3.0 * qa[k] - lap[(size_t)im1 * b + k]);
+            out[k] -= d;
+        }
+        return;
+    }
     if (m->bflag[a] || m->bflag[c]) s4 = 0.0; /* stencil truncated at boundaries */
     for (int k = 0; k < b; ++k) {
         double d = s2 * lam * (qb[k] - qa[k]);
         if (s4 > 0.0) d -= s4 * lam * (lap[(size_t)c * b + k] - lap[(size_t)a * b + k]);
         out[k] -= d;
     }
+}
+
+/* A line mesh: the interior faces are exactly (i, i+1), i = 0 .. n-2 (the reference's
+   build_mesh_1d, mesh.cpp:85-127, in any face order).  There every interior node has the
+   unique neighbours i-1 and i+1, and the order-2 terms use the reference's 1D stencil
+   verbatim (disc_euler.cpp:113-119,145-157) instead of its edge-based form. */
+int or_mesh_is_line(const or_mesh* m) {
+    if (m->n < 2) return 0;
+    int cnt = 0;
+    unsigned char* seen = (unsigned char*)calloc((size_t)m->n, 1);
+    int ok = 1;
+    for (int f = 0; f < m->nf && ok; ++f) {
+        if (m->fbc[f] >= 0) continue;
+        const int a = m->fa[f];
+        if (m->fb[f] != a + 1 || a < 0 || a + 1 >= m->n || seen[a]) ok = 0;
+        else { seen[a] = 1; ++cnt; }
+    }
+    free(seen);
+    return ok && cnt == m->n - 1;
 }
 
 /* viscous flux of the SA-like model (b = 6 only; no reference counterpart) */
@@ -399,7 +431,7 @@ static void node_source(const or_mesh* m, int i, const double* W, double* out) {
 static int face_flux1(const or_mesh* m, int f, const double* W, const double* wref, int mode,
                       const double* forcing, int nforcing, double* out) {
     if (m->fbc[f] >= 0) return boundary_face_flux(m, f, W, wref, mode, forcing, nforcing, out);
-    interior_face_flux(m, f, W, 1, NULL, NULL, out);
+    interior_face_flux(m, f, W, 1, NULL, NULL, 0, out);
     if (m->b == 6) {
         double vf[6];
         viscous_face_flux(m, f, W, vf);
@@ -410,9 +442,20 @@ static int face_flux1(const or_mesh* m, int f, const double* W, const double* wr
 
 /* order-2 node pre-pass: pressure switch (disc_euler.cpp:113-119, ghost per boundary face)
    and undivided Laplacian of Q (the 1D (a-1, b+1) stencil of :145-157 in edge form) */
-static void jst_prepass(const or_mesh* m, const double* W, double* nu, double* lap) {
+static void jst_prepass(const or_mesh* m, const double* W, double* nu, double* lap, int line) {
     const int b = m->b;
     double qi[6], qj[6];
+    if (line) { /* pressure_switch (disc_euler.cpp:113-119) with clamped neighbours; lap = Q */
+        const int n = m->n;
+        for (int i = 0; i < n; ++i) {
+            const int im = i - 1 < 0 ? 0 : i - 1;
+            const int ip = i + 1 > n - 1 ? n - 1 : i + 1;
+            const double pm = W[(size_t)im * b + 4], pc = W[(size_t)i * b + 4], pp = W[(size_t)ip * b + 4];
+            nu[i] = fabs(pp - 2.0 * pc + pm) / (pp + 2.0 * pc + pm);
+            e_prim_to_cons(b, W + (size_t)i * b, m->gamma, lap + (size_t)i * b);
+        }
+        return;
+    }
     for (int i = 0; i < m->n; ++i) {
         const double pi = W[(size_t)i * b + 4];
         double num = 0.0, den = 0.0;
@@ -444,10 +487,12 @@ int or_residual(const or_mesh* m, const double* W, const double* wref, int order
     if (need_vis) memset(vis, 0, sizeof(double) * (size_t)n * b);
     double* nu = NULL;
     double* lap = NULL;
+    int line = 0;
     if (order == 2) {
         nu = (double*)malloc(sizeof(double) * n);
         lap = (double*)malloc(sizeof(double) * (size_t)n * b);
-        jst_prepass(m, W, nu, lap);
+        line = or_mesh_is_line(m);
+        jst_prepass(m, W, nu, lap, line);
     }
     double flux[6];
     int st = OR_OK;
@@ -460,7 +505,7 @@ int or_residual(const or_mesh* m, const double* W, const double* wref, int order
             continue;
         }
         const int c = m->fb[f];
-        interior_face_flux(m, f, W, order, nu, lap, flux);
+        interior_face_flux(m, f, W, order, nu, lap, line, flux);
         for (int k = 0; k < b; ++k) {
             inv[(size_t)a * b + k] += flux[k];
             inv[(size_t)c * b + k] -= flux[k];

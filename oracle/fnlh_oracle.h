@@ -129,6 +129,9 @@ typedef struct {
 } or_mesh;
 
 int or_prim_to_cons(int b, int n, double gamma, const double* W, double* Q);
+/* 1 when the interior faces are exactly (i, i+1), i = 0..n-2: the order-2 terms then use the
+   reference's 1D stencil verbatim (disc_euler.cpp:113-119,145-157) */
+int or_mesh_is_line(const or_mesh* m);
 int or_cons_to_prim(int b, int n, double gamma, const double* Q, double* W);
 int or_transform_jacobian(int b, int n, double gamma, const double* W, double* M);
 

@@ -45,6 +45,9 @@ def lib():
         L = C.CDLL(LIB_PATH)
         L.fnlh_last_error.restype = C.c_char_p
         L.fnlh_launch_count.restype = C.c_longlong
+        L.fnlh_pow_mode_info.restype = C.c_char_p
+        L.fnlh_pow.restype = C.c_double
+        L.fnlh_pow.argtypes = [C.c_double, C.c_double]
         _LIB = L
     return _LIB
 
@@ -53,6 +56,12 @@ def check(st):
     if st:
         L = lib()
         raise FnlhError(st, L.fnlh_last_error().decode(), L.fnlh_last_error_node(), L.fnlh_last_error_stage())
+
+
+def pow_mode():
+    """The device's boundary-state pow: "glibc" (the reference's libm restated bit for bit,
+    csrc/libm_pow.cuh) or "cr" (correctly rounded; FNLH_POW=cr or the libm check failed)."""
+    return "glibc" if lib().fnlh_pow_mode() == 0 else "cr"
 
 
 def require_gpu():

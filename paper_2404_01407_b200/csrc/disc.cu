@@ -38,6 +38,16 @@ __global__ void k_jst_prepass(MeshDev m, const double* __restrict__ W, double* _
     if (i >= m.n) return;
     if (skip && *skip == 0.0) return;
     const double* wi = W + (size_t)i * B;
+    if (m.line) {  // pressure_switch (disc_euler.cpp:113-119), clamped neighbours; lap = Q
+        const int im = i > 0 ? i - 1 : 0, ip = i + 1 < m.n ? i + 1 : m.n - 1;
+        const double pm = W[(size_t)im * B + 4], pc = wi[4], pp = W[(size_t)ip * B + 4];
+        nu[i] = fabs(pp - 2.0 * pc + pm) / (pp + 2.0 * pc + pm);
+        double q[B];
+        prim_to_cons<B>(wi, m.gamma, q);
+#pragma unroll
+        for (int k = 0; k < B; ++k) lap[(size_t)i * B + k] = q[k];
+        return;
+    }
     const double pi = wi[4];
     double num = 0.0, den = 0.0;
     double L[B], qi[B], qj[B];
@@ -88,7 +98,11 @@ __global__ void k_face_flux(MeshDev m, const double* __restrict__ W, const doubl
         double wa[B], wc[B];
         load_vec<B>(W + (size_t)a * B, wa);
         load_vec<B>(W + (size_t)c * B, wc);
-        if (order == 2)
+        if (order == 2 && m.line) {  // the reference's stencil (a-1, a, b, b+1), truncated at the ends
+            const bool trunc = a - 1 < 0 || c + 1 >= m.n;
+            interior_face_flux<B>(m, f, wa, wc, 2, nu[a], nu[c], trunc, trunc ? nullptr : lap + (size_t)(a - 1) * B,
+                                  trunc ? nullptr : lap + (size_t)(c + 1) * B, out, true);
+        } else if (order == 2)
             interior_face_flux<B>(m, f, wa, wc, 2, nu[a], nu[c], m.bflag[a] || m.bflag[c], lap + (size_t)a * B,
                                   lap + (size_t)c * B, out);
         else
@@ -897,7 +911,24 @@ DeviceDisc::DeviceDisc(const MeshArrays& m, const DevicePattern* pattern) : pat_
         if (nf_int_ >= 0) fdpart_.alloc((std::size_t)n * m.b * m.b);
     }
     bflag_.upload(m.bflag, n);
-    if (nf_int_ >= 0 && !packed_disabled()) {  // interior face records of the packed residual
+    int line = 0;  // the reference's line mesh: interior faces exactly (i, i+1), i = 0 .. n-2
+    {
+        std::vector<char> seen(n, 0);
+        int cnt = 0;
+        bool ok = n >= 2;
+        for (int f = 0; f < nfc && ok; ++f) {
+            if (m.fbc[f] >= 0) continue;
+            const int a = m.fa[f];
+            if (a < 0 || a + 1 >= n || m.fb[f] != a + 1 || seen[a]) ok = false;
+            else {
+                seen[a] = 1;
+                ++cnt;
+            }
+        }
+        line = ok && cnt == n - 1;
+    }
+    if (const double* T = libm_pow_tables()) powtab_.upload(T, kPowTabDoubles);
+    if (nf_int_ >= 0 && !packed_disabled() && !line) {  // interior face records of the packed residual
         std::vector<double> g((std::size_t)nf_int_ * 8);
         for (int f = 0; f < nf_int_; ++f) {
             double* r = g.data() + (std::size_t)f * 8;
@@ -938,7 +969,7 @@ DeviceDisc::DeviceDisc(const MeshArrays& m, const DevicePattern* pattern) : pat_
     e_ba_.upload(eba.data(), nfc);
     view_ = MeshDev{n, nfc, m.b, fa_.ptr, fb_.ptr, fbc_.ptr, ford_.ptr, fn_.ptr, farea_.ptr, fnh_.ptr, fvis_.ptr,
                     vol_.ptr, closure_.ptr, mu_.ptr, nf_ptr_.ptr, nf_idx_.ptr, bflag_.ptr, m.gamma, m.gas_constant,
-                    m.p0, m.T0, m.p_out, m.nt_in, m.forcing_scale, nf_code_.ptr};
+                    m.p0, m.T0, m.p_out, m.nt_in, m.forcing_scale, nf_code_.ptr, powtab_.ptr, line};
     qscale_.alloc(8);
     ensure_contexts(1);
     err_.alloc(1);

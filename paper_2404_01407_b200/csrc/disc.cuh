@@ -93,6 +93,7 @@ private:
     DeviceBuffer<int> fa_, fb_, fbc_, ford_, nf_ptr_, nf_idx_, nf_code_, bflag_, e_ab_, e_ba_;
     DeviceBuffer<double> fn_, farea_, fnh_, fvis_, vol_, closure_, mu_;
     DeviceBuffer<double> fgeo_;    // interior face records of the packed order-2 residual
+    DeviceBuffer<double> powtab_;  // glibc's pow tables (libm_pow.cuh), empty: correctly rounded pow
     DeviceBuffer<double> qscale_;
     DeviceBuffer<unsigned long long> err_;
     unsigned long long* cur_err_ = nullptr;

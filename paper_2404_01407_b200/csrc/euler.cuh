@@ -5,7 +5,7 @@
 #pragma once
 
 #include "common.cuh"
-#include "cr_pow.cuh"
+#include "libm_pow.cuh"
 
 namespace fnlh {
 
@@ -31,6 +31,11 @@ struct MeshDev {
     // the other endpoint j as j (this node is fa: the face flux adds) or -(j + 1) (this node
     // is fb: it subtracts) -- the gathers need no random reads of fa / fb / fbc
     const int* __restrict__ nf_code;
+    // glibc's pow tables (libm_pow.cuh) or nullptr: the correctly rounded pow
+    const double* __restrict__ powtab;
+    // 1: the interior faces are exactly (i, i+1) -- the reference's line mesh, whose order-2
+    // terms use its 1D stencil verbatim (disc_euler.cpp:113-119,145-157)
+    int line;
 };
 
 constexpr int kBoundaryFace = -2147483647 - 1;
@@ -116,7 +121,7 @@ __device__ __forceinline__ int steady_inlet(const MeshDev& m, const double* wint
     if (!(cb > 0.0)) return 2;
     if (fabs(ub) >= cb) return 4;
     const double tb = cb * cb / (g * R);
-    const double pb = m.p0 * cr_pow(tb / m.T0, g / (g - 1.0));
+    const double pb = m.p0 * bc_pow(m.powtab, tb / m.T0, g / (g - 1.0));
     s.w[0] = pb / (R * tb);
     s.w[1] = ub * -nh[0];
     s.w[2] = ub * -nh[1];
@@ -132,7 +137,7 @@ template <int B>
 __device__ __forceinline__ int steady_outlet(const MeshDev& m, const double* wint, const double* nh, BState& s) {
     const double g = m.gamma;
     const double pb = m.p_out;
-    const double rhob = wint[0] * cr_pow(pb / wint[4], 1.0 / g);
+    const double rhob = wint[0] * bc_pow(m.powtab, pb / wint[4], 1.0 / g);
     const double cb = sqrt(g * pb / rhob);
     const double c_int = sqrt(g * wint[4] / wint[0]);
     const double un = wint[1] * nh[0] + wint[2] * nh[1] + wint[3] * nh[2];
@@ -222,7 +227,7 @@ template <int B>
 __device__ __forceinline__ void interior_flux_core(double g, const double* n, const double* nh, double area,
                                                    const double* wa, const double* wc, int order, double nua,
                                                    double nub, bool trunc, const double* lapa, const double* lapc,
-                                                   double* out) {
+                                                   double* out, bool line = false) {
     double fa[6], fb[6], qa[6], qb[6];
     phys_flux<B>(wa, g, n, fa);
     phys_flux<B>(wc, g, n, fb);
@@ -246,6 +251,15 @@ __device__ __forceinline__ void interior_flux_core(double g, const double* n, co
     double s4 = kKappa4 - s2;
     if (!(s4 > 0.0)) s4 = 0.0;
     if (trunc) s4 = 0.0;
+    if (line) {  // lapa = Q(a-1), lapc = Q(b+1): the 1D 4th difference (disc_euler.cpp:150-155)
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            double d = s2 * lam * (qb[k] - qa[k]);
+            if (s4 > 0.0) d -= s4 * lam * (lapc[k] - 3.0 * qb[k] + 3.0 * qa[k] - lapa[k]);
+            out[k] -= d;
+        }
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < B; ++k) {
         double d = s2 * lam * (qb[k] - qa[k]);
@@ -257,9 +271,10 @@ __device__ __forceinline__ void interior_flux_core(double g, const double* n, co
 template <int B>
 __device__ __forceinline__ void interior_face_flux(const MeshDev& m, int f, const double* wa, const double* wc,
                                                    int order, double nua, double nub, bool trunc,
-                                                   const double* lapa, const double* lapc, double* out) {
+                                                   const double* lapa, const double* lapc, double* out,
+                                                   bool line = false) {
     interior_flux_core<B>(m.gamma, m.fn + 3 * (size_t)f, m.fnh + 3 * (size_t)f, m.farea[f], wa, wc, order, nua, nub,
-                          trunc, lapa, lapc, out);
+                          trunc, lapa, lapc, out, line);
 }
 
 // SA-like viscous flux (b = 6 only)

@@ -15,6 +15,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from oracle.oracle import Oracle  # noqa: E402
+from paper_2404_01407_b200._lib import pow_mode  # noqa: E402
 from paper_2404_01407_b200.cases import make_case  # noqa: E402
 from paper_2404_01407_b200.solver import FnlhSolver  # noqa: E402
 
@@ -30,7 +31,7 @@ for arg in (sys.argv[1:] or ["c1", "c2"]):
     c.pseudo_steps = int(k) if k else c.pseudo_steps
     nw = int(w) if w else min(len(c.omegas), os.cpu_count() or 1)
     g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
-    o = Oracle(pow_mode="cr", workers=nw).solver(c.mesh, c.mesh.pattern(), c.scheme,
+    o = Oracle(pow_mode=pow_mode(), workers=nw).solver(c.mesh, c.mesh.pattern(), c.scheme,
                                                                          c.omegas, c.forcing, c.mean0)
     worst_m = worst_z = 0.0
     t0 = time.time()

@@ -29,6 +29,8 @@ def ref():
 
 @pytest.fixture(scope="session")
 def orc_dev():
-    """The restatement evaluating boundary-state pow like the device (correctly rounded)."""
+    """The restatement evaluating boundary-state pow like the device (glibc's rounding when the
+    library's libm check passed, which is the reference's; else correctly rounded)."""
     from oracle.oracle import Oracle
-    return Oracle(pow_mode="cr")
+    from paper_2404_01407_b200._lib import pow_mode
+    return Oracle(pow_mode=pow_mode())

@@ -11,6 +11,7 @@ import numpy as np  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 from oracle.oracle import Oracle  # noqa: E402
+from paper_2404_01407_b200._lib import pow_mode  # noqa: E402
 from paper_2404_01407_b200.cases import make_case  # noqa: E402
 from paper_2404_01407_b200.shard import HarmonicShards  # noqa: E402
 
@@ -20,7 +21,7 @@ def main():
     dist.init_process_group("gloo")
     rank = dist.get_rank()
     c = make_case(name, scale=scale, nh=nh)
-    s = Oracle(pow_mode="cr").solver(c.mesh, c.mesh.pattern(), c.scheme, c.omegas, c.forcing, c.mean0)
+    s = Oracle(pow_mode=pow_mode()).solver(c.mesh, c.mesh.pattern(), c.scheme, c.omegas, c.forcing, c.mean0)
     sh = HarmonicShards(s, nh, c.mesh.n * c.mesh.b)
     hist = []
     for _ in range(steps):

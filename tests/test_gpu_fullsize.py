@@ -14,6 +14,7 @@ import numpy as np
 import pytest
 
 from helpers import rel
+from paper_2404_01407_b200._lib import pow_mode
 from paper_2404_01407_b200.cases import make_case
 
 pytestmark = pytest.mark.gpu
@@ -29,7 +30,7 @@ def test_c2_full_size_history_vs_oracle(c2):
     from paper_2404_01407_b200.solver import FnlhSolver
     c = c2
     g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
-    o = Oracle(pow_mode="cr", workers=min(3, os.cpu_count() or 1)).solver(c.mesh, c.mesh.pattern(), c.scheme,
+    o = Oracle(pow_mode=pow_mode(), workers=min(3, os.cpu_count() or 1)).solver(c.mesh, c.mesh.pattern(), c.scheme,
                                                                          c.omegas, c.forcing, c.mean0)
     for it in range(2):
         eg, eo = g.outer_iteration(), o.outer_iteration()

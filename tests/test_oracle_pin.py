@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 from helpers import (NOZZLE_CASE, embed, extract, extract_blocks, forcing_triplets, line_mesh_from_ref, rel)
+from paper_2404_01407_b200._lib import pow_mode
 from paper_2404_01407_b200.mesh import structured_sector
 
 
@@ -103,12 +104,12 @@ def test_nozzle_second_order_and_perturbation(nozzle, orc):
     W5 = embed(W3, noz.n)
     ri, _ = noz.residual(W3, 2)
     oi, _ = orc.residual(m, W5, 2)
-    assert rel(extract(oi, noz.n), ri) < 1e-13
+    assert np.array_equal(extract(oi, noz.n), ri)  # the 1D stencil on line meshes (disc_euler.cpp:113-157)
     f3 = np.array([1.0, -2.0, 30.0])
     Wp = W3 * 1.0001
     ri, _ = noz.residual(Wp, 2, mode=1, wref=W3, forcing=f3)
     oi, _ = orc.residual(m, embed(Wp, noz.n), 2, mode=1, wref=embed(W3, noz.n), forcing=forcing_triplets(f3))
-    assert rel(extract(oi, noz.n), ri) < 1e-13
+    assert np.array_equal(extract(oi, noz.n), ri)
 
 
 def test_nozzle_linearized_residual_and_df(nozzle, orc):
@@ -117,15 +118,18 @@ def test_nozzle_linearized_residual_and_df(nozzle, orc):
     f3 = noz.forcing[0]
     ri, _ = noz.linearized_residual(W3, what3, noz.omega[0], f3)
     oi, _ = orc.linearized_residual(m, W5, embed(what3, noz.n, np.complex128), noz.omega[0], forcing_triplets(f3))
-    assert rel(extract(oi, noz.n), ri) < 1e-10
+    assert np.array_equal(extract(oi, noz.n), ri)
     amps3 = np.stack([what3, 0.5 * what3])
     df3 = noz.deterministic_flux(W3, noz.omega, amps3)
     df5 = orc.deterministic_flux(m, W5, noz.omega, np.stack([embed(a, noz.n, np.complex128) for a in amps3]))
-    assert rel(extract(df5, noz.n), df3) < 1e-10
+    assert np.array_equal(extract(df5, noz.n), df3)
 
 
 def test_nozzle_solver_history(ref, orc):
-    """Full FnlhSolver (driver.cpp:157-333) vs the restated outer iteration, 10 steps."""
+    """Full FnlhSolver (driver.cpp:157-333) vs the restated outer iteration, 20 steps: with
+    the reference's own 1D JST stencil on the line mesh and glibc's pow the restatement is
+    the reference bit for bit (states equal; the RMS differ only by the sqrt(5/3) rescaling
+    of the b = 5 embedding)."""
     case = NOZZLE_CASE.format(nx=64, nh=2)
     rs = ref.solver(case)
     noz = rs.noz
@@ -133,15 +137,14 @@ def test_nozzle_solver_history(ref, orc):
     forc = np.stack([forcing_triplets(f) for f in noz.forcing])
     osv = orc.solver(m, noz.pattern(5), dict(implicit=1), noz.omega, forc, embed(noz.initial_mean(), noz.n))
     s = np.sqrt(5 / 3)  # RMS over n*b dofs: b = 5 here, 3 in the reference
-    for it in range(10):
+    for it in range(20):
         er, eo = rs.outer_iteration(), osv.outer_iteration()
-        tol = 1e-12 if it == 0 else 1e-7
-        assert abs(eo["resid_mean"] * s / er["resid_mean"] - 1) < tol
-        assert abs(eo["rz"] * s / er["rz"] - 1) < tol
+        assert abs(eo["resid_mean"] * s / er["resid_mean"] - 1) < 1e-14, (it, eo, er)
+        assert abs(eo["rz"] * s / er["rz"] - 1) < 1e-14, (it, eo, er)
     mr, ar = rs.state()
     mo, ao = osv.state()
-    assert rel(extract(mo, noz.n), mr) < 1e-12
-    assert rel(np.stack([extract(a, noz.n) for a in ao]), ar) < 1e-8
+    assert np.array_equal(extract(mo, noz.n), mr)
+    assert np.array_equal(np.stack([extract(a, noz.n) for a in ao]), ar)
 
 
 def test_oracle_harmonic_workers_bitwise():
@@ -152,7 +155,7 @@ def test_oracle_harmonic_workers_bitwise():
     c = make_case("c2", scale=0.05, nh=3)
     out = []
     for w in (1, 3):
-        s = Oracle(pow_mode="cr", workers=w).solver(c.mesh, c.mesh.pattern(), c.scheme, c.omegas, c.forcing, c.mean0)
+        s = Oracle(pow_mode=pow_mode(), workers=w).solver(c.mesh, c.mesh.pattern(), c.scheme, c.omegas, c.forcing, c.mean0)
         hist = [s.outer_iteration() for _ in range(2)]
         out.append(([(e["resid_mean"], e["rz"]) for e in hist], s.state(), s.reports()))
     (h1, (m1, a1), r1), (h3, (m3, a3), r3) = out
@@ -183,10 +186,9 @@ def test_nozzle_explicit_multigrid_history(ref, orc, levels):
     s = np.sqrt(5 / 3)
     for it in range(10):
         er, eo = rs.outer_iteration(), osv.outer_iteration()
-        tol = 1e-12 if it == 0 else 1e-7
-        assert abs(eo["resid_mean"] * s / er["resid_mean"] - 1) < tol, (it, eo, er)
-        assert abs(eo["rz"] * s / er["rz"] - 1) < tol, (it, eo, er)
+        assert abs(eo["resid_mean"] * s / er["resid_mean"] - 1) < 1e-14, (it, eo, er)
+        assert abs(eo["rz"] * s / er["rz"] - 1) < 1e-14, (it, eo, er)
     mr, ar = rs.state()
     mo, ao = osv.state()
-    assert rel(extract(mo, noz.n), mr) < 1e-10
-    assert rel(np.stack([extract(a, noz.n) for a in ao]), ar) < 1e-8
+    assert np.array_equal(extract(mo, noz.n), mr)
+    assert np.array_equal(np.stack([extract(a, noz.n) for a in ao]), ar)
