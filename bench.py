@@ -1,22 +1,30 @@
 #!/usr/bin/env python
-"""Benchmark of the FNLH implicit pseudo-time hot path on B200 (see DESIGN.md).
+"""Benchmark of the FNLH implicit pseudo-time hot path on B200 (see DESIGN.md section 5).
 
-Workload: BASELINE.json configs[1] (C2): annular hex sector 128x64x48, 410,865 nodes,
-5 conservative variables, 3 harmonics, implicit scheme (tol 1e-2, <= 10 sweeps).
+Workload: BASELINE.json configs[3] (C4), the largest configuration that fits one GPU:
+hex sector 256x128x128, 4,276,737 nodes, 5 conservative variables, 10 harmonics,
+implicit scheme (tol 1e-2, <= 10 sweeps), harmonics in 8 lanes (SchemeConfig::workers).
 A step is one pseudo-step (FnlhSolver::outer_iteration, driver.cpp:157-333): FD
 Jacobian, A5 + real ILU(0), per harmonic complex ILU(0) + RK(5,3) with the
-linearized residual and ILU-Richardson sweeps, DF, mean RK(5,3).
+linearized residual and ILU-Richardson sweeps, DF, mean RK(5,3).  --config c2 runs C2.
 
   value = block-row updates performed in the timed steps (sum over every stage solve
           of iterations x N) / device time of the timed steps, all ranks
   e2e   = same through the C ABI with host buffers (state uploaded and downloaded
           every step)
-  roofline = the harmonic relaxation sweep (smoothed_solve iteration), algorithmic
-          bytes of the stored-factor ILU formula / measured sweep time
+  roofline = the harmonic relaxation sweep (smoothed_solve iteration) as the product
+          runs it (all lanes in one batched launch pair), algorithmic bytes
+          (rb_sweep_bytes) / CUDA-event time of the batched sweep
 
-Multi-GPU (--gpus N under torchrun): independent replicas (one C2 instance per
-rank, no collective), "scaling": "weak".  --impl reference: the CPU path (oracle
-restatement whose generic layers are bitwise the reference's) on rank 0.
+--impl reference: the reference's own CPU implementation on the same full-size C4
+harmonic systems (oracle/_ref: the unmodified reference compiled from its sources):
+its Ilu<complex>::factorize and smoothed_solve sweeps on min(N_h, cores, memory)
+concurrent harmonic workers (driver.cpp:246-265), rank 0 only; the mesh, pattern and
+FD Jacobian are built on the host (the restatement), so no product code is loaded.
+
+Multi-GPU (--gpus N under torchrun): --mode shard (default for N > 1) relaxes the
+harmonics of one C4 instance on their owner ranks (h % N) with the fields exchanged by
+NCCL broadcast, "scaling": "strong"; --mode replicas runs one instance per rank.
 """
 from __future__ import annotations
 
@@ -117,65 +125,168 @@ def rb_sweep_bytes(n, n0, e, b, lanes=1):
     return (n + 2 * e) * b * b * 8 + lanes * per_lane
 
 
-def cpu_baseline(config, scale, seconds_hint=20.0):
-    """The CPU path on the host cores: the oracle restatement (generic LA bitwise the
-    reference's) running full pseudo-steps of the same configuration at a reduced size."""
-    from oracle.oracle import Oracle
-    from paper_2404_01407_b200.cases import make_case
+ALPHA5 = 1.0  # rk.hpp:27, alpha of stage 5 (the operator every stage solve uses)
 
-    c = make_case(config, scale=scale)
-    workers = max(1, min(len(c.omegas), os.cpu_count() or 1))  # the reference's harmonic workers
-    orc = Oracle(workers=workers)
-    s = orc.solver(c.mesh, c.mesh.pattern(), c.scheme, c.omegas, c.forcing, c.mean0)
-    rows = 0
+
+def host_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count() or 1
+
+
+def ref_worker_count(n_h, per_worker_bytes, reserve=16e9):
+    """The reference's harmonic workers that fit: min(N_h, host cores, host memory)."""
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 64e9
+    return max(1, min(n_h, os.cpu_count() or 1, int((avail - reserve) // per_worker_bytes)))
+
+
+class RefHarmonicWorkers:
+    """Full-size harmonic systems on the reference's own objects (oracle/_ref, the unmodified
+    reference): A5 = build_lhs_mean(J) (rk.cpp:5-30) shared read-only, and per worker the
+    complex workspace shift_diagonal(A5, i omega V / (Gamma alpha_5)) (build_lhs_harmonic,
+    rk.cpp:32-39), Ilu<complex>::factorize (sparse.cpp:187-257) and smoothed_solve sweeps
+    (sparse.hpp:295-331) -- what one harmonic worker of driver.cpp:246-265 holds."""
+
+    def __init__(self, case, pat, J, n_workers):
+        import threading
+        from oracle.oracle import RefLib
+        self.ref = RefLib()
+        sch = case.scheme
+        sigma = sch["sigma_cfl"] if sch["sigma_cfl"] > 0 else 50.0  # driver.hpp:33-41 implicit default
+        A5 = self.ref.build_lhs_mean(pat, J, 1, sigma, sch["eps_relax"], 5)
+        self.lhs = self.ref.lhs_create(pat, A5)
+        del A5
+        n, b = case.mesh.n, case.mesh.b
+        ga5 = (1.0 / sch["eps_relax"]) * ALPHA5
+        rng = np.random.default_rng(4242)
+        self.workers = [None] * n_workers
+        self.factor_s = [0.0] * n_workers
+        self.n = n
+
+        def make(t):
+            shift = case.omegas[t] * case.mesh.vol / ga5
+            rhs = rng_rhs[t]
+            self.workers[t], self.factor_s[t] = self.ref.hworker_create(self.lhs, shift, rhs)
+
+        rng_rhs = [rng.standard_normal(n * b) + 1j * rng.standard_normal(n * b) for _ in range(n_workers)]
+        th = [threading.Thread(target=make, args=(t,)) for t in range(n_workers)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        if any(w is None for w in self.workers):
+            raise RuntimeError("reference harmonic worker setup failed")
+
+    def sweep_all(self, count=None):
+        """One smoothed_solve iteration on each of the first `count` workers concurrently
+        (ctypes releases the GIL): wall seconds."""
+        import threading
+        ws = self.workers[: count or len(self.workers)]
+        th = [threading.Thread(target=self.ref.hworker_sweeps, args=(w, 1)) for w in ws]
+        t0 = time.perf_counter()
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        return time.perf_counter() - t0
+
+    def close(self):
+        for w in self.workers:
+            if w:
+                self.ref.hworker_destroy(w)
+        self.ref.lhs_destroy(self.lhs)
+
+
+def per_worker_bytes(n, nnzb, b):
+    """Host bytes of one reference harmonic worker: complex workspace + Ilu<complex> (vals,
+    diag_lu, diag_inv, pivots) + the smoothed_solve vectors."""
+    return nnzb * b * b * 16 * 2 + n * b * b * 16 * 2 + n * b * 4 + 6 * n * b * 16
+
+
+def cpu_baseline(case, pat, J):
+    """The reference's own CPU path (oracle/_ref) on a bounded sample of the same workload:
+    the full-size harmonic systems of this configuration, one Richardson sweep each, with
+    1 worker (1 core) and with min(N_h, cores, memory) concurrent workers."""
+    model, cores = host_info()
+    n, b = case.mesh.n, case.mesh.b
+    W = ref_worker_count(len(case.omegas), per_worker_bytes(n, len(pat["col_idx"]), b))
     t0 = time.perf_counter()
-    steps = 0
-    while True:
-        s.outer_iteration()
-        steps += 1
-        if time.perf_counter() - t0 > seconds_hint or steps >= 3:
-            break
-    dt = time.perf_counter() - t0
-    rows = sum(r[0] for r in s.reports()) * c.mesh.n
-    return {"value": rows / dt, "unit": UNIT, "cores": workers, "kind": "port",
-            "sample": f"{steps} pseudo-step(s) of {config} at scale {scale} ({c.mesh.n} nodes, "
-                      f"{len(c.omegas)} harmonics), oracle/fnlh_oracle.c, {workers} harmonic worker thread(s) "
-                      f"(host has {os.cpu_count()}), {dt:.1f} s"}
+    rw = RefHarmonicWorkers(case, pat, J, W)
+    setup = time.perf_counter() - t0
+    t1 = rw.sweep_all(1)
+    tw = rw.sweep_all(W)
+    rw.close()
+    return {"value": W * n / tw, "unit": UNIT, "cores": W, "kind": "reference",
+            "one_core": {"value": n / t1, "unit": UNIT, "seconds_per_sweep": t1},
+            "workers": W, "seconds_per_sweep": tw, "host": {"cpu_model": model, "nproc": cores},
+            "factorize_seconds_per_worker": round(max(rw.factor_s), 2),
+            "sample": f"one smoothed_solve sweep of each of {W} full-size {case.name} harmonic system(s) "
+                      f"({n} nodes, nnzb {len(pat['col_idx'])}) on the reference's Ilu<complex> / smoothed_solve "
+                      f"(oracle/_ref), {W} concurrent worker thread(s) on {cores} host cores ({model}); the 1-core "
+                      f"number is one worker alone; setup (shift_diagonal + factorize, not timed) {setup:.0f} s"}
 
 
 def reference_arm(args):
+    """The reference's CPU implementation of the path, on the same full-size workload."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    from paper_2404_01407_b200.cases import make_case
     from oracle.oracle import Oracle
+    from paper_2404_01407_b200.cases import make_case
 
-    scale = args.ref_scale
-    c = make_case(args.config, scale=scale)
-    workers = max(1, min(len(c.omegas), os.cpu_count() or 1))  # all the threads the reference's scheme uses
-    orc = Oracle(workers=workers)
-    s = orc.solver(c.mesh, c.mesh.pattern(), c.scheme, c.omegas, c.forcing, c.mean0)
-    for _ in range(args.warmup):
-        s.outer_iteration()
-    r0 = sum(r[0] for r in s.reports())
     t0 = time.perf_counter()
+    c = make_case(args.config, scale=args.scale, device=False)  # host restatement: no product code loaded
+    pat = c.mesh.pattern(device=False)
+    J, _ = Oracle().fd_jacobian(c.mesh, pat, c.mean0)  # the restatement (bitwise the device's, tests)
+    n, b = c.mesh.n, c.mesh.b
+    W = ref_worker_count(len(c.omegas), per_worker_bytes(n, len(pat["col_idx"]), b))
+    rw = RefHarmonicWorkers(c, pat, J, W)
+    del J
+    setup = time.perf_counter() - t0
+    for _ in range(args.warmup):
+        rw.sweep_all()
+    wall = 0.0
     for _ in range(args.steps):
-        s.outer_iteration()
-    dt = time.perf_counter() - t0
-    rows = (sum(r[0] for r in s.reports()) - r0) * c.mesh.n
-    v = rows / dt
+        wall += rw.sweep_all()
+    rw.close()
+    v = W * n * args.steps / wall
+    model, cores = host_info()
+    loaded = [ln.split()[-1] for ln in open("/proc/self/maps") if "libfnlh_b200" in ln]
+    E = (len(pat["col_idx"]) - n) // 2
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
-            "config": {"workload": f"{args.config} pseudo-step, CPU sample at scale {scale} ({c.mesh.n} nodes)",
-                       "harmonics": len(c.omegas), "l2": "inputs resident in host memory"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "port",
-                             "sample": f"{args.steps} pseudo-steps of {args.config} at scale {scale} "
-                                       f"({c.mesh.n} nodes), oracle/fnlh_oracle.c, {workers} harmonic worker "
-                                       f"thread(s) (host has {os.cpu_count()})"},
+            "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, cases.py)",
+            "config": workload_config(c, n, E, b),
+            "step": f"one smoothed_solve sweep (Ilu<complex>::apply + Bsr::matvec + norm, sparse.hpp:315-329) of "
+                    f"each of {W} full-size harmonic systems, one reference harmonic worker thread each",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": W, "kind": "reference",
+                             "host": {"cpu_model": model, "nproc": cores},
+                             "sample": f"{args.steps} timed steps x {W} concurrent full-size {args.config} harmonic "
+                                       f"sweeps on oracle/_ref (the unmodified reference), {cores} host cores "
+                                       f"({model}); setup (host mesh, FD Jacobian, shift_diagonal, factorize) "
+                                       f"{setup:.0f} s untimed"},
+            "product_library_loaded": bool(loaded),
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def workload_config(c, n, E, b):
+    """The workload keys, identical on both arms (same_config); run details go to "details"."""
+    a5 = (n + 2 * E) * b * b * 8
+    return {"workload": f"{c.name}: {c.description}", "nodes": n, "edges": E, "b": b, "harmonics": len(c.omegas),
+            "l2": f"inputs larger than L2 (the shared LHS A5 alone is {a5 / 1e9:.2f} GB)"}
 
 
 def main():
@@ -184,14 +295,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c4")
     ap.add_argument("--scale", type=float, default=1.0)
-    ap.add_argument("--ref-scale", type=float, default=0.4)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweeps", type=int, default=10, help="sweeps in the roofline leg")
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "shard"],
-                    help="N>1: independent C2 replicas per rank (weak scaling) or one C2 instance with its "
-                         "harmonics sharded over the ranks, fields exchanged by NCCL broadcast (strong scaling)")
+    ap.add_argument("--mode", default="shard", choices=["replicas", "shard"],
+                    help="N>1: one instance with its harmonics sharded over the ranks, fields exchanged by NCCL "
+                         "broadcast (strong scaling, default), or independent replicas per rank (weak scaling)")
     ap.add_argument("--workers", type=int, default=0,
                     help="harmonic lanes (SchemeConfig::workers); 0 = one per harmonic (<= 8)")
     args = ap.parse_args()
@@ -326,13 +436,15 @@ def main():
         b1 = rb_sweep_bytes(n, info["n0"], E, b, 1)
         single = {"ms_per_launch": ms1, "bytes_per_launch": b1, "achieved": b1 / (ms1 * 1e-3) / 1e9,
                   "frac": b1 / (ms1 * 1e-3) / 1e9 / peak, "unit": "GB/s"}
-    traffic = None
+    traffic, traffic_src = None, None
     try:  # dram read + write of the same kernels from the committed ncu --set full capture
-        name = "r1_sweep_ncu_c2_lanes3.json" if lanes == 3 else "r1_sweep_ncu_c2.json"
-        with open(os.path.join(ROOT, "profiles", name)) as f:
-            prof = json.load(f)
-        if info["red_black"] and args.config == "c2" and args.scale == 1.0 and prof.get("lanes", 1) == lanes:
-            traffic = prof["traffic_bytes_per_sweep"]
+        name = {("c4", 8): "r2_sweep_ncu_c4_lanes8.json", ("c2", 3): "r1_sweep_ncu_c2_lanes3.json",
+                ("c2", 1): "r1_sweep_ncu_c2.json"}.get((args.config, lanes))
+        if name and info["red_black"] and args.scale == 1.0:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                prof = json.load(f)
+            if prof.get("lanes", 1) == lanes:
+                traffic, traffic_src = prof["traffic_bytes_per_sweep"], f"profiles/{name}"
     except Exception:
         pass
 
@@ -340,9 +452,10 @@ def main():
             "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong" if shard else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, cases.py)",
-            "config": {"workload": f"{args.config}: {c.description}", "nodes": n, "edges": E, "b": b,
-                       "harmonics": len(c.omegas), "pseudo_step": "outer_iteration (FD J, ILU, RK x (N_h+1), DF)",
-                       "l2": f"inputs larger than L2 (LHS {s.lhs_bytes() / 1e9:.2f} GB resident)",
+            "config": workload_config(c, n, E, b),
+            "details": {
+                       "pseudo_step": "outer_iteration (FD J, ILU, RK x (N_h+1), DF)",
+                       "resident": f"LHS {s.lhs_bytes() / 1e9:.2f} GB in HBM",
                        "parallelism": (f"harmonics sharded over {world} ranks (NCCL broadcast of fields)" if shard
                                        else f"replicas x{world}" if world > 1 else "1 GPU"),
                        "sweeps_per_step": sweeps / args.steps, "lhs_bytes": s.lhs_bytes(),
@@ -350,13 +463,17 @@ def main():
                        "step_split_ms": {k: round(v, 3) for k, v in phase.items()}},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "kernel": kname, "bytes_formula": formula,
+                         "traffic": traffic, "traffic_source": traffic_src, "kernel": kname, "bytes_formula": formula,
                          "bytes_per_launch": bytes_sweep, "ms_per_launch": sweep_ms, "peak_kind": peak_kind,
                          "sweep_rows_per_s": lanes * n / (sweep_ms * 1e-3), "single_lane": single},
             "clocks": clk, "gpu_launches": launches}
     if rank == 0 and world == 1 and not args.no_cpu:
-        try:
-            line["cpu_baseline"] = cpu_baseline(args.config, args.ref_scale)
+        try:  # the reference's CPU sweep on the same full-size systems; J from the device (bitwise the host's)
+            del mean_h, amps_h
+            from paper_2404_01407_b200.solver import Discretization
+            J, _ = Discretization(m, pat).fd_jacobian(c.mean0)
+            line["cpu_baseline"] = cpu_baseline(c, pat, J)
+            del J
         except Exception as ex:  # the baseline is informative; never fail the bench on it
             line["cpu_baseline"] = {"value": None, "error": str(ex)}
     if rank == 0:

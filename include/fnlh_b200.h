@@ -197,6 +197,10 @@ int fnlh_solver_outer_iteration_host(fnlh_solver* s, const double* mean_in, cons
      harmonic's stage-1 norm and its linear reports (nrep[h] of them, concatenated in
      harmonic order).  fnlh_solver_outer_iteration == phase_harmonics(NULL) + phase_mean. */
 int fnlh_solver_phase_harmonics(fnlh_solver* s, const int* owned, double* h_norm);
+/* the harmonic whose error the last phase_harmonics returned (the first failing one by
+   index, driver.cpp:262-264), or -1 when it succeeded or failed before the harmonics; lets
+   a sharded caller rethrow the lowest failing harmonic's error on every rank */
+int fnlh_solver_failed_harmonic(const fnlh_solver* s, int* h);
 /* linear reports of harmonic h from the last phase_harmonics (count in *n, at most max copied) */
 int fnlh_solver_harmonic_reports(const fnlh_solver* s, int h, fnlh_linear_report* out, int max, int* n);
 int fnlh_solver_phase_mean(fnlh_solver* s, const double* h_norm, const int* nrep, const fnlh_linear_report* reps,

@@ -898,6 +898,7 @@ struct or_solver {
     report_list reports;
     int iter;
     report_list* hrep; /* per harmonic, from the last phase_harmonics */
+    int failed_h;      /* harmonic of the error the last phase_harmonics returned, -1 none */
     double* hnorm;
     or_ilu_z* ws_extra; /* per-worker complex workspaces (or_set_workers) */
     int nlev;           /* coarse multigrid levels (explicit scheme) */
@@ -913,6 +914,7 @@ or_solver* or_solver_create(const or_mesh* m, const or_pattern* p, const or_sche
                             const int* index, const double* omega, const ocplx* forcing, int nforcing,
                             const double* mean0) {
     or_solver* S_ = (or_solver*)xcalloc(1, sizeof(or_solver));
+    S_->failed_h = -1;
     S_->mesh = *m;
     S_->pat = *p;
     S_->sch = *s;
@@ -1328,11 +1330,15 @@ int or_solver_phase_harmonics(or_solver* s, const int* owned, double* hnorm_out)
                 break;
             }
     }
-    for (int h = 0; h < nh && !st; ++h) st = hst[h];
+    s->failed_h = -1;
+    for (int h = 0; h < nh && !st; ++h)
+        if ((st = hst[h])) s->failed_h = h;
     if (hnorm_out)
         for (int h = 0; h < nh; ++h) hnorm_out[h] = hnorm[h];
     return st;
 }
+
+int or_solver_failed_harmonic(const or_solver* s) { return s->failed_h; }
 
 int or_solver_harmonic_reports(const or_solver* s, int h, or_linear_report* out, int max) {
     for (int k = 0; k < s->hrep[h].n && k < max; ++k) out[k] = s->hrep[h].v[k];

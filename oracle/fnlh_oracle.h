@@ -175,6 +175,8 @@ or_solver* or_solver_create(const or_mesh* m, const or_pattern* p, const or_sche
 void or_solver_destroy(or_solver* s);
 int or_solver_outer_iteration(or_solver* s, or_entry* e, double* resid_h);
 int or_solver_phase_harmonics(or_solver* s, const int* owned, double* hnorm_out);
+/* harmonic whose error the last phase_harmonics returned (-1: none / before the harmonics) */
+int or_solver_failed_harmonic(const or_solver* s);
 /* harmonic worker threads (SchemeConfig::workers, driver.cpp:246-265), process-wide */
 void or_set_workers(int w);
 /* append a coarse multigrid level (explicit scheme): parent maps the current coarsest

@@ -157,6 +157,43 @@ class Oracle:
         self._check(fn(C.byref(P), ptr(A), ptr(rhs), C.byref(f), _d(tol), _i(max_iter), ptr(x), C.byref(rep)))
         return x, (rep.iterations, rep.initial_residual, rep.final_residual, bool(rep.converged))
 
+    # -- full-size harmonic workers (bench.py --impl reference): the reference's own objects
+    def lhs_create(self, pat, A5):
+        """The shared real LHS A5 on its pattern (Bsr<real>); keep the handle alive while
+        workers use it."""
+        self._lhs_keep = [np.ascontiguousarray(pat["row_ptr"]), np.ascontiguousarray(pat["col_idx"]),
+                          np.ascontiguousarray(A5, np.float64)]
+        b, n = int(pat["b"]), len(pat["row_ptr"]) - 1
+        self.lib.ref_lhs_create.restype = _p
+        h = self.lib.ref_lhs_create(_i(b), _i(n), ptr(self._lhs_keep[0]), ptr(self._lhs_keep[1]), ptr(self._lhs_keep[2]))
+        if not h:
+            self._check(7)
+        return h
+
+    def hworker_create(self, lhs, shift_im, rhs):
+        """One harmonic worker: shift_diagonal into its complex workspace + Ilu factorize.
+        Returns (handle, factorization seconds)."""
+        fs = _d()
+        self.lib.ref_hworker_create.restype = _p
+        sh = np.ascontiguousarray(shift_im, np.float64)
+        r = np.ascontiguousarray(rhs, np.complex128)
+        h = self.lib.ref_hworker_create(_p(lhs), ptr(sh), ptr(r), C.byref(fs))
+        if not h:
+            self._check(7)
+        return h, fs.value
+
+    def hworker_sweeps(self, w, sweeps):
+        """smoothed_solve of `sweeps` iterations on the worker's system: (seconds, final norm)."""
+        t, f = _d(), _d()
+        self._check(self.lib.ref_hworker_sweeps(_p(w), _i(sweeps), C.byref(t), C.byref(f)))
+        return t.value, f.value
+
+    def hworker_destroy(self, w):
+        self.lib.ref_hworker_destroy(_p(w))
+
+    def lhs_destroy(self, h):
+        self.lib.ref_lhs_destroy(_p(h))
+
     def build_lhs_mean(self, pat, J, implicit, sigma, eps, stage):
         A = np.zeros_like(J)
         P = self.pattern(pat)
@@ -275,6 +312,9 @@ class OracleSolver:
         own = None if owned is None else np.ascontiguousarray(owned, np.int32)
         self.o._check(self.o.mode().or_solver_phase_harmonics(_p(self.h), ptr(own), ptr(hn)))
         return hn[: self.nh].copy()
+
+    def failed_harmonic(self):
+        return self.o.lib.or_solver_failed_harmonic(_p(self.h))
 
     def harmonic_reports(self, h):
         arr = (OrReport * 256)()
@@ -433,6 +473,43 @@ class RefLib:
         b, n, rp, ci, _ = self._csr(pat)
         t = fn(_i(b), _i(n), rp, ci, ptr(A), ptr(rhs), _i(sweeps), C.byref(fs))
         return t, fs.value
+
+    # -- full-size harmonic workers (bench.py --impl reference): the reference's own objects
+    def lhs_create(self, pat, A5):
+        """The shared real LHS A5 on its pattern (Bsr<real>); keep the handle alive while
+        workers use it."""
+        self._lhs_keep = [np.ascontiguousarray(pat["row_ptr"]), np.ascontiguousarray(pat["col_idx"]),
+                          np.ascontiguousarray(A5, np.float64)]
+        b, n = int(pat["b"]), len(pat["row_ptr"]) - 1
+        self.lib.ref_lhs_create.restype = _p
+        h = self.lib.ref_lhs_create(_i(b), _i(n), ptr(self._lhs_keep[0]), ptr(self._lhs_keep[1]), ptr(self._lhs_keep[2]))
+        if not h:
+            self._check(7)
+        return h
+
+    def hworker_create(self, lhs, shift_im, rhs):
+        """One harmonic worker: shift_diagonal into its complex workspace + Ilu factorize.
+        Returns (handle, factorization seconds)."""
+        fs = _d()
+        self.lib.ref_hworker_create.restype = _p
+        sh = np.ascontiguousarray(shift_im, np.float64)
+        r = np.ascontiguousarray(rhs, np.complex128)
+        h = self.lib.ref_hworker_create(_p(lhs), ptr(sh), ptr(r), C.byref(fs))
+        if not h:
+            self._check(7)
+        return h, fs.value
+
+    def hworker_sweeps(self, w, sweeps):
+        """smoothed_solve of `sweeps` iterations on the worker's system: (seconds, final norm)."""
+        t, f = _d(), _d()
+        self._check(self.lib.ref_hworker_sweeps(_p(w), _i(sweeps), C.byref(t), C.byref(f)))
+        return t.value, f.value
+
+    def hworker_destroy(self, w):
+        self.lib.ref_hworker_destroy(_p(w))
+
+    def lhs_destroy(self, h):
+        self.lib.ref_lhs_destroy(_p(h))
 
     def build_lhs_mean(self, pat, J, implicit, sigma, eps, stage):
         A = np.zeros_like(J)

@@ -229,6 +229,68 @@ int ref_build_lhs_mean(int b, int rows, const int* row_ptr, const int* col_idx, 
     });
 }
 
+// ---- full-size harmonic workers (bench.py --impl reference) ----------------------
+// The objects one reference harmonic worker holds (driver.cpp:117, 213-216): the shared
+// real LHS A5 on its pattern, the worker's complex workspace filled by shift_diagonal
+// (sparse.cpp:157-171, as build_lhs_harmonic does, rk.cpp:32-39), its Ilu<cplx>
+// (sparse.cpp:187-257), and smoothed_solve (sparse.hpp:295-331) on them.  Several
+// workers may run concurrently from host threads (distinct workers, shared read-only A5).
+struct RefLhs {
+    PatternPtr p;
+    Bsr<real> A5;
+};
+struct RefWorker {
+    const RefLhs* lhs;
+    Bsr<cplx> M;
+    Ilu<cplx> f;
+    BlockVec<cplx> rhs, x;
+};
+
+void* ref_lhs_create(int b, int rows, const int* row_ptr, const int* col_idx, const double* A5) {
+    RefLhs* out = nullptr;
+    guarded([&] {
+        auto h = std::make_unique<RefLhs>();
+        h->p = pattern_from_csr(b, rows, row_ptr, col_idx, nullptr);
+        h->A5 = bsr_from<real>(h->p, A5);
+        out = h.release();
+    });
+    return out;
+}
+void ref_lhs_destroy(void* h) { delete static_cast<RefLhs*>(h); }
+
+// shift_diagonal(A5, i shift) into the worker's workspace, then Ilu::factorize (timed)
+void* ref_hworker_create(void* lhs, const double* shift_im, const std::complex<double>* rhs, double* factor_seconds) {
+    RefWorker* out = nullptr;
+    guarded([&] {
+        auto w = std::make_unique<RefWorker>();
+        w->lhs = static_cast<const RefLhs*>(lhs);
+        const int n = w->lhs->A5.rows(), b = w->lhs->A5.b();
+        std::vector<cplx> s(n);
+        for (int i = 0; i < n; ++i) s[i] = cplx(0.0, shift_im[i]);
+        shift_diagonal(w->lhs->A5, s, w->M);
+        const auto t0 = std::chrono::steady_clock::now();
+        w->f.factorize(w->M);
+        const auto t1 = std::chrono::steady_clock::now();
+        if (factor_seconds) *factor_seconds = std::chrono::duration<double>(t1 - t0).count();
+        w->rhs = vec_from<cplx>(b, n, rhs);
+        out = w.release();
+    });
+    return out;
+}
+void ref_hworker_destroy(void* h) { delete static_cast<RefWorker*>(h); }
+
+// one smoothed_solve of `sweeps` iterations from x = 0 (tol 1e-300: every sweep runs)
+int ref_hworker_sweeps(void* h, int sweeps, double* seconds, double* final_residual) {
+    return guarded([&] {
+        RefWorker* w = static_cast<RefWorker*>(h);
+        const auto t0 = std::chrono::steady_clock::now();
+        const LinearSolveReport rep = smoothed_solve(w->M, w->rhs, w->f, 1e-300, sweeps, w->x);
+        const auto t1 = std::chrono::steady_clock::now();
+        if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+        if (final_residual) *final_residual = rep.final_residual;
+    });
+}
+
 // ---- pattern / adjacency builders (sparse.cpp:91-117, mesh.cpp:44-59) ----------
 
 // make_pattern on an edge list; col_idx capacity rows + 2 ne; returns nnzb in *nnz

@@ -30,11 +30,11 @@ def _needs(obj, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src, headers, verbose):
-    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+def _compile(src, headers, verbose, obj_dir=OBJ, extra=()):
+    obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
     if not _needs(obj, [src] + headers):
         return obj, False
-    cmd = [NVCC] + ARCH + COMMON + ["-c", src, "-o", obj]
+    cmd = [NVCC] + ARCH + COMMON + list(extra) + ["-c", src, "-o", obj]
     if src.endswith(".cpp"):
         cmd = [NVCC] + COMMON + ["-x", "c++", "-c", src, "-o", obj]
     if verbose:
@@ -45,22 +45,24 @@ def _compile(src, headers, verbose):
     return obj, True
 
 
-def build(verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(verbose: bool = False, lib: str = LIB, obj_dir: str = OBJ, extra=()) -> str:
+    """Compile every source for sm_100a and link `lib`.  `extra` nvcc flags and a separate
+    `obj_dir` / `lib` build a measurement variant (profiles/) without touching the product."""
+    os.makedirs(obj_dir, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     headers = sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.hpp")) +
                      glob.glob(os.path.join(ROOT, "include", "*.h")))
     with cf.ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 4)) as ex:
-        results = list(ex.map(lambda s: _compile(s, headers, verbose), srcs))
+        results = list(ex.map(lambda s: _compile(s, headers, verbose, obj_dir, extra), srcs))
     objs = [o for o, _ in results]
-    if any(c for _, c in results) or not os.path.exists(LIB) or _needs(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
+    if any(c for _, c in results) or not os.path.exists(lib) or _needs(lib, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-lcudart"]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

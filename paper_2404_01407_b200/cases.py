@@ -54,9 +54,11 @@ SPECS = {
 
 
 def make_case(name: str, scale: float = 1.0, nh: int | None = None, implicit: bool = True, permute: bool = True,
-              workers: int = 1, **overrides) -> Case:
+              workers: int = 1, device: bool | None = None, **overrides) -> Case:
     """Build config `name` ('c1'..'c5').  `scale` shrinks the cell counts (parity tests run
-    the same configuration at sizes the CPU oracle finishes in seconds)."""
+    the same configuration at sizes the CPU oracle finishes in seconds).  `device`: build the
+    mesh with the library's kernels (None: when a GPU is present) or on the host (False, the
+    bit-identical restatement: the CPU reference arm, which must not load the library)."""
     spec = dict(SPECS[name])
     spec.update(overrides)
     ci, cj, ck = spec["cells"]
@@ -76,7 +78,7 @@ def make_case(name: str, scale: float = 1.0, nh: int | None = None, implicit: bo
     nt_in = 1e-3 if b == 6 else 0.0
     m = structured_sector(ci, cj, ck, geometry=spec["geometry"], periodic_j=spec["periodic_j"], tets=spec["tets"],
                           jitter=spec.get("jitter", 0.0), seed=spec["seed"], b=b, permute=permute, gas=gas,
-                          nt_in=nt_in, mu_range=spec.get("mu_range"))
+                          nt_in=nt_in, mu_range=spec.get("mu_range"), device=device, order=spec.get("order", "rcm"))
     n = m.n
     W = np.zeros((n, b))
     W[:, 0] = 1.0 * (1.0 + 0.01 * rng.uniform(-1, 1, n))

@@ -10,14 +10,13 @@
 
 using namespace fnlh;
 
+// rb / n0 are decided once in fnlh_pattern_create and read-only afterwards, so one pattern
+// handle may serve concurrent solves from several host threads (the shim's harmonic workers)
 struct fnlh_pattern {
     std::unique_ptr<DevicePattern> p;
-    int rb = -1;  // -1 unknown, 0 no, 1 yes (2-colour colour-major, single partition)
+    int rb = 0;  // 1: 2-colour colour-major ordering with one partition (rb.cuh)
     int n0 = 0;
-    bool use_rb() {
-        if (rb < 0) rb = rb_eligible(*p, &n0) ? 1 : 0;
-        return rb == 1 && fnlh::rb_enabled();
-    }
+    bool use_rb() const { return rb == 1 && fnlh::rb_enabled(); }
 };
 
 namespace {
@@ -96,7 +95,7 @@ int matvec_impl(const fnlh_pattern* p, const double* A, int A_complex, const dou
 }
 
 template <class S>
-int solve_rb(fnlh_pattern* p, const double* A, const double* shift_im, const double* rhs, double tol, int max_iter,
+int solve_rb(const fnlh_pattern* p, const double* A, const double* shift_im, const double* rhs, double tol, int max_iter,
              double* x, fnlh_linear_report* rep) {
     const DevicePattern* dp = p->p.get();
     const std::size_t len = (std::size_t)dp->rows * dp->b;
@@ -182,6 +181,7 @@ int fnlh_pattern_create(int b, int rows, const int* row_ptr, const int* col_idx,
     return guarded([&] {
         auto h = std::make_unique<fnlh_pattern>();
         h->p = std::make_unique<DevicePattern>(b, rows, row_ptr, col_idx, partition);
+        h->rb = rb_eligible(*h->p, &h->n0) ? 1 : 0;
         *out = h.release();
     });
 }
@@ -228,12 +228,11 @@ int fnlh_smoothed_solve(const fnlh_pattern* p, int is_complex, const double* A, 
                         const double* shift_im, const double* rhs, double tol_rel, int max_iter, double* x,
                         fnlh_linear_report* rep) {
     return guarded([&] {
-        fnlh_pattern* pm = const_cast<fnlh_pattern*>(p);
-        if (!A_complex && pm->use_rb()) {  // the 2-colour fused path (rb.cuh)
+        if (!A_complex && p->use_rb()) {  // the 2-colour fused path (rb.cuh)
             if (is_complex)
-                solve_rb<cplx>(pm, A, shift_im, rhs, tol_rel, max_iter, x, rep);
+                solve_rb<cplx>(p, A, shift_im, rhs, tol_rel, max_iter, x, rep);
             else
-                solve_rb<double>(pm, A, nullptr, rhs, tol_rel, max_iter, x, rep);
+                solve_rb<double>(p, A, nullptr, rhs, tol_rel, max_iter, x, rep);
             return;
         }
         if (is_complex)
@@ -246,7 +245,6 @@ int fnlh_smoothed_solve(const fnlh_pattern* p, int is_complex, const double* A, 
 int fnlh_pattern_is_red_black(fnlh_pattern* p, int* n0) {
     return guarded([&] {
         *n0 = -1;
-        if (p->rb < 0) p->rb = rb_eligible(*p->p, &p->n0) ? 1 : 0;
         if (p->rb == 1) *n0 = p->n0;
     });
 }
@@ -254,7 +252,6 @@ int fnlh_pattern_is_red_black(fnlh_pattern* p, int* n0) {
 int fnlh_rb_factorize(fnlh_pattern* p, int is_complex, const double* A, const double* shift_im, double* diag_lu,
                       int* diag_piv, double* inv0) {
     return guarded([&] {
-        if (p->rb < 0) p->rb = rb_eligible(*p->p, &p->n0) ? 1 : 0;
         if (p->rb != 1) throw ShapeError("pattern is not a 2-colour colour-major ordering with one partition");
         if (is_complex)
             rb_factor_impl<cplx>(p, A, shift_im, diag_lu, diag_piv, inv0);

@@ -195,6 +195,10 @@ int fnlh_solver_phase_harmonics(fnlh_solver* s, const int* owned, double* h_norm
     });
 }
 
+int fnlh_solver_failed_harmonic(const fnlh_solver* s, int* h) {
+    return guarded([&] { *h = s->s->failed_harmonic(); });
+}
+
 int fnlh_solver_harmonic_reports(const fnlh_solver* s, int h, fnlh_linear_report* out, int max, int* n) {
     return guarded([&] {
         const auto& hr = s->s->last_h_reports();

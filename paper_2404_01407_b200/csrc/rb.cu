@@ -1055,12 +1055,10 @@ void rb_smoothed_solve_batch(const RbSystem& A, const RbMember<S>* mem, int P, d
     const int g0 = A.grid0 * P, g1 = A.grid1 * P;
     RB_DISPATCH(L.b, {
         const std::size_t sm = (std::size_t)maxoff * B * kT * sizeof(S);
-        static const bool attr = [] {  // once per instantiation (thread-safe static initialization)
-            FNLH_CUDA(cudaFuncSetAttribute(k_rb_colour0<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            FNLH_CUDA(cudaFuncSetAttribute(k_rbx_colour1<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            return true;
-        }();
-        (void)attr;
+        // every call: function attributes belong to the current device's context (a process may
+        // drive several GPUs, fnlh_set_device), and setting one is a host-side table update
+        FNLH_CUDA(cudaFuncSetAttribute(k_rb_colour0<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        FNLH_CUDA(cudaFuncSetAttribute(k_rbx_colour1<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         if (rb_sweep_mode() == 1) {
             for (int s = 1; s <= max_iter; ++s) {
                 { ::fnlh::note_launch(); k_rb_forward1<B, S><<<g1, kT, 0, stm>>>(sd, T, s); }

@@ -694,6 +694,7 @@ void DeviceSolver::phase_harmonics(const int* owned) {
     cudaStream_t st = ws_->stream;
     FNLH_CUDA(cudaEventRecord(ev0_, st));
     ++iter_;
+    failed_h_ = -1;
     const int n = disc_->n(), b = disc_->b();
     const std::size_t len = disc_->len();
     const double gamma = disc_->view().gamma;
@@ -805,13 +806,19 @@ void DeviceSolver::phase_harmonics(const int* owned) {
                 h_norm[h] = step.stage1_residual_norm;
                 h_reps[h] = std::move(step.linear_reports);
             } catch (...) {
-                if (!parallel) throw;
+                if (!parallel) {
+                    failed_h_ = h;
+                    throw;
+                }
                 herr[h] = std::current_exception();
             }
         }
     }
     for (int h = 0; h < nh_; ++h)
-        if (herr[h]) std::rethrow_exception(herr[h]);
+        if (herr[h]) {
+            failed_h_ = h;
+            std::rethrow_exception(herr[h]);
+        }
     if (amps_download_ && nh_) {  // updated harmonic fields home while DF and the mean step run
         FNLH_CUDA(cudaEventRecord(ev_h_, st));
         FNLH_CUDA(cudaStreamWaitEvent(cs_, ev_h_, 0));

@@ -97,6 +97,8 @@ public:
     // harmonic fields: J, A5, mean ILU and the owned harmonics' RK steps
     // (owned: nh flags, nullptr = all) ...
     void phase_harmonics(const int* owned);
+    // harmonic whose error the last phase_harmonics rethrew (-1: none, or an error before the harmonics)
+    int failed_harmonic() const { return failed_h_; }
     const std::vector<double>& last_h_norm() const { return h_norm_; }
     const std::vector<std::vector<LinearSolveReport>>& last_h_reports() const { return h_reps_; }
     // ... then DF from every harmonic field, the mean RK step and the monitor, given every
@@ -200,6 +202,7 @@ private:
     std::vector<std::unique_ptr<HarmonicLane>> lanes_;  // batched harmonic path (workers > 1), else empty
     std::vector<LinearSolveReport> reports_;
     int iter_ = 0;
+    int failed_h_ = -1;
     double cum_seconds_ = 0.0;
     cudaEvent_t ev0_, ev1_, evp_[3];
     cudaStream_t cs_ = nullptr;          // copy stream of outer_iteration_host

@@ -329,14 +329,29 @@ def _sector_dual_device(Xu, ci, cj, ck, periodic_j, tets):
     return ea, eb, en, vol
 
 
+def morton_key(i, j, k) -> np.ndarray:
+    """Z-order key of non-negative index triples (bits interleaved k, j, i from the top)."""
+    key = np.zeros(len(i), np.int64)
+    for bit in range(21):
+        for t, v in enumerate((i, j, k)):
+            key |= ((np.asarray(v, np.int64) >> bit) & 1) << (3 * bit + t)
+    return key
+
+
 def structured_sector(ci, cj, ck, *, geometry="annular", length=2.0, pitch_deg=10.0, r_in=0.5, r_out=1.0,
                       width=1.0, height=0.5, periodic_j=False, tets=False, jitter=0.0, seed=0, b=5, permute=True,
-                      gas=None, nt_in=0.0, mu_range=None, device=None):
+                      gas=None, nt_in=0.0, mu_range=None, device=None, order="rcm"):
     """Hex (or Kuhn 6-tet) sector mesh, node-centred median dual.
 
     i: axial (inlet i=0, outlet i=ci), j: pitch, k: span/radius.  Walls (hub, casing,
     non-periodic pitch sides) enter through the closure source.  Returns a Mesh3D in
     colour-major RCM order (2 colours for hex, 8 for Kuhn tets).
+
+    order: the node numbering inside each colour -- "rcm" (seeded permutation, then reverse
+    Cuthill-McKee) or "morton" (Z-order of the (i, j, k) index triple: a cache-oblivious
+    renumbering for locality, so the neighbours a row gathers were touched recently by the
+    rows around it).  On a 2-colour ordering the ILU(0) entries do not depend on the order
+    inside a colour (only the summation order of each row's Schur update does).
 
     device: compute the dual geometry (per-cell dual-face normals, their per-edge sums,
     node volumes) with the sm_100a kernels of csrc/meshgen.cu (bitwise equal to the host
@@ -404,14 +419,19 @@ def structured_sector(ci, cj, ck, *, geometry="annular", length=2.0, pitch_deg=1
     if periodic_j and not tets:
         assert cj % 2 == 0, "periodic 2-colouring needs an even pitch count"
 
-    # ordering: seeded permutation -> RCM -> colour-major (stable)
+    # ordering: seeded permutation -> RCM (or Morton) -> colour-major (stable)
     perm0 = rng.permutation(n) if permute else np.arange(n)        # perm0[new] = old
-    inv0 = np.empty(n, np.int64)
-    inv0[perm0] = np.arange(n)
-    ra, rb = inv0[ea], inv0[eb]
-    rcm = rcm_order(n, ra, rb, device)                               # rcm[pos] = permuted id
-    rank = np.empty(n, np.int64)
-    rank[perm0[rcm]] = np.arange(n)                                  # rank[old] = RCM position
+    if order == "morton":
+        rank = morton_key(In.reshape(-1), Jn.reshape(-1), Kn.reshape(-1))  # rank[old], gid order
+    elif order == "rcm":
+        inv0 = np.empty(n, np.int64)
+        inv0[perm0] = np.arange(n)
+        ra, rb = inv0[ea], inv0[eb]
+        rcm = rcm_order(n, ra, rb, device)                           # rcm[pos] = permuted id
+        rank = np.empty(n, np.int64)
+        rank[perm0[rcm]] = np.arange(n)                              # rank[old] = RCM position
+    else:
+        raise ValueError(f"unknown node order {order!r}")
     order = np.lexsort((rank, col))                                  # order[new] = old
     new = np.empty(n, np.int64)
     new[order] = np.arange(n)

@@ -12,8 +12,10 @@ summation order; partial reconstructions are never all-reduced).
 
 The reference runs the same decomposition on host threads (`workers`,
 driver.cpp:246-265): every harmonic runs, successful ones are committed, and the first
-error by harmonic index is rethrown.  Here a failing rank's error is broadcast and raised
-on every rank after the exchange, so all ranks leave the iteration in the same state.
+error by harmonic index is rethrown.  Here every owner's field is broadcast even when a
+rank failed, and the error of the lowest failing harmonic (FnlhError, original code) is
+raised on every rank after the exchange, so all ranks leave the iteration in the same
+state.
 
 `solver` is anything with phase_harmonics / harmonic_reports / phase_mean and either
 copy_amps (device solver: FnlhSolver, fields staged through a torch CUDA buffer) or
@@ -48,8 +50,13 @@ class HarmonicShards:
         src = owner(h, self.world)
         if self._buf is not None:  # device fields: stage through one buffer, NCCL broadcast
             if self.rank == src:
-                self.s.copy_amps(h, self._buf.data_ptr(), True)
+                self.s.copy_amps(h, self._buf.data_ptr(), True)  # returns once _buf holds the field
             dist.broadcast(self._buf, src=src, group=self.group)
+            # dist.broadcast only orders torch's current stream after the collective; the
+            # library copies on its own stream, so wait here: the receiver must not read _buf
+            # before the data lands, the sender must not overwrite it (next harmonic) while
+            # NCCL still reads it
+            torch.cuda.current_stream(self._buf.device).synchronize()
             if self.rank != src:
                 self.s.copy_amps(h, self._buf.data_ptr(), False)
         else:
@@ -60,22 +67,32 @@ class HarmonicShards:
                 self.s.put_amps(h, t.numpy().view("complex128"))
 
     def outer_iteration(self):
+        """phase_harmonics on the owned harmonics, exchange, phase_mean.  Errors follow the
+        reference's workers (driver.cpp:246-265): every harmonic runs, the owner's field of
+        every harmonic (committed or, on the sequential path, left untouched) is broadcast so
+        all ranks stay identical, and every rank raises the error of the lowest failing
+        harmonic index with its original code / node / stage."""
         err = None
         h_norm = None
         try:
             h_norm = self.s.phase_harmonics(self.owned)
         except Exception as ex:  # captured, agreed on below (driver.cpp:248-264)
-            err = f"{type(ex).__name__}: {ex}"
+            fh = self.s.failed_harmonic() if hasattr(self.s, "failed_harmonic") else -1
+            err = (fh, getattr(ex, "code", 7), str(ex), getattr(ex, "node", -1), getattr(ex, "stage", -1),
+                   type(ex).__name__)
         mine = {h: (float(h_norm[h]), self.s.harmonic_reports(h)) for h in range(self.nh)
                 if self.owned[h]} if err is None else {}
         gathered = [None] * self.world
         dist.all_gather_object(gathered, (err, mine), group=self.group)
-        errors = [(r, e) for r, (e, _) in enumerate(gathered) if e is not None]
-        for h in range(self.nh):  # fields of every harmonic current on every rank
-            if gathered[owner(h, self.world)][0] is None:
-                self._exchange_field(h)
-        if errors:
-            raise RuntimeError(f"harmonic shard failed on rank {errors[0][0]}: {errors[0][1]}")
+        for h in range(self.nh):  # every field current on every rank, failing ranks included
+            self._exchange_field(h)
+        errors = [e for e, _ in gathered if e is not None]
+        if errors:  # errors before the harmonics (-1) are the same on every rank and come first
+            fh, code, msg, node, stage, kind = min(errors, key=lambda e: e[0])
+            from ._lib import FnlhError
+            e = FnlhError(code, f"harmonic shard (harmonic {fh}): {msg}", node, stage)
+            e.harmonic = fh
+            raise e
         norms, reports = [0.0] * self.nh, [[] for _ in range(self.nh)]
         for _, m in gathered:
             for h, (nv, reps) in m.items():

@@ -182,6 +182,12 @@ class FnlhSolver:
         check(lib().fnlh_solver_phase_harmonics(self.h, ptr(own), ptr(hn)))
         return hn[: self.nh].copy()
 
+    def failed_harmonic(self):
+        """Harmonic whose error the last phase_harmonics raised (-1: none / before the harmonics)."""
+        h = _i()
+        check(lib().fnlh_solver_failed_harmonic(self.h, C.byref(h)))
+        return h.value
+
     def harmonic_reports(self, h):
         arr = (LinearReport * 256)()
         n = _i()

@@ -73,3 +73,13 @@ def rel(a, b):
 
 
 NOZZLE_CASE = "kind = nozzle-euler\nnx = {nx}\nharmonics = {nh}\nbase_omega = 500\n"
+
+
+def assert_reports_match(ra, rb, tol=1e-14):
+    """Linear-solve reports of two runs whose harmonics ran in different lane batches: the
+    iteration counts and convergence flags equal, the norms to `tol` (the 2-colour sweep sums
+    its CTA partials over row blocks whose size depends on the lane count, rb.cuh)."""
+    assert len(ra) == len(rb)
+    assert [(r[0], r[3]) for r in ra] == [(r[0], r[3]) for r in rb]
+    for a, b in zip(ra, rb):
+        assert abs(a[1] - b[1]) <= tol * abs(a[1]) and abs(a[2] - b[2]) <= tol * abs(a[2]), (a, b)
