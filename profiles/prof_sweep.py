@@ -14,7 +14,8 @@ args = sys.argv[1:]
 scale = float(args[0]) if args and args[0][0].isdigit() else 1.0
 P = int(args[args.index("--batch") + 1]) if "--batch" in args else 1
 case = args[args.index("--case") + 1] if "--case" in args else "c2"
-c = make_case(case, scale=scale, workers=P)
+kw = {"order": args[args.index("--order") + 1]} if "--order" in args else {}
+c = make_case(case, scale=scale, workers=P, **kw)
 s = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
 if "--step" in args:
     s.outer_iteration()
