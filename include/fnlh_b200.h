@@ -94,6 +94,40 @@ int fnlh_smoothed_solve(const fnlh_pattern* p, int is_complex, const double* A, 
                         const double* shift_im, const double* rhs, double tol_rel, int max_iter, double* x,
                         fnlh_linear_report* rep);
 
+/* ---- L1, persistent operator handles (the drop-in at the reference's call sites) ----
+   The reference builds A5 once per outer iteration and, per harmonic worker, factorizes
+   once per harmonic (driver.cpp:213-216: build_lhs_harmonic + Ilu::factorize) and then
+   solves once per RK stage with the same factors (rk.cpp:82-85: smoothed_solve).  These
+   handles keep that structure on the device: the LHS is uploaded once, each worker's
+   factors stay resident in its own workspace, and a stage solve moves only rhs and x.
+
+   fnlh_lhs    the shared real LHS (J / A5: Bsr<real>, sparse.hpp:136-157) on a pattern,
+               resident in HBM in the layouts the kernels read (2-colour SELL-32, or BSR +
+               sliced copy).  fnlh_lhs_upload replaces the values (reference BSR layout,
+               nnzb*b*b doubles).  Replaces the Bsr<real> A5 of driver.cpp:67,179-181.
+   fnlh_prec   one worker's Ilu<S> workspace (sparse.cpp:187-257; the per-worker Ilu of
+               driver.cpp:117) on an fnlh_lhs: fnlh_prec_factorize factorizes A (real,
+               shift_im NULL) or the harmonic operator A + i diag(shift_im) (complex; the
+               reference's build_lhs_harmonic -> shift_diagonal -> factorize, rk.cpp:32-39,
+               sparse.cpp:157-171), the complex matrix never materialized.
+   fnlh_richardson  smoothed_solve<S, Ilu<S>> (sparse.hpp:295-331) on the prec's operator
+               and factors: host rhs / x (BlockVec layout, complex interleaved), x0 = 0.
+   *_bytes     device bytes held, for the reference's LHS accounting
+               (detail::lhs_alloc_register / lhs_alloc_release, sparse.hpp:34-37).
+   Handles are not shared between concurrent calls except the read-only fnlh_lhs, which
+   any number of precs (host threads) may use at once. */
+typedef struct fnlh_lhs fnlh_lhs;
+typedef struct fnlh_prec fnlh_prec;
+int fnlh_lhs_create(const fnlh_pattern* p, fnlh_lhs** out);
+int fnlh_lhs_upload(fnlh_lhs* A, const double* vals);
+int fnlh_lhs_bytes(const fnlh_lhs* A, long long* bytes);
+void fnlh_lhs_destroy(fnlh_lhs* A);
+int fnlh_prec_create(const fnlh_lhs* A, int is_complex, fnlh_prec** out);
+int fnlh_prec_factorize(fnlh_prec* f, const double* shift_im);
+int fnlh_prec_bytes(const fnlh_prec* f, long long* bytes);
+void fnlh_prec_destroy(fnlh_prec* f);
+int fnlh_richardson(fnlh_prec* f, const double* rhs, double tol_rel, int max_iter, double* x, fnlh_linear_report* rep);
+
 /* 2-colour fast path (rb.cuh): *n0 = size of colour 0 when the pattern is a colour-major
    2-colour ordering with one partition, else -1.  fnlh_set_red_black(0) forces the general
    level-scheduled kernels everywhere.  fnlh_set_rb_sweep selects the 2-colour sweep:

@@ -7,17 +7,10 @@
 #include "capi_util.hpp"
 #include "la.cuh"
 #include "rb.cuh"
+#include "capi_types.hpp"
 
 using namespace fnlh;
 
-// rb / n0 are decided once in fnlh_pattern_create and read-only afterwards, so one pattern
-// handle may serve concurrent solves from several host threads (the shim's harmonic workers)
-struct fnlh_pattern {
-    std::unique_ptr<DevicePattern> p;
-    int rb = 0;  // 1: 2-colour colour-major ordering with one partition (rb.cuh)
-    int n0 = 0;
-    bool use_rb() const { return rb == 1 && fnlh::rb_enabled(); }
-};
 
 namespace {
 

@@ -145,3 +145,72 @@ def rb_factorize(pat: Pattern, A, shift_im=None):
     check(lib().fnlh_rb_factorize(pat.h, _i(1 if cplx else 0), ptr(f64(A)), ptr(None if shift_im is None else f64(shift_im)),
                                   ptr(v(dlu)), ptr(piv), ptr(v(inv0))))
     return dict(diag_lu=dlu, diag_piv=piv, inv0=inv0[: n0 * b * b], n0=n0)
+
+
+class Lhs:
+    """The shared real LHS (Bsr<real> A5, sparse.hpp:136-157) resident on the device
+    (include/fnlh_b200.h fnlh_lhs): uploaded once, read by any number of Ilu workspaces."""
+
+    def __init__(self, pat: Pattern, A=None):
+        self.pat = pat
+        h = C.c_void_p()
+        check(lib().fnlh_lhs_create(pat.h, C.byref(h)))
+        self.h = h
+        if A is not None:
+            self.upload(A)
+
+    def upload(self, A):
+        check(lib().fnlh_lhs_upload(self.h, ptr(f64(A))))
+
+    def bytes(self):
+        v = C.c_longlong()
+        check(lib().fnlh_lhs_bytes(self.h, C.byref(v)))
+        return v.value
+
+    def __del__(self):
+        try:
+            lib().fnlh_lhs_destroy(self.h)
+        except Exception:
+            pass
+
+
+class Ilu:
+    """One worker's Ilu<S> workspace on a device Lhs (fnlh_prec): factorize() for the real
+    operator (Ilu<real>, the mean flow), factorize(shift_im) for the harmonic operator
+    A5 + i diag(shift_im) (build_lhs_harmonic + Ilu<cplx>::factorize, driver.cpp:213-216);
+    solve() is smoothed_solve on the resident factors (rk.cpp:82-85)."""
+
+    def __init__(self, A: Lhs, is_complex: bool):
+        self.A = A
+        self.cplx = bool(is_complex)
+        h = C.c_void_p()
+        check(lib().fnlh_prec_create(A.h, _i(1 if is_complex else 0), C.byref(h)))
+        self.h = h
+
+    def factorize(self, shift_im=None):
+        sh = None if shift_im is None else f64(shift_im)
+        check(lib().fnlh_prec_factorize(self.h, ptr(sh)))
+
+    def solve(self, rhs, tol_rel, max_iter):
+        """-> (x, (iterations, initial norm, final norm, converged))"""
+        if self.cplx:
+            r = as_pairs(rhs)
+            x = np.zeros(len(r) // 2, np.complex128)
+        else:
+            r = f64(rhs)
+            x = np.zeros(len(r))
+        rep = LinearReport()
+        check(lib().fnlh_richardson(self.h, ptr(r), _d(tol_rel), _i(max_iter), ptr(x.view(np.float64)),
+                                    C.byref(rep)))
+        return x, rep.as_tuple()
+
+    def bytes(self):
+        v = C.c_longlong()
+        check(lib().fnlh_prec_bytes(self.h, C.byref(v)))
+        return v.value
+
+    def __del__(self):
+        try:
+            lib().fnlh_prec_destroy(self.h)
+        except Exception:
+            pass

@@ -126,3 +126,44 @@ def test_richardson_config_errors(meshes):
         assert e.value.kind == "ConfigError"
     x, rep = la.smoothed_solve(P, A, np.zeros(m.n), 0.1, 3)
     assert rep == (0, 0.0, 0.0, True) and not x.any()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scale,rb", [(0.1, True), (0.1, False)])
+def test_persistent_handles_stage_solves_bitwise(ref, scale, rb):
+    """fnlh_lhs / fnlh_prec / fnlh_richardson (the drop-in at driver.cpp:213-216 and
+    rk.cpp:82-85): A5 uploaded once, one worker factorizes A5 + i shift once and solves five
+    stage right-hand sides on the resident factors; every solve equals the reference's
+    smoothed_solve on the materialized complex operator bitwise (iterates, iteration counts)."""
+    from paper_2404_01407_b200 import la
+    from paper_2404_01407_b200.cases import make_case
+    c = make_case("c2", scale=scale)
+    pat = c.mesh.pattern()
+    rng = np.random.default_rng(7)
+    n, b = c.mesh.n, c.mesh.b
+    A = rng.standard_normal((len(pat["col_idx"]), b, b)) * 0.1
+    A[pat["diag_idx"]] += 4 * np.eye(b)
+    shift = rng.uniform(0.5, 2.0, n)
+    Az = A.astype(np.complex128)
+    Az[pat["diag_idx"]] += 1j * np.eye(b) * shift[:, None, None]
+    la.set_red_black(rb)
+    try:
+        P = la.Pattern.from_dict(pat)
+        L = la.Lhs(P, A.reshape(-1))
+        w = la.Ilu(L, True)
+        w.factorize(shift)
+        for k in range(5):
+            rhs = rng.standard_normal(n * b) + 1j * rng.standard_normal(n * b)
+            xd, rd = w.solve(rhs, 1e-3, 6)
+            xr, rr = ref.smoothed_solve(pat, Az.reshape(-1), rhs, 1e-3, 6)
+            assert np.array_equal(xd, xr) and rd[0] == rr[0] and rd[3] == rr[3], (k, rd, rr)
+            assert abs(rd[2] - rr[2]) <= 1e-14 * rr[2]
+        m = la.Ilu(L, False)
+        m.factorize()
+        rhs = rng.standard_normal(n * b)
+        xd, rd = m.solve(rhs, 1e-3, 6)
+        xr, rr = ref.smoothed_solve(pat, A.reshape(-1), rhs, 1e-3, 6)
+        assert np.array_equal(xd, xr) and rd[0] == rr[0]
+        assert L.bytes() > 0 and w.bytes() > m.bytes() > 0
+    finally:
+        la.set_red_black(True)
