@@ -145,3 +145,42 @@ def test_c4_full_size_memory_contract():
             assert math.isfinite(e["resid_mean"]) and math.isfinite(e["rz"]) and len(e["resid_h"]) == 10
         del g
     assert lhs[1] == lhs[10]
+
+
+def _used_bytes():
+    import torch
+    torch.cuda.synchronize()
+    free, total = torch.cuda.mem_get_info()
+    return total - free
+
+
+@pytest.mark.parametrize("workers,nh_pair", [(1, (1, 10)), (8, (8, 10))])
+def test_c4_measured_device_memory_contract(workers, nh_pair):
+    """The memory contract measured, not self-reported: device memory in use (cudaMemGetInfo)
+    after building the C4 solver and running one outer iteration, for two harmonic counts at
+    the same number of workspaces (workers = 1: the paper's single reused workspace; 8 lanes:
+    one workspace per lane, as the reference's workers).  The difference must be exactly the
+    per-harmonic state -- field N b complex + boundary forcing -- up to allocation
+    granularity: no LHS buffer grows with N_h."""
+    import gc
+    from paper_2404_01407_b200.solver import FnlhSolver
+    used, lhs, per_h = {}, {}, None
+    for nh in nh_pair:
+        gc.collect()
+        base = _used_bytes()
+        c = make_case("c4", nh=nh, workers=workers)
+        g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
+        g.outer_iteration()
+        used[nh] = _used_bytes() - base
+        lhs[nh] = g.lhs_bytes()
+        per_h = c.mesh.n * c.mesh.b * 16 + c.forcing.shape[1] * 16
+        del g
+        gc.collect()
+    lo, hi = nh_pair
+    grow = used[hi] - used[lo]
+    expect = (hi - lo) * per_h
+    print(f"workers={workers}: device bytes {used}, lhs {lhs}, growth {grow / 1e6:.1f} MB "
+          f"(per-harmonic state {expect / 1e6:.1f} MB)")
+    assert lhs[lo] == lhs[hi]
+    assert abs(grow - expect) <= 64 * 2**20, (grow, expect)  # allocation granularity
+    assert grow < 0.05 * lhs[lo]  # one complex workspace would be ~12 GB at C4
