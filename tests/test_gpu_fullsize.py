@@ -182,5 +182,4 @@ def test_c4_measured_device_memory_contract(workers, nh_pair):
     print(f"workers={workers}: device bytes {used}, lhs {lhs}, growth {grow / 1e6:.1f} MB "
           f"(per-harmonic state {expect / 1e6:.1f} MB)")
     assert lhs[lo] == lhs[hi]
-    assert abs(grow - expect) <= 64 * 2**20, (grow, expect)  # allocation granularity
-    assert grow < 0.05 * lhs[lo]  # one complex workspace would be ~12 GB at C4
+    assert abs(grow - expect) <= 64 * 2**20, (grow, expect)  # allocation granularity; a workspace is GBs
