@@ -61,6 +61,12 @@ const char* fnlh_pow_mode_info(void);
 double fnlh_pow(double x, double y);
 /* number of CUDA kernels this library has launched (monotonic) */
 long long fnlh_launch_count(void);
+/* Guard builds only (-DFNLH_GUARD, a measurement variant of the library): every device
+   buffer carries 4 KiB guard zones of 0xFF bytes on both sides (the reference's
+   CountedBuffer canaries, sparse.hpp:40-100); *bad_bytes = guard bytes overwritten so far
+   (live buffers and freed ones), *blocks = live guarded buffers.  Product builds return
+   FNLH_UNSUPPORTED. */
+int fnlh_guard_check(long long* bad_bytes, long long* blocks);
 
 /* ---- L1: block-sparse LA --------------------------------------------------- */
 

@@ -36,7 +36,7 @@ def _compile(src, headers, verbose, obj_dir=OBJ, extra=()):
         return obj, False
     cmd = [NVCC] + ARCH + COMMON + list(extra) + ["-c", src, "-o", obj]
     if src.endswith(".cpp"):
-        cmd = [NVCC] + COMMON + ["-x", "c++", "-c", src, "-o", obj]
+        cmd = [NVCC] + COMMON + list(extra) + ["-x", "c++", "-c", src, "-o", obj]
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -63,6 +63,15 @@ def build(verbose: bool = False, lib: str = LIB, obj_dir: str = OBJ, extra=()) -
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     return lib
+
+
+GUARD_LIB = os.path.join(HERE, "libfnlh_b200_guard.so")
+
+
+def build_guard(verbose: bool = False) -> str:
+    """The guard build (guard.cpp, -DFNLH_GUARD): the same sources with guard zones around
+    every device buffer, run by tests/test_gpu_guard.py in place of a sanitizer."""
+    return build(verbose, lib=GUARD_LIB, obj_dir=os.path.join(HERE, "build", "obj_guard"), extra=("-DFNLH_GUARD",))
 
 
 if __name__ == "__main__":

@@ -61,7 +61,7 @@ struct DeviceBuffer {
     std::size_t n = 0;
     DeviceBuffer() = default;
     explicit DeviceBuffer(std::size_t count) { alloc(count); }
-    ~DeviceBuffer() { cudaFree(ptr); }
+    ~DeviceBuffer() { fnlh::dfree(ptr); }
     DeviceBuffer(const DeviceBuffer&) = delete;
     DeviceBuffer& operator=(const DeviceBuffer&) = delete;
     DeviceBuffer(DeviceBuffer&& o) noexcept : ptr(o.ptr), n(o.n) {
@@ -70,7 +70,7 @@ struct DeviceBuffer {
     }
     DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
         if (this != &o) {
-            cudaFree(ptr);
+            fnlh::dfree(ptr);
             ptr = o.ptr;
             n = o.n;
             o.ptr = nullptr;
@@ -80,10 +80,10 @@ struct DeviceBuffer {
     }
     void alloc(std::size_t count) {
         if (count == n && ptr) return;
-        cudaFree(ptr);
+        fnlh::dfree(ptr);
         ptr = nullptr;
         n = count;
-        FNLH_CUDA(cudaMalloc(&ptr, std::max<std::size_t>(count, 1) * sizeof(T)));
+        FNLH_CUDA_ALLOC(&ptr, std::max<std::size_t>(count, 1) * sizeof(T));
     }
     void upload(const T* h, std::size_t count) {
         alloc(count);

@@ -26,6 +26,8 @@ namespace fnlh {
             throw ::fnlh::CudaError(std::string(#call) + ": " + cudaGetErrorString(err__));        \
     } while (0)
 
+#define FNLH_CUDA_ALLOC(p, bytes) ::fnlh::dmalloc(p, bytes)
+
 struct CudaError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
@@ -36,6 +38,13 @@ struct CudaError : std::runtime_error {
 // threads driving distinct handles, another thread's legacy-stream traffic can otherwise
 // delay it past the first kernels.
 inline void legacy_sync() { FNLH_CUDA(cudaStreamSynchronize(cudaStreamLegacy)); }
+
+// every device allocation of the library (guard.cpp): cudaMalloc / cudaFree, or guarded
+// allocations in a -DFNLH_GUARD measurement build
+void dmalloc(void** p, std::size_t bytes);
+void dfree(void* p);
+template <class T>
+inline void dmalloc(T** p, std::size_t bytes) { dmalloc(reinterpret_cast<void**>(p), bytes); }
 
 // count of kernel launches issued by this library (bench.py "gpu_launches"); atomic: the
 // C ABI may be called concurrently from several host threads with distinct handles

@@ -938,11 +938,11 @@ DevicePattern::DevicePattern(int b_, int rows_, const int* row_ptr_, const int* 
             }
         }
         auto upl2 = [](long long** d, const std::vector<long long>& h) {
-            FNLH_CUDA(cudaMalloc(d, std::max<std::size_t>(h.size(), 1) * sizeof(long long)));
+            FNLH_CUDA_ALLOC(d, std::max<std::size_t>(h.size(), 1) * sizeof(long long));
             if (!h.empty()) FNLH_CUDA(cudaMemcpy(*d, h.data(), h.size() * sizeof(long long), cudaMemcpyHostToDevice));
         };
         auto up2 = [](int** d, const std::vector<int>& h) {
-            FNLH_CUDA(cudaMalloc(d, std::max<std::size_t>(h.size(), 1) * sizeof(int)));
+            FNLH_CUDA_ALLOC(d, std::max<std::size_t>(h.size(), 1) * sizeof(int));
             if (!h.empty()) FNLH_CUDA(cudaMemcpy(*d, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice));
         };
         upl2(&mbase, mb);
@@ -958,11 +958,11 @@ DevicePattern::DevicePattern(int b_, int rows_, const int* row_ptr_, const int* 
             br_[pos] = i;
         }
     auto up = [](int** d, const std::vector<int>& h) {
-        FNLH_CUDA(cudaMalloc(d, std::max<std::size_t>(h.size(), 1) * sizeof(int)));
+        FNLH_CUDA_ALLOC(d, std::max<std::size_t>(h.size(), 1) * sizeof(int));
         if (!h.empty()) FNLH_CUDA(cudaMemcpy(*d, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice));
     };
     auto upl = [](long long** d, const std::vector<long long>& h) {
-        FNLH_CUDA(cudaMalloc(d, std::max<std::size_t>(h.size(), 1) * sizeof(long long)));
+        FNLH_CUDA_ALLOC(d, std::max<std::size_t>(h.size(), 1) * sizeof(long long));
         if (!h.empty()) FNLH_CUDA(cudaMemcpy(*d, h.data(), h.size() * sizeof(long long), cudaMemcpyHostToDevice));
     };
     up(&row_ptr, h_row_ptr);
@@ -991,7 +991,7 @@ DevicePattern::DevicePattern(int b_, int rows_, const int* row_ptr_, const int* 
             ko[i + 1] = ko[i] + c;
         }
         upl(&kjo, ko);
-        FNLH_CUDA(cudaMalloc(&kj, std::max<long long>(ko[rows], 1) * sizeof(long long)));
+        FNLH_CUDA_ALLOC(&kj, std::max<long long>(ko[rows], 1) * sizeof(long long));
         if (rows) { ::fnlh::note_launch(); k_build_kj<<<nblocks(rows), kThreads>>>(dev(*this), kj); }
         FNLH_CUDA(cudaGetLastError());
     }
@@ -999,26 +999,26 @@ DevicePattern::DevicePattern(int b_, int rows_, const int* row_ptr_, const int* 
 }
 
 DevicePattern::~DevicePattern() {
-    cudaFree(row_ptr);
-    cudaFree(col_idx);
-    cudaFree(diag_idx);
-    cudaFree(part);
-    cudaFree(fwd_rows);
-    cudaFree(bwd_rows);
+    fnlh::dfree(row_ptr);
+    fnlh::dfree(col_idx);
+    fnlh::dfree(diag_idx);
+    fnlh::dfree(part);
+    fnlh::dfree(fwd_rows);
+    fnlh::dfree(bwd_rows);
     for (void* q : {(void*)ent, (void*)lbase, (void*)ubase, (void*)lcolb, (void*)ucolb, (void*)nlow, (void*)nup,
                     (void*)lcols, (void*)ucols, (void*)dpos, (void*)blk_e, (void*)blk_row, (void*)mbase,
                     (void*)mcolb, (void*)mcols, (void*)mblk_e, (void*)kjo, (void*)kj})
-        cudaFree(q);
+        fnlh::dfree(q);
 }
 
 template <class S>
 DeviceIlu<S>::DeviceIlu(const DevicePattern* pat) : p(pat) {
     const std::size_t bb = (std::size_t)p->b * p->b;
     const std::size_t dr = (std::size_t)p->n_dslices * 32;
-    FNLH_CUDA(cudaMalloc(&vals, std::max<std::size_t>(p->sell_elems, 1) * sizeof(S)));
-    FNLH_CUDA(cudaMalloc(&diag_lu, std::max<std::size_t>(dr * bb, 1) * sizeof(S)));
-    FNLH_CUDA(cudaMalloc(&diag_piv, std::max<std::size_t>(dr * p->b, 1) * sizeof(int)));
-    FNLH_CUDA(cudaMalloc(&diag_inv, (std::size_t)p->rows * bb * sizeof(S)));
+    FNLH_CUDA_ALLOC(&vals, std::max<std::size_t>(p->sell_elems, 1) * sizeof(S));
+    FNLH_CUDA_ALLOC(&diag_lu, std::max<std::size_t>(dr * bb, 1) * sizeof(S));
+    FNLH_CUDA_ALLOC(&diag_piv, std::max<std::size_t>(dr * p->b, 1) * sizeof(int));
+    FNLH_CUDA_ALLOC(&diag_inv, (std::size_t)p->rows * bb * sizeof(S));
     // padding slots stay zero (never read as live entries)
     FNLH_CUDA(cudaMemset(vals, 0, std::max<std::size_t>(p->sell_elems, 1) * sizeof(S)));
     legacy_sync();
@@ -1026,10 +1026,10 @@ DeviceIlu<S>::DeviceIlu(const DevicePattern* pat) : p(pat) {
 
 template <class S>
 DeviceIlu<S>::~DeviceIlu() {
-    cudaFree(vals);
-    cudaFree(diag_lu);
-    cudaFree(diag_piv);
-    cudaFree(diag_inv);
+    fnlh::dfree(vals);
+    fnlh::dfree(diag_lu);
+    fnlh::dfree(diag_piv);
+    fnlh::dfree(diag_inv);
 }
 
 template <class S>
@@ -1070,22 +1070,22 @@ void DeviceIlu<S>::download(S* vals_out, S* diag_lu_out, int* diag_piv_out, S* d
 Workspace::Workspace(std::size_t max_len) : vec_len(max_len) {
     FNLH_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     n_partials = 32768;  // >= kMvBlocks * kMaxLanes + 2 kMaxLanes + 16
-    FNLH_CUDA(cudaMalloc(&partials, n_partials * sizeof(double)));
-    FNLH_CUDA(cudaMalloc(&scalars, 64 * sizeof(double)));
+    FNLH_CUDA_ALLOC(&partials, n_partials * sizeof(double));
+    FNLH_CUDA_ALLOC(&scalars, 64 * sizeof(double));
     FNLH_CUDA(cudaMallocHost(&h_scalars, 64 * sizeof(double)));
-    FNLH_CUDA(cudaMalloc(&status, 8 * sizeof(int)));
+    FNLH_CUDA_ALLOC(&status, 8 * sizeof(int));
     FNLH_CUDA(cudaMallocHost(&h_status, 8 * sizeof(int)));
     FNLH_CUDA(cudaMallocHost(&h_flags, 2 * kMaxLanes * sizeof(int)));
     for (auto& e : flag_ev) FNLH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    for (auto& v : vec) FNLH_CUDA(cudaMalloc(&v, std::max<std::size_t>(max_len, 1) * sizeof(cplx)));
+    for (auto& v : vec) FNLH_CUDA_ALLOC(&v, std::max<std::size_t>(max_len, 1) * sizeof(cplx));
 }
 
 Workspace::~Workspace() {
-    for (auto& v : vec) cudaFree(v);
-    cudaFree(partials);
-    cudaFree(scalars);
+    for (auto& v : vec) fnlh::dfree(v);
+    fnlh::dfree(partials);
+    fnlh::dfree(scalars);
     cudaFreeHost(h_scalars);
-    cudaFree(status);
+    fnlh::dfree(status);
     cudaFreeHost(h_status);
     cudaFreeHost(h_flags);
     for (auto& e : flag_ev)

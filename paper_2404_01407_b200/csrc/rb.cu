@@ -907,15 +907,15 @@ bool rb_eligible(const DevicePattern& p, int* n0) {
 template <class S>
 RbIlu<S>::RbIlu(const DevicePattern* pat, int n0_) : p(pat), n0(n0_) {
     const std::size_t bb = (std::size_t)p->b * p->b;
-    FNLH_CUDA(cudaMalloc(&diag_lu, packed_rows() * bb * sizeof(S)));
-    FNLH_CUDA(cudaMalloc(&diag_piv, packed_rows() * p->b * sizeof(int)));
-    FNLH_CUDA(cudaMalloc(&inv0, std::max<std::size_t>((std::size_t)n0 * bb, 1) * sizeof(S)));
+    FNLH_CUDA_ALLOC(&diag_lu, packed_rows() * bb * sizeof(S));
+    FNLH_CUDA_ALLOC(&diag_piv, packed_rows() * p->b * sizeof(int));
+    FNLH_CUDA_ALLOC(&inv0, std::max<std::size_t>((std::size_t)n0 * bb, 1) * sizeof(S));
 }
 template <class S>
 RbIlu<S>::~RbIlu() {
-    cudaFree(diag_lu);
-    cudaFree(diag_piv);
-    cudaFree(inv0);
+    fnlh::dfree(diag_lu);
+    fnlh::dfree(diag_piv);
+    fnlh::dfree(inv0);
 }
 template <class S>
 std::size_t RbIlu<S>::bytes() const {

@@ -1,7 +1,8 @@
 """Full-size, full-length parity of the outer iteration against the CPU restatement (whose
 linear algebra is bitwise the reference's): BASELINE C1 (20 pseudo-steps) and C2 (50), the
 device path as bench.py runs it (C2: 3 harmonic lanes), the restatement with the
-reference's harmonic worker threads.  Prints per-step relative differences of the mean and
+reference's harmonic worker threads.  The device solver runs as bench.py builds it:
+workers = min(N_h, 8) harmonic lanes.  Prints per-step relative differences of the mean and
 harmonic residual norms, the linear-iteration counts, and the final state difference.
 Usage: python profiles/parity_long.py [c1 c2 c3:2 c4:1:3 ...]   (name[:steps[:oracle
 workers]], default the BASELINE step count and one worker per harmonic)"""
@@ -27,7 +28,8 @@ def rel(a, b):
 for arg in (sys.argv[1:] or ["c1", "c2"]):
     name, _, rest = arg.partition(":")
     k, _, w = rest.partition(":")  # name[:steps[:oracle workers]] (C4: each worker holds 24 GB)
-    c = make_case(name, workers=3)
+    c = make_case(name)
+    c = make_case(name, workers=min(len(c.omegas), 8))  # the bench's harmonic lanes
     c.pseudo_steps = int(k) if k else c.pseudo_steps
     nw = int(w) if w else min(len(c.omegas), os.cpu_count() or 1)
     g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
@@ -45,7 +47,7 @@ for arg in (sys.argv[1:] or ["c1", "c2"]):
     mg, ag = g.state()
     mo, ao = o.state()
     same_iters = [r[0] for r in g.reports()] == [r[0] for r in o.reports()]
-    print(json.dumps(dict(case=name, nodes=c.mesh.n, steps=c.pseudo_steps, max_rel_resid_mean=worst_m,
+    print(json.dumps(dict(case=name, nodes=c.mesh.n, steps=c.pseudo_steps, device_lanes=g.lanes(), oracle_workers=nw, max_rel_resid_mean=worst_m,
                           max_rel_rz=worst_z, final_mean_rel=rel(mg, mo), final_amps_rel=rel(ag, ao),
                           identical_linear_iteration_counts=same_iters, wall_s=round(time.time() - t0, 1))),
           flush=True)
