@@ -309,6 +309,13 @@ int fnlh_make_pattern(int rows, long long n_edges, const int* ea, const int* eb,
    scipy.sparse.csgraph.reverse_cuthill_mckee(graph, symmetric_mode=True) (the ordering step
    of the configurations' mesh generator).  Degrees must be <= 255. */
 int fnlh_rcm(int n, const int* row_ptr, const int* col_idx, const int* starts, int* perm);
+/* Greedy colouring of the graph of a CSR pattern (Jones-Plassmann rounds on the device):
+   colour[i] in [0, *ncolours), no two neighbours share a colour, at most 64 colours.
+   Deterministic for a given seed (node priorities from splitmix64(seed + i)); equal to
+   mesh.py::greedy_colouring.  Meshes without a structural colouring get a colour-major
+   ordering from it (each colour one ILU(0) level: the level-scheduled path's levels). */
+int fnlh_greedy_colour(int n, const int* row_ptr, const int* col_idx, unsigned long long seed, int* colour,
+                       int* ncolours);
 /* Mesh::build_adjacency (mesh.cpp:44-59) and the derived arrays of mesh.py::from_faces on
    the device: per face (fa, fb = -1 on boundary faces, fn [nf][3]) the area, unit normal
    and viscous weight area / |x_fb - x_fa| (0 on boundary faces or without coords); per

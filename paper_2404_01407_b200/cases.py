@@ -78,7 +78,8 @@ def make_case(name: str, scale: float = 1.0, nh: int | None = None, implicit: bo
     nt_in = 1e-3 if b == 6 else 0.0
     m = structured_sector(ci, cj, ck, geometry=spec["geometry"], periodic_j=spec["periodic_j"], tets=spec["tets"],
                           jitter=spec.get("jitter", 0.0), seed=spec["seed"], b=b, permute=permute, gas=gas,
-                          nt_in=nt_in, mu_range=spec.get("mu_range"), device=device, order=spec.get("order", "rcm"))
+                          nt_in=nt_in, mu_range=spec.get("mu_range"), device=device, order=spec.get("order", "rcm"),
+                          colouring=spec.get("colouring", "structural"))
     n = m.n
     W = np.zeros((n, b))
     W[:, 0] = 1.0 * (1.0 + 0.01 * rng.uniform(-1, 1, n))

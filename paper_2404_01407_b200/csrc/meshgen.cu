@@ -427,6 +427,52 @@ __global__ void k_rcm_start(int v, long long base, long long* __restrict__ pos, 
     frontier[0] = v;
 }
 
+
+// ---- greedy colouring (Jones-Plassmann) -------------------------------------
+// Priority of node i: the high 32 bits of splitmix64(seed + i) above the node id, so every
+// priority is distinct.  One round: an uncoloured node whose priority exceeds that of every
+// uncoloured neighbour takes the smallest colour no coloured neighbour holds.  Colours are
+// read from the previous round's array (double buffer): the result does not depend on
+// thread timing, and mesh.py::greedy_colouring restates it exactly on the host.
+__host__ __device__ inline unsigned long long jp_priority(int i, unsigned long long seed) {
+    unsigned long long z = seed + (unsigned long long)(unsigned int)i * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return (z & 0xFFFFFFFF00000000ull) | (unsigned long long)(unsigned int)i;
+}
+__global__ void k_jp_round(int n, const int* __restrict__ row_ptr, const int* __restrict__ col_idx,
+                           unsigned long long seed, const int* __restrict__ colour, int* __restrict__ colour_next,
+                           int* __restrict__ remaining, int* __restrict__ overflow) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int ci_ = colour[i];
+    if (ci_ >= 0) {
+        colour_next[i] = ci_;
+        return;
+    }
+    const unsigned long long pi = jp_priority(i, seed);
+    unsigned long long used = 0;
+    bool top = true;
+    for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+        const int j = col_idx[e];
+        if (j == i) continue;
+        const int cj = colour[j];
+        if (cj >= 0) {
+            if (cj < 64) used |= 1ull << cj;
+        } else if (jp_priority(j, seed) > pi) {
+            top = false;
+        }
+    }
+    if (top) {
+        const int c = __ffsll((long long)~used) - 1;
+        if (c < 0) atomicExch(overflow, 1);
+        colour_next[i] = c < 0 ? 63 : c;
+    } else {
+        colour_next[i] = -1;
+        atomicAdd(remaining, 1);
+    }
+}
 }  // namespace fnlh
 
 using namespace fnlh;
@@ -671,6 +717,36 @@ int fnlh_mesh_derive(int n, int nf, const int* fa, const int* fb, const double* 
         download(nf_idx, nidx.ptr, (std::size_t)total);
         download(closure, cl.ptr, 3LL * n);
         download(bflag, bf.ptr, n);
+    });
+}
+
+int fnlh_greedy_colour(int n, const int* row_ptr, const int* col_idx, unsigned long long seed, int* colour,
+                       int* ncolours) {
+    return guarded([&] {
+        if (n < 1) throw ShapeError("greedy_colour: n must be >= 1");
+        const long long nnz = row_ptr[n];
+        DeviceBuffer<int> rp, ci, c0(n), c1(n), rem(1), ovf(1);
+        rp.upload(row_ptr, (std::size_t)n + 1);
+        ci.upload(col_idx, (std::size_t)nnz);
+        FNLH_CUDA(cudaMemset(c0.ptr, 0xff, n * sizeof(int)));
+        FNLH_CUDA(cudaMemset(ovf.ptr, 0, sizeof(int)));
+        int left = n, rounds = 0;
+        while (left > 0) {
+            FNLH_CUDA(cudaMemset(rem.ptr, 0, sizeof(int)));
+            note_launch();
+            k_jp_round<<<nb(n), kT>>>(n, rp.ptr, ci.ptr, seed, c0.ptr, c1.ptr, rem.ptr, ovf.ptr);
+            FNLH_CUDA(cudaGetLastError());
+            std::swap(c0.ptr, c1.ptr);
+            FNLH_CUDA(cudaMemcpy(&left, rem.ptr, sizeof(int), cudaMemcpyDeviceToHost));
+            if (++rounds > n) throw std::runtime_error("greedy_colour: no progress");
+        }
+        int over = 0;
+        FNLH_CUDA(cudaMemcpy(&over, ovf.ptr, sizeof(int), cudaMemcpyDeviceToHost));
+        if (over) throw UnsupportedCaseError("greedy_colour: more than 64 colours");
+        download(colour, c0.ptr, (std::size_t)n);
+        int mx = -1;
+        for (int i = 0; i < n; ++i) mx = std::max(mx, colour[i]);
+        *ncolours = mx + 1;
     });
 }
 

@@ -306,6 +306,74 @@ def rcm_order(n, ea, eb, device=None):
     return np.asarray(reverse_cuthill_mckee(G, symmetric_mode=True), np.int64)
 
 
+def graph_csr(n, ea, eb):
+    """CSR adjacency + diagonal of the graph with edges (ea, eb): the host restatement of
+    make_pattern's structure (sparse.cpp:91-117), rows with ascending unique columns."""
+    a = np.asarray(ea, np.int64)
+    c = np.asarray(eb, np.int64)
+    rows = np.concatenate([np.arange(n), a, c])
+    cols = np.concatenate([np.arange(n), c, a])
+    key = np.unique(rows * n + cols)
+    rows = (key // n).astype(np.int32)
+    row_ptr = np.zeros(n + 1, np.int32)
+    np.cumsum(np.bincount(rows, minlength=n), out=row_ptr[1:])
+    return row_ptr, (key % n).astype(np.int32)
+
+
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def jp_priority(idx, seed):
+    """Jones-Plassmann node priorities: splitmix64(seed + i * golden) high 32 bits above the
+    node id (all distinct) -- meshgen.cu jp_priority, restated with wrapping uint64 math."""
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed) + np.asarray(idx, np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z ^= z >> np.uint64(31)
+    return (z & np.uint64(0xFFFFFFFF00000000)) | np.asarray(idx, np.uint64)
+
+
+def greedy_colouring(n, row_ptr, col_idx, seed=0x5EED, device=None):
+    """Greedy colouring by Jones-Plassmann rounds: an uncoloured node whose priority beats
+    every uncoloured neighbour's takes the smallest colour no coloured neighbour holds
+    (colours of the previous round only).  On the device (fnlh_greedy_colour) when one is
+    present; the host loop below is its exact restatement (the checker)."""
+    if device is None:
+        device = _device_available()
+    rp = np.ascontiguousarray(row_ptr, np.int32)
+    ci = np.ascontiguousarray(col_idx, np.int32)
+    if device:
+        import ctypes as C
+        from ._lib import check, lib, ptr
+        out = np.empty(n, np.int32)
+        k = C.c_int()
+        check(lib().fnlh_greedy_colour(C.c_int(n), ptr(rp), ptr(ci), C.c_ulonglong(seed), ptr(out), C.byref(k)))
+        return out
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    off = ci != rows
+    rows, cols = rows[off], ci[off]
+    prio = jp_priority(np.arange(n), seed)
+    colour = np.full(n, -1, np.int64)
+    while (colour < 0).any():
+        unc = colour < 0
+        # the largest priority among each node's uncoloured neighbours (0: none)
+        nb_unc = unc[cols]
+        best = np.zeros(n, np.uint64)
+        np.maximum.at(best, rows[nb_unc], prio[cols[nb_unc]])
+        used = np.zeros(n, np.uint64)
+        col_nb = ~nb_unc
+        np.bitwise_or.at(used, rows[col_nb], np.left_shift(np.uint64(1), colour[cols[col_nb]].astype(np.uint64)))
+        top = unc & (prio > best)
+        u = used[top]
+        free = ~u & (u + np.uint64(1))  # lowest zero bit
+        c = np.round(np.log2(free.astype(np.float64))).astype(np.int64)
+        if (c >= 64).any() or (u == _M64).any():
+            raise RuntimeError("greedy_colouring: more than 64 colours")
+        colour[top] = c
+    return colour.astype(np.int32)
+
+
 def _sector_dual_device(Xu, ci, cj, ck, periodic_j, tets):
     """The same geometry from the sm_100a kernels (csrc/meshgen.cu, fnlh_sector_dual_*)."""
     import ctypes as C
@@ -340,7 +408,7 @@ def morton_key(i, j, k) -> np.ndarray:
 
 def structured_sector(ci, cj, ck, *, geometry="annular", length=2.0, pitch_deg=10.0, r_in=0.5, r_out=1.0,
                       width=1.0, height=0.5, periodic_j=False, tets=False, jitter=0.0, seed=0, b=5, permute=True,
-                      gas=None, nt_in=0.0, mu_range=None, device=None, order="rcm"):
+                      gas=None, nt_in=0.0, mu_range=None, device=None, order="rcm", colouring="structural"):
     """Hex (or Kuhn 6-tet) sector mesh, node-centred median dual.
 
     i: axial (inlet i=0, outlet i=ci), j: pitch, k: span/radius.  Walls (hub, casing,
@@ -352,6 +420,10 @@ def structured_sector(ci, cj, ck, *, geometry="annular", length=2.0, pitch_deg=1
     renumbering for locality, so the neighbours a row gathers were touched recently by the
     rows around it).  On a 2-colour ordering the ILU(0) entries do not depend on the order
     inside a colour (only the summation order of each row's Schur update does).
+
+    colouring: "structural" ((i+j+k) mod 2 for hex, the 8 Kuhn colours for tets) or "greedy":
+    the Jones-Plassmann colouring of the seeded-permuted node graph (greedy_colouring), as a
+    mesh without structured indices gets -- then colour-major with RCM inside each colour.
 
     device: compute the dual geometry (per-cell dual-face normals, their per-edge sums,
     node volumes) with the sm_100a kernels of csrc/meshgen.cu (bitwise equal to the host
@@ -421,6 +493,13 @@ def structured_sector(ci, cj, ck, *, geometry="annular", length=2.0, pitch_deg=1
 
     # ordering: seeded permutation -> RCM (or Morton) -> colour-major (stable)
     perm0 = rng.permutation(n) if permute else np.arange(n)        # perm0[new] = old
+    if colouring == "greedy":  # colours of the permuted graph, as an unstructured mesh has them
+        inv_p = np.empty(n, np.int64)
+        inv_p[perm0] = np.arange(n)
+        rp_, ci_ = graph_csr(n, inv_p[ea], inv_p[eb])
+        col = greedy_colouring(n, rp_, ci_, seed=seed + 1, device=device)[inv_p].astype(np.int32)
+    elif colouring != "structural":
+        raise ValueError(f"unknown colouring {colouring!r}")
     if order == "morton":
         rank = morton_key(In.reshape(-1), Jn.reshape(-1), Kn.reshape(-1))  # rank[old], gid order
     elif order == "rcm":
