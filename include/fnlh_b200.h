@@ -241,6 +241,21 @@ int fnlh_solver_phase_harmonics(fnlh_solver* s, const int* owned, double* h_norm
    index, driver.cpp:262-264), or -1 when it succeeded or failed before the harmonics; lets
    a sharded caller rethrow the lowest failing harmonic's error on every rank */
 int fnlh_solver_failed_harmonic(const fnlh_solver* s, int* h);
+/* deterministic_flux split over its quadrature points (residual_ops.cpp:145-160), so ranks
+   can share the nq residual evaluations and still sum them in the reference's k order:
+     df_points       nq (4 l_max + 2, or 1 when every frequency is 0)
+     df_terms        R(W(t_k)) for k in [k0, k1) into terms_dev ((k1-k0) * N*b doubles,
+                     device), from the solver's current mean and harmonic fields
+     df_accumulate   acc_dev += terms in order (first != 0: acc starts as terms[0], the
+                     reference's sum from k = 0); chained over consecutive ranges it equals
+                     the single-device sum bit for bit
+     set_external_df the next phase_mean takes DF = acc/nq - R(mean) from acc_dev (N*b
+                     doubles, device) instead of evaluating the quadrature itself
+   Each call synchronizes before it returns (the caller's collectives see finished data). */
+int fnlh_solver_df_points(fnlh_solver* s, int* nq);
+int fnlh_solver_df_terms(fnlh_solver* s, int k0, int k1, void* terms_dev);
+int fnlh_solver_df_accumulate(fnlh_solver* s, const void* terms_dev, int count, void* acc_dev, int first);
+int fnlh_solver_set_external_df(fnlh_solver* s, const void* acc_dev);
 /* linear reports of harmonic h from the last phase_harmonics (count in *n, at most max copied) */
 int fnlh_solver_harmonic_reports(const fnlh_solver* s, int h, fnlh_linear_report* out, int max, int* n);
 int fnlh_solver_phase_mean(fnlh_solver* s, const double* h_norm, const int* nrep, const fnlh_linear_report* reps,

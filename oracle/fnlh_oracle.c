@@ -890,6 +890,7 @@ struct or_solver {
     double* mean;   /* n*b */
     ocplx* amps;    /* nh*n*b */
     double* df;
+    const double* ext_acc; /* or_solver_set_external_df: the chained quadrature sum */
     double *J, *A5, *M, *MLU, *P, *PLU;
     int *Mpiv, *Ppiv;
     or_ilu_d ilu_mean;
@@ -1345,6 +1346,71 @@ int or_solver_harmonic_reports(const or_solver* s, int h, or_linear_report* out,
     return s->hrep[h].n;
 }
 
+/* deterministic_flux split over its quadrature points (shard.py), the restatement of
+   fnlh_solver_df_*: the same sums in the same k order as or_deterministic_flux */
+static int df_nq(const or_solver* s, double* base, int* lmax) {
+    *lmax = 0;
+    const int st = base_frequency(s->nh, s->omega, base, lmax);
+    if (st) return -st;
+    return *lmax == 0 ? 1 : 4 * *lmax + 2;
+}
+int or_solver_df_points(const or_solver* s) {
+    double base;
+    int lmax;
+    return df_nq(s, &base, &lmax);
+}
+int or_solver_df_terms(or_solver* s, int k0, int k1, double* terms) {
+    const or_mesh* m = &s->mesh;
+    const size_t len = (size_t)m->n * m->b;
+    double base;
+    int lmax;
+    const int nq = df_nq(s, &base, &lmax);
+    if (nq < 0) return -nq;
+    if (k0 < 0 || k1 > nq || k0 > k1) return or_fail(OR_SHAPE, -1, -1, "df_terms: range outside [0, nq)");
+    double* w = (double*)malloc(sizeof(double) * len);
+    int st = OR_OK;
+    const double period = lmax == 0 ? 0.0 : 2.0 * acos(-1.0) / base;
+    for (int k = k0; k < k1 && !st; ++k) {
+        const double t = lmax == 0 ? 0.0 : period * k / nq;
+        reconstruct(m->n, m->b, s->mean, s->nh, s->omega, s->amps, t, w);
+        st = or_residual(m, w, NULL, 2, 0, NULL, 0, 0, terms + (size_t)(k - k0) * len, NULL);
+    }
+    free(w);
+    return st;
+}
+void or_solver_df_accumulate(const or_solver* s, const double* terms, int count, double* acc, int first) {
+    const size_t len = (size_t)s->mesh.n * s->mesh.b;
+    if (first) memset(acc, 0, sizeof(double) * len);  /* the reference's zero-initialised acc */
+    for (int j = 0; j < count; ++j)
+        for (size_t q = 0; q < len; ++q) acc[q] += terms[(size_t)j * len + q];
+}
+void or_solver_set_external_df(or_solver* s, const double* acc) { s->ext_acc = acc; }
+
+static int df_from_acc(or_solver* s, const double* acc_in) {
+    const or_mesh* m = &s->mesh;
+    const size_t len = (size_t)m->n * m->b;
+    memset(s->df, 0, sizeof(double) * len);
+    double base;
+    int lmax;
+    const int nq = df_nq(s, &base, &lmax);
+    if (nq < 0) return -nq;
+    int any_amp = 0;
+    for (size_t k = 0; k < (size_t)s->nh * len && !any_amp; ++k)
+        if (s->amps[k] != 0) any_amp = 1;
+    if (!any_amp) return OR_OK;
+    double* acc = (double*)malloc(sizeof(double) * len);
+    double* inv = (double*)malloc(sizeof(double) * len);
+    memcpy(acc, acc_in, sizeof(double) * len);
+    if (lmax != 0)
+        for (size_t q = 0; q < len; ++q) acc[q] /= nq;
+    const int st = or_residual(m, s->mean, NULL, 2, 0, NULL, 0, 0, inv, NULL);
+    if (!st)
+        for (size_t q = 0; q < len; ++q) s->df[q] = acc[q] - inv[q];
+    free(acc);
+    free(inv);
+    return st;
+}
+
 int or_solver_phase_mean(or_solver* s, const double* hnorm, const int* nrep, const or_linear_report* reps,
                          or_entry* e, double* resid_h) {
     const or_mesh* m = &s->mesh;
@@ -1355,8 +1421,14 @@ int or_solver_phase_mean(or_solver* s, const double* hnorm, const int* nrep, con
     report_list hreps = {0};
     for (int h = 0, q = 0; h < nh; ++h)
         for (int k = 0; k < nrep[h]; ++k, ++q) reports_push(&hreps, &reps[q]);
-    /* deterministic flux from the fresh harmonic fields */
-    st = or_deterministic_flux(m, s->mean, nh, s->index, s->omega, s->amps, s->df);
+    /* deterministic flux from the fresh harmonic fields (or from a quadrature sum chained
+       across ranks: DF = acc / nq - R(mean), residual_ops.cpp:152-159) */
+    if (s->ext_acc) {
+        st = df_from_acc(s, s->ext_acc);
+        s->ext_acc = NULL;
+    } else {
+        st = or_deterministic_flux(m, s->mean, nh, s->index, s->omega, s->amps, s->df);
+    }
     if (st) {
         free(hreps.v);
         return st;

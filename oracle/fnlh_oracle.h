@@ -177,6 +177,11 @@ int or_solver_outer_iteration(or_solver* s, or_entry* e, double* resid_h);
 int or_solver_phase_harmonics(or_solver* s, const int* owned, double* hnorm_out);
 /* harmonic whose error the last phase_harmonics returned (-1: none / before the harmonics) */
 int or_solver_failed_harmonic(const or_solver* s);
+/* deterministic_flux split over quadrature points (the restatement of fnlh_solver_df_*) */
+int or_solver_df_points(const or_solver* s);
+int or_solver_df_terms(or_solver* s, int k0, int k1, double* terms);
+void or_solver_df_accumulate(const or_solver* s, const double* terms, int count, double* acc, int first);
+void or_solver_set_external_df(or_solver* s, const double* acc);
 /* harmonic worker threads (SchemeConfig::workers, driver.cpp:246-265), process-wide */
 void or_set_workers(int w);
 /* append a coarse multigrid level (explicit scheme): parent maps the current coarsest

@@ -316,6 +316,19 @@ class OracleSolver:
     def failed_harmonic(self):
         return self.o.lib.or_solver_failed_harmonic(_p(self.h))
 
+    # deterministic_flux split over quadrature points (host pointers)
+    def df_points(self):
+        return self.o.lib.or_solver_df_points(_p(self.h))
+
+    def df_terms(self, k0, k1, terms_ptr):
+        self.o._check(self.o.lib.or_solver_df_terms(_p(self.h), _i(k0), _i(k1), _p(terms_ptr)))
+
+    def df_accumulate(self, terms_ptr, count, acc_ptr, first):
+        self.o.lib.or_solver_df_accumulate(_p(self.h), _p(terms_ptr), _i(count), _p(acc_ptr), _i(1 if first else 0))
+
+    def set_external_df(self, acc_ptr):
+        self.o.lib.or_solver_set_external_df(_p(self.h), _p(acc_ptr))
+
     def harmonic_reports(self, h):
         arr = (OrReport * 256)()
         k = self.o.lib.or_solver_harmonic_reports(_p(self.h), _i(h), arr, _i(256))

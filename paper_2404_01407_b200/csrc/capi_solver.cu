@@ -195,6 +195,24 @@ int fnlh_solver_phase_harmonics(fnlh_solver* s, const int* owned, double* h_norm
     });
 }
 
+int fnlh_solver_df_points(fnlh_solver* s, int* nq) {
+    return guarded([&] { *nq = s->s->df_points(); });
+}
+
+int fnlh_solver_df_terms(fnlh_solver* s, int k0, int k1, void* terms_dev) {
+    return guarded([&] { s->s->df_terms(k0, k1, static_cast<double*>(terms_dev)); });
+}
+
+int fnlh_solver_df_accumulate(fnlh_solver* s, const void* terms_dev, int count, void* acc_dev, int first) {
+    return guarded([&] {
+        s->s->df_accumulate(static_cast<const double*>(terms_dev), count, static_cast<double*>(acc_dev), first != 0);
+    });
+}
+
+int fnlh_solver_set_external_df(fnlh_solver* s, const void* acc_dev) {
+    return guarded([&] { s->s->set_external_df(static_cast<const double*>(acc_dev)); });
+}
+
 int fnlh_solver_failed_harmonic(const fnlh_solver* s, int* h) {
     return guarded([&] { *h = s->s->failed_harmonic(); });
 }

@@ -1236,6 +1236,73 @@ void DeviceDisc::deterministic_flux(const double* mean, const std::vector<const 
     if (!deferred) raise_if_err(st, "deterministic_flux");
 }
 
+int DeviceDisc::df_points(const std::vector<double>& omega) {
+    double base;
+    int lmax;
+    base_frequency(omega, base, lmax);
+    return lmax == 0 ? 1 : 4 * lmax + 2;
+}
+
+void DeviceDisc::df_terms(const double* mean, const std::vector<const cplx*>& amps, const std::vector<double>& omega,
+                          int k0, int k1, double* terms, cudaStream_t st) {
+    const std::size_t L = len();
+    const int nh = static_cast<int>(amps.size());
+    if (nh > 64) throw ConfigError("deterministic_flux: at most 64 harmonics");
+    double base;
+    int lmax;
+    base_frequency(omega, base, lmax);
+    const int nq = lmax == 0 ? 1 : 4 * lmax + 2;
+    if (k0 < 0 || k1 > nq || k0 > k1) throw ShapeError("df_terms: quadrature range outside [0, nq)");
+    if (omega != df_omega_ || !df_ph_.ptr) {  // the same phase table deterministic_flux builds
+        std::vector<std::complex<double>> ph((std::size_t)nq * std::max(nh, 1));
+        const double period = lmax == 0 ? 0.0 : 2.0 * std::acos(-1.0) / base;
+        for (int k = 0; k < nq; ++k) {
+            const double t = lmax == 0 ? 0.0 : period * k / nq;
+            for (int h = 0; h < nh; ++h) ph[(std::size_t)k * nh + h] = std::exp(std::complex<double>(0.0, omega[h] * t));
+        }
+        FNLH_CUDA(cudaStreamSynchronize(st));
+        df_ph_.upload(reinterpret_cast<const cplx*>(ph.data()), ph.size());
+        df_omega_ = omega;
+    }
+    AmpList al{};
+    for (int h = 0; h < nh; ++h) al.a[h] = amps[h];
+    for (int k = k0; k < k1; ++k) {
+        { ::fnlh::note_launch(); k_reconstruct<<<nb((long long)L), kT, 0, st>>>(L, mean, al, nh, df_ph_.ptr + (std::size_t)k * nh, C().real[0].ptr); }
+        residual(C().real[0].ptr, nullptr, 2, 0, nullptr, 0, false, terms + (std::size_t)(k - k0) * L, nullptr, st);
+    }
+    FNLH_CUDA(cudaGetLastError());
+    raise_if_err(st, "deterministic_flux");
+}
+
+void DeviceDisc::df_accumulate(const double* terms, int count, double* acc, bool first, cudaStream_t st) {
+    const std::size_t L = len();
+    for (int j = 0; j < count; ++j) {
+        ::fnlh::note_launch();
+        k_accumulate<<<nb((long long)L), kT, 0, st>>>(L, terms + (std::size_t)j * L, acc, first && j == 0);
+    }
+    FNLH_CUDA(cudaGetLastError());
+}
+
+void DeviceDisc::df_finish(const double* mean, const std::vector<const cplx*>& amps, const std::vector<double>& omega,
+                           const double* acc, double* df, cudaStream_t st, bool deferred) {
+    const std::size_t L = len();
+    double base;
+    int lmax;
+    base_frequency(omega, base, lmax);
+    const int nq = lmax == 0 ? 1 : 4 * lmax + 2;
+    if (!df_flag_.ptr) df_flag_.alloc(1);
+    FNLH_CUDA(cudaMemsetAsync(df_flag_.ptr, 0, sizeof(int), st));
+    for (std::size_t h = 0; h < amps.size(); ++h) {
+        ::fnlh::note_launch();
+        k_any_nonzero<<<std::min(nb((long long)L), 592), kT, 0, st>>>(L, amps[h], df_flag_.ptr);
+    }
+    double* inv = C().real[1].ptr;
+    residual(mean, nullptr, 2, 0, nullptr, 0, false, inv, nullptr, st);
+    { ::fnlh::note_launch(); k_df_finish<<<nb((long long)L), kT, 0, st>>>(L, (double)nq, acc, inv, df, lmax == 0 ? 0 : 1, df_flag_.ptr); }
+    FNLH_CUDA(cudaGetLastError());
+    if (!deferred) raise_if_err(st, "deterministic_flux");
+}
+
 // ---------------------------------------------------------------------------
 template <class S>
 void stage_blend(double beta, const S* vf, S* vb, std::size_t len, cudaStream_t st) {

@@ -72,6 +72,19 @@ public:
                             const std::vector<double>& omega, double* df, cudaStream_t st, bool deferred = false,
                             const std::vector<cudaStream_t>& side = {});
 
+    // deterministic_flux in pieces, for quadrature points split across ranks
+    // (residual_ops.cpp:145-160): the number of points; the residuals R(W(t_k)) of points
+    // [k0, k1) into terms (k1-k0 vectors); their in-order sum into acc (first: acc = terms[0],
+    // the k = 0 start of the reference's sum); DF = acc / nq - R(mean) with the zero-amplitude
+    // rule.  Chaining df_accumulate over consecutive ranges in k order reproduces
+    // deterministic_flux bit for bit.  Errors throw (df_terms, df_finish synchronize).
+    int df_points(const std::vector<double>& omega);
+    void df_terms(const double* mean, const std::vector<const cplx*>& amps, const std::vector<double>& omega,
+                  int k0, int k1, double* terms, cudaStream_t st);
+    void df_accumulate(const double* terms, int count, double* acc, bool first, cudaStream_t st);
+    void df_finish(const double* mean, const std::vector<const cplx*>& amps, const std::vector<double>& omega,
+                   const double* acc, double* df, cudaStream_t st, bool deferred);
+
     const int* df_active() const { return df_flag_.ptr; }  // set by the last deterministic_flux
     // scratch contexts: the residual / linearized-residual temporaries of context k, so k
     // independent evaluations can run concurrently on k streams (harmonic lanes)

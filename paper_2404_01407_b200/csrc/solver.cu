@@ -827,6 +827,21 @@ void DeviceSolver::phase_harmonics(const int* owned) {
     }
 }
 
+int DeviceSolver::df_points() { return disc_->df_points(omega_); }
+
+void DeviceSolver::df_terms(int k0, int k1, double* terms) {
+    const std::size_t len = disc_->len();
+    std::vector<const cplx*> amps;
+    for (int h = 0; h < nh_; ++h) amps.push_back(amps_.ptr + (std::size_t)h * len);
+    disc_->df_terms(mean_.ptr, amps, omega_, k0, k1, terms, ws_->stream);
+    FNLH_CUDA(cudaStreamSynchronize(ws_->stream));
+}
+
+void DeviceSolver::df_accumulate(const double* terms, int count, double* acc, bool first) {
+    disc_->df_accumulate(terms, count, acc, first, ws_->stream);
+    FNLH_CUDA(cudaStreamSynchronize(ws_->stream));
+}
+
 ConvergenceEntry DeviceSolver::phase_mean(const std::vector<double>& h_norm,
                                           const std::vector<std::vector<LinearSolveReport>>& h_reps) {
     cudaStream_t st = ws_->stream;
@@ -843,7 +858,12 @@ ConvergenceEntry DeviceSolver::phase_mean(const std::vector<double>& h_norm,
     disc_->redirect_err(stage_err_.ptr + 10);
     std::vector<cudaStream_t> side;  // the lanes' streams take quadrature points concurrently
     for (std::size_t m = 1; m < lanes_.size(); ++m) side.push_back(lanes_[m]->stream);
-    disc_->deterministic_flux(mean_.ptr, amps, omega_, df_.ptr, st, /*deferred=*/true, side);
+    if (ext_df_acc_) {  // the quadrature sum chained across ranks (df_terms / df_accumulate)
+        disc_->df_finish(mean_.ptr, amps, omega_, ext_df_acc_, df_.ptr, st, /*deferred=*/true);
+        ext_df_acc_ = nullptr;
+    } else {
+        disc_->deterministic_flux(mean_.ptr, amps, omega_, df_.ptr, st, /*deferred=*/true, side);
+    }
     disc_->redirect_err(nullptr);
 
     FNLH_CUDA(cudaEventRecord(evp_[2], st));  // DF done

@@ -99,6 +99,14 @@ public:
     void phase_harmonics(const int* owned);
     // harmonic whose error the last phase_harmonics rethrew (-1: none, or an error before the harmonics)
     int failed_harmonic() const { return failed_h_; }
+    // deterministic_flux split over quadrature points (shard.py: ranks chain the in-order sum,
+    // residual_ops.cpp:145-160): the point count; R(W(t_k)) for k in [k0, k1) into device
+    // `terms`; their in-order sum into device `acc`; and acc as the DF source of the next
+    // phase_mean.  All synchronize before returning.
+    int df_points();
+    void df_terms(int k0, int k1, double* terms);
+    void df_accumulate(const double* terms, int count, double* acc, bool first);
+    void set_external_df(const double* acc) { ext_df_acc_ = acc; }
     const std::vector<double>& last_h_norm() const { return h_norm_; }
     const std::vector<std::vector<LinearSolveReport>>& last_h_reports() const { return h_reps_; }
     // ... then DF from every harmonic field, the mean RK step and the monitor, given every
@@ -203,6 +211,7 @@ private:
     std::vector<LinearSolveReport> reports_;
     int iter_ = 0;
     int failed_h_ = -1;
+    const double* ext_df_acc_ = nullptr;
     double cum_seconds_ = 0.0;
     cudaEvent_t ev0_, ev1_, evp_[3];
     cudaStream_t cs_ = nullptr;          // copy stream of outer_iteration_host

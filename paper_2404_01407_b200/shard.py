@@ -6,9 +6,11 @@ relaxed on rank h % world.  Each rank holds a replica of the mesh, A5, the mean 
 its own complex ILU workspace(s) (LHS bytes per rank independent of N_h).  The only
 exchange is the harmonic fields themselves, once per outer iteration, before the
 deterministic flux: one broadcast per harmonic from its owner over NCCL (NVLink /
-NVSwitch).  DF and the mean step then run redundantly, in the same order, on every rank,
-so every rank holds bitwise the same state as a single-GPU run (no reduction changes any
-summation order; partial reconstructions are never all-reduced).
+NVSwitch).  DF's nq quadrature residuals are then shared out in consecutive blocks of
+points and their sum is chained rank to rank in k order (one N b vector per hop, then one
+broadcast), and the mean step runs redundantly on every rank, so every rank holds bitwise
+the same state as a single-GPU run (no reduction changes any summation order; partial
+sums are never all-reduced).
 
 The reference runs the same decomposition on host threads (`workers`,
 driver.cpp:246-265): every harmonic runs, successful ones are committed, and the first
@@ -33,8 +35,9 @@ def owner(h: int, world: int) -> int:
 
 
 class HarmonicShards:
-    def __init__(self, solver, nh: int, field_len: int, group=None, device=None):
+    def __init__(self, solver, nh: int, field_len: int, group=None, device=None, split_df=True):
         self.s = solver
+        self.split_df = split_df and hasattr(solver, "df_terms")
         self.nh = nh
         self.group = group
         self.rank = dist.get_rank(group)
@@ -43,8 +46,10 @@ class HarmonicShards:
         self.device = device
         self.field_len = field_len  # complex entries per harmonic field (N * b)
         self._buf = None
+        self.tdev = torch.device(device or "cuda") if hasattr(solver, "copy_amps") else torch.device("cpu")
         if hasattr(solver, "copy_amps"):
-            self._buf = torch.empty(2 * field_len, dtype=torch.float64, device=device or "cuda")
+            self._buf = torch.empty(2 * field_len, dtype=torch.float64, device=self.tdev)
+        self._terms = self._acc = None
 
     def _exchange_field(self, h: int):
         src = owner(h, self.world)
@@ -97,4 +102,57 @@ class HarmonicShards:
         for _, m in gathered:
             for h, (nv, reps) in m.items():
                 norms[h], reports[h] = nv, reps
+        if self.split_df and self.world > 1:
+            self._deterministic_flux()
         return self.s.phase_mean(norms, reports)
+
+    def _sync(self):
+        if self.tdev.type == "cuda":
+            torch.cuda.current_stream(self.tdev).synchronize()
+
+    def _deterministic_flux(self):
+        """DF with its nq quadrature residuals shared out: rank r evaluates the consecutive
+        points [r K, (r+1) K) (fnlh_solver_df_terms), then the in-order sum is chained rank
+        to rank -- receive the running sum, add the own terms in k order, pass it on -- so it
+        is the reference's sequential sum (residual_ops.cpp:145-152) bit for bit; the last
+        rank broadcasts it and every rank finishes DF = acc / nq - R(mean) in phase_mean."""
+        nq = self.s.df_points()
+        K = -(-nq // self.world)
+        k0, k1 = min(nq, self.rank * K), min(nq, (self.rank + 1) * K)
+        L = self.field_len
+        if self._acc is None:
+            self._acc = torch.zeros(L, dtype=torch.float64, device=self.tdev)
+            self._terms = torch.empty(max(K, 1) * L, dtype=torch.float64, device=self.tdev)
+        err = None
+        try:
+            if k1 > k0:
+                self.s.df_terms(k0, k1, self._terms.data_ptr())
+        except Exception as ex:  # the lowest rank's error is the reference's first (lowest k)
+            err = (getattr(ex, "code", 7), str(ex), getattr(ex, "node", -1), getattr(ex, "stage", -1))
+        errs = [None] * self.world
+        dist.all_gather_object(errs, err, group=self.group)
+        bad = [e for e in errs if e is not None]
+        if bad:
+            from ._lib import FnlhError
+            code, msg, node, stage = bad[0]
+            raise FnlhError(code, f"deterministic_flux (sharded): {msg}", node, stage)
+        src = lambda r: dist.get_global_rank(self.group, r) if self.group is not None else r  # noqa: E731
+        # NCCL moves the device vector directly; gloo (tests) only does point to point on host tensors
+        wire = self._acc.cpu() if (self.tdev.type == "cuda" and dist.get_backend(self.group) == "gloo") else self._acc
+        if self.rank > 0:
+            dist.recv(wire, src=src(self.rank - 1), group=self.group)
+            if wire is not self._acc:
+                self._acc.copy_(wire)
+            self._sync()
+        if k1 > k0:
+            self.s.df_accumulate(self._terms.data_ptr(), k1 - k0, self._acc.data_ptr(), k0 == 0)
+        if wire is not self._acc:
+            wire.copy_(self._acc)
+        if self.rank < self.world - 1:
+            dist.send(wire, dst=src(self.rank + 1), group=self.group)
+            self._sync()
+        dist.broadcast(wire, src=src(self.world - 1), group=self.group)
+        if wire is not self._acc:
+            self._acc.copy_(wire)
+        self._sync()
+        self.s.set_external_df(self._acc.data_ptr())

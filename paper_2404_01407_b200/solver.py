@@ -182,6 +182,22 @@ class FnlhSolver:
         check(lib().fnlh_solver_phase_harmonics(self.h, ptr(own), ptr(hn)))
         return hn[: self.nh].copy()
 
+    # deterministic_flux split over quadrature points (shard.py; include/fnlh_b200.h)
+    def df_points(self):
+        nq = _i()
+        check(lib().fnlh_solver_df_points(self.h, C.byref(nq)))
+        return nq.value
+
+    def df_terms(self, k0, k1, terms_ptr):
+        check(lib().fnlh_solver_df_terms(self.h, _i(k0), _i(k1), C.c_void_p(terms_ptr)))
+
+    def df_accumulate(self, terms_ptr, count, acc_ptr, first):
+        check(lib().fnlh_solver_df_accumulate(self.h, C.c_void_p(terms_ptr), _i(count), C.c_void_p(acc_ptr),
+                                              _i(1 if first else 0)))
+
+    def set_external_df(self, acc_ptr):
+        check(lib().fnlh_solver_set_external_df(self.h, C.c_void_p(acc_ptr)))
+
     def failed_harmonic(self):
         """Harmonic whose error the last phase_harmonics raised (-1: none / before the harmonics)."""
         h = _i()
