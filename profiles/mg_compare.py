@@ -50,6 +50,11 @@ def run(name, scale, nh, scheme_over, drop, cap):
                 break
             orders.append([o, h["iter"] + 1, round(h["seconds"], 3)])
         out[f"{name}_orders"] = orders
+        # the lowest value reached and where, and how far the run climbed back from it
+        # (a residual that rises again after its minimum: the run is diverging slowly)
+        k_min = min(range(len(hist)), key=lambda q: hist[q][key])
+        out[f"{name}_min"] = [hist[k_min][key], k_min + 1, round(hist[k_min]["seconds"], 3)]
+        out[f"{name}_end_over_min"] = hist[-1][key] / max(hist[k_min][key], 1e-300)
     return out
 
 
@@ -61,6 +66,7 @@ def main():
     ap.add_argument("--drop", type=float, default=3.0)
     ap.add_argument("--max", type=int, default=4000)
     ap.add_argument("--cfl-explicit", type=float, default=1.0)
+    ap.add_argument("--max-implicit", type=int, default=0, help="iteration cap of the implicit arm (0: --max)")
     ap.add_argument("--arms", default="implicit,explicit_1grid,explicit_mg2,explicit_mg3")
     a = ap.parse_args()
     arms = {
@@ -73,7 +79,8 @@ def main():
     for k, v in arms.items():
         if k not in a.arms.split(","):
             continue
-        out[k] = run(a.case, a.scale, a.nh, v, a.drop, a.max)
+        cap = a.max_implicit if (k == "implicit" and a.max_implicit) else a.max
+        out[k] = run(a.case, a.scale, a.nh, v, a.drop, cap)
         print(k, json.dumps(out[k]), flush=True)
     print(json.dumps(dict(case=a.case, scale=a.scale, nh=a.nh, drop=a.drop, arms=out)))
 
