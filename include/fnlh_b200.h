@@ -237,6 +237,13 @@ int fnlh_solver_outer_iteration_host(fnlh_solver* s, const double* mean_in, cons
      harmonic's stage-1 norm and its linear reports (nrep[h] of them, concatenated in
      harmonic order).  fnlh_solver_outer_iteration == phase_harmonics(NULL) + phase_mean. */
 int fnlh_solver_phase_harmonics(fnlh_solver* s, const int* owned, double* h_norm);
+/* CUDA graphs (default on; FNLH_GRAPHS=0 in the environment turns them off at load): the
+   launch sequences of the outer iteration without a host synchronization inside -- the
+   five stages of each RK step on the 2-colour and explicit paths, and each harmonic
+   batch's factorizations + stages -- are captured once per call site and replayed; the
+   per-step synchronization that reads the error words stays outside, so results and
+   error semantics are those of the launch-by-launch path.  0 disables (A/B, tests). */
+void fnlh_set_graphs(int enable);
 /* the harmonic whose error the last phase_harmonics returned (the first failing one by
    index, driver.cpp:262-264), or -1 when it succeeded or failed before the harmonics; lets
    a sharded caller rethrow the lowest failing harmonic's error on every rank */

@@ -195,6 +195,8 @@ int fnlh_solver_phase_harmonics(fnlh_solver* s, const int* owned, double* h_norm
     });
 }
 
+void fnlh_set_graphs(int enable) { fnlh::graphs_enabled() = enable != 0; }
+
 int fnlh_solver_df_points(fnlh_solver* s, int* nq) {
     return guarded([&] { *nq = s->s->df_points(); });
 }

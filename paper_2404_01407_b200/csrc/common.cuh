@@ -49,7 +49,11 @@ inline void dmalloc(T** p, std::size_t bytes) { dmalloc(reinterpret_cast<void**>
 // count of kernel launches issued by this library (bench.py "gpu_launches"); atomic: the
 // C ABI may be called concurrently from several host threads with distinct handles
 std::atomic<long long>& launch_count();
-inline void note_launch() { launch_count().fetch_add(1, std::memory_order_relaxed); }
+inline thread_local long long tl_launches = 0;  // this host thread's launches (graph capture accounting)
+inline void note_launch() {
+    launch_count().fetch_add(1, std::memory_order_relaxed);
+    ++tl_launches;
+}
 
 // std::complex<double> layout (re, im), reference arithmetic order.
 struct alignas(16) cplx {

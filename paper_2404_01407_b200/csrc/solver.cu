@@ -2,6 +2,7 @@
 // (driver.cpp:157-379, rk.cpp:41-99), calling the sm_100a kernels of la.cu / disc.cu.
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <type_traits>
 
@@ -99,6 +100,53 @@ void shifted_blocks(const double* P, const double* vol, int b, int n, double ome
     { ::fnlh::note_launch(); k_shifted_blocks<<<nb(n), kT, 0, st>>>(P, vol, b, n, omega, out); }
 }
 
+std::atomic<int>& graphs_enabled() {
+    static std::atomic<int> on{[] {
+        const char* e = std::getenv("FNLH_GRAPHS");
+        return e ? std::atoi(e) : 1;
+    }()};
+    return on;
+}
+
+template <class F>
+void DeviceSolver::captured(const std::string& key, F&& body) {
+    cudaStream_t st = ws_->stream;
+    GraphEntry& g = graphs_[key];
+    if (!graphs_enabled() || g.failed) {
+        body();
+        return;
+    }
+    if (!g.exec) {
+        const long long l0 = tl_launches;
+        FNLH_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        cudaGraph_t graph = nullptr;
+        bool ok = true;
+        try {
+            body();
+        } catch (...) {
+            ok = false;
+        }
+        const cudaError_t e = cudaStreamEndCapture(st, &graph);
+        if (!ok || e != cudaSuccess || !graph ||
+            cudaGraphInstantiate(&g.exec, graph, cudaGraphInstantiateFlagAutoFreeOnLaunch) != cudaSuccess) {
+            (void)cudaGetLastError();
+            if (graph) cudaGraphDestroy(graph);
+            g.exec = nullptr;
+            g.failed = true;  // a host synchronization inside: launch by launch from now on
+            launch_count().fetch_sub(tl_launches - l0);
+            tl_launches = l0;
+            body();
+            return;
+        }
+        cudaGraphDestroy(graph);
+        g.launches = tl_launches - l0;
+        launch_count().fetch_sub(g.launches);  // counted when the graph runs
+        tl_launches = l0;
+    }
+    FNLH_CUDA(cudaGraphLaunch(g.exec, st));
+    launch_count().fetch_add(g.launches);
+}
+
 DeviceSolver::DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int* col_idx, const int* partition,
                            const SchemeConfig& scheme, int nh, const int* index, const double* omega,
                            const double* forcing_pairs, int nforcing, const double* mean0)
@@ -186,6 +234,8 @@ DeviceSolver::DeviceSolver(const MeshArrays& mesh, const int* row_ptr, const int
 }
 
 DeviceSolver::~DeviceSolver() {
+    for (auto& kv : graphs_)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     cudaEventDestroy(ev0_);
     cudaEventDestroy(ev1_);
     for (auto& e : evp_) cudaEventDestroy(e);
@@ -278,15 +328,18 @@ RkStepResult DeviceSolver::rk_step(S* state, Eval&& eval, Apply&& apply, Solve&&
     S* rhs = reinterpret_cast<S*>(rk_[4].ptr);
     S* x = reinterpret_cast<S*>(rk_[5].ptr);
     S* stage = reinterpret_cast<S*>(rk_[6].ptr);
+    RkStepResult res;
+    LinearSolveReport host_rep[5];
+    bool have_host[5] = {false, false, false, false, false};
+    const double gfac = sch_.implicit ? 1.0 / sch_.eps_relax : sigma_;  // rk.hpp:34
+    auto stages = [&] {
+    res = RkStepResult{};
+    for (int k = 0; k < 5; ++k) have_host[k] = false;
     FNLH_CUDA(cudaMemcpyAsync(state0, state, len * sizeof(S), cudaMemcpyDeviceToDevice, st));
     FNLH_CUDA(cudaMemcpyAsync(stage, state, len * sizeof(S), cudaMemcpyDeviceToDevice, st));
     FNLH_CUDA(cudaMemsetAsync(vis_blend, 0, len * sizeof(S), st));
     FNLH_CUDA(cudaMemsetAsync(vis_fresh, 0, len * sizeof(S), st));
     FNLH_CUDA(cudaMemsetAsync(stage_err_.ptr, 0xff, 10 * sizeof(unsigned long long), st));
-    RkStepResult res;
-    LinearSolveReport host_rep[5];
-    bool have_host[5] = {false, false, false, false, false};
-    const double gfac = sch_.implicit ? 1.0 / sch_.eps_relax : sigma_;  // rk.hpp:34
     for (int k = 1; k <= 5; ++k) {
         const double beta = kBeta[k - 1];
         const bool fresh = beta != 0.0;
@@ -318,6 +371,14 @@ RkStepResult DeviceSolver::rk_step(S* state, Eval&& eval, Apply&& apply, Solve&&
         check_finite<S>(stage, len, d->err(), st);
         d->redirect_err(nullptr);
     }
+    };
+    // the general path's solves are host-driven (a synchronization per solve): no graph
+    if ((sch_.implicit && rbA_) || !sch_.implicit)
+        captured("rk:" + field + ":" + std::to_string(level) + ":" + std::to_string((std::uintptr_t)state) +
+                     (mg_forcing ? ":fas" : "") + ":" + std::to_string(rb_sweep_mode().load()),
+                 stages);
+    else
+        stages();
     unsigned long long errs[11];
     RbControl ctls[5];
     int fac[2] = {0, 0x7fffffff};
@@ -508,6 +569,7 @@ void DeviceSolver::harmonic_batch(const int* hs, int P, std::vector<double>& h_n
     LaneReport lrep[kMaxBatch][5];
     int ldiv[kMaxBatch][5] = {};
     LinearSolveReport hrep[kMaxBatch][5];
+    auto batch = [&] {
     FNLH_CUDA(cudaEventRecord(ev_stage_, st));
     for (int m = 0; m < P; ++m) {  // build_lhs_harmonic + factorize per lane (driver.cpp:213-216)
         HarmonicLane& ln = *lanes_[m];
@@ -596,6 +658,14 @@ void DeviceSolver::harmonic_batch(const int* hs, int P, std::vector<double>& h_n
             check_finite<cplx>(ln.v[6].ptr, len, disc_->err(), st);
             disc_->redirect_err(nullptr);
         }
+    }
+    };
+    if (rbA_) {  // factorizations + five stages of P lanes: one graph per batch of harmonics
+        std::string key = "batch:" + std::to_string(rb_sweep_mode().load());
+        for (int m = 0; m < P; ++m) key += ":" + std::to_string(hs[m]);
+        captured(key, batch);
+    } else {  // level-scheduled lanes synchronize per solve
+        batch();
     }
     struct Rec {
         unsigned long long errs[10];

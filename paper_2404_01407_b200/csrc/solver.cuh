@@ -7,6 +7,7 @@
 #include <exception>
 #include <memory>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "disc.cuh"
@@ -78,6 +79,14 @@ struct RkStepResult {  // rk.hpp:68-72
     int viscous_evaluations = 0;
     std::vector<LinearSolveReport> linear_reports;
 };
+
+// CUDA graphs for the launch sequences of the outer iteration that contain no host
+// synchronization: the five stages of an RK step (residual / linearized residual, stage
+// arithmetic, the device-gated Richardson sweeps) and a harmonic batch's factorizations +
+// stages.  Captured once per call site (key), replayed every outer iteration; the host
+// synchronization that reads the step's error words stays outside.  fnlh_set_graphs(0)
+// (or FNLH_GRAPHS=0) enqueues the same work launch by launch.
+std::atomic<int>& graphs_enabled();
 
 class DeviceSolver {
 public:
@@ -211,6 +220,16 @@ private:
     std::vector<LinearSolveReport> reports_;
     int iter_ = 0;
     int failed_h_ = -1;
+    struct GraphEntry {
+        cudaGraphExec_t exec = nullptr;
+        long long launches = 0;  // kernels in the graph (the library's launch counter on replay)
+        bool failed = false;     // not capturable: run launch by launch
+    };
+    std::unordered_map<std::string, GraphEntry> graphs_;
+    // run `body` (enqueues on ws_->stream, forks/joins other streams through events) as the
+    // graph cached under `key`, capturing it on first use
+    template <class F>
+    void captured(const std::string& key, F&& body);
     const double* ext_df_acc_ = nullptr;
     double cum_seconds_ = 0.0;
     cudaEvent_t ev0_, ev1_, evp_[3];

@@ -110,6 +110,12 @@ def smoothed_solve(pat: Pattern, A, rhs, tol_rel, max_iter, shift_im=None):
     return x, rep.as_tuple()
 
 
+def set_graphs(enable: bool):
+    """CUDA-graph replay of the outer iteration's synchronization-free launch sequences
+    (include/fnlh_b200.h fnlh_set_graphs); off = launch by launch, same results."""
+    lib().fnlh_set_graphs(_i(1 if enable else 0))
+
+
 def set_red_black(enable: bool):
     """Enable / disable the 2-colour fused sweep (rb.cuh) in favour of the level-scheduled kernels."""
     lib().fnlh_set_red_black(_i(1 if enable else 0))

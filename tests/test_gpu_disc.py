@@ -372,3 +372,33 @@ def test_concurrent_handles_from_host_threads():
         (hs, (ms, as_)), (hp, (mp, ap)) = seq[k], par[k]
         assert hs == hp, specs[k]
         assert np.array_equal(ms, mp) and np.array_equal(as_, ap), specs[k]
+
+
+@pytest.mark.parametrize("name,scale,workers,implicit", [("c1", 1.0, 1, True), ("c2", 0.06, 3, True),
+                                                         ("c1", 0.5, 1, False)])
+def test_cuda_graphs_bitwise_and_faster(name, scale, workers, implicit):
+    """fnlh_set_graphs: the RK-step stages and harmonic batches replayed as CUDA graphs give
+    bitwise the launch-by-launch histories, states and reports; C1 (launch-bound) gets
+    faster."""
+    from paper_2404_01407_b200 import la
+    from paper_2404_01407_b200.solver import FnlhSolver
+    out = {}
+    try:
+        for graphs in (False, True):
+            la.set_graphs(graphs)
+            c = make_case(name, scale=scale, workers=workers, implicit=implicit)
+            g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
+            hist = [g.outer_iteration() for _ in range(4)]
+            ms = [g.counters()["last_ms"]]
+            for _ in range(3):
+                g.outer_iteration()
+                ms.append(g.counters()["last_ms"])
+            out[graphs] = (hist, g.state(), g.reports(), min(ms))
+    finally:
+        la.set_graphs(True)
+    (h0, (m0, a0), r0, t0), (h1, (m1, a1), r1, t1) = out[False], out[True]
+    assert [(e["resid_mean"], e["rz"]) for e in h0] == [(e["resid_mean"], e["rz"]) for e in h1]
+    assert np.array_equal(m0, m1) and np.array_equal(a0, a1) and r0 == r1
+    print(f"{name} scale {scale}: {t0:.3f} ms per pseudo-step launch by launch, {t1:.3f} ms with graphs")
+    if name == "c1" and implicit:
+        assert t1 < t0
