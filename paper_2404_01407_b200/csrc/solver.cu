@@ -112,7 +112,7 @@ template <class F>
 void DeviceSolver::captured(const std::string& key, F&& body) {
     cudaStream_t st = ws_->stream;
     GraphEntry& g = graphs_[key];
-    if (!graphs_enabled() || g.failed) {
+    if (!graphs_enabled() || g.failed || g.calls++ == 0) {
         body();
         return;
     }

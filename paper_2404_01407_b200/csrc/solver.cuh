@@ -224,6 +224,7 @@ private:
         cudaGraphExec_t exec = nullptr;
         long long launches = 0;  // kernels in the graph (the library's launch counter on replay)
         bool failed = false;     // not capturable: run launch by launch
+        int calls = 0;           // the first call runs launch by launch (lazy set-up happens there)
     };
     std::unordered_map<std::string, GraphEntry> graphs_;
     // run `body` (enqueues on ws_->stream, forks/joins other streams through events) as the
