@@ -81,7 +81,8 @@ def main(d):
     res = {}
     for rep in sorted(glob.glob(os.path.join(d, "r2_c4_k_*.ncu-rep"))):
         for r in ncu_rows(rep):
-            key = next((k for k in f if k in r["name"].replace("fnlh::cplx", "cplx")), None)
+            nm = r["name"].replace("fnlh::cplx", "cplx").replace("(int)", "")
+            key = next((k for k in f if k in nm), None)
             if key is None or key in res:
                 continue
             by, formula = f[key]
