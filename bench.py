@@ -246,7 +246,8 @@ def reference_arm(args):
     from paper_2404_01407_b200.cases import make_case
 
     t0 = time.perf_counter()
-    c = make_case(args.config, scale=args.scale, device=False)  # host restatement: no product code loaded
+    ov = {"order": args.order} if args.order else {}
+    c = make_case(args.config, scale=args.scale, device=False, **ov)  # host restatement: no product code loaded
     pat = c.mesh.pattern(device=False)
     J, _ = Oracle().fd_jacobian(c.mesh, pat, c.mean0)  # the restatement (bitwise the device's, tests)
     n, b = c.mesh.n, c.mesh.b
@@ -298,6 +299,8 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--order", default=None, choices=["rcm", "morton"],
+                    help="node numbering inside each colour (default: the configuration's)")
     ap.add_argument("--sweeps", type=int, default=10, help="sweeps in the roofline leg")
     ap.add_argument("--mode", default="shard", choices=["replicas", "shard"],
                     help="N>1: one instance with its harmonics sharded over the ranks, fields exchanged by NCCL "
@@ -324,9 +327,10 @@ def main():
 
     require_gpu()
     check(lib().fnlh_set_device(local))  # this rank's GPU for the library's own runtime calls
-    c = make_case(args.config, scale=args.scale)
+    ov = {"order": args.order} if args.order else {}
+    c = make_case(args.config, scale=args.scale, **ov)
     if args.workers != 1:
-        c = make_case(args.config, scale=args.scale, workers=args.workers or min(len(c.omegas), 8))
+        c = make_case(args.config, scale=args.scale, workers=args.workers or min(len(c.omegas), 8), **ov)
     m = c.mesh
     pat = m.pattern()
     n, b = m.n, m.b
