@@ -143,7 +143,10 @@ int fnlh_richardson(fnlh_prec* f, const double* rhs, double tol_rel, int max_ite
        (2 kernels per sweep);
      1 the same arithmetic as three kernels per sweep (K_F, K_B, K_R);
      2 one pass over A per sweep, L_ik r_k applied as A_ik (U_kk^{-1} r_k): the same
-       preconditioner, iterates equal to rounding, not bitwise. */
+       preconditioner, iterates equal to rounding, not bitwise;
+     3 mode 0's arithmetic (bitwise) with edge-parallel kernels: one thread per (row,
+       off-diagonal block) forms the block products, the row's sums are then taken in the
+       reference's order from shared memory (at most 6 off-diagonal blocks per row). */
 int fnlh_pattern_is_red_black(fnlh_pattern* p, int* n0);
 /* compact factors of the 2-colour ILU(0): pivot LU + piv for every row, inv(U_kk) for colour 0 */
 int fnlh_rb_factorize(fnlh_pattern* p, int is_complex, const double* A, const double* shift_im, double* diag_lu,

@@ -9,6 +9,9 @@ namespace fnlh {
 namespace {
 
 constexpr int kT = 128;  // 4 slices of 32 rows per CTA
+#ifndef RBE_MINB
+#define RBE_MINB 2  // resident CTAs per SM of the edge-parallel kernels (192 threads each)
+#endif
 inline int nb(long long n) { return static_cast<int>((n + kT - 1) / kT); }
 
 struct SellDev {
@@ -54,6 +57,37 @@ __device__ __forceinline__ void ablock(const SellDev& L, const RowRef& r, int e,
 }
 
 __device__ __forceinline__ int acol(const SellDev& L, const RowRef& r, int e) { return __ldg(L.cols + r.cbase + e * 32); }
+
+// lu_solve_reg (block_lu_solve, dense.hpp:91-109) reading the LU entries from memory as it
+// uses them (row phase of the edge-parallel kernels: no 25-entry register block)
+template <int B, class S>
+__device__ __forceinline__ void lu_solve_mem(const S* __restrict__ lu, long long stride, const int (&piv)[B], S (&x)[B]) {
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+        const int p = piv[k];
+#pragma unroll
+        for (int r = k + 1; r < B; ++r)
+            if (r == p) {
+                S t = x[k];
+                x[k] = x[r];
+                x[r] = t;
+            }
+    }
+#pragma unroll
+    for (int r = 1; r < B; ++r) {
+        S acc = x[r];
+#pragma unroll
+        for (int c = 0; c < r; ++c) acc -= lu[(r * B + c) * stride] * x[c];
+        x[r] = acc;
+    }
+#pragma unroll
+    for (int r = B - 1; r >= 0; --r) {
+        S acc = x[r];
+#pragma unroll
+        for (int c = r + 1; c < B; ++c) acc -= lu[(r * B + c) * stride] * x[c];
+        x[r] = acc / lu[(r * B + r) * stride];
+    }
+}
 
 // pivot blocks (diag_lu) and pivots are stored slice-major like A: row i -> slice s,
 // lane l; element k of the row at [s][k][l], so a warp's k-th load is 32 consecutive
@@ -138,6 +172,24 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     if (threadIdx.x == 0)
         for (int w = 0; w < kT / 32; ++w) s += red[w];
     return s;
+}
+
+// fixed-order sum of partials by a CTA of any size (deterministic run to run); thread 0
+// receives the sum
+__device__ double ordered_sum_n(const double* __restrict__ p, int n, double* red) {
+    const int nt = blockDim.x;
+    double s = 0.0;
+    const int chunk = (n + nt - 1) / nt;
+    const int b0 = threadIdx.x * chunk, b1 = min(n, b0 + chunk);
+    for (int k = b0; k < b1; ++k) s += __ldcg(p + k);
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+    __shared__ double wsum[32];
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = s;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < (nt + 31) / 32; ++w) t += wsum[w];
+    return t;
 }
 
 // fixed-order sum of partials by one CTA (deterministic run to run)
@@ -531,6 +583,236 @@ __global__ void __launch_bounds__(kT) k_rbx_colour1(SellDev L, const RbTab<S> T,
     __syncthreads();
     if (!last) return;
     const double tot = ordered_sum(partials, grid0 + nct, red);
+    if (threadIdx.x == 0) {
+        const double nrm = sqrt(tot);
+        ctl->iterations = sweep;
+        ctl->final_residual = nrm;
+        if (!isfinite(nrm)) {
+            ctl->status = 6;
+            ctl->done = 1;
+        } else if (nrm <= ctl->target) {
+            ctl->converged = 1;
+            ctl->done = 1;
+        } else if (sweep >= max_iter) {
+            ctl->done = 1;
+        }
+        *counter = 0u;
+    }
+}
+
+
+
+// ---- K_B, edge-parallel (fnlh_set_rb_sweep(3)) -------------------------------------
+// k_rb_colour0's arithmetic with one thread per (row, upper block): warp q of the CTA (one
+// SELL slice of colour-0 rows) forms block slot q+1's backward product A_ij z_j and
+// residual product A_ij (x_j + z_j) into shared memory; warp 0 then takes the backward sum
+// in descending slot order, the pivot solve and x += z, and the residual row with the
+// diagonal block first and the parked products ascending -- the row-serial sequence.
+template <int B, class S>
+__global__ void __launch_bounds__(192, RBE_MINB) k_rbe_colour0(SellDev L, const RbTab<S> T, int sweep, int E) {
+    const int P_ = T.P, h_ = blockIdx.x % P_, cta = blockIdx.x / P_;
+    const S* __restrict__ diag_lu = T.diag_lu[h_];
+    const int* __restrict__ piv = T.piv[h_];
+    const double* __restrict__ shift = T.shift[h_];
+    const S* __restrict__ rhs = T.rhs[h_];
+    S* __restrict__ x = T.x[h_];
+    S* __restrict__ z = T.z[h_];
+    S* __restrict__ r = T.r[h_];
+    RbControl* ctl = T.ctl[h_];
+    double* __restrict__ partials = T.parts[h_];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    S* Bk = reinterpret_cast<S*>(smem_raw);       // [slot-1][rw][lane]: A_ij z_j
+    S* Mk = Bk + (std::size_t)E * B * 32;         // [slot-1][rw][lane]: A_ij (x_j + z_j)
+    if (ctl->done) return;
+    const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+    const int i = cta * 32 + lane;
+    const bool row_ok = i < L.n0;
+    RowRef rr{};
+    if (row_ok) rr = row_ref(L, i);
+    const int e = q + 1;
+    if (row_ok && e < rr.deg) {
+        const int j = acol(L, rr, e);
+        S zj[B], xj[B];
+        ld<B>(z + (size_t)j * B, zj);
+        ld<B>(x + (size_t)j * B, xj);
+#pragma unroll
+        for (int k = 0; k < B; ++k) xj[k] += zj[k];  // colour-1 x += z ahead of K_R
+        double A[2 * pairs<B>()];
+        ablock<B>(L, rr, e, A);
+#pragma unroll
+        for (int rw = 0; rw < B; ++rw) {
+            S accb = zero<S>(), accm = zero<S>();
+#pragma unroll
+            for (int c = 0; c < B; ++c) {
+                const double a = A[rw * B + c];
+                accb += rmul(a, zj[c]);
+                accm += rmul(a, xj[c]);
+            }
+            Bk[((size_t)q * B + rw) * 32 + lane] = accb;
+            Mk[((size_t)q * B + rw) * 32 + lane] = accm;
+        }
+    }
+    __syncthreads();
+    double loc = 0.0;
+    if (q == 0 && row_ok) {
+        S t[B];
+        ld<B>((sweep == 1 ? rhs : r) + (size_t)i * B, t);  // forward: colour 0 rows copy r
+        for (int ee = rr.deg - 1; ee >= 1; --ee)
+#pragma unroll
+            for (int rw = 0; rw < B; ++rw) t[rw] -= Bk[((size_t)(ee - 1) * B + rw) * 32 + lane];
+        const LuRef q_ = lu_ref<B>(L, i);
+        int pv[B];
+#pragma unroll
+        for (int k = 0; k < B; ++k) pv[k] = piv[q_.pv + 32 * k];
+        lu_solve_mem<B>(diag_lu + q_.lu, 32, pv, t);
+        S xi[B];
+        ld<B>(x + (size_t)i * B, xi);
+#pragma unroll
+        for (int k = 0; k < B; ++k) xi[k] += t[k];  // x += z (sparse.hpp:317)
+        st<B>(x + (size_t)i * B, xi);
+        S y[B];
+#pragma unroll
+        for (int k = 0; k < B; ++k) y[k] = zero<S>();
+        blk_matvec_add<B, S>(L, rr, 0, xi, shift != nullptr, shift ? shift[i] : 0.0, y);  // diagonal block first
+        for (int ee = 1; ee < rr.deg; ++ee)
+#pragma unroll
+            for (int rw = 0; rw < B; ++rw) y[rw] += Mk[((size_t)(ee - 1) * B + rw) * 32 + lane];
+        S bi[B];
+        ld<B>(rhs + (size_t)i * B, bi);
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            const S v = bi[k] - y[k];
+            r[(size_t)i * B + k] = v;
+            loc += sq(v);
+        }
+    }
+    double v = loc;
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    if (threadIdx.x == 0) partials[cta] = v;
+}
+
+// ---- K_RF, edge-parallel (fnlh_set_rb_sweep(3)) ------------------------------------
+// The same arithmetic as k_rbx_colour1 with one thread per (row, lower block): a CTA is one
+// SELL slice of colour-1 rows (32 rows, warp e = block slot e), so all of a row's
+// neighbour gathers (x_k, r_k, inv(U_kk)) are in flight at once instead of one block after
+// another.  Each thread forms its block's residual product A_ik x_k and forward product
+// L_ik r_k (L_ik rebuilt in the reference's order) into shared memory; warp 0 then sums
+// them per row in ascending block order (then the diagonal), exactly the sequence of the
+// row-serial kernel, so the iterates are bitwise the same.
+template <int B, class S>
+__global__ void __launch_bounds__(192, RBE_MINB) k_rbe_colour1(SellDev L, const RbTab<S> T, int grid0, int sweep, int max_iter,
+                                                     int forward, int E) {
+    const int P_ = T.P, h_ = blockIdx.x % P_, cta = blockIdx.x / P_;
+    [[maybe_unused]] const int nct = gridDim.x / P_;
+    const S* __restrict__ diag_lu = T.diag_lu[h_];
+    const int* __restrict__ piv = T.piv[h_];
+    const S* __restrict__ inv0 = T.inv0[h_];
+    const double* __restrict__ shift = T.shift[h_];
+    const S* __restrict__ rhs = T.rhs[h_];
+    S* __restrict__ x = T.x[h_];
+    S* __restrict__ z = T.z[h_];
+    S* __restrict__ r = T.r[h_];
+    RbControl* ctl = T.ctl[h_];
+    unsigned int* counter = &ctl->counter;
+    double* __restrict__ partials = T.parts[h_];
+    __shared__ double red[kT / 32];
+    __shared__ bool last;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    S* Q = reinterpret_cast<S*>(smem_raw);        // [slot][rw][lane]: A_ik x_k
+    S* Pf = Q + (std::size_t)E * B * 32;          // [slot][rw][lane]: L_ik r_k
+    if (ctl->done) return;
+    const int lane = threadIdx.x & 31, e = threadIdx.x >> 5;
+    const int i = L.n0 + cta * 32 + lane;
+    const bool row_ok = i < L.n;
+    RowRef rr{};
+    int dg = 0;
+    if (row_ok) {
+        rr = row_ref(L, i);
+        dg = rr.deg - 1;
+    }
+    if (row_ok && e < dg) {
+        const int kk = acol(L, rr, e);
+        double A[2 * pairs<B>()];
+        ablock<B>(L, rr, e, A);
+        S xk[B];
+        ld<B>(x + (size_t)kk * B, xk);
+#pragma unroll
+        for (int rw = 0; rw < B; ++rw) {
+            S acc = zero<S>();
+#pragma unroll
+            for (int c = 0; c < B; ++c) acc += rmul(A[rw * B + c], xk[c]);
+            Q[((size_t)e * B + rw) * 32 + lane] = acc;
+        }
+        if (forward) {
+            S rk[B];
+            ld<B>(r + (size_t)kk * B, rk);
+            const S* __restrict__ U = inv0 + (size_t)kk * B * B;
+            S acc[B];
+#pragma unroll
+            for (int rw = 0; rw < B; ++rw) acc[rw] = zero<S>();
+#pragma unroll
+            for (int c = 0; c < B; ++c) {
+                S uc[B];
+#pragma unroll
+                for (int m = 0; m < B; ++m) uc[m] = U[m * B + c];
+#pragma unroll
+                for (int rw = 0; rw < B; ++rw) {
+                    S lrc = zero<S>();
+#pragma unroll
+                    for (int m = 0; m < B; ++m) lrc += rmul(A[rw * B + m], uc[m]);
+                    acc[rw] += lrc * rk[c];
+                }
+            }
+#pragma unroll
+            for (int rw = 0; rw < B; ++rw) Pf[((size_t)e * B + rw) * 32 + lane] = acc[rw];
+        }
+    }
+    __syncthreads();
+    double loc = 0.0;
+    if (e == 0 && row_ok) {
+        S xi[B], zi[B], y[B];
+        ld<B>(x + (size_t)i * B, xi);
+        ld<B>(z + (size_t)i * B, zi);
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            xi[k] += zi[k];
+            y[k] = zero<S>();
+        }
+        st<B>(x + (size_t)i * B, xi);
+        for (int q = 0; q < dg; ++q)
+#pragma unroll
+            for (int rw = 0; rw < B; ++rw) y[rw] += Q[((size_t)q * B + rw) * 32 + lane];
+        blk_matvec_add<B, S>(L, rr, dg, xi, shift != nullptr, shift ? shift[i] : 0.0, y);
+        S ri[B];
+        ld<B>(rhs + (size_t)i * B, ri);
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            ri[k] -= y[k];
+            loc += sq(ri[k]);
+        }
+        if (forward) {
+            for (int q = 0; q < dg; ++q)
+#pragma unroll
+                for (int rw = 0; rw < B; ++rw) ri[rw] -= Pf[((size_t)q * B + rw) * 32 + lane];
+            const LuRef q_ = lu_ref<B>(L, i);
+            int pv[B];
+#pragma unroll
+            for (int k = 0; k < B; ++k) pv[k] = piv[q_.pv + 32 * k];
+            lu_solve_mem<B>(diag_lu + q_.lu, 32, pv, ri);
+            st<B>(z + (size_t)i * B, ri);
+        }
+    }
+    // CTA partial in row order (one slice), then the last CTA's decision
+    double v = loc;
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    if (threadIdx.x == 0) {
+        partials[grid0 + cta] = v;
+        __threadfence();
+        last = atomicAdd(counter, 1u) == nct - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    const double tot = ordered_sum_n(partials, grid0 + nct, red);
     if (threadIdx.x == 0) {
         const double nrm = sqrt(tot);
         ctl->iterations = sweep;
@@ -989,7 +1271,7 @@ RbSystem::RbSystem(const DevicePattern* p, int n0) : p_(p) {
     legacy_sync();
     grid0 = nb(n0);
     grid1 = nb(n - n0);
-    partials.alloc(std::max(grid0 + grid1, nb((long long)n * b)) + 8);
+    partials.alloc(std::max((n0 + 31) / 32 + (n - n0 + 31) / 32, nb((long long)n * b)) + 8);  // edge-parallel: one per slice
 }
 
 void RbSystem::load(const double* A_csr, cudaStream_t stm) {
@@ -1059,7 +1341,19 @@ void rb_smoothed_solve_batch(const RbSystem& A, const RbMember<S>* mem, int P, d
         // drive several GPUs, fnlh_set_device), and setting one is a host-side table update
         FNLH_CUDA(cudaFuncSetAttribute(k_rb_colour0<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         FNLH_CUDA(cudaFuncSetAttribute(k_rbx_colour1<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        if (rb_sweep_mode() == 1) {
+        const int E = maxoff;
+        if (rb_sweep_mode() == 3) {  // edge-parallel colour-1 kernel (same arithmetic, bitwise)
+            const std::size_t sme = (std::size_t)2 * E * B * 32 * sizeof(S);
+            FNLH_CUDA(cudaFuncSetAttribute(k_rbe_colour1<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sme));
+            if (32 * E > 192) throw ShapeError("rb: edge-parallel sweep needs <= 6 lower blocks per row");
+            FNLH_CUDA(cudaFuncSetAttribute(k_rbe_colour0<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sme));
+            const int ns0 = (L.n0 + 31) / 32, ns1 = (L.n - L.n0 + 31) / 32;
+            { ::fnlh::note_launch(); k_rb_forward1<B, S><<<g1, kT, 0, stm>>>(sd, T, 1); }
+            for (int s = 1; s <= max_iter; ++s) {
+                { ::fnlh::note_launch(); k_rbe_colour0<B, S><<<ns0 * P, 32 * E, sme, stm>>>(sd, T, s, E); }
+                { ::fnlh::note_launch(); k_rbe_colour1<B, S><<<ns1 * P, 32 * E, sme, stm>>>(sd, T, ns0, s, max_iter, s < max_iter ? 1 : 0, E); }
+            }
+        } else if (rb_sweep_mode() == 1) {
             for (int s = 1; s <= max_iter; ++s) {
                 { ::fnlh::note_launch(); k_rb_forward1<B, S><<<g1, kT, 0, stm>>>(sd, T, s); }
                 { ::fnlh::note_launch(); k_rb_colour0<B, S><<<g0, kT, sm, stm>>>(sd, T, s); }

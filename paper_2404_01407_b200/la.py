@@ -121,13 +121,14 @@ def set_red_black(enable: bool):
     lib().fnlh_set_red_black(_i(1 if enable else 0))
 
 
-RB_EXACT, RB_EXACT_SPLIT, RB_ONEPASS = 0, 1, 2
+RB_EXACT, RB_EXACT_SPLIT, RB_ONEPASS, RB_EDGE = 0, 1, 2, 3
 
 
 def set_rb_sweep(mode: int):
     """2-colour sweep variant (include/fnlh_b200.h fnlh_set_rb_sweep): RB_EXACT (default,
     bitwise reference iterates, 2 kernels/sweep), RB_EXACT_SPLIT (same, 3 kernels/sweep),
-    RB_ONEPASS (one pass over A, iterates equal to rounding)."""
+    RB_ONEPASS (one pass over A, iterates equal to rounding), RB_EDGE (bitwise, the colour-1
+    kernel edge-parallel: one thread per (row, lower block))."""
     check(lib().fnlh_set_rb_sweep(_i(mode)))
 
 

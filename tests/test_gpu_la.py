@@ -56,7 +56,8 @@ def test_ilu_factor_apply_solve(ref, meshes, b, cplx, kind):
     # the 2-colour sweep in reference order (bitwise; fused and split kernels), the one-pass
     # 2-colour sweep (same preconditioner applied as A_ik (U_kk^-1 r_k): equal to rounding),
     # and the general level-scheduled path (bitwise)
-    for rb, mode in ((True, la.RB_EXACT), (True, la.RB_EXACT_SPLIT), (True, la.RB_ONEPASS), (False, la.RB_EXACT)):
+    for rb, mode in ((True, la.RB_EXACT), (True, la.RB_EXACT_SPLIT), (True, la.RB_ONEPASS), (True, la.RB_EDGE),
+                     (False, la.RB_EXACT)):
         la.set_red_black(rb)
         la.set_rb_sweep(mode)
         exact = mode != la.RB_ONEPASS or kind == "tet"
