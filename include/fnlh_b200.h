@@ -146,7 +146,10 @@ int fnlh_richardson(fnlh_prec* f, const double* rhs, double tol_rel, int max_ite
        preconditioner, iterates equal to rounding, not bitwise;
      3 mode 0's arithmetic (bitwise) with edge-parallel kernels: one thread per (row,
        off-diagonal block) forms the block products, the row's sums are then taken in the
-       reference's order from shared memory (at most 6 off-diagonal blocks per row). */
+       reference's order from shared memory (at most 6 off-diagonal blocks per row);
+     4 mode 0's kernels and arithmetic (bitwise, the same norms) with lane-warp CTAs for a
+       batch of P > 1 systems sharing A: a CTA is one 32-row slice for up to 4 systems, one
+       warp each, so the systems' loads of the shared A blocks meet in L1. */
 int fnlh_pattern_is_red_black(fnlh_pattern* p, int* n0);
 /* compact factors of the 2-colour ILU(0): pivot LU + piv for every row, inv(U_kk) for colour 0 */
 int fnlh_rb_factorize(fnlh_pattern* p, int is_complex, const double* A, const double* shift_im, double* diag_lu,

@@ -257,7 +257,7 @@ void fnlh_set_red_black(int enable) { fnlh::rb_enabled() = enable != 0; }
 
 int fnlh_set_rb_sweep(int mode) {
     return guarded([&] {
-        if (mode < 0 || mode > 3) throw ConfigError("fnlh_set_rb_sweep: mode must be 0, 1, 2 or 3");
+        if (mode < 0 || mode > 4) throw ConfigError("fnlh_set_rb_sweep: mode must be 0..4");
         fnlh::rb_sweep_mode() = mode;
     });
 }

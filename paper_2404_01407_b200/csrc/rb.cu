@@ -1,5 +1,6 @@
 // rb.cu -- 2-colour fused ILU(0)-Richardson sweep (see rb.cuh for the derivation).
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "rb.cuh"
@@ -50,13 +51,73 @@ __device__ __forceinline__ void ablock(const SellDev& L, const RowRef& r, int e,
     const double2* base = reinterpret_cast<const double2*>(L.vals + r.vbase) + (long long)e * pairs<B>() * 32;
 #pragma unroll
     for (int p = 0; p < pairs<B>(); ++p) {
+#if RB_L1HINT & 4
+        double2 v;
+        asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(base + (long long)p * 32));
+#else
         const double2 v = __ldg(base + (long long)p * 32);
+#endif
         A[2 * p] = v.x;
         A[2 * p + 1] = v.y;
     }
 }
 
 __device__ __forceinline__ int acol(const SellDev& L, const RowRef& r, int e) { return __ldg(L.cols + r.cbase + e * 32); }
+
+// L1 cache hints (measurement switch RB_L1HINT, bit flags): 1 = gathered neighbour data
+// (inv(U_kk), x_k, r_k, z_j) loaded L1::evict_last, 2 = a row's own streamed operands (vectors,
+// pivot LU) L1::no_allocate, 4 = the A blocks L1::no_allocate -- so that the L1 keeps the
+// operands several rows share instead of the ones read once
+#ifndef RB_L1HINT
+#define RB_L1HINT 0
+#endif
+__device__ __forceinline__ cplx ldh_keep(const cplx* p) {
+    cplx v;
+    asm("ld.global.L1::evict_last.v2.f64 {%0,%1}, [%2];" : "=d"(v.re), "=d"(v.im) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ldh_keep(const double* p) {
+    double v;
+    asm("ld.global.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ cplx ldh_once(const cplx* p) {
+    cplx v;
+    asm("ld.global.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.re), "=d"(v.im) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ldh_once(const double* p) {
+    double v;
+    asm("ld.global.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+// gathered operand of a neighbour row / streamed operand of the own row
+template <class S>
+__device__ __forceinline__ S ld_nb(const S* p) {
+#if RB_L1HINT & 1
+    return ldh_keep(p);
+#else
+    return *p;
+#endif
+}
+template <class S>
+__device__ __forceinline__ S ld_own(const S* p) {
+#if RB_L1HINT & 2
+    return ldh_once(p);
+#else
+    return *p;
+#endif
+}
+template <int B, class S>
+__device__ __forceinline__ void ldn(const S* __restrict__ p, S (&v)[B]) {
+#pragma unroll
+    for (int k = 0; k < B; ++k) v[k] = ld_nb(p + k);
+}
+template <int B, class S>
+__device__ __forceinline__ void ldo(const S* __restrict__ p, S (&v)[B]) {
+#pragma unroll
+    for (int k = 0; k < B; ++k) v[k] = ld_own(p + k);
+}
 
 // lu_solve_reg (block_lu_solve, dense.hpp:91-109) reading the LU entries from memory as it
 // uses them (row phase of the edge-parallel kernels: no 25-entry register block)
@@ -107,7 +168,7 @@ template <int B, class S>
 __device__ __forceinline__ void ld_lu(const S* __restrict__ dlu, const int* __restrict__ piv, const LuRef& q,
                                       S (&lu)[B * B], int (&pv)[B]) {
 #pragma unroll
-    for (int k = 0; k < B * B; ++k) lu[k] = dlu[q.lu + 32 * k];
+    for (int k = 0; k < B * B; ++k) lu[k] = ld_own(dlu + q.lu + 32 * k);
 #pragma unroll
     for (int k = 0; k < B; ++k) pv[k] = piv[q.pv + 32 * k];
 }
@@ -200,6 +261,36 @@ __device__ double ordered_sum(const double* __restrict__ p, int n, double* red) 
     for (int k = b0; k < b1; ++k) s += p[k];
     __syncthreads();
     return block_sum(s, red);
+}
+
+// Lane-warp kernels (fnlh_set_rb_sweep(4)): the same total as ordered_sum over the 128-row
+// partials q[k] of the 128-thread kernels, formed by ONE warp from per-slice (32-row)
+// partials w: q[k] = ((w[4k] + w[4k+1]) + w[4k+2]) + w[4k+3] (block_sum's order), colour-0
+// slices at [0, 4 grid0), colour-1 slices from 4 grid0; each thread plays the four virtual
+// threads lane, lane+32, lane+64, lane+96 of the 128-thread reduction.  Thread 0 gets the sum.
+__device__ double ordered_sum_lw(const double* __restrict__ p, int grid0, int grid1, int ns0, int ns1) {
+    const int n = grid0 + grid1, lane = threadIdx.x & 31;
+    const int chunk = (n + kT - 1) / kT;
+    double sv[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        const int vt = v * 32 + lane;
+        const int b0 = vt * chunk, b1 = min(n, b0 + chunk);
+        double s = 0.0;
+        for (int k = b0; k < b1; ++k) {
+            const int lim = k < grid0 ? ns0 - 4 * k : ns1 - 4 * (k - grid0);  // slices of this group that exist
+            double q = 0.0;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) q += w < lim ? __ldcg(p + 4 * k + w) : 0.0;
+            s += q;
+        }
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+        sv[v] = s;
+    }
+    double t = 0.0;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) t += sv[v];
+    return t;
 }
 
 // per-member operand table of a batched sweep: P independent systems that share the
@@ -331,9 +422,22 @@ __global__ void __launch_bounds__(kT) k_rb_forward1(SellDev L, const RbTab<S> T,
 // (sparse.cpp:280-290) and A_e (x_j + z_j) is parked in shared memory; after the
 // pivot solve and x += z the residual row is summed in ascending order
 // (sparse.hpp:317-319).  Every block is read from HBM once.
-template <int B, class S>
-__global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const RbTab<S> T, int sweep) {
-    const int P_ = T.P, h_ = blockIdx.x % P_, cta = blockIdx.x / P_;
+template <int B, class S, bool LW = false>
+__global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const RbTab<S> T, int sweep, int G = 0) {
+    // LW (lane-warp, fnlh_set_rb_sweep(4)): a CTA is ONE slice of 32 rows for G lanes of the
+    // batch, warp w serving lane (blockIdx.x % ng) G + w, so the lanes' loads of the shared A
+    // blocks and column indices meet in L1 instead of each going to L2
+    const int P_ = T.P;
+    int h_, cta;
+    if constexpr (LW) {
+        const int ng = (P_ + G - 1) / G;
+        h_ = (blockIdx.x % ng) * G + (threadIdx.x >> 5);
+        cta = blockIdx.x / ng;
+        if (h_ >= P_) return;
+    } else {
+        h_ = blockIdx.x % P_;
+        cta = blockIdx.x / P_;
+    }
     [[maybe_unused]] const int nct = gridDim.x / P_;
     [[maybe_unused]] const S* __restrict__ diag_lu = T.diag_lu[h_];
     [[maybe_unused]] const int* __restrict__ piv = T.piv[h_];
@@ -351,17 +455,18 @@ __global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const RbTab<S> T, 
     S* park = reinterpret_cast<S*>(smem_raw);  // [slot][row][tid]
     if (ctl->done) return;
     const int tid = threadIdx.x;
-    const int i = cta * kT + tid;
+    const int nt = LW ? (int)blockDim.x : kT;  // park stride
+    const int i = LW ? cta * 32 + (tid & 31) : cta * kT + tid;
     double loc = 0.0;
     if (i < L.n0) {
         const RowRef rr = row_ref(L, i);
         S t[B];
-        ld<B>((sweep == 1 ? rhs : r) + (size_t)i * B, t);  // forward: colour 0 rows copy r
+        ldo<B>((sweep == 1 ? rhs : r) + (size_t)i * B, t);  // forward: colour 0 rows copy r
         for (int e = rr.deg - 1; e >= 1; --e) {
             const int j = acol(L, rr, e);
             S zj[B], xj[B];
-            ld<B>(z + (size_t)j * B, zj);
-            ld<B>(x + (size_t)j * B, xj);
+            ldn<B>(z + (size_t)j * B, zj);
+            ldn<B>(x + (size_t)j * B, xj);
 #pragma unroll
             for (int k = 0; k < B; ++k) xj[k] += zj[k];  // colour-1 x += z ahead of K_R
             double A[2 * pairs<B>()];
@@ -376,7 +481,7 @@ __global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const RbTab<S> T, 
                     accm += rmul(a, xj[c]);
                 }
                 t[rw] -= accb;
-                park[((e - 1) * B + rw) * kT + tid] = accm;
+                park[((e - 1) * B + rw) * nt + tid] = accm;
             }
         }
         S lu[B * B];
@@ -384,7 +489,7 @@ __global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const RbTab<S> T, 
         ld_lu<B>(diag_lu, piv, lu_ref<B>(L, i), lu, pv);
         lu_solve_reg<B>(lu, pv, t);
         S xi[B];
-        ld<B>(x + (size_t)i * B, xi);
+        ldo<B>(x + (size_t)i * B, xi);
 #pragma unroll
         for (int k = 0; k < B; ++k) xi[k] += t[k];  // x += z (sparse.hpp:317)
         st<B>(x + (size_t)i * B, xi);
@@ -395,9 +500,9 @@ __global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const RbTab<S> T, 
         blk_matvec_add<B, S>(L, rr, 0, xi, shift != nullptr, s, y);  // diagonal block first
         for (int e = 1; e < rr.deg; ++e)
 #pragma unroll
-            for (int rw = 0; rw < B; ++rw) y[rw] += park[((e - 1) * B + rw) * kT + tid];
+            for (int rw = 0; rw < B; ++rw) y[rw] += park[((e - 1) * B + rw) * nt + tid];
         S bi[B];
-        ld<B>(rhs + (size_t)i * B, bi);
+        ldo<B>(rhs + (size_t)i * B, bi);
 #pragma unroll
         for (int k = 0; k < B; ++k) {
             const S v = bi[k] - y[k];
@@ -405,8 +510,14 @@ __global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const RbTab<S> T, 
             loc += sq(v);
         }
     }
-    const double bs = block_sum(loc, red);
-    if (tid == 0) partials[cta] = bs;
+    if constexpr (LW) {  // per-slice partial (ordered_sum_lw regroups them 4 by 4)
+        double v = loc;
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+        if ((tid & 31) == 0) partials[cta] = v;
+    } else {
+        const double bs = block_sum(loc, red);
+        if (tid == 0) partials[cta] = bs;
+    }
 }
 
 // ---- K_R: colour 1 residual rows + stopping rule ------------------------------
@@ -491,10 +602,23 @@ __global__ void __launch_bounds__(kT) k_rb_resid1(SellDev L, const RbTab<S> T, i
 // L_ik r_k with L_ik = A_ik inv(U_kk) rebuilt as in K_F; the L_ik r_k products are
 // parked in shared memory because the forward sum starts from r_i, which is known only
 // after the residual row is complete (zf = r_i - L r_k1 - L r_k2 ..., sparse.cpp:267-278).
-template <int B, class S>
-__global__ void __launch_bounds__(kT) k_rbx_colour1(SellDev L, const RbTab<S> T, int grid0, int sweep, int max_iter, int forward) {
-    const int P_ = T.P, h_ = blockIdx.x % P_, cta = blockIdx.x / P_;
-    [[maybe_unused]] const int nct = gridDim.x / P_;
+template <int B, class S, bool LW = false>
+__global__ void __launch_bounds__(kT, LW ? 3 : 0) k_rbx_colour1(SellDev L, const RbTab<S> T, int grid0, int sweep, int max_iter, int forward,
+                                                    int G = 0) {
+    const int P_ = T.P;
+    int h_, cta, nct_;
+    if constexpr (LW) {  // see k_rb_colour0: one slice, G lanes, warp = lane
+        const int ng = (P_ + G - 1) / G;
+        h_ = (blockIdx.x % ng) * G + (threadIdx.x >> 5);
+        cta = blockIdx.x / ng;
+        nct_ = gridDim.x / ng;
+        if (h_ >= P_) return;
+    } else {
+        h_ = blockIdx.x % P_;
+        cta = blockIdx.x / P_;
+        nct_ = gridDim.x / P_;
+    }
+    [[maybe_unused]] const int nct = nct_;
     [[maybe_unused]] const S* __restrict__ diag_lu = T.diag_lu[h_];
     [[maybe_unused]] const int* __restrict__ piv = T.piv[h_];
     [[maybe_unused]] const S* __restrict__ inv0 = T.inv0[h_];
@@ -510,14 +634,14 @@ __global__ void __launch_bounds__(kT) k_rbx_colour1(SellDev L, const RbTab<S> T,
     __shared__ bool last;
     if (ctl->done) return;
     const int tid = threadIdx.x;
-    const int i = L.n0 + cta * kT + tid;
+    const int i = LW ? L.n0 + cta * 32 + (tid & 31) : L.n0 + cta * kT + tid;
     double loc = 0.0;
     if (i < L.n) {
         const RowRef rr = row_ref(L, i);
         const int dg = rr.deg - 1;
         S xi[B], zi[B], y[B];
-        ld<B>(x + (size_t)i * B, xi);
-        ld<B>(z + (size_t)i * B, zi);
+        ldo<B>(x + (size_t)i * B, xi);
+        ldo<B>(z + (size_t)i * B, zi);
 #pragma unroll
         for (int k = 0; k < B; ++k) {
             xi[k] += zi[k];
@@ -527,12 +651,12 @@ __global__ void __launch_bounds__(kT) k_rbx_colour1(SellDev L, const RbTab<S> T,
         // pass 1: the residual row of sweep s, ascending (lower blocks, then the diagonal)
         for (int e = 0; e < dg; ++e) {
             S xk[B];
-            ld<B>(x + (size_t)acol(L, rr, e) * B, xk);
+            ldn<B>(x + (size_t)acol(L, rr, e) * B, xk);
             blk_matvec_add<B, S>(L, rr, e, xk, false, 0.0, y);
         }
         blk_matvec_add<B, S>(L, rr, dg, xi, shift != nullptr, shift ? shift[i] : 0.0, y);
         S ri[B];
-        ld<B>(rhs + (size_t)i * B, ri);
+        ldo<B>(rhs + (size_t)i * B, ri);
 #pragma unroll
         for (int k = 0; k < B; ++k) {
             ri[k] -= y[k];
@@ -544,7 +668,7 @@ __global__ void __launch_bounds__(kT) k_rbx_colour1(SellDev L, const RbTab<S> T,
             for (int e = 0; e < dg; ++e) {
                 const int kk = acol(L, rr, e);
                 S rk[B];
-                ld<B>(r + (size_t)kk * B, rk);
+                ldn<B>(r + (size_t)kk * B, rk);
                 const S* __restrict__ U = inv0 + (size_t)kk * B * B;
                 double A[2 * pairs<B>()];
                 ablock<B>(L, rr, e, A);
@@ -555,7 +679,7 @@ __global__ void __launch_bounds__(kT) k_rbx_colour1(SellDev L, const RbTab<S> T,
                 for (int c = 0; c < B; ++c) {
                     S uc[B];
 #pragma unroll
-                    for (int m = 0; m < B; ++m) uc[m] = U[m * B + c];
+                    for (int m = 0; m < B; ++m) uc[m] = ld_nb(U + m * B + c);
 #pragma unroll
                     for (int rw = 0; rw < B; ++rw) {
                         S lrc = zero<S>();
@@ -573,6 +697,37 @@ __global__ void __launch_bounds__(kT) k_rbx_colour1(SellDev L, const RbTab<S> T,
             lu_solve_reg<B>(lu, pv, ri);
             st<B>(z + (size_t)i * B, ri);
         }
+    }
+    if constexpr (LW) {
+        // per-slice partial; the warp that completes its lane's count takes the decision
+        double v = loc;
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+        int lastw = 0;
+        if ((tid & 31) == 0) {
+            partials[4 * grid0 + cta] = v;
+            __threadfence();
+            lastw = atomicAdd(counter, 1u) == (unsigned)(nct - 1);
+        }
+        lastw = __shfl_sync(0xffffffffu, lastw, 0);
+        if (!lastw) return;
+        __threadfence();
+        const double tot = ordered_sum_lw(partials, grid0, (L.n - L.n0 + kT - 1) / kT, (L.n0 + 31) / 32, nct);
+        if ((tid & 31) == 0) {
+            const double nrm = sqrt(tot);
+            ctl->iterations = sweep;
+            ctl->final_residual = nrm;
+            if (!isfinite(nrm)) {
+                ctl->status = 6;
+                ctl->done = 1;
+            } else if (nrm <= ctl->target) {
+                ctl->converged = 1;
+                ctl->done = 1;
+            } else if (sweep >= max_iter) {
+                ctl->done = 1;
+            }
+            *counter = 0u;
+        }
+        return;
     }
     const double bs = block_sum(loc, red);
     if (threadIdx.x == 0) {
@@ -1271,7 +1426,7 @@ RbSystem::RbSystem(const DevicePattern* p, int n0) : p_(p) {
     legacy_sync();
     grid0 = nb(n0);
     grid1 = nb(n - n0);
-    partials.alloc(std::max((n0 + 31) / 32 + (n - n0 + 31) / 32, nb((long long)n * b)) + 8);  // edge-parallel: one per slice
+    partials.alloc(std::max(4 * (grid0 + grid1), nb((long long)n * b)) + 8);  // slice-granular variants: 4 per 128-row group
 }
 
 void RbSystem::load(const double* A_csr, cudaStream_t stm) {
@@ -1359,7 +1514,19 @@ void rb_smoothed_solve_batch(const RbSystem& A, const RbMember<S>* mem, int P, d
                 { ::fnlh::note_launch(); k_rb_colour0<B, S><<<g0, kT, sm, stm>>>(sd, T, s); }
                 { ::fnlh::note_launch(); k_rb_resid1<B, S><<<g1, kT, 0, stm>>>(sd, T, A.grid0, s, max_iter); }
             }
-        } else if (rb_sweep_mode() == 0) {
+        } else if (rb_sweep_mode() == 4 && P > 1) {  // lane-warp CTAs (same arithmetic and norms, bitwise)
+            int gmax = 4;  // lanes per CTA (measurement override: FNLH_RB_LW_G=1..4)
+            if (const char* e = std::getenv("FNLH_RB_LW_G")) gmax = std::min(4, std::max(1, std::atoi(e)));
+            const int ng = (P + gmax - 1) / gmax, G = (P + ng - 1) / ng;
+            const int ns0 = (L.n0 + 31) / 32, ns1 = (L.n - L.n0 + 31) / 32;
+            const std::size_t smw = (std::size_t)maxoff * B * 32 * G * sizeof(S);
+            FNLH_CUDA(cudaFuncSetAttribute(k_rb_colour0<B, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            { ::fnlh::note_launch(); k_rb_forward1<B, S><<<g1, kT, 0, stm>>>(sd, T, 1); }
+            for (int s = 1; s <= max_iter; ++s) {
+                { ::fnlh::note_launch(); k_rb_colour0<B, S, true><<<ns0 * ng, 32 * G, smw, stm>>>(sd, T, s, G); }
+                { ::fnlh::note_launch(); k_rbx_colour1<B, S, true><<<ns1 * ng, 32 * G, 0, stm>>>(sd, T, A.grid0, s, max_iter, s < max_iter ? 1 : 0, G); }
+            }
+        } else if (rb_sweep_mode() == 0 || rb_sweep_mode() == 4) {
             { ::fnlh::note_launch(); k_rb_forward1<B, S><<<g1, kT, 0, stm>>>(sd, T, 1); }
             for (int s = 1; s <= max_iter; ++s) {
                 { ::fnlh::note_launch(); k_rb_colour0<B, S><<<g0, kT, sm, stm>>>(sd, T, s); }

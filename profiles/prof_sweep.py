@@ -20,7 +20,11 @@ s = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
 if "--step" in args:
     s.outer_iteration()
 names = {la.RB_EXACT: "exact", la.RB_EXACT_SPLIT: "exact-split", la.RB_ONEPASS: "one-pass"}
+names[la.RB_EDGE] = "edge-parallel"
+names[la.RB_LANEWARP] = "lane-warp"
 modes = list(names) if "--all" in args else [la.RB_ONEPASS if "--onepass" in args else la.RB_EXACT]
+if "--mode" in args:
+    modes = [int(args[args.index("--mode") + 1])]
 for mode in modes:
     la.set_rb_sweep(mode)
     if "--only-batch" not in args:
