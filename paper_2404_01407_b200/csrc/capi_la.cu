@@ -142,7 +142,14 @@ int rb_factor_impl(fnlh_pattern* p, const double* A, const double* shift_im, dou
         for (int i = 0; i < dp->rows; ++i)
             for (int k = 0; k < b; ++k) diag_piv[(std::size_t)i * b + k] = pk[f.packed_base(i, b) + 32 * k];
     }
-    if (inv0) download(reinterpret_cast<S*>(inv0), f.inv0, (std::size_t)p->n0 * bb);
+    if (inv0) {  // rb_uix: the device layout of a block (row-major unless a measurement build says otherwise)
+        std::vector<S> cm((std::size_t)p->n0 * bb);
+        download(cm.data(), f.inv0, cm.size());
+        S* out = reinterpret_cast<S*>(inv0);
+        for (int k = 0; k < p->n0; ++k)
+            for (int m = 0; m < b; ++m)
+                for (int c = 0; c < b; ++c) out[(std::size_t)k * bb + m * b + c] = cm[(std::size_t)k * bb + rb_uix(b, m, c)];
+    }
     return 0;
 }
 
@@ -257,7 +264,7 @@ void fnlh_set_red_black(int enable) { fnlh::rb_enabled() = enable != 0; }
 
 int fnlh_set_rb_sweep(int mode) {
     return guarded([&] {
-        if (mode < 0 || mode > 4) throw ConfigError("fnlh_set_rb_sweep: mode must be 0..4");
+        if (mode < 0 || mode > 6) throw ConfigError("fnlh_set_rb_sweep: mode must be 0..6");
         fnlh::rb_sweep_mode() = mode;
     });
 }

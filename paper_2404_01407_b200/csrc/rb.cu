@@ -1,6 +1,7 @@
 // rb.cu -- 2-colour fused ILU(0)-Richardson sweep (see rb.cuh for the derivation).
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "rb.cuh"
@@ -40,6 +41,18 @@ __device__ __forceinline__ RowRef row_ref(const SellDev& L, int i) {
 template <int B>
 __host__ __device__ constexpr int pairs() { return (B * B + 1) / 2; }
 
+// element (m, c) of a stored inv(U_kk) block (RbIlu::inv0).  Row-major: the loads of the first
+// column the L_ik rebuild consumes touch every other 32-byte sector of the block, which brings
+// most of the later columns into L1 with them (column-major blocks measured 2-3 % slower)
+template <int B>
+__host__ __device__ constexpr int uix(int m, int c) {
+#ifdef RB_U_COLMAJOR  // measurement build: column-major blocks (a column = one contiguous run)
+    return c * B + m;
+#else
+    return m * B + c;
+#endif
+}
+
 template <int B>
 __device__ __forceinline__ double aval(const SellDev& L, const RowRef& r, int e, int k) {
     return __ldg(L.vals + r.vbase + ((long long)(e * pairs<B>() + (k >> 1)) * 32) * 2 + (k & 1));
@@ -70,6 +83,33 @@ __device__ __forceinline__ int acol(const SellDev& L, const RowRef& r, int e) { 
 // operands several rows share instead of the ones read once
 #ifndef RB_L1HINT
 #define RB_L1HINT 0
+#endif
+// measurement switches of k_rbx_colour1 / k_rb_colour0: RB_IDXPF = load an edge's column index
+// one edge ahead (no index -> gather round trip inside the edge), RB_UHOIST = issue all b x b
+// loads of inv(U_kk) at the top of the edge (one round trip instead of one per column, more
+// registers), RB_C1_MINB = resident-CTA hint of k_rbx_colour1 (0: the compiler's choice)
+#ifndef RB_IDXPF
+#define RB_IDXPF 1
+#endif
+#ifndef RB_UHOIST
+#define RB_UHOIST 1
+#endif
+#ifndef RB_C1_MINB
+#define RB_C1_MINB 3
+#endif
+// RB_XPF / RB_RPF / RB_C0PF: the gathered vectors (x_k of the residual pass, r_k of the forward
+// pass, z_j and x_j of the colour-0 kernel) loaded one edge ahead into registers
+#ifndef RB_XPF
+#define RB_XPF 0
+#endif
+#ifndef RB_RPF
+#define RB_RPF 0
+#endif
+#ifndef RB_C0PF
+#define RB_C0PF 0
+#endif
+#ifndef RB_UPF  // prefetch.global.L1 of the whole inv(U_kk) block at the top of its edge
+#define RB_UPF 0
 #endif
 __device__ __forceinline__ cplx ldh_keep(const cplx* p) {
     cplx v;
@@ -268,7 +308,8 @@ __device__ double ordered_sum(const double* __restrict__ p, int n, double* red) 
 // partials w: q[k] = ((w[4k] + w[4k+1]) + w[4k+2]) + w[4k+3] (block_sum's order), colour-0
 // slices at [0, 4 grid0), colour-1 slices from 4 grid0; each thread plays the four virtual
 // threads lane, lane+32, lane+64, lane+96 of the 128-thread reduction.  Thread 0 gets the sum.
-__device__ double ordered_sum_lw(const double* __restrict__ p, int grid0, int grid1, int ns0, int ns1) {
+__device__ double ordered_sum_lw(const double* __restrict__ p, int grid0, int grid1, int ns0, int ns1,
+                                 bool c0_slices = true) {
     const int n = grid0 + grid1, lane = threadIdx.x & 31;
     const int chunk = (n + kT - 1) / kT;
     double sv[4];
@@ -280,8 +321,12 @@ __device__ double ordered_sum_lw(const double* __restrict__ p, int grid0, int gr
         for (int k = b0; k < b1; ++k) {
             const int lim = k < grid0 ? ns0 - 4 * k : ns1 - 4 * (k - grid0);  // slices of this group that exist
             double q = 0.0;
+            if (!c0_slices && k < grid0) {  // colour 0 came from the 128-row kernel: q[k] itself at [k]
+                q = __ldcg(p + k);
+            } else {
 #pragma unroll
-            for (int w = 0; w < 4; ++w) q += w < lim ? __ldcg(p + 4 * k + w) : 0.0;
+                for (int w = 0; w < 4; ++w) q += w < lim ? __ldcg(p + 4 * k + w) : 0.0;
+            }
             s += q;
         }
         for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
@@ -398,7 +443,7 @@ __global__ void __launch_bounds__(kT) k_rb_forward1(SellDev L, const RbTab<S> T,
         for (int c = 0; c < B; ++c) {
             S uc[B];
 #pragma unroll
-            for (int m = 0; m < B; ++m) uc[m] = U[m * B + c];
+            for (int m = 0; m < B; ++m) uc[m] = U[uix<B>(m, c)];
 #pragma unroll
             for (int rw = 0; rw < B; ++rw) {
                 S lrc = zero<S>();
@@ -462,11 +507,36 @@ __global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const RbTab<S> T, 
         const RowRef rr = row_ref(L, i);
         S t[B];
         ldo<B>((sweep == 1 ? rhs : r) + (size_t)i * B, t);  // forward: colour 0 rows copy r
+#if RB_IDXPF
+        int jn = rr.deg > 1 ? acol(L, rr, rr.deg - 1) : 0;
+#endif
+#if RB_IDXPF && RB_C0PF
+        S zn[B], xn[B];
+        ldn<B>(z + (size_t)jn * B, zn);
+        ldn<B>(x + (size_t)jn * B, xn);
+#endif
         for (int e = rr.deg - 1; e >= 1; --e) {
+#if RB_IDXPF
+            [[maybe_unused]] const int j = jn;
+            jn = acol(L, rr, e > 1 ? e - 1 : e);
+#else
             const int j = acol(L, rr, e);
+#endif
             S zj[B], xj[B];
+#if RB_IDXPF && RB_C0PF
+#pragma unroll
+            for (int k = 0; k < B; ++k) {
+                zj[k] = zn[k];
+                xj[k] = xn[k];
+            }
+            if (e > 1) {
+                ldn<B>(z + (size_t)jn * B, zn);
+                ldn<B>(x + (size_t)jn * B, xn);
+            }
+#else
             ldn<B>(z + (size_t)j * B, zj);
             ldn<B>(x + (size_t)j * B, xj);
+#endif
 #pragma unroll
             for (int k = 0; k < B; ++k) xj[k] += zj[k];  // colour-1 x += z ahead of K_R
             double A[2 * pairs<B>()];
@@ -603,7 +673,7 @@ __global__ void __launch_bounds__(kT) k_rb_resid1(SellDev L, const RbTab<S> T, i
 // parked in shared memory because the forward sum starts from r_i, which is known only
 // after the residual row is complete (zf = r_i - L r_k1 - L r_k2 ..., sparse.cpp:267-278).
 template <int B, class S, bool LW = false>
-__global__ void __launch_bounds__(kT, LW ? 3 : 0) k_rbx_colour1(SellDev L, const RbTab<S> T, int grid0, int sweep, int max_iter, int forward,
+__global__ void __launch_bounds__(kT, LW ? 3 : RB_C1_MINB) k_rbx_colour1(SellDev L, const RbTab<S> T, int grid0, int sweep, int max_iter, int forward,
                                                     int G = 0) {
     const int P_ = T.P;
     int h_, cta, nct_;
@@ -649,11 +719,37 @@ __global__ void __launch_bounds__(kT, LW ? 3 : 0) k_rbx_colour1(SellDev L, const
         }
         st<B>(x + (size_t)i * B, xi);
         // pass 1: the residual row of sweep s, ascending (lower blocks, then the diagonal)
+#if RB_IDXPF && RB_XPF
+        {
+            int kn = acol(L, rr, dg > 1 ? 1 : 0);
+            S xn[B];
+            ldn<B>(x + (size_t)acol(L, rr, 0) * B, xn);
+            for (int e = 0; e < dg; ++e) {
+                S xk[B];
+#pragma unroll
+                for (int k = 0; k < B; ++k) xk[k] = xn[k];
+                const int kc = kn;
+                kn = acol(L, rr, e + 2 < dg ? e + 2 : e);
+                if (e + 1 < dg) ldn<B>(x + (size_t)kc * B, xn);
+                blk_matvec_add<B, S>(L, rr, e, xk, false, 0.0, y);
+            }
+        }
+#elif RB_IDXPF
+        int kn = dg > 0 ? acol(L, rr, 0) : 0;
+        for (int e = 0; e < dg; ++e) {
+            const int kc = kn;
+            kn = acol(L, rr, e + 1 < dg ? e + 1 : e);
+            S xk[B];
+            ldn<B>(x + (size_t)kc * B, xk);
+            blk_matvec_add<B, S>(L, rr, e, xk, false, 0.0, y);
+        }
+#else
         for (int e = 0; e < dg; ++e) {
             S xk[B];
             ldn<B>(x + (size_t)acol(L, rr, e) * B, xk);
             blk_matvec_add<B, S>(L, rr, e, xk, false, 0.0, y);
         }
+#endif
         blk_matvec_add<B, S>(L, rr, dg, xi, shift != nullptr, shift ? shift[i] : 0.0, y);
         S ri[B];
         ldo<B>(rhs + (size_t)i * B, ri);
@@ -665,13 +761,44 @@ __global__ void __launch_bounds__(kT, LW ? 3 : 0) k_rbx_colour1(SellDev L, const
         // pass 2: forward substitution of sweep s+1 from r_i, the row's blocks again (now
         // L2-resident), L_ik = A_ik inv(U_kk) rebuilt in the reference's order
         if (forward) {
+#if RB_IDXPF
+            int kn2 = dg > 0 ? acol(L, rr, 0) : 0;
+#endif
+#if RB_IDXPF && RB_RPF
+            S rn[B];
+            ldn<B>(r + (size_t)kn2 * B, rn);
+#endif
             for (int e = 0; e < dg; ++e) {
+#if RB_IDXPF
+                const int kk = kn2;
+                kn2 = acol(L, rr, e + 1 < dg ? e + 1 : e);
+#else
                 const int kk = acol(L, rr, e);
+#endif
                 S rk[B];
+#if RB_IDXPF && RB_RPF
+#pragma unroll
+                for (int k = 0; k < B; ++k) rk[k] = rn[k];
+                if (e + 1 < dg) ldn<B>(r + (size_t)kn2 * B, rn);
+#else
                 ldn<B>(r + (size_t)kk * B, rk);
+#endif
                 const S* __restrict__ U = inv0 + (size_t)kk * B * B;
+#if RB_UPF
+#pragma unroll
+                for (int q = 0; q < (int)(B * B * sizeof(S) + 127) / 128; ++q)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(U) + 128 * q));
+#endif
+#if RB_UHOIST
+                S Ub[B * B];
+#pragma unroll
+                for (int q = 0; q < B * B; ++q) Ub[q] = ld_nb(U + q);
+#endif
                 double A[2 * pairs<B>()];
                 ablock<B>(L, rr, e, A);
+#if RB_UHOIST
+                asm volatile("" ::: "memory");  // every load of the edge is issued before its arithmetic
+#endif
                 S acc[B];
 #pragma unroll
                 for (int rw = 0; rw < B; ++rw) acc[rw] = zero<S>();
@@ -679,7 +806,11 @@ __global__ void __launch_bounds__(kT, LW ? 3 : 0) k_rbx_colour1(SellDev L, const
                 for (int c = 0; c < B; ++c) {
                     S uc[B];
 #pragma unroll
-                    for (int m = 0; m < B; ++m) uc[m] = ld_nb(U + m * B + c);
+#if RB_UHOIST
+                    for (int m = 0; m < B; ++m) uc[m] = Ub[uix<B>(m, c)];
+#else
+                    for (int m = 0; m < B; ++m) uc[m] = ld_nb(U + uix<B>(m, c));
+#endif
 #pragma unroll
                     for (int rw = 0; rw < B; ++rw) {
                         S lrc = zero<S>();
@@ -756,6 +887,264 @@ __global__ void __launch_bounds__(kT, LW ? 3 : 0) k_rbx_colour1(SellDev L, const
 }
 
 
+
+// ---- K_RF, staged (fnlh_set_rb_sweep(5)) ---------------------------------------------
+// k_rbx_colour1's arithmetic (bitwise, the same norms) with every operand of the forward
+// substitution fetched ahead of its use:
+//   * a CTA is one 32-row slice for up to 4 lanes of the batch (warp = lane); the slice's A
+//     blocks -- one contiguous SELL region -- are copied to shared memory once (cp.async) and
+//     serve both passes of all the CTA's lanes (A leaves L2 once per CTA instead of twice per
+//     lane);
+//   * inv(U_kk) streams through a per-thread ring of B + 1 columns in shared memory
+//     (cp.async, one commit group per column): while a thread rebuilds
+//     L_ik column c, the remaining columns of the edge and the first of the next are already
+//     in flight, so the thread never waits a round trip per column;
+//   * the column indices two edges ahead, and x_k / r_k one edge ahead, live in registers.
+// Two CTAs per SM (<= 255 registers): 8 warps whose loads are all issued an edge early.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+#ifndef RBS_MINB
+#define RBS_MINB 2
+#endif
+// RINGED = false (measurement): inv(U_kk) by ordinary loads through L1 as in k_rbx_colour1, only
+// the A blocks staged in shared memory
+template <int B, bool RINGED = true>
+__global__ void __launch_bounds__(kT, RBS_MINB) k_rbs_colour1(SellDev L, const RbTab<cplx> T, int grid0, int sweep, int max_iter,
+                                                       int forward, int G, int abytes, int c0_slices) {
+    using S = cplx;
+    constexpr int RING = B + 1;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const double2* As = reinterpret_cast<const double2*>(smem_raw);  // [slot][pair][lane]
+    S* ring = reinterpret_cast<S*>(smem_raw + abytes);               // [RING][B][thread]
+    const int P_ = T.P, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+    const int ng = (P_ + G - 1) / G;
+    const int h_ = (blockIdx.x % ng) * G + (tid >> 5);
+    const int cta = blockIdx.x / ng, nct = gridDim.x / ng;
+    const int i = L.n0 + cta * 32 + lane;
+    // a warp whose lane does not exist or has stopped only helps with the A copy; a CTA of such
+    // warps leaves at once
+    const bool warp_on = h_ < P_ && !T.ctl[h_ < P_ ? h_ : 0]->done;
+    if (!__syncthreads_or(warp_on)) return;
+    // the slice's A blocks: every thread of the CTA copies its share (group 0)
+    {
+        const int sl = L.nslices0 + cta;
+        const long long v0 = L.slice_val[sl], v1 = L.slice_val[sl + 1];
+        const char* src = reinterpret_cast<const char*>(L.vals + v0);
+        const int bytes = (int)((v1 - v0) * 8);
+        for (int o = tid * 16; o < bytes; o += nt * 16) cp_async16(smem_raw + o, src + o);
+        cp_async_commit();
+    }
+    const bool active = warp_on && i < L.n;  // rows past the end idle but stay for the warp's sums
+    RbControl* ctl = T.ctl[warp_on ? h_ : 0];
+    const S* __restrict__ inv0 = T.inv0[warp_on ? h_ : 0];
+    S* __restrict__ x = T.x[warp_on ? h_ : 0];
+    S* __restrict__ r = T.r[warp_on ? h_ : 0];
+    RowRef rr{};
+    int dg = 0, k0 = 0, k1 = 0, k2 = 0;
+    if (active) {
+        rr = row_ref(L, i);
+        dg = rr.deg - 1;
+        k0 = acol(L, rr, 0);  // padding slots hold the row itself: always a valid load
+        k1 = acol(L, rr, dg > 1 ? 1 : 0);
+        k2 = acol(L, rr, dg > 2 ? 2 : 0);
+    }
+    // ring prologue: columns 0 .. RING-1 of the forward pass (edge 0, then column 0 of edge 1)
+    const bool fwd = RINGED && active && forward;
+    if (fwd) {
+#pragma unroll
+        for (int j = 0; j < RING; ++j) {
+            const int de = j / B, c = j % B;
+            if (de < dg) {
+                const S* src = inv0 + (size_t)(de == 0 ? k0 : k1) * B * B;
+#pragma unroll
+                for (int m = 0; m < B; ++m) cp_async16(ring + ((size_t)(j * B + m) * nt + tid), src + uix<B>(m, c));
+            }
+            cp_async_commit();
+        }
+        cp_async_wait<RING>();  // group 0 (A) has landed; the ring may still be in flight
+    } else {
+        cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (!warp_on) return;
+    const S* __restrict__ diag_lu = T.diag_lu[h_];
+    const int* __restrict__ piv = T.piv[h_];
+    const double* __restrict__ shift = T.shift[h_];
+    const S* __restrict__ rhs = T.rhs[h_];
+    S* __restrict__ z = T.z[h_];
+    unsigned int* counter = &ctl->counter;
+    double* __restrict__ partials = T.parts[h_];
+    double loc = 0.0;
+    if (active) {
+        S xi[B], zi[B], y[B];
+        ld<B>(x + (size_t)i * B, xi);
+        ld<B>(z + (size_t)i * B, zi);
+        S bi[B];
+        ld<B>(rhs + (size_t)i * B, bi);
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            xi[k] += zi[k];
+            y[k] = zero<S>();
+        }
+        st<B>(x + (size_t)i * B, xi);
+        // pass 1: residual row of sweep s (ascending lower blocks, then the diagonal), A from
+        // shared memory, x_k one edge ahead
+        {
+            int ka = k0, kb = k1;
+            S xn[B];
+            ld<B>(x + (size_t)ka * B, xn);
+            for (int e = 0; e < dg; ++e) {
+                S xk[B];
+#pragma unroll
+                for (int k = 0; k < B; ++k) xk[k] = xn[k];
+                ka = kb;
+                kb = acol(L, rr, e + 2 < dg ? e + 2 : e);
+                if (e + 1 < dg) ld<B>(x + (size_t)ka * B, xn);
+                double A[2 * pairs<B>()];
+#pragma unroll
+                for (int p = 0; p < pairs<B>(); ++p) {
+                    const double2 v = As[(e * pairs<B>() + p) * 32 + lane];
+                    A[2 * p] = v.x;
+                    A[2 * p + 1] = v.y;
+                }
+#pragma unroll
+                for (int rw = 0; rw < B; ++rw) {
+                    S acc = zero<S>();
+#pragma unroll
+                    for (int c = 0; c < B; ++c) acc += rmul(A[rw * B + c], xk[c]);
+                    y[rw] += acc;
+                }
+            }
+            double A[2 * pairs<B>()];
+#pragma unroll
+            for (int p = 0; p < pairs<B>(); ++p) {
+                const double2 v = As[(dg * pairs<B>() + p) * 32 + lane];
+                A[2 * p] = v.x;
+                A[2 * p + 1] = v.y;
+            }
+            const double sft = shift ? shift[i] : 0.0;
+#pragma unroll
+            for (int rw = 0; rw < B; ++rw) {  // blk_matvec_add with the shifted diagonal
+                S acc = zero<S>();
+#pragma unroll
+                for (int c = 0; c < B; ++c) {
+                    const double a = A[rw * B + c];
+                    if (shift != nullptr && rw == c)
+                        acc += mk(a + 0.0, 0.0 + sft) * xi[c];
+                    else
+                        acc += rmul(a, xi[c]);
+                }
+                y[rw] += acc;
+            }
+        }
+        S ri[B];
+#pragma unroll
+        for (int k = 0; k < B; ++k) {
+            ri[k] = bi[k] - y[k];
+            loc += sq(ri[k]);
+        }
+        // pass 2: forward substitution of sweep s+1; inv(U_kk) columns from the ring
+        if (forward) {
+            S rn[B];
+            ld<B>(r + (size_t)k0 * B, rn);
+            for (int e = 0; e < dg; ++e) {
+                S rk[B];
+#pragma unroll
+                for (int k = 0; k < B; ++k) rk[k] = rn[k];
+                if (e + 1 < dg) ld<B>(r + (size_t)k1 * B, rn);
+                const int k3 = acol(L, rr, e + 3 < dg ? e + 3 : e);
+                double A[2 * pairs<B>()];
+#pragma unroll
+                for (int p = 0; p < pairs<B>(); ++p) {
+                    const double2 v = As[(e * pairs<B>() + p) * 32 + lane];
+                    A[2 * p] = v.x;
+                    A[2 * p + 1] = v.y;
+                }
+                S acc[B];
+#pragma unroll
+                for (int rw = 0; rw < B; ++rw) acc[rw] = zero<S>();
+#pragma unroll
+                for (int c = 0; c < B; ++c) {
+                    // column j = e B + c sits in ring slot j % RING; RING - 1 younger groups may be pending
+                    S uc[B];
+                    if constexpr (!RINGED) {
+                        const S* __restrict__ U = inv0 + (size_t)k0 * B * B;
+#pragma unroll
+                        for (int m = 0; m < B; ++m) uc[m] = U[uix<B>(m, c)];
+                    } else {
+                    cp_async_wait<RING - 1>();
+                    const int slot = (e * B + c) % RING;
+#pragma unroll
+                    for (int m = 0; m < B; ++m) uc[m] = ring[(size_t)(slot * B + m) * nt + tid];
+                    // refill the slot with column j + RING: edge e + de, column cn
+                    {
+                        const int de = (c + RING) / B, cn = (c + RING) % B;
+                        if (e + de < dg) {
+                            const S* src = inv0 + (size_t)(de == 1 ? k1 : k2) * B * B;
+#pragma unroll
+                            for (int m = 0; m < B; ++m) cp_async16(ring + ((size_t)(slot * B + m) * nt + tid), src + uix<B>(m, cn));
+                        }
+                        cp_async_commit();
+                    }
+                    }
+#pragma unroll
+                    for (int rw = 0; rw < B; ++rw) {
+                        S lrc = zero<S>();
+#pragma unroll
+                        for (int m = 0; m < B; ++m) lrc += rmul(A[rw * B + m], uc[m]);
+                        acc[rw] += lrc * rk[c];
+                    }
+                }
+#pragma unroll
+                for (int rw = 0; rw < B; ++rw) ri[rw] -= acc[rw];
+                k0 = k1;
+                k1 = k2;
+                k2 = k3;
+            }
+            S lu[B * B];
+            int pv[B];
+            ld_lu<B>(diag_lu, piv, lu_ref<B>(L, i), lu, pv);
+            lu_solve_reg<B>(lu, pv, ri);
+            st<B>(z + (size_t)i * B, ri);
+        }
+    }
+    // per-slice partial; the warp that completes its lane's count takes the decision
+    double v = loc;
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    int lastw = 0;
+    if (lane == 0) {
+        partials[4 * grid0 + cta] = v;
+        __threadfence();
+        lastw = atomicAdd(counter, 1u) == (unsigned)(nct - 1);
+    }
+    lastw = __shfl_sync(0xffffffffu, lastw, 0);
+    if (!lastw) return;
+    __threadfence();
+    const double tot = ordered_sum_lw(partials, grid0, (L.n - L.n0 + kT - 1) / kT, (L.n0 + 31) / 32, nct, c0_slices != 0);
+    if (lane == 0) {
+        const double nrm = sqrt(tot);
+        ctl->iterations = sweep;
+        ctl->final_residual = nrm;
+        if (!isfinite(nrm)) {
+            ctl->status = 6;
+            ctl->done = 1;
+        } else if (nrm <= ctl->target) {
+            ctl->converged = 1;
+            ctl->done = 1;
+        } else if (sweep >= max_iter) {
+            ctl->done = 1;
+        }
+        *counter = 0u;
+    }
+}
 
 // ---- K_B, edge-parallel (fnlh_set_rb_sweep(3)) -------------------------------------
 // k_rb_colour0's arithmetic with one thread per (row, upper block): warp q of the CTA (one
@@ -909,7 +1298,7 @@ __global__ void __launch_bounds__(192, RBE_MINB) k_rbe_colour1(SellDev L, const 
             for (int c = 0; c < B; ++c) {
                 S uc[B];
 #pragma unroll
-                for (int m = 0; m < B; ++m) uc[m] = U[m * B + c];
+                for (int m = 0; m < B; ++m) uc[m] = U[uix<B>(m, c)];
 #pragma unroll
                 for (int rw = 0; rw < B; ++rw) {
                     S lrc = zero<S>();
@@ -1239,7 +1628,7 @@ __global__ void k_rb_factor0(SellDev L, const double* __restrict__ shift, S* __r
         for (int r = 0; r < B; ++r) col[r] = (r == c) ? one<S>() : zero<S>();
         lu_solve_reg<B>(A, pv, col);
 #pragma unroll
-        for (int r = 0; r < B; ++r) inv0[(size_t)i * B * B + r * B + c] = col[r];
+        for (int r = 0; r < B; ++r) inv0[(size_t)i * B * B + uix<B>(r, c)] = col[r];
     }
 }
 
@@ -1269,7 +1658,7 @@ __global__ void k_rb_factor1(SellDev L, const int* __restrict__ row_ptr, const l
             for (int c = 0; c < B; ++c) {
                 S acc = zero<S>();
 #pragma unroll
-                for (int m = 0; m < B; ++m) acc += from_real<S>(aval<B>(L, rr, e, r * B + m)) * U[m * B + c];
+                for (int m = 0; m < B; ++m) acc += from_real<S>(aval<B>(L, rr, e, r * B + m)) * U[uix<B>(m, c)];
                 Lb[r * B + c] = acc;
             }
         // U_ii -= L_ik U_ki, U_ki = complex(A_ki) (block_matmul_sub, dense.hpp:42-52)
@@ -1526,7 +1915,25 @@ void rb_smoothed_solve_batch(const RbSystem& A, const RbMember<S>* mem, int P, d
                 { ::fnlh::note_launch(); k_rb_colour0<B, S, true><<<ns0 * ng, 32 * G, smw, stm>>>(sd, T, s, G); }
                 { ::fnlh::note_launch(); k_rbx_colour1<B, S, true><<<ns1 * ng, 32 * G, 0, stm>>>(sd, T, A.grid0, s, max_iter, s < max_iter ? 1 : 0, G); }
             }
-        } else if (rb_sweep_mode() == 0 || rb_sweep_mode() == 4) {
+        } else if ((rb_sweep_mode() == 5 || rb_sweep_mode() == 6) && P > 1 && std::is_same<S, cplx>::value &&
+                   (std::size_t)(maxoff + 1) * pairs<B>() * 512 + (std::size_t)(B + 1) * B * 128 * sizeof(cplx) <= 113 * 1024) {
+            // staged colour-1 kernel (same arithmetic and norms, bitwise); colour 0 as mode 0
+            if constexpr (std::is_same<S, cplx>::value) {
+                const int ng = (P + 3) / 4, G = (P + ng - 1) / ng;
+                const int ns1 = (L.n - L.n0 + 31) / 32;
+                const int abytes = (maxoff + 1) * pairs<B>() * 512;
+                const bool ringed = rb_sweep_mode() == 5;
+                const std::size_t sms = (std::size_t)abytes + (ringed ? (std::size_t)(B + 1) * B * 32 * G * sizeof(cplx) : 0);
+                FNLH_CUDA(cudaFuncSetAttribute(k_rbs_colour1<B, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms));
+                FNLH_CUDA(cudaFuncSetAttribute(k_rbs_colour1<B, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sms));
+                { ::fnlh::note_launch(); k_rb_forward1<B, S><<<g1, kT, 0, stm>>>(sd, T, 1); }
+                for (int s = 1; s <= max_iter; ++s) {
+                    { ::fnlh::note_launch(); k_rb_colour0<B, S><<<g0, kT, sm, stm>>>(sd, T, s); }
+                    if (ringed) { ::fnlh::note_launch(); k_rbs_colour1<B, true><<<ns1 * ng, 32 * G, sms, stm>>>(sd, T, A.grid0, s, max_iter, s < max_iter ? 1 : 0, G, abytes, 0); }
+                    else { ::fnlh::note_launch(); k_rbs_colour1<B, false><<<ns1 * ng, 32 * G, sms, stm>>>(sd, T, A.grid0, s, max_iter, s < max_iter ? 1 : 0, G, abytes, 0); }
+                }
+            }
+        } else if (rb_sweep_mode() == 0 || rb_sweep_mode() >= 4) {
             { ::fnlh::note_launch(); k_rb_forward1<B, S><<<g1, kT, 0, stm>>>(sd, T, 1); }
             for (int s = 1; s <= max_iter; ++s) {
                 { ::fnlh::note_launch(); k_rb_colour0<B, S><<<g0, kT, sm, stm>>>(sd, T, s); }

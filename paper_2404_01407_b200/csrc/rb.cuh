@@ -67,13 +67,22 @@ inline std::atomic<int>& rb_sweep_mode() {
 // is the pattern a 2-colour colour-major ordering with one partition?
 bool rb_eligible(const DevicePattern& p, int* n0);
 
+// element (m, c) of a stored inv(U_kk) block (row-major; rb.cu uix)
+inline int rb_uix(int b, int m, int c) {
+#ifdef RB_U_COLMAJOR
+    return c * b + m;
+#else
+    return m * b + c;
+#endif
+}
+
 template <class S>
 struct RbIlu {
     const DevicePattern* p = nullptr;
     int n0 = 0;
     S* diag_lu = nullptr;   // pivot LUs, slice-major [slice][k][lane] (rows padded to 32 per colour)
     int* diag_piv = nullptr;  // same layout, b per row
-    S* inv0 = nullptr;      // n0*b*b, inv(U_kk) of colour 0 rows
+    S* inv0 = nullptr;      // n0*b*b, inv(U_kk) of colour 0 rows, each block row-major (rb_uix)
     RbIlu(const DevicePattern* pat, int n0_);
     ~RbIlu();
     RbIlu(const RbIlu&) = delete;

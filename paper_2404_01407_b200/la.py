@@ -121,7 +121,7 @@ def set_red_black(enable: bool):
     lib().fnlh_set_red_black(_i(1 if enable else 0))
 
 
-RB_EXACT, RB_EXACT_SPLIT, RB_ONEPASS, RB_EDGE, RB_LANEWARP = 0, 1, 2, 3, 4
+RB_EXACT, RB_EXACT_SPLIT, RB_ONEPASS, RB_EDGE, RB_LANEWARP, RB_STAGED, RB_ASTAGED = 0, 1, 2, 3, 4, 5, 6
 
 
 def set_rb_sweep(mode: int):

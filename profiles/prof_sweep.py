@@ -22,6 +22,8 @@ if "--step" in args:
 names = {la.RB_EXACT: "exact", la.RB_EXACT_SPLIT: "exact-split", la.RB_ONEPASS: "one-pass"}
 names[la.RB_EDGE] = "edge-parallel"
 names[la.RB_LANEWARP] = "lane-warp"
+names[la.RB_STAGED] = "staged"
+names[la.RB_ASTAGED] = "A-staged"
 modes = list(names) if "--all" in args else [la.RB_ONEPASS if "--onepass" in args else la.RB_EXACT]
 if "--mode" in args:
     modes = [int(args[args.index("--mode") + 1])]

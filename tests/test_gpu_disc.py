@@ -141,14 +141,16 @@ def test_workers_batched_harmonics(name, scale, nh):
 @pytest.mark.parametrize("lanes", [2, 3, 5, 8])
 def test_lanewarp_batched_sweep_bitwise(lanes):
     """fnlh_set_rb_sweep(4): lane-warp CTAs (one 32-row slice for up to 4 lanes, a warp per lane,
-    the shared A blocks meeting in L1) run mode 0's arithmetic and form the same norms, so
-    histories, states and linear reports (iterations, residual norms) are bitwise mode 0's --
-    full and ragged lane groups (2, 3, 3+2, 4+4), a ragged last slice and last 128-row group."""
+    the shared A blocks meeting in L1) and fnlh_set_rb_sweep(5): the staged colour-1 kernel (the
+    slice's A blocks in shared memory for all the CTA's lanes, inv(U_kk) columns through a
+    cp.async ring) run mode 0's arithmetic and form the same norms, so histories, states and
+    linear reports (iterations, residual norms) are bitwise mode 0's -- full and ragged lane
+    groups (2, 3, 3+2, 4+4), a ragged last slice and last 128-row group."""
     from paper_2404_01407_b200 import la
     from paper_2404_01407_b200.solver import FnlhSolver
     runs = {}
     try:
-        for mode in (la.RB_EXACT, la.RB_LANEWARP):
+        for mode in (la.RB_EXACT, la.RB_LANEWARP, la.RB_STAGED, la.RB_ASTAGED):
             la.set_rb_sweep(mode)
             c = make_case("c2", scale=0.09, nh=lanes, workers=lanes)
             g = FnlhSolver(c.mesh, c.scheme, c.omegas, c.forcing, c.mean0)
@@ -157,11 +159,13 @@ def test_lanewarp_batched_sweep_bitwise(lanes):
             runs[mode] = (hist, g.state(), g.reports())
     finally:
         la.set_rb_sweep(la.RB_EXACT)
-    (h0, (m0, a0), r0), (h4, (m4, a4), r4) = runs[la.RB_EXACT], runs[la.RB_LANEWARP]
-    assert np.array_equal(m0, m4) and np.array_equal(a0, a4)
-    assert [e["resid_mean"] for e in h0] == [e["resid_mean"] for e in h4]
-    assert [e["rz"] for e in h0] == [e["rz"] for e in h4]
-    assert r0 == r4
+    h0, (m0, a0), r0 = runs[la.RB_EXACT]
+    for mode in (la.RB_LANEWARP, la.RB_STAGED, la.RB_ASTAGED):
+        h4, (m4, a4), r4 = runs[mode]
+        assert np.array_equal(m0, m4) and np.array_equal(a0, a4), mode
+        assert [e["resid_mean"] for e in h0] == [e["resid_mean"] for e in h4], mode
+        assert [e["rz"] for e in h0] == [e["rz"] for e in h4], mode
+        assert r0 == r4, mode
 
 
 @pytest.mark.parametrize("workers", [1, 3])
