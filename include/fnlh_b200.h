@@ -149,7 +149,12 @@ int fnlh_richardson(fnlh_prec* f, const double* rhs, double tol_rel, int max_ite
        reference's order from shared memory (at most 6 off-diagonal blocks per row);
      4 mode 0's kernels and arithmetic (bitwise, the same norms) with lane-warp CTAs for a
        batch of P > 1 systems sharing A: a CTA is one 32-row slice for up to 4 systems, one
-       warp each, so the systems' loads of the shared A blocks meet in L1. */
+       warp each, so the systems' loads of the shared A blocks meet in L1;
+     5 lane-warp CTAs whose slice of A sits in shared memory for both passes of all their
+       systems and whose inv(U_kk) columns stream through a per-thread cp.async ring one
+       edge ahead (complex batches, P > 1; bitwise, the same norms);
+     6 as 5 without the ring (inv(U_kk) through L1).
+   Modes 3-6 are measured variants: every one is slower than mode 0. */
 int fnlh_pattern_is_red_black(fnlh_pattern* p, int* n0);
 /* compact factors of the 2-colour ILU(0): pivot LU + piv for every row, inv(U_kk) for colour 0 */
 int fnlh_rb_factorize(fnlh_pattern* p, int is_complex, const double* A, const double* shift_im, double* diag_lu,

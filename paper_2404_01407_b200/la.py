@@ -128,7 +128,9 @@ def set_rb_sweep(mode: int):
     """2-colour sweep variant (include/fnlh_b200.h fnlh_set_rb_sweep): RB_EXACT (default,
     bitwise reference iterates, 2 kernels/sweep), RB_EXACT_SPLIT (same, 3 kernels/sweep),
     RB_ONEPASS (one pass over A, iterates equal to rounding), RB_EDGE (bitwise, the colour-1
-    kernel edge-parallel: one thread per (row, lower block))."""
+    kernel edge-parallel: one thread per (row, lower block)), RB_LANEWARP / RB_STAGED /
+    RB_ASTAGED (bitwise; batches of P > 1 systems: lane-warp CTAs, with A in shared memory and a
+    cp.async ring for inv(U_kk), or A in shared memory only) -- measured variants, DESIGN 4.1."""
     check(lib().fnlh_set_rb_sweep(_i(mode)))
 
 

@@ -13,7 +13,7 @@ def main(path, title=""):
     for r in data:
         if len(r) <= vi:
             continue
-        name = r[ki].split('(')[0].replace('void ', '').replace('unnamed>::', '')
+        name = r[ki].split('(')[0].replace('void ', '').replace('fnlh::<unnamed>::', '').replace('unnamed>::', '')
         v = float(r[vi].replace(',', '')) * {'nsecond': 1, 'usecond': 1e3, 'msecond': 1e6}.get(r[ui], 1)
         agg[name][0] += 1
         agg[name][1] += v
