@@ -668,10 +668,12 @@ __global__ void __launch_bounds__(kT) k_rb_resid1(SellDev L, const RbTab<S> T, i
 }
 
 // ---- K_RF: colour 1 residual of sweep s fused with the forward substitution of s+1 --
-// Both walk the row's lower blocks A_ik: y += A_ik x_k (residual, ascending) and
-// L_ik r_k with L_ik = A_ik inv(U_kk) rebuilt as in K_F; the L_ik r_k products are
-// parked in shared memory because the forward sum starts from r_i, which is known only
-// after the residual row is complete (zf = r_i - L r_k1 - L r_k2 ..., sparse.cpp:267-278).
+// Two passes over the row's lower blocks A_ik: y += A_ik x_k (residual, ascending), then --
+// r_i is known only once the residual row is complete and the forward sum starts from it
+// (zf = r_i - L r_k1 - L r_k2 ..., sparse.cpp:267-278) -- L_ik r_k with L_ik = A_ik inv(U_kk)
+// rebuilt as in K_F, the row's blocks read again (L1 / L2).  Every load of an edge (the b x b
+// inv(U_kk), A_ik, r_k) is issued before its arithmetic and the column index one edge ahead
+// (RB_UHOIST, RB_IDXPF): -3 % at 3 resident CTAs, DESIGN 4.1.
 template <int B, class S, bool LW = false>
 __global__ void __launch_bounds__(kT, LW ? 3 : RB_C1_MINB) k_rbx_colour1(SellDev L, const RbTab<S> T, int grid0, int sweep, int max_iter, int forward,
                                                     int G = 0) {
