@@ -64,12 +64,7 @@ __device__ __forceinline__ void ablock(const SellDev& L, const RowRef& r, int e,
     const double2* base = reinterpret_cast<const double2*>(L.vals + r.vbase) + (long long)e * pairs<B>() * 32;
 #pragma unroll
     for (int p = 0; p < pairs<B>(); ++p) {
-#if RB_L1HINT & 4
-        double2 v;
-        asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(base + (long long)p * 32));
-#else
         const double2 v = __ldg(base + (long long)p * 32);
-#endif
         A[2 * p] = v.x;
         A[2 * p + 1] = v.y;
     }
@@ -77,13 +72,6 @@ __device__ __forceinline__ void ablock(const SellDev& L, const RowRef& r, int e,
 
 __device__ __forceinline__ int acol(const SellDev& L, const RowRef& r, int e) { return __ldg(L.cols + r.cbase + e * 32); }
 
-// L1 cache hints (measurement switch RB_L1HINT, bit flags): 1 = gathered neighbour data
-// (inv(U_kk), x_k, r_k, z_j) loaded L1::evict_last, 2 = a row's own streamed operands (vectors,
-// pivot LU) L1::no_allocate, 4 = the A blocks L1::no_allocate -- so that the L1 keeps the
-// operands several rows share instead of the ones read once
-#ifndef RB_L1HINT
-#define RB_L1HINT 0
-#endif
 // measurement switches of k_rbx_colour1 / k_rb_colour0: RB_IDXPF = load an edge's column index
 // one edge ahead (no index -> gather round trip inside the edge), RB_UHOIST = issue all b x b
 // loads of inv(U_kk) at the top of the edge (one round trip instead of one per column, more
@@ -97,67 +85,6 @@ __device__ __forceinline__ int acol(const SellDev& L, const RowRef& r, int e) { 
 #ifndef RB_C1_MINB
 #define RB_C1_MINB 3
 #endif
-// RB_XPF / RB_RPF / RB_C0PF: the gathered vectors (x_k of the residual pass, r_k of the forward
-// pass, z_j and x_j of the colour-0 kernel) loaded one edge ahead into registers
-#ifndef RB_XPF
-#define RB_XPF 0
-#endif
-#ifndef RB_RPF
-#define RB_RPF 0
-#endif
-#ifndef RB_C0PF
-#define RB_C0PF 0
-#endif
-#ifndef RB_UPF  // prefetch.global.L1 of the whole inv(U_kk) block at the top of its edge
-#define RB_UPF 0
-#endif
-__device__ __forceinline__ cplx ldh_keep(const cplx* p) {
-    cplx v;
-    asm("ld.global.L1::evict_last.v2.f64 {%0,%1}, [%2];" : "=d"(v.re), "=d"(v.im) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ double ldh_keep(const double* p) {
-    double v;
-    asm("ld.global.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ cplx ldh_once(const cplx* p) {
-    cplx v;
-    asm("ld.global.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.re), "=d"(v.im) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ double ldh_once(const double* p) {
-    double v;
-    asm("ld.global.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-    return v;
-}
-// gathered operand of a neighbour row / streamed operand of the own row
-template <class S>
-__device__ __forceinline__ S ld_nb(const S* p) {
-#if RB_L1HINT & 1
-    return ldh_keep(p);
-#else
-    return *p;
-#endif
-}
-template <class S>
-__device__ __forceinline__ S ld_own(const S* p) {
-#if RB_L1HINT & 2
-    return ldh_once(p);
-#else
-    return *p;
-#endif
-}
-template <int B, class S>
-__device__ __forceinline__ void ldn(const S* __restrict__ p, S (&v)[B]) {
-#pragma unroll
-    for (int k = 0; k < B; ++k) v[k] = ld_nb(p + k);
-}
-template <int B, class S>
-__device__ __forceinline__ void ldo(const S* __restrict__ p, S (&v)[B]) {
-#pragma unroll
-    for (int k = 0; k < B; ++k) v[k] = ld_own(p + k);
-}
 
 // lu_solve_reg (block_lu_solve, dense.hpp:91-109) reading the LU entries from memory as it
 // uses them (row phase of the edge-parallel kernels: no 25-entry register block)
@@ -208,7 +135,7 @@ template <int B, class S>
 __device__ __forceinline__ void ld_lu(const S* __restrict__ dlu, const int* __restrict__ piv, const LuRef& q,
                                       S (&lu)[B * B], int (&pv)[B]) {
 #pragma unroll
-    for (int k = 0; k < B * B; ++k) lu[k] = ld_own(dlu + q.lu + 32 * k);
+    for (int k = 0; k < B * B; ++k) lu[k] = dlu[q.lu + 32 * k];
 #pragma unroll
     for (int k = 0; k < B; ++k) pv[k] = piv[q.pv + 32 * k];
 }
@@ -506,14 +433,9 @@ __global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const RbTab<S> T, 
     if (i < L.n0) {
         const RowRef rr = row_ref(L, i);
         S t[B];
-        ldo<B>((sweep == 1 ? rhs : r) + (size_t)i * B, t);  // forward: colour 0 rows copy r
+        ld<B>((sweep == 1 ? rhs : r) + (size_t)i * B, t);  // forward: colour 0 rows copy r
 #if RB_IDXPF
         int jn = rr.deg > 1 ? acol(L, rr, rr.deg - 1) : 0;
-#endif
-#if RB_IDXPF && RB_C0PF
-        S zn[B], xn[B];
-        ldn<B>(z + (size_t)jn * B, zn);
-        ldn<B>(x + (size_t)jn * B, xn);
 #endif
         for (int e = rr.deg - 1; e >= 1; --e) {
 #if RB_IDXPF
@@ -523,20 +445,8 @@ __global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const RbTab<S> T, 
             const int j = acol(L, rr, e);
 #endif
             S zj[B], xj[B];
-#if RB_IDXPF && RB_C0PF
-#pragma unroll
-            for (int k = 0; k < B; ++k) {
-                zj[k] = zn[k];
-                xj[k] = xn[k];
-            }
-            if (e > 1) {
-                ldn<B>(z + (size_t)jn * B, zn);
-                ldn<B>(x + (size_t)jn * B, xn);
-            }
-#else
-            ldn<B>(z + (size_t)j * B, zj);
-            ldn<B>(x + (size_t)j * B, xj);
-#endif
+            ld<B>(z + (size_t)j * B, zj);
+            ld<B>(x + (size_t)j * B, xj);
 #pragma unroll
             for (int k = 0; k < B; ++k) xj[k] += zj[k];  // colour-1 x += z ahead of K_R
             double A[2 * pairs<B>()];
@@ -559,7 +469,7 @@ __global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const RbTab<S> T, 
         ld_lu<B>(diag_lu, piv, lu_ref<B>(L, i), lu, pv);
         lu_solve_reg<B>(lu, pv, t);
         S xi[B];
-        ldo<B>(x + (size_t)i * B, xi);
+        ld<B>(x + (size_t)i * B, xi);
 #pragma unroll
         for (int k = 0; k < B; ++k) xi[k] += t[k];  // x += z (sparse.hpp:317)
         st<B>(x + (size_t)i * B, xi);
@@ -572,7 +482,7 @@ __global__ void __launch_bounds__(kT) k_rb_colour0(SellDev L, const RbTab<S> T, 
 #pragma unroll
             for (int rw = 0; rw < B; ++rw) y[rw] += park[((e - 1) * B + rw) * nt + tid];
         S bi[B];
-        ldo<B>(rhs + (size_t)i * B, bi);
+        ld<B>(rhs + (size_t)i * B, bi);
 #pragma unroll
         for (int k = 0; k < B; ++k) {
             const S v = bi[k] - y[k];
@@ -712,8 +622,8 @@ __global__ void __launch_bounds__(kT, LW ? 3 : RB_C1_MINB) k_rbx_colour1(SellDev
         const RowRef rr = row_ref(L, i);
         const int dg = rr.deg - 1;
         S xi[B], zi[B], y[B];
-        ldo<B>(x + (size_t)i * B, xi);
-        ldo<B>(z + (size_t)i * B, zi);
+        ld<B>(x + (size_t)i * B, xi);
+        ld<B>(z + (size_t)i * B, zi);
 #pragma unroll
         for (int k = 0; k < B; ++k) {
             xi[k] += zi[k];
@@ -721,40 +631,25 @@ __global__ void __launch_bounds__(kT, LW ? 3 : RB_C1_MINB) k_rbx_colour1(SellDev
         }
         st<B>(x + (size_t)i * B, xi);
         // pass 1: the residual row of sweep s, ascending (lower blocks, then the diagonal)
-#if RB_IDXPF && RB_XPF
-        {
-            int kn = acol(L, rr, dg > 1 ? 1 : 0);
-            S xn[B];
-            ldn<B>(x + (size_t)acol(L, rr, 0) * B, xn);
-            for (int e = 0; e < dg; ++e) {
-                S xk[B];
-#pragma unroll
-                for (int k = 0; k < B; ++k) xk[k] = xn[k];
-                const int kc = kn;
-                kn = acol(L, rr, e + 2 < dg ? e + 2 : e);
-                if (e + 1 < dg) ldn<B>(x + (size_t)kc * B, xn);
-                blk_matvec_add<B, S>(L, rr, e, xk, false, 0.0, y);
-            }
-        }
-#elif RB_IDXPF
+#if RB_IDXPF
         int kn = dg > 0 ? acol(L, rr, 0) : 0;
         for (int e = 0; e < dg; ++e) {
             const int kc = kn;
             kn = acol(L, rr, e + 1 < dg ? e + 1 : e);
             S xk[B];
-            ldn<B>(x + (size_t)kc * B, xk);
+            ld<B>(x + (size_t)kc * B, xk);
             blk_matvec_add<B, S>(L, rr, e, xk, false, 0.0, y);
         }
 #else
         for (int e = 0; e < dg; ++e) {
             S xk[B];
-            ldn<B>(x + (size_t)acol(L, rr, e) * B, xk);
+            ld<B>(x + (size_t)acol(L, rr, e) * B, xk);
             blk_matvec_add<B, S>(L, rr, e, xk, false, 0.0, y);
         }
 #endif
         blk_matvec_add<B, S>(L, rr, dg, xi, shift != nullptr, shift ? shift[i] : 0.0, y);
         S ri[B];
-        ldo<B>(rhs + (size_t)i * B, ri);
+        ld<B>(rhs + (size_t)i * B, ri);
 #pragma unroll
         for (int k = 0; k < B; ++k) {
             ri[k] -= y[k];
@@ -766,10 +661,6 @@ __global__ void __launch_bounds__(kT, LW ? 3 : RB_C1_MINB) k_rbx_colour1(SellDev
 #if RB_IDXPF
             int kn2 = dg > 0 ? acol(L, rr, 0) : 0;
 #endif
-#if RB_IDXPF && RB_RPF
-            S rn[B];
-            ldn<B>(r + (size_t)kn2 * B, rn);
-#endif
             for (int e = 0; e < dg; ++e) {
 #if RB_IDXPF
                 const int kk = kn2;
@@ -778,23 +669,12 @@ __global__ void __launch_bounds__(kT, LW ? 3 : RB_C1_MINB) k_rbx_colour1(SellDev
                 const int kk = acol(L, rr, e);
 #endif
                 S rk[B];
-#if RB_IDXPF && RB_RPF
-#pragma unroll
-                for (int k = 0; k < B; ++k) rk[k] = rn[k];
-                if (e + 1 < dg) ldn<B>(r + (size_t)kn2 * B, rn);
-#else
-                ldn<B>(r + (size_t)kk * B, rk);
-#endif
+                ld<B>(r + (size_t)kk * B, rk);
                 const S* __restrict__ U = inv0 + (size_t)kk * B * B;
-#if RB_UPF
-#pragma unroll
-                for (int q = 0; q < (int)(B * B * sizeof(S) + 127) / 128; ++q)
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(U) + 128 * q));
-#endif
 #if RB_UHOIST
                 S Ub[B * B];
 #pragma unroll
-                for (int q = 0; q < B * B; ++q) Ub[q] = ld_nb(U + q);
+                for (int q = 0; q < B * B; ++q) Ub[q] = U[q];
 #endif
                 double A[2 * pairs<B>()];
                 ablock<B>(L, rr, e, A);
@@ -811,7 +691,7 @@ __global__ void __launch_bounds__(kT, LW ? 3 : RB_C1_MINB) k_rbx_colour1(SellDev
 #if RB_UHOIST
                     for (int m = 0; m < B; ++m) uc[m] = Ub[uix<B>(m, c)];
 #else
-                    for (int m = 0; m < B; ++m) uc[m] = ld_nb(U + uix<B>(m, c));
+                    for (int m = 0; m < B; ++m) uc[m] = U[uix<B>(m, c)];
 #endif
 #pragma unroll
                     for (int rw = 0; rw < B; ++rw) {
