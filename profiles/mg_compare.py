@@ -16,6 +16,7 @@ from paper_2404_01407_b200.solver import FnlhSolver  # noqa: E402
 
 
 STOP_MEAN = False
+CKPT, CKPT_AFTER = "", 3300.0
 
 
 def run(name, scale, nh, scheme_over, drop, cap):
@@ -32,9 +33,28 @@ def run(name, scale, nh, scheme_over, drop, cap):
             # the same loop entry by entry (as cli.py drives it), left as soon as the MEAN residual
             # has dropped by `drop` orders -- for arms whose harmonic residual never gets there
             hist, reason = [], "iteration-cap"
-            for _ in range(cap):
+            it0, s0, t_call = 0, 0.0, time.time()
+            if CKPT and os.path.exists(CKPT + ".npz"):
+                # continue a run a previous call had to leave (one gpurun call is at most 3,600 s):
+                # the explicit scheme's whole state is (mean, amps); device seconds add up
+                import numpy as np
+                z = np.load(CKPT + ".npz")
+                g.set_state(z["mean"], z["amps"])
+                hist = [dict(iter=int(a), resid_mean=float(b), rz=float(c_), seconds=float(d)) for a, b, c_, d in z["hist"]]
+                it0, s0 = len(hist), hist[-1]["seconds"]
+                print(f"# resumed from {CKPT}.npz at iteration {it0}, {s0:.1f} device s", flush=True)
+            for _ in range(it0, cap):
                 e = g.outer_iteration()
-                hist.append(dict(iter=e["iter"], resid_mean=e["resid_mean"], rz=e["rz"], seconds=e["seconds"]))
+                hist.append(dict(iter=len(hist), resid_mean=e["resid_mean"], rz=e["rz"], seconds=s0 + e["seconds"]))
+                e = hist[-1]
+                if CKPT and (time.time() - t_call > CKPT_AFTER):
+                    import numpy as np
+                    mean, amps = g.state()
+                    np.savez(CKPT, mean=mean, amps=amps,
+                             hist=np.array([[h["iter"], h["resid_mean"], h["rz"], h["seconds"]] for h in hist]))
+                    print(f"# checkpoint at iteration {len(hist)}, {e['seconds']:.1f} device s -> {CKPT}.npz", flush=True)
+                    reason = "checkpointed"
+                    break
                 if len(hist) % 2000 == 0:
                     print(f"# {len(hist)} iterations, {e['seconds']:.1f} s, mean residual {e['resid_mean']:.4e} "
                           f"({hist[0]['resid_mean'] / e['resid_mean']:.3e}x down), rz {e['rz']:.4e}", flush=True)
@@ -86,9 +106,11 @@ def main():
     ap.add_argument("--max-implicit", type=int, default=0, help="iteration cap of the implicit arm (0: --max)")
     ap.add_argument("--arms", default="implicit,explicit_1grid,explicit_mg2,explicit_mg3")
     ap.add_argument("--stop-mean", action="store_true", help="leave an arm once its mean residual reached the drop")
+    ap.add_argument("--checkpoint", default="", help="with --stop-mean: resume from / save to this path (.npz)")
+    ap.add_argument("--checkpoint-after", type=float, default=3300.0, help="wall seconds after which to save and leave")
     a = ap.parse_args()
-    global STOP_MEAN
-    STOP_MEAN = a.stop_mean
+    global STOP_MEAN, CKPT, CKPT_AFTER
+    STOP_MEAN, CKPT, CKPT_AFTER = a.stop_mean, a.checkpoint, a.checkpoint_after
     arms = {
         "implicit": dict(implicit=1, workers=a.nh),
         "explicit_1grid": dict(implicit=0, sigma_cfl=a.cfl_explicit),
