@@ -142,13 +142,13 @@ int rb_factor_impl(fnlh_pattern* p, const double* A, const double* shift_im, dou
         for (int i = 0; i < dp->rows; ++i)
             for (int k = 0; k < b; ++k) diag_piv[(std::size_t)i * b + k] = pk[f.packed_base(i, b) + 32 * k];
     }
-    if (inv0) {  // rb_uix: the device layout of a block (row-major unless a measurement build says otherwise)
-        std::vector<S> cm((std::size_t)p->n0 * bb);
-        download(cm.data(), f.inv0, cm.size());
+    if (inv0) {  // slice-major on the device (rb_uoff); the C ABI returns row-major blocks per node
+        std::vector<S> dv((std::size_t)32 * ((p->n0 + 31) / 32) * bb);
+        download(dv.data(), f.inv0, dv.size());
         S* out = reinterpret_cast<S*>(inv0);
         for (int k = 0; k < p->n0; ++k)
             for (int m = 0; m < b; ++m)
-                for (int c = 0; c < b; ++c) out[(std::size_t)k * bb + m * b + c] = cm[(std::size_t)k * bb + rb_uix(b, m, c)];
+                for (int c = 0; c < b; ++c) out[(std::size_t)k * bb + m * b + c] = dv[rb_uoff(b, k, m, c)];
     }
     return 0;
 }

@@ -41,17 +41,29 @@ __device__ __forceinline__ RowRef row_ref(const SellDev& L, int i) {
 template <int B>
 __host__ __device__ constexpr int pairs() { return (B * B + 1) / 2; }
 
-// element (m, c) of a stored inv(U_kk) block (RbIlu::inv0).  Row-major: the loads of the first
-// column the L_ik rebuild consumes touch every other 32-byte sector of the block, which brings
-// most of the later columns into L1 with them (column-major blocks measured 2-3 % slower)
+// inv(U_kk) of the colour-0 rows (RbIlu::inv0) is stored slice-major like the pivot LUs: node k
+// -> slice k / 32, lane k % 32, element (m, c) of its block at [slice][m B + c][lane].  In a
+// bandwidth-reducing (RCM) order the 32 rows of a warp gather from (nearly) consecutive
+// neighbours, so the warp's load of one block element is a few contiguous 16-byte runs -- 4
+// cache lines instead of 32 -- which is what the L1 tag stage was busy with (RB_U_AOS: the
+// earlier one-block-per-node array, kept as a measurement build).
 template <int B>
-__host__ __device__ constexpr int uix(int m, int c) {
-#ifdef RB_U_COLMAJOR  // measurement build: column-major blocks (a column = one contiguous run)
-    return c * B + m;
+__host__ __device__ __forceinline__ std::size_t ubase(int node) {
+#ifdef RB_U_AOS
+    return (std::size_t)node * B * B;
 #else
-    return m * B + c;
+    return (std::size_t)(node >> 5) * 32 * B * B + (node & 31);
 #endif
 }
+template <int B>
+__host__ __device__ constexpr int uix(int m, int c) {
+#ifdef RB_U_AOS
+    return m * B + c;
+#else
+    return (m * B + c) * 32;
+#endif
+}
+
 
 template <int B>
 __device__ __forceinline__ double aval(const SellDev& L, const RowRef& r, int e, int k) {
@@ -358,7 +370,7 @@ __global__ void __launch_bounds__(kT) k_rb_forward1(SellDev L, const RbTab<S> T,
         const int kk = acol(L, rr, e);
         S zk[B];
         ld<B>(rv + (size_t)kk * B, zk);
-        const S* __restrict__ U = inv0 + (size_t)kk * B * B;
+        const S* __restrict__ U = inv0 + ubase<B>(kk);
         double A[2 * pairs<B>()];
         ablock<B>(L, rr, e, A);
         S acc[B];
@@ -670,11 +682,11 @@ __global__ void __launch_bounds__(kT, LW ? 3 : RB_C1_MINB) k_rbx_colour1(SellDev
 #endif
                 S rk[B];
                 ld<B>(r + (size_t)kk * B, rk);
-                const S* __restrict__ U = inv0 + (size_t)kk * B * B;
+                const S* __restrict__ U = inv0 + ubase<B>(kk);
 #if RB_UHOIST
                 S Ub[B * B];
 #pragma unroll
-                for (int q = 0; q < B * B; ++q) Ub[q] = U[q];
+                for (int q = 0; q < B * B; ++q) Ub[q] = U[uix<B>(q / B, q % B)];
 #endif
                 double A[2 * pairs<B>()];
                 ablock<B>(L, rr, e, A);
@@ -689,7 +701,7 @@ __global__ void __launch_bounds__(kT, LW ? 3 : RB_C1_MINB) k_rbx_colour1(SellDev
                     S uc[B];
 #pragma unroll
 #if RB_UHOIST
-                    for (int m = 0; m < B; ++m) uc[m] = Ub[uix<B>(m, c)];
+                    for (int m = 0; m < B; ++m) uc[m] = Ub[m * B + c];
 #else
                     for (int m = 0; m < B; ++m) uc[m] = U[uix<B>(m, c)];
 #endif
@@ -845,7 +857,7 @@ __global__ void __launch_bounds__(kT, RBS_MINB) k_rbs_colour1(SellDev L, const R
         for (int j = 0; j < RING; ++j) {
             const int de = j / B, c = j % B;
             if (de < dg) {
-                const S* src = inv0 + (size_t)(de == 0 ? k0 : k1) * B * B;
+                const S* src = inv0 + ubase<B>(de == 0 ? k0 : k1);
 #pragma unroll
                 for (int m = 0; m < B; ++m) cp_async16(ring + ((size_t)(j * B + m) * nt + tid), src + uix<B>(m, c));
             }
@@ -958,7 +970,7 @@ __global__ void __launch_bounds__(kT, RBS_MINB) k_rbs_colour1(SellDev L, const R
                     // column j = e B + c sits in ring slot j % RING; RING - 1 younger groups may be pending
                     S uc[B];
                     if constexpr (!RINGED) {
-                        const S* __restrict__ U = inv0 + (size_t)k0 * B * B;
+                        const S* __restrict__ U = inv0 + ubase<B>(k0);
 #pragma unroll
                         for (int m = 0; m < B; ++m) uc[m] = U[uix<B>(m, c)];
                     } else {
@@ -970,7 +982,7 @@ __global__ void __launch_bounds__(kT, RBS_MINB) k_rbs_colour1(SellDev L, const R
                     {
                         const int de = (c + RING) / B, cn = (c + RING) % B;
                         if (e + de < dg) {
-                            const S* src = inv0 + (size_t)(de == 1 ? k1 : k2) * B * B;
+                            const S* src = inv0 + ubase<B>(de == 1 ? k1 : k2);
 #pragma unroll
                             for (int m = 0; m < B; ++m) cp_async16(ring + ((size_t)(slot * B + m) * nt + tid), src + uix<B>(m, cn));
                         }
@@ -1172,7 +1184,7 @@ __global__ void __launch_bounds__(192, RBE_MINB) k_rbe_colour1(SellDev L, const 
         if (forward) {
             S rk[B];
             ld<B>(r + (size_t)kk * B, rk);
-            const S* __restrict__ U = inv0 + (size_t)kk * B * B;
+            const S* __restrict__ U = inv0 + ubase<B>(kk);
             S acc[B];
 #pragma unroll
             for (int rw = 0; rw < B; ++rw) acc[rw] = zero<S>();
@@ -1510,7 +1522,7 @@ __global__ void k_rb_factor0(SellDev L, const double* __restrict__ shift, S* __r
         for (int r = 0; r < B; ++r) col[r] = (r == c) ? one<S>() : zero<S>();
         lu_solve_reg<B>(A, pv, col);
 #pragma unroll
-        for (int r = 0; r < B; ++r) inv0[(size_t)i * B * B + uix<B>(r, c)] = col[r];
+        for (int r = 0; r < B; ++r) inv0[ubase<B>(i) + uix<B>(r, c)] = col[r];
     }
 }
 
@@ -1532,7 +1544,7 @@ __global__ void k_rb_factor1(SellDev L, const int* __restrict__ row_ptr, const l
     const int e0 = row_ptr[i];
     for (int e = 0; e < dg; ++e) {
         const int kk = acol(L, rr, e);
-        const S* U = inv0 + (size_t)kk * B * B;
+        const S* U = inv0 + ubase<B>(kk);
         S Lb[B * B];
 #pragma unroll
         for (int r = 0; r < B; ++r)
@@ -1617,7 +1629,7 @@ RbIlu<S>::RbIlu(const DevicePattern* pat, int n0_) : p(pat), n0(n0_) {
     const std::size_t bb = (std::size_t)p->b * p->b;
     FNLH_CUDA_ALLOC(&diag_lu, packed_rows() * bb * sizeof(S));
     FNLH_CUDA_ALLOC(&diag_piv, packed_rows() * p->b * sizeof(int));
-    FNLH_CUDA_ALLOC(&inv0, std::max<std::size_t>((std::size_t)n0 * bb, 1) * sizeof(S));
+    FNLH_CUDA_ALLOC(&inv0, std::max<std::size_t>((std::size_t)32 * ((n0 + 31) / 32) * bb, 1) * sizeof(S));
 }
 template <class S>
 RbIlu<S>::~RbIlu() {
@@ -1628,7 +1640,7 @@ RbIlu<S>::~RbIlu() {
 template <class S>
 std::size_t RbIlu<S>::bytes() const {
     const std::size_t bb = (std::size_t)p->b * p->b;
-    return (packed_rows() * bb + (std::size_t)n0 * bb) * sizeof(S) + packed_rows() * p->b * sizeof(int);
+    return (packed_rows() * bb + (std::size_t)32 * ((n0 + 31) / 32) * bb) * sizeof(S) + packed_rows() * p->b * sizeof(int);
 }
 
 RbSystem::RbSystem(const DevicePattern* p, int n0) : p_(p) {

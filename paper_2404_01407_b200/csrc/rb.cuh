@@ -67,12 +67,12 @@ inline std::atomic<int>& rb_sweep_mode() {
 // is the pattern a 2-colour colour-major ordering with one partition?
 bool rb_eligible(const DevicePattern& p, int* n0);
 
-// element (m, c) of a stored inv(U_kk) block (row-major; rb.cu uix)
-inline int rb_uix(int b, int m, int c) {
-#ifdef RB_U_COLMAJOR
-    return c * b + m;
+// element (m, c) of node k's inv(U_kk) block in RbIlu::inv0 (slice-major; rb.cu ubase / uix)
+inline std::size_t rb_uoff(int b, int k, int m, int c) {
+#ifdef RB_U_AOS
+    return (std::size_t)k * b * b + m * b + c;
 #else
-    return m * b + c;
+    return (std::size_t)(k >> 5) * 32 * b * b + (std::size_t)(m * b + c) * 32 + (k & 31);
 #endif
 }
 
@@ -82,7 +82,7 @@ struct RbIlu {
     int n0 = 0;
     S* diag_lu = nullptr;   // pivot LUs, slice-major [slice][k][lane] (rows padded to 32 per colour)
     int* diag_piv = nullptr;  // same layout, b per row
-    S* inv0 = nullptr;      // n0*b*b, inv(U_kk) of colour 0 rows, each block row-major (rb_uix)
+    S* inv0 = nullptr;      // inv(U_kk) of colour 0 rows, slice-major [slice][element][lane] (rb_uoff), rows padded to 32
     RbIlu(const DevicePattern* pat, int n0_);
     ~RbIlu();
     RbIlu(const RbIlu&) = delete;
