@@ -299,7 +299,7 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--order", default=None, choices=["rcm", "morton"],
+    ap.add_argument("--order", default=None, choices=["rcm", "morton", "lex", "lexk"],
                     help="node numbering inside each colour (default: the configuration's)")
     ap.add_argument("--sweeps", type=int, default=10, help="sweeps in the roofline leg")
     ap.add_argument("--mode", default="shard", choices=["replicas", "shard"],

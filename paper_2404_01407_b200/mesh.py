@@ -416,7 +416,7 @@ def structured_sector(ci, cj, ck, *, geometry="annular", length=2.0, pitch_deg=1
     colour-major RCM order (2 colours for hex, 8 for Kuhn tets).
 
     order: the node numbering inside each colour -- "rcm" (seeded permutation, then reverse
-    Cuthill-McKee) or "morton" (Z-order of the (i, j, k) index triple: a cache-oblivious
+    Cuthill-McKee), "lex" / "lexk" (lexicographic in the index triple) or "morton" (Z-order of the (i, j, k) index triple: a cache-oblivious
     renumbering for locality, so the neighbours a row gathers were touched recently by the
     rows around it).  On a 2-colour ordering the ILU(0) entries do not depend on the order
     inside a colour (only the summation order of each row's Schur update does).
@@ -502,6 +502,12 @@ def structured_sector(ci, cj, ck, *, geometry="annular", length=2.0, pitch_deg=1
         raise ValueError(f"unknown colouring {colouring!r}")
     if order == "morton":
         rank = morton_key(In.reshape(-1), Jn.reshape(-1), Kn.reshape(-1))  # rank[old], gid order
+    elif order in ("lex", "lexk"):
+        # lexicographic index order: every neighbour slot of 32 consecutive rows is one
+        # contiguous run of nodes ("lex": i fastest; "lexk": k fastest)
+        I_, J_, K_ = (a.reshape(-1).astype(np.int64) for a in (In, Jn, Kn))
+        mi, mj, mk = int(I_.max()) + 1, int(J_.max()) + 1, int(K_.max()) + 1
+        rank = (K_ * mj + J_) * mi + I_ if order == "lex" else (I_ * mj + J_) * mk + K_
     elif order == "rcm":
         inv0 = np.empty(n, np.int64)
         inv0[perm0] = np.arange(n)

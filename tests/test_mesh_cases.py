@@ -41,6 +41,22 @@ def test_colour_major_ordering(tets, ncol):
     assert not np.any(m.colour[m.fa[inter]] == m.colour[m.fb[inter]])
 
 
+@pytest.mark.parametrize("order", ["rcm", "morton", "lex", "lexk"])
+def test_orders_inside_a_colour_keep_the_ilu_pattern(order):
+    """The numbering inside each colour is free on a 2-colour ordering: every order is
+    colour-major, a permutation of the same nodes, with the same geometry per node."""
+    m = structured_sector(9, 7, 5, seed=2, order=order)
+    ref = structured_sector(9, 7, 5, seed=2, order="rcm")
+    assert (np.diff(m.colour) >= 0).all() and (m.colour == ref.colour).all()
+    key = lambda q: sorted(map(tuple, np.round(q.coords, 12)))  # noqa: E731
+    assert key(m) == key(ref)
+    ia = np.lexsort(np.round(m.coords, 12).T)
+    ib = np.lexsort(np.round(ref.coords, 12).T)
+    assert np.array_equal(m.vol[ia], ref.vol[ib])
+    pat = m.pattern()
+    assert len(pat["col_idx"]) == len(ref.pattern()["col_idx"])
+
+
 def test_node_face_csr_ascending():
     m = structured_sector(5, 4, 3, seed=5)
     for i in range(m.n):
